@@ -1,0 +1,188 @@
+/*
+ * sn_abi.h — C ABI of libsn100.so, the B200 (sm_100a) kernels behind the
+ * Super Apriel per-layer mixer step (arXiv 2604.19877).
+ *
+ * Drop-in position: the reference's placement vocabulary
+ * (R/pkg/src/placeopt/placements.py:19-105 — MixerCatalog / Placement with
+ * codes A=FA, S=SWA, K=KDA, G=GDN) selects, per layer, which of these mixer
+ * entry points the layer loop launches.  The reference ships no mixer code
+ * (R/SPEC.md:8 scopes it out); each entry point below replaces the mixer the
+ * paper describes (R/§6 R/PAPER.md:827-865) and that its
+ * serving stack runs through vLLM/FLA/FlashInfer.
+ *
+ * Conventions (all functions):
+ *   - plain device pointers + sizes; no allocation inside any call; every
+ *     launch is enqueued on `stream` (a cudaStream_t passed as void*), so all
+ *     of them are CUDA-graph capturable.  Lengths/positions are read from
+ *     device arrays, never from the host.
+ *   - `dtype` is the activation/weight I/O type (SN_BF16 or SN_F32).  Recurrent
+ *     states, softmax statistics and the residual stream are always fp32.
+ *   - return SN_OK or an error code; the message is in sn_last_error()
+ *     (thread-local).  Nothing aborts or throws across the ABI.
+ *   - stateless and reentrant; concurrency comes from streams / processes.
+ *
+ * Layouts (HBM):
+ *   paged KV (FA):      k_cache/v_cache [num_pages][Hkv][page_size][D]   ("HND" pages:
+ *                       one head's page is one contiguous page_size*D run, fed by
+ *                       cp.async.bulk); block_table [B][max_blocks] int32.
+ *   ring KV (SWA):      same page pool; a sequence owns window/page_size pages and
+ *                       position p lives at ring slot p % window.
+ *   recurrent state:    float [slots][Hv][D(v)][D(k)]  (each value column's key
+ *                       vector contiguous: one coalesced 512 B row per column).
+ *   conv ring:          T [slots][C][W]; the input at position p lives at slot p % W.
+ */
+#ifndef SN_ABI_H_
+#define SN_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SN_ABI_VERSION 1
+
+typedef enum { SN_OK = 0, SN_EINVAL = 1, SN_ECUDA = 2, SN_EUNSUPPORTED = 3 } sn_status;
+typedef enum { SN_F32 = 0, SN_BF16 = 1 } sn_dtype;
+
+/* Thread-local text of the last error (empty string if none). */
+const char* sn_last_error(void);
+int sn_abi_version(void);
+
+/* ---------------------------------------------------------------- trunk
+ * Shared trunk of every layer (R/PAPER.md:175-182, 855-856): embedding,
+ * pre-norms, SiLU-gated FFN, final norm, greedy sampler.                  */
+
+/* residual[r,:] = table[tokens[r],:] (fp32).  If seq_lens/positions are
+ * non-NULL this is also the decode-step prologue: positions[b] = seq_lens[b];
+ * seq_lens[b] += 1 for b < rows (so every later kernel of the step sees the
+ * new token's position and the post-append length).                        */
+sn_status sn_embed(const int32_t* tokens, const void* table, float* residual,
+                   int32_t* seq_lens, int32_t* positions, int rows, int dim,
+                   int dtype, void* stream);
+
+/* if delta != NULL: residual += delta;  out = rmsnorm(residual) * weight.  */
+sn_status sn_add_rmsnorm(const void* delta, float* residual, const void* weight,
+                         void* out, int rows, int dim, float eps, int dtype,
+                         void* stream);
+
+/* out[r,i] = silu(gate_up[r,i]) * gate_up[r,ffn+i]                         */
+sn_status sn_silu_mul(const void* gate_up, void* out, int rows, int ffn, int dtype,
+                      void* stream);
+
+/* out_tokens[r] = argmax_v logits[r,v] (lowest index on ties).             */
+sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens,
+                    int dtype, void* stream);
+
+/* ---------------------------------------------------------------- FA / SWA
+ * R/PAPER.md:1540-1563 (GQA + RoPE; SWA = same weights shape, window mask
+ * j in (t-w, t]).  Replaces the paged-KV attention backend the paper serves
+ * with (FlashInfer in vLLM, R/PAPER.md:1793).                               */
+
+/* Rotary embedding (rotate-half) on q and k of a fused qkv row
+ * [q Hq*D | k Hkv*D | v Hkv*D], then append k,v at the row's position into
+ * the page pool (window==0: slot = pos; window>0: ring slot = pos % window,
+ * rows older than seq_lens[seq]-window are not written).  q_out [rows][Hq][D];
+ * k_out/v_out [rows][Hkv][D] optional (prefill attention input).            */
+sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq,
+                            const int32_t* row_pos, const int32_t* seq_lens,
+                            const float* inv_freq, void* q_out, void* k_out,
+                            void* v_out, void* k_cache, void* v_cache,
+                            const int32_t* block_table, int rows, int Hq, int Hkv,
+                            int D, int page_size, int max_blocks, int window,
+                            int dtype, void* stream);
+
+/* Split-KV flash-decode over the page pool: one CTA per (split, kv head,
+ * sequence); each split streams split_pages pages of one head through a
+ * cp.async.bulk/mbarrier ring in shared memory; the GQA group of Hq/Hkv query
+ * heads shares every K/V byte read.  The last CTA of a (seq, head) merges
+ * the split partials (no second launch).  window==0 → FA over seq_lens[b]
+ * keys; window>0 → SWA over min(seq_lens[b], window) ring slots.
+ * workspace: sn_attn_decode_workspace_bytes(); counters: B*Hkv int32 zeroed
+ * once at allocation (the kernel leaves them zero).                       */
+size_t sn_attn_decode_workspace_bytes(int B, int Hq, int Hkv, int D, int max_splits);
+sn_status sn_attn_decode(const void* q, const void* k_cache, const void* v_cache,
+                         const int32_t* block_table, const int32_t* seq_lens,
+                         void* out, float* workspace, int32_t* counters, int B,
+                         int Hq, int Hkv, int D, int page_size, int max_blocks,
+                         int window, int split_pages, int max_splits, float scale,
+                         int dtype, void* stream);
+
+/* Causal (window==0) or sliding-window prefill attention over contiguous
+ * per-sequence q [rows][Hq][D], k/v [rows][Hkv][D] (cu_seqlens, int32).     */
+sn_status sn_attn_prefill(const void* q, const void* k, const void* v,
+                          const int32_t* cu_seqlens, void* out, int num_seqs,
+                          int rows, int Hq, int Hkv, int D, int window,
+                          float scale, int dtype, void* stream);
+
+/* ---------------------------------------------------------------- GDN / KDA
+ * R/PAPER.md:1565-1625.  Decode = one fused kernel per layer: causal-conv
+ * update (+SiLU), L2-norm q,k, gates, delta-rule state update in place,
+ * o = S^T q, gated RMSNorm.  State in HBM is touched exactly once (read +
+ * write), in coalesced 512 B column rows.
+ *
+ * GDN proj row layout (one fused in-proj GEMM output, R/PAPER.md:1584-1587):
+ *   [ q Hk*D | k Hk*D | v Hv*D | z Hv*D | b Hv | a Hv ]   conv channels = q|k|v
+ *   g = -exp(A_log[h]) * softplus(a + dt_bias[h]),  beta = sigmoid(b),
+ *   out = RMSNorm(o) * norm_w * silu(z)                                      */
+sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring,
+                        const void* conv_w, float* state, const int32_t* slot_idx,
+                        const int32_t* positions, const float* A_log,
+                        const float* dt_bias, const void* norm_w, void* out, int B,
+                        int Hk, int Hv, int D, int conv_width, float scale,
+                        float eps_l2, float eps_norm, int dtype, void* stream);
+
+/* KDA proj row layout: [ q H*D | k H*D | v H*D | f1 R | g1 R | b H ]
+ *   g[h,i] = -exp(A_log[h]) * softplus((f1 @ f2_w^T)[h*D+i] + dt_bias[h*D+i])
+ *   gate   = g1 @ g2_w^T + g2_b ;  out = RMSNorm(o) * norm_w * sigmoid(gate)
+ *   (f2_w, g2_w: [H*D][R] row-major; the second low-rank factors are fused
+ *    into the decode kernel)                                                 */
+sn_status sn_kda_decode(const void* proj, int proj_stride, void* conv_ring,
+                        const void* conv_w, float* state, const int32_t* slot_idx,
+                        const int32_t* positions, const float* A_log,
+                        const float* dt_bias, const void* f2_w, const void* g2_w,
+                        const void* g2_b, const void* norm_w, void* out, int B,
+                        int H, int D, int rank, int conv_width, float scale,
+                        float eps_l2, float eps_norm, int dtype, void* stream);
+
+/* Prefill building blocks (sequences packed by cu_seqlens, starting from an
+ * empty state/conv ring).                                                  */
+/* y[t, c] = silu(sum_w conv_w[c,w] * x[t-(W-1)+w, c]) for c < channels (x
+ * row stride x_stride); leaves the conv ring of slot_idx[s] in the decode
+ * layout.                                                                   */
+sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv_w,
+                          void* conv_ring, const int32_t* cu_seqlens,
+                          const int32_t* slot_idx, int num_seqs, int rows,
+                          int channels, int width, int dtype, void* stream);
+
+/* Per-token gate prep: qn/kn = l2norm(q/k) (qn also * scale), fp32 [rows][Hk][D];
+ * gexp = exp(g) fp32 ([rows][Hv] for GDN, [rows][Hv][D] for KDA);
+ * beta fp32 [rows][Hv].  kind: 0 = GDN (a, b read from proj), 1 = KDA
+ * (f = pre-softplus gate [rows][Hv*D] from the f2 GEMM, b from proj).       */
+sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj,
+                        int proj_stride, int b_off, int a_off, const void* f,
+                        const float* A_log, const float* dt_bias, float* qn,
+                        float* kn, float* gexp, float* beta, int rows, int Hk,
+                        int Hv, int D, float scale, float eps_l2, int dtype,
+                        void* stream);
+
+/* Recurrent scan over each sequence: o[t] (fp32 [rows][Hv][D]) and the final
+ * state written to state[slot_idx[s]] (read first if init_state != 0).      */
+sn_status sn_delta_scan(int kind, const float* qn, const float* kn,
+                        const void* qkv_conv, int v_off, int qkv_stride,
+                        const float* gexp, const float* beta, float* o,
+                        float* state, const int32_t* slot_idx,
+                        const int32_t* cu_seqlens, int num_seqs, int Hk, int Hv,
+                        int D, int init_state, int dtype, void* stream);
+
+/* out[r,h,:] = RMSNorm(o[r,h,:]) * norm_w * act(gate[r, h*D + :]),
+ * act: 0 = silu (GDN), 1 = sigmoid (KDA).  gate row stride gate_stride.    */
+sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride,
+                           const void* norm_w, void* out, int rows, int H, int D,
+                           float eps, int act, int dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SN_ABI_H_ */

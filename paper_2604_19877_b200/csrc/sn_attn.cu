@@ -1,0 +1,290 @@
+// FA / SWA mixers (R/PAPER.md:1540-1563): GQA attention with RoPE over a paged
+// KV pool (FA) or a per-sequence ring of `window` slots in the same pool (SWA).
+//
+// Decode cost model (R/PAPER.md:1548-1556): reading K and V is 2*t*Hkv*D*b bytes
+// per layer per sequence at intensity ~Hq/(2*Hkv*b) flop/byte, so decode is an
+// HBM stream.  This file holds the bookkeeping kernels (RoPE + KV append),
+// the CUDA-core split-KV decode (fp32 I/O and cross-check path), and prefill.
+// The bf16 tensor-core decode lives in sn_attn_tc.cu.
+#include "sn_common.cuh"
+#include "sn_attn.cuh"
+
+namespace sn {
+
+// ------------------------------------------------------------------ RoPE + append
+// grid (rows), block: one thread per rotary pair of every head.
+template <typename T>
+__global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ row_seq,
+                                      const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
+                                      const float* __restrict__ inv_freq, T* __restrict__ q_out,
+                                      T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
+                                      T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
+                                      int Hkv, int D, int page_size, int max_blocks, int window) {
+  const int r = blockIdx.x;
+  const int seq = row_seq ? row_seq[r] : r;
+  const int pos = row_pos[r];
+  const int half = D / 2;
+  const int stride = (Hq + 2 * Hkv) * D;
+  const T* row = qkv + (size_t)r * stride;
+  // cache slot for this row (or -1 when an SWA row is already outside the window)
+  int slot = window > 0 ? pos % window : pos;
+  bool write = true;
+  if (window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window) write = false;
+  const int page = block_table[(size_t)seq * max_blocks + slot / page_size];
+  const int off = slot % page_size;
+  for (int idx = threadIdx.x; idx < (Hq + Hkv) * half; idx += blockDim.x) {
+    const int head = idx / half, i = idx - head * half;
+    const float ang = (float)pos * inv_freq[i];
+    float sn, cs;
+    sincosf(ang, &sn, &cs);
+    const T* src = row + head * D;  // q heads then k heads are contiguous in the row
+    const float x1 = io<T>::ld(src + i), x2 = io<T>::ld(src + i + half);
+    const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+    if (head < Hq) {
+      T* dst = q_out + ((size_t)r * Hq + head) * D;
+      io<T>::st(dst + i, y1);
+      io<T>::st(dst + i + half, y2);
+    } else {
+      const int hk = head - Hq;
+      if (k_out) {
+        T* dst = k_out + ((size_t)r * Hkv + hk) * D;
+        io<T>::st(dst + i, y1);
+        io<T>::st(dst + i + half, y2);
+      }
+      if (write) {
+        T* dst = k_cache + (((size_t)page * Hkv + hk) * page_size + off) * D;
+        io<T>::st(dst + i, y1);
+        io<T>::st(dst + i + half, y2);
+      }
+    }
+  }
+  for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
+    const int hk = idx / D, d = idx - hk * D;
+    const T val = row[(Hq + Hkv) * D + idx];
+    if (v_out) v_out[((size_t)r * Hkv + hk) * D + d] = val;
+    if (write) v_cache[(((size_t)page * Hkv + hk) * page_size + off) * D + d] = val;
+  }
+}
+
+// ------------------------------------------------------------------ CUDA-core decode
+// CTA = (split, kv head, seq), 4 warps; warp w takes keys w, w+4, ... of the split,
+// keeps its own online-softmax state, the 4 states merge in smem.
+template <typename T, int D, int GMAX>
+__global__ void __launch_bounds__(128) attn_decode_simt_kernel(AttnDecodeArgs a) {
+  constexpr int EPL = D / 32;
+  __shared__ float s_q[GMAX][D];
+  __shared__ float s_m[4][GMAX], s_l[4][GMAX];
+  __shared__ float s_o[4][GMAX][D];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+  const int G = a.Hq / a.Hkv;
+  const int len = a.seq_lens[b];
+  const int n_keys = a.window > 0 ? min(len, a.window) : len;
+  const int split_keys = a.split_pages * a.page_size;
+  const int num_splits = max(1, (n_keys + split_keys - 1) / split_keys);
+  if (split >= num_splits) return;
+  const int k0 = split * split_keys, k1 = min(n_keys, k0 + split_keys);
+  const T* Q = reinterpret_cast<const T*>(a.q);
+  const T* Kc = reinterpret_cast<const T*>(a.k_cache);
+  const T* Vc = reinterpret_cast<const T*>(a.v_cache);
+  const float qscale = a.scale * 1.4426950408889634f;
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int g = idx / D, d = idx - g * D;
+    s_q[g][d] = io<T>::ld(Q + ((size_t)b * a.Hq + hk * G + g) * D + d) * qscale;
+  }
+  __syncthreads();
+  float m[GMAX], l[GMAX], o[GMAX][EPL];
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) o[g][e] = 0.f;
+  }
+  const int32_t* bt = a.block_table + (size_t)b * a.max_blocks;
+  for (int key = k0 + warp; key < k1; key += 4) {
+    const int page = bt[key / a.page_size], off = key % a.page_size;
+    const size_t base = (((size_t)page * a.Hkv + hk) * a.page_size + off) * D;
+    float kv[EPL], vv[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      kv[e] = io<T>::ld(Kc + base + lane + 32 * e);
+      vv[e] = io<T>::ld(Vc + base + lane + 32 * e);
+    }
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+      if (g < G) {
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) s += s_q[g][lane + 32 * e] * kv[e];
+        s = warp_sum(s);
+        const float mn = fmaxf(m[g], s);
+        const float alpha = exp2f(m[g] - mn), p = exp2f(s - mn);
+        l[g] = l[g] * alpha + p;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) o[g][e] = o[g][e] * alpha + p * vv[e];
+        m[g] = mn;
+      }
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < GMAX; ++g) {
+    if (g < G) {
+      if (lane == 0) { s_m[warp][g] = m[g]; s_l[warp][g] = l[g]; }
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) s_o[warp][g][lane + 32 * e] = o[g][e];
+    }
+  }
+  __syncthreads();
+  // merge the 4 warps into one partial (m, l, o unnormalised)
+  float* ws_o = a.workspace;
+  float* ws_ml = a.workspace + (size_t)a.B * a.Hkv * a.max_splits * G * D;
+  const size_t part = ((size_t)b * a.Hkv + hk) * a.max_splits + split;
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int g = idx / D, d = idx - g * D;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][g]);
+    float L = 0.f, O = 0.f;
+    for (int w = 0; w < 4; ++w) {
+      const float f = s_m[w][g] == -INFINITY ? 0.f : exp2f(s_m[w][g] - M);
+      L += s_l[w][g] * f;
+      O += s_o[w][g][d] * f;
+    }
+    ws_o[(part * G + g) * D + d] = O;
+    if (d == 0) { ws_ml[(part * G + g) * 2] = M; ws_ml[(part * G + g) * 2 + 1] = L; }
+  }
+  finish_split<T>(a, b, hk, num_splits, G, D);
+}
+
+// ------------------------------------------------------------------ prefill (CUDA cores)
+// One warp per (query row, q head); keys in blocks of 32: lane j scores key j
+// (full-D dot, q broadcast from smem), warp-level online softmax, then lanes
+// switch to owning D/32 output dims for the P.V accumulation.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                           const T* __restrict__ v, const int32_t* __restrict__ cu,
+                                                           T* __restrict__ out, int num_seqs, int rows, int Hq,
+                                                           int Hkv, int window, float scale) {
+  constexpr int EPL = D / 32;
+  __shared__ float s_q[4][D];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * 4 + warp;
+  const int h = blockIdx.y;
+  if (r >= rows) return;
+  int s = 0;
+  while (s + 1 < num_seqs && cu[s + 1] <= r) ++s;
+  const int t0 = cu[s];
+  const int i = r - t0;
+  const int G = Hq / Hkv, hk = h / G;
+  const float qscale = scale * 1.4426950408889634f;
+  for (int d = lane; d < D; d += 32) s_q[warp][d] = io<T>::ld(q + ((size_t)r * Hq + h) * D + d) * qscale;
+  __syncwarp();
+  const int j_lo = window > 0 ? max(0, i - window + 1) : 0;
+  float m = -INFINITY, l = 0.f, o[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) o[e] = 0.f;
+  for (int jb = j_lo; jb <= i; jb += 32) {
+    const int j = jb + lane;
+    float sc = -INFINITY;
+    if (j <= i) {
+      const T* kr = k + ((size_t)(t0 + j) * Hkv + hk) * D;
+      float acc = 0.f;
+      for (int d = 0; d < D; d += 8) {
+        float f[8];
+        load8<T>(kr + d, f);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) acc += f[x] * s_q[warp][d + x];
+      }
+      sc = acc;
+    }
+    const float mn = fmaxf(m, warp_max(sc));
+    const float p = j <= i ? exp2f(sc - mn) : 0.f;
+    const float alpha = exp2f(m - mn);
+    l = l * alpha + warp_sum(p);
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) o[e] *= alpha;
+    const int nk = min(32, i - jb + 1);
+    for (int x = 0; x < nk; ++x) {
+      const float px = __shfl_sync(0xffffffffu, p, x);
+      const T* vr = v + ((size_t)(t0 + jb + x) * Hkv + hk) * D;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) o[e] += px * io<T>::ld(vr + lane + 32 * e);
+    }
+    m = mn;
+  }
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) io<T>::st(out + ((size_t)r * Hq + h) * D + lane + 32 * e, o[e] * inv);
+}
+
+sn_status attn_decode_tc_bf16(const AttnDecodeArgs& a, int D, cudaStream_t st);  // sn_attn_tc.cu
+
+}  // namespace sn
+
+using namespace sn;
+
+extern "C" {
+
+sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq, const int32_t* row_pos,
+                            const int32_t* seq_lens, const float* inv_freq, void* q_out, void* k_out,
+                            void* v_out, void* k_cache, void* v_cache, const int32_t* block_table, int rows,
+                            int Hq, int Hkv, int D, int page_size, int max_blocks, int window, int dtype,
+                            void* stream) {
+  SN_REQUIRE(rows > 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0 && D % 2 == 0, "sn_rope_kv_append: bad shape");
+  SN_REQUIRE(page_size > 0 && (window == 0 || window % page_size == 0),
+             "sn_rope_kv_append: window %d must be a multiple of page_size %d", window, page_size);
+  SN_REQUIRE(qkv && row_pos && inv_freq && q_out && k_cache && v_cache && block_table,
+             "sn_rope_kv_append: NULL pointer argument");
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    rope_kv_append_kernel<T><<<rows, 256, 0, (cudaStream_t)stream>>>(
+        (const T*)qkv, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache,
+        (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
+    return check_launch("sn_rope_kv_append");
+  });
+}
+
+size_t sn_attn_decode_workspace_bytes(int B, int Hq, int Hkv, int D, int max_splits) {
+  const size_t G = Hkv > 0 ? (size_t)(Hq / Hkv) : 0;
+  return (size_t)B * Hkv * max_splits * G * (D + 2) * sizeof(float);
+}
+
+sn_status sn_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* block_table,
+                         const int32_t* seq_lens, void* out, float* workspace, int32_t* counters, int B, int Hq,
+                         int Hkv, int D, int page_size, int max_blocks, int window, int split_pages,
+                         int max_splits, float scale, int dtype, void* stream) {
+  SN_REQUIRE(B > 0 && Hkv > 0 && Hq % Hkv == 0 && Hq / Hkv <= 8, "sn_attn_decode: bad heads Hq=%d Hkv=%d", Hq, Hkv);
+  SN_REQUIRE(split_pages > 0 && max_splits > 0, "sn_attn_decode: bad split config");
+  SN_REQUIRE(window == 0 || window % page_size == 0, "sn_attn_decode: window %% page_size != 0");
+  SN_REQUIRE(q && k_cache && v_cache && block_table && seq_lens && out && workspace && counters,
+             "sn_attn_decode: NULL pointer argument");
+  AttnDecodeArgs a{q, k_cache, v_cache, block_table, seq_lens, out, workspace, counters, B, Hq, Hkv,
+                   page_size, max_blocks, window, split_pages, max_splits, scale};
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool force_simt = (dtype & SN_ATTN_FORCE_SIMT) != 0;
+  dtype &= ~SN_ATTN_FORCE_SIMT;
+  if (dtype == SN_BF16 && !force_simt && (D == 128 || D == 64) && page_size == 64)
+    return attn_decode_tc_bf16(a, D, st);
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    dim3 grid(max_splits, Hkv, B);
+    if (D == 128) attn_decode_simt_kernel<T, 128, 8><<<grid, 128, 0, st>>>(a);
+    else if (D == 64) attn_decode_simt_kernel<T, 64, 8><<<grid, 128, 0, st>>>(a);
+    else { set_error("sn_attn_decode: D=%d unsupported", D); return SN_EUNSUPPORTED; }
+    return check_launch("sn_attn_decode");
+  });
+}
+
+sn_status sn_attn_prefill(const void* q, const void* k, const void* v, const int32_t* cu_seqlens, void* out,
+                          int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale, int dtype,
+                          void* stream) {
+  SN_REQUIRE(num_seqs > 0 && rows > 0 && Hkv > 0 && Hq % Hkv == 0, "sn_attn_prefill: bad shape");
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    dim3 grid(ceil_div(rows, 4), Hq);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (D == 128) attn_prefill_kernel<T, 128><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, cu_seqlens, (T*)out, num_seqs, rows, Hq, Hkv, window, scale);
+    else if (D == 64) attn_prefill_kernel<T, 64><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, cu_seqlens, (T*)out, num_seqs, rows, Hq, Hkv, window, scale);
+    else { set_error("sn_attn_prefill: D=%d unsupported", D); return SN_EUNSUPPORTED; }
+    return check_launch("sn_attn_prefill");
+  });
+}
+
+}  // extern "C"

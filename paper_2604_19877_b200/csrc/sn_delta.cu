@@ -1,0 +1,533 @@
+// GDN / KDA gated delta-rule mixers (R/PAPER.md:1565-1625).
+//
+//   GDN: S_t = e^{g_t} (I - b_t k_t k_t^T) S_{t-1} + b_t k_t v_t^T       (scalar gate / value head)
+//   KDA: S_t = (I - b_t k_t k_t^T) diag(e^{g_t}) S_{t-1} + b_t k_t v_t^T  (per-key-channel gate)
+//   o_t = S_t^T q_t, then gated RMSNorm and the out-projection (a GEMM outside).
+//
+// Unstated details pinned from FLA 0.5.1: L2-norm
+// x/sqrt(sum x^2 + 1e-6) (3P-FLA/modules/l2norm.py:40-43), q scaled by D^-1/2,
+// gates g = -exp(A_log) * softplus(raw + dt_bias) (3P-FLA/ops/*/gate.py), beta =
+// sigmoid, causal conv width 4 with SiLU (3P-FLA/modules/conv/short_conv.py:201-243),
+// output norm RMSNorm(o) * w * act(gate) with act = silu (GDN) / sigmoid (KDA)
+// (3P-FLA/modules/fused_norm_gate.py:94-100).
+//
+// Decode kernel (the hot path): one CTA per (value head, sequence).  The CTA
+//   1. runs the conv update for its q/k/v channels against the per-sequence
+//      conv ring (slot p % W holds the input of position p, so CTAs that share
+//      a key head never race: they read slots != pos % W, one of them writes it),
+//   2. L2-normalises q,k, computes the gate(s) and beta (KDA: the second
+//      low-rank factors of the gate / output gate are fused here as 128x128
+//      matvecs whose weights stay L2-resident across the batch),
+//   3. streams the fp32 state once: every warp owns D/8 value columns; a
+//      column's D key entries are one coalesced 512 B row (float4 per lane);
+//      both dot products (k and q against the decayed state) are taken from the
+//      same registers, using  q.S_new = (q*e^g).S + (q.k) u,
+//   4. applies the gated RMSNorm over the head and writes bf16/fp32 output.
+// The state is read once and written once: 2*D*D*4 bytes per (sequence, head).
+#include "sn_common.cuh"
+
+namespace sn {
+
+struct DeltaDecodeArgs {
+  const void* proj;
+  int proj_stride;
+  void* conv_ring;
+  const void* conv_w;
+  float* state;
+  const int32_t* slot_idx;
+  const int32_t* positions;
+  const float* A_log;
+  const float* dt_bias;
+  const void* f2_w;
+  const void* g2_w;
+  const void* g2_b;
+  const void* norm_w;
+  void* out;
+  int Hk, Hv, rank, W, conv_channels;
+  int q_off, k_off, v_off, z_off, b_off, a_off, f1_off, g1_off;
+  float scale, eps_l2, eps_norm;
+};
+
+template <int EPL> struct vecf;
+template <> struct vecf<4> {
+  static __device__ __forceinline__ void ld(const float* p, float* v) {
+    float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct vecf<2> {
+  static __device__ __forceinline__ void ld(const float* p, float* v) {
+    float2 t = *reinterpret_cast<const float2*>(p);
+    v[0] = t.x; v[1] = t.y;
+  }
+  static __device__ __forceinline__ void st(float* p, const float* v) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+
+// Dot of a T row (len R, 16B aligned) with an fp32 smem vector.
+template <typename T>
+__device__ __forceinline__ float row_dot(const T* __restrict__ row, const float* vec, int R) {
+  float acc = 0.f;
+  for (int r = 0; r < R; r += 8) {
+    float w[8];
+    load8<T>(row + r, w);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += w[k] * vec[r + k];
+  }
+  return acc;
+}
+
+constexpr int kDecodeThreads = 256;
+
+template <typename T, int D, bool KDA>
+__global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const DeltaDecodeArgs a) {
+  constexpr int NW = kDecodeThreads / 32;
+  constexpr int EPL = D / 32;     // key entries per lane
+  constexpr int CPW = D / NW;     // value columns per warp
+  constexpr int NB = 4;           // columns in flight per warp
+  static_assert(CPW % NB == 0, "columns per warp must be a multiple of NB");
+
+  __shared__ __align__(16) float s_q[D];
+  __shared__ __align__(16) float s_k[D];
+  __shared__ __align__(16) float s_v[D];
+  __shared__ __align__(16) float s_eg[D];
+  __shared__ __align__(16) float s_gate[D];
+  __shared__ __align__(16) float s_o[D];
+  __shared__ __align__(16) float s_f1[KDA ? 256 : 1];
+  __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
+  __shared__ float s_red[NW];
+  __shared__ float s_beta;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int G = a.Hv / a.Hk, kh = h / G;
+  const int slot = a.slot_idx ? a.slot_idx[b] : b;
+  const int pos = a.positions[b];
+  const int W = a.W;
+  const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
+  T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * W;
+  const T* cw = reinterpret_cast<const T*>(a.conv_w);
+
+  // ---- 1. causal conv update + SiLU for q (key head), k (key head), v (this head)
+  for (int c = tid; c < 3 * D; c += kDecodeThreads) {
+    const int part = c / D, i = c - part * D;
+    const int ch = part == 0 ? a.q_off + kh * D + i : (part == 1 ? a.k_off + kh * D + i : a.v_off + h * D + i);
+    const float x = io<T>::ld(prow + ch);
+    const T* wrow = cw + (size_t)ch * W;
+    T* rrow = ring + (size_t)ch * W;
+    float acc = io<T>::ld(wrow + W - 1) * x;
+    for (int d = 1; d < W; ++d) {
+      const int p = pos - d;
+      if (p >= 0) acc += io<T>::ld(wrow + W - 1 - d) * io<T>::ld(rrow + (p % W));
+    }
+    const float y = silu_f(acc);
+    if (part == 2 || (h % G) == 0) io<T>::st(rrow + (pos % W), x);
+    (part == 0 ? s_q : part == 1 ? s_k : s_v)[i] = y;
+  }
+  if (KDA) {
+    for (int r = tid; r < a.rank; r += kDecodeThreads) {
+      s_f1[r] = io<T>::ld(prow + a.f1_off + r);
+      s_g1[r] = io<T>::ld(prow + a.g1_off + r);
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. L2 norms, gates, beta
+  float qq = 0.f, kk = 0.f;
+  for (int i = tid; i < D; i += kDecodeThreads) { qq += s_q[i] * s_q[i]; kk += s_k[i] * s_k[i]; }
+  qq = block_sum(qq, s_red);
+  kk = block_sum(kk, s_red);
+  const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
+  const float negA = -expf(a.A_log[h]);
+  if (!KDA) {
+    const float graw = io<T>::ld(prow + a.a_off + h) + a.dt_bias[h];
+    const float eg = expf(negA * softplus_f(graw));
+    for (int i = tid; i < D; i += kDecodeThreads) {
+      s_eg[i] = eg;
+      s_gate[i] = io<T>::ld(prow + a.z_off + h * D + i);
+    }
+  } else {
+    const T* f2 = reinterpret_cast<const T*>(a.f2_w);
+    const T* g2 = reinterpret_cast<const T*>(a.g2_w);
+    const T* g2b = reinterpret_cast<const T*>(a.g2_b);
+    for (int c = tid; c < 2 * D; c += kDecodeThreads) {
+      const int i = c % D;
+      const int row = h * D + i;
+      if (c < D) {
+        const float f = row_dot<T>(f2 + (size_t)row * a.rank, s_f1, a.rank);
+        s_eg[i] = expf(negA * softplus_f(f + a.dt_bias[row]));
+      } else {
+        s_gate[i] = row_dot<T>(g2 + (size_t)row * a.rank, s_g1, a.rank) + io<T>::ld(g2b + row);
+      }
+    }
+  }
+  if (tid == 0) s_beta = sigmoid_f(io<T>::ld(prow + a.b_off + h));
+  __syncthreads();
+  float qk = 0.f;
+  for (int i = tid; i < D; i += kDecodeThreads) {
+    const float qi = s_q[i] * rq, ki = s_k[i] * rk;
+    s_q[i] = qi;
+    s_k[i] = ki;
+    qk += qi * ki;
+  }
+  qk = block_sum(qk, s_red);  // (contains the __syncthreads that publishes s_q/s_k)
+  const float beta = s_beta;
+
+  // ---- 3. stream the state: warp owns columns [warp*CPW, +CPW), lane owns keys [lane*EPL, +EPL)
+  float kr[EPL], eg[EPL], kg[EPL], qg[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const int i = lane * EPL + e;
+    kr[e] = s_k[i];
+    eg[e] = s_eg[i];
+    kg[e] = s_k[i] * eg[e];
+    qg[e] = s_q[i] * eg[e];
+  }
+  float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
+#pragma unroll 1
+  for (int c0 = warp * CPW; c0 < (warp + 1) * CPW; c0 += NB) {
+    float s[NB][EPL];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
+    float kd[NB], qd[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      kd[n] = 0.f;
+      qd[n] = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        kd[n] += kg[e] * s[n][e];
+        qd[n] += qg[e] * s[n][e];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int n = 0; n < NB; ++n) {
+        kd[n] += __shfl_xor_sync(0xffffffffu, kd[n], o);
+        qd[n] += __shfl_xor_sync(0xffffffffu, qd[n], o);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const float u = beta * (s_v[c0 + n] - kd[n]);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) s[n][e] = eg[e] * s[n][e] + kr[e] * u;
+      vecf<EPL>::st(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
+      if (lane == 0) s_o[c0 + n] = qd[n] + qk * u;
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. gated RMSNorm over the head
+  float oo = 0.f;
+  for (int j = tid; j < D; j += kDecodeThreads) oo += s_o[j] * s_o[j];
+  oo = block_sum(oo, s_red);
+  const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
+  const T* nw = reinterpret_cast<const T*>(a.norm_w);
+  T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
+  for (int j = tid; j < D; j += kDecodeThreads) {
+    const float gz = s_gate[j];
+    const float act = KDA ? sigmoid_f(gz) : silu_f(gz);
+    io<T>::st(out + j, s_o[j] * rstd * io<T>::ld(nw + j) * act);
+  }
+}
+
+// =====================================================================
+// Prefill building blocks (sequences packed by cu_seqlens).
+
+// Causal conv + SiLU over time.  Thread per (channel, time chunk of 64).
+template <typename T>
+__global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __restrict__ y,
+                                    const T* __restrict__ w, T* __restrict__ ring,
+                                    const int32_t* __restrict__ cu, const int32_t* __restrict__ slot_idx,
+                                    int channels, int W) {
+  constexpr int CH = 64;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = blockIdx.z;
+  if (c >= channels) return;
+  const int t0 = cu[s], L = cu[s + 1] - t0;
+  const int p0 = blockIdx.y * CH;
+  if (p0 >= L) return;
+  const int p1 = min(p0 + CH, L);
+  float wt[8];
+  for (int d = 0; d < W; ++d) wt[d] = io<T>::ld(w + (size_t)c * W + d);
+  float hist[8];  // hist[d] = x at position p-1-d
+  for (int d = 0; d < W - 1; ++d) {
+    const int p = p0 - 1 - d;
+    hist[d] = p >= 0 ? io<T>::ld(x + (size_t)(t0 + p) * x_stride + c) : 0.f;
+  }
+  for (int p = p0; p < p1; ++p) {
+    const float xv = io<T>::ld(x + (size_t)(t0 + p) * x_stride + c);
+    float acc = wt[W - 1] * xv;
+    for (int d = 1; d < W; ++d) acc += wt[W - 1 - d] * hist[d - 1];
+    io<T>::st(y + (size_t)(t0 + p) * channels + c, silu_f(acc));
+    for (int d = W - 2; d > 0; --d) hist[d] = hist[d - 1];
+    if (W > 1) hist[0] = xv;
+  }
+  if (p1 == L) {  // the chunk holding the last position leaves the ring for decode
+    const int slot = slot_idx ? slot_idx[s] : s;
+    T* rrow = ring + ((size_t)slot * channels + c) * W;
+    for (int d = 1; d < W; ++d) {
+      const int p = L - d;
+      const float v = p >= 0 ? io<T>::ld(x + (size_t)(t0 + p) * x_stride + c) : 0.f;
+      io<T>::st(rrow + (((p % W) + W) % W), v);
+    }
+  }
+}
+
+// Per (row, value head): l2-normalised q/k, exp(gate), beta.
+template <typename T, int D, bool KDA>
+__global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv, const T* __restrict__ proj,
+                                                       int proj_stride, int b_off, int a_off,
+                                                       const T* __restrict__ f, const float* __restrict__ A_log,
+                                                       const float* __restrict__ dt_bias, float* __restrict__ qn,
+                                                       float* __restrict__ kn, float* __restrict__ gexp,
+                                                       float* __restrict__ beta, int Hk, int Hv, float scale,
+                                                       float eps_l2) {
+  __shared__ float red[D / 32];
+  const int r = blockIdx.y, h = blockIdx.x, i = threadIdx.x;
+  const int G = Hv / Hk, kh = h / G;
+  const int qkv_stride = 2 * Hk * D + Hv * D;
+  const T* row = qkv + (size_t)r * qkv_stride;
+  const float q = io<T>::ld(row + kh * D + i), k = io<T>::ld(row + Hk * D + kh * D + i);
+  const float qq = block_sum(q * q, red);
+  const float kk = block_sum(k * k, red);
+  if (h % G == 0) {
+    qn[((size_t)r * Hk + kh) * D + i] = q * rsqrtf(qq + eps_l2) * scale;
+    kn[((size_t)r * Hk + kh) * D + i] = k * rsqrtf(kk + eps_l2);
+  }
+  const T* prow = proj + (size_t)r * proj_stride;
+  const float negA = -expf(A_log[h]);
+  if (KDA) {
+    const float fv = io<T>::ld(f + (size_t)r * Hv * D + h * D + i);
+    gexp[((size_t)r * Hv + h) * D + i] = expf(negA * softplus_f(fv + dt_bias[h * D + i]));
+  } else if (i == 0) {
+    gexp[(size_t)r * Hv + h] = expf(negA * softplus_f(io<T>::ld(prow + a_off + h) + dt_bias[h]));
+  }
+  if (i == 0) beta[(size_t)r * Hv + h] = sigmoid_f(io<T>::ld(prow + b_off + h));
+}
+
+// Recurrent scan: CTA = 4 warps x 8 value columns of one (sequence, head); state in registers.
+template <typename T, int D, bool KDA>
+__global__ void __launch_bounds__(128) delta_scan_kernel(const float* __restrict__ qn, const float* __restrict__ kn,
+                                                         const T* __restrict__ qkv, int v_off, int qkv_stride,
+                                                         const float* __restrict__ gexp, const float* __restrict__ beta,
+                                                         float* __restrict__ o, float* __restrict__ state,
+                                                         const int32_t* __restrict__ slot_idx,
+                                                         const int32_t* __restrict__ cu, int Hk, int Hv,
+                                                         int init_state) {
+  constexpr int EPL = D / 32, CPW = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cg = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  const int G = Hv / Hk, kh = h / G;
+  const int c0 = (cg * 4 + warp) * CPW;
+  const int slot = slot_idx ? slot_idx[s] : s;
+  const int t0 = cu[s], t1 = cu[s + 1];
+  float* S = state + ((size_t)slot * Hv + h) * D * D;
+  float st[CPW][EPL];
+#pragma unroll
+  for (int n = 0; n < CPW; ++n)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) st[n][e] = init_state ? S[(size_t)(c0 + n) * D + lane * EPL + e] : 0.f;
+
+  for (int t = t0; t < t1; ++t) {
+    float q[EPL], k[EPL], eg[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const int i = lane * EPL + e;
+      q[e] = qn[((size_t)t * Hk + kh) * D + i];
+      k[e] = kn[((size_t)t * Hk + kh) * D + i];
+      eg[e] = KDA ? gexp[((size_t)t * Hv + h) * D + i] : gexp[(size_t)t * Hv + h];
+    }
+    const float bt = beta[(size_t)t * Hv + h];
+    float qk = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) qk += q[e] * k[e];
+    qk = warp_sum(qk);
+    float vv = lane < CPW ? io<T>::ld(qkv + (size_t)t * qkv_stride + v_off + h * D + c0 + lane) : 0.f;
+#pragma unroll
+    for (int n = 0; n < CPW; ++n) {
+      float kd = 0.f, qd = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        kd += k[e] * eg[e] * st[n][e];
+        qd += q[e] * eg[e] * st[n][e];
+      }
+      kd = warp_sum(kd);
+      qd = warp_sum(qd);
+      const float u = bt * (__shfl_sync(0xffffffffu, vv, n) - kd);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) st[n][e] = eg[e] * st[n][e] + k[e] * u;
+      if (lane == 0) o[((size_t)t * Hv + h) * D + c0 + n] = qd + qk * u;
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < CPW; ++n)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) S[(size_t)(c0 + n) * D + lane * EPL + e] = st[n][e];
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(D) gated_rmsnorm_kernel(const float* __restrict__ o, const T* __restrict__ gate,
+                                                          int gate_stride, const T* __restrict__ w,
+                                                          T* __restrict__ out, int H, float eps, int act) {
+  __shared__ float red[D / 32];
+  const int r = blockIdx.y, h = blockIdx.x, j = threadIdx.x;
+  const float v = o[((size_t)r * H + h) * D + j];
+  const float ss = block_sum(v * v, red);
+  const float rstd = rsqrtf(ss / (float)D + eps);
+  const float gz = io<T>::ld(gate + (size_t)r * gate_stride + h * D + j);
+  const float a = act ? sigmoid_f(gz) : silu_f(gz);
+  io<T>::st(out + ((size_t)r * H + h) * D + j, v * rstd * io<T>::ld(w + j) * a);
+}
+
+template <bool KDA>
+static sn_status launch_delta_decode(const DeltaDecodeArgs& a, int B, int D, int dtype, cudaStream_t st) {
+  dim3 grid(a.Hv, B);
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    if (D == 128) delta_decode_kernel<T, 128, KDA><<<grid, kDecodeThreads, 0, st>>>(a);
+    else if (D == 64) delta_decode_kernel<T, 64, KDA><<<grid, kDecodeThreads, 0, st>>>(a);
+    else { set_error("delta decode: head dim %d unsupported (64 or 128)", D); return SN_EUNSUPPORTED; }
+    return check_launch(KDA ? "sn_kda_decode" : "sn_gdn_decode");
+  });
+}
+
+}  // namespace sn
+
+using namespace sn;
+
+namespace sn {
+template <typename T, int D, bool K>
+static void launch_prep(dim3 grid, cudaStream_t st, const void* qkv_conv, const void* proj, int proj_stride,
+                        int b_off, int a_off, const void* f, const float* A_log, const float* dt_bias, float* qn,
+                        float* kn, float* gexp, float* beta, int Hk, int Hv, float scale, float eps_l2) {
+  delta_prep_kernel<T, D, K><<<grid, D, 0, st>>>((const T*)qkv_conv, (const T*)proj, proj_stride, b_off, a_off,
+                                                 (const T*)f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, scale,
+                                                 eps_l2);
+}
+
+template <typename T, int D, bool K>
+static void launch_scan(dim3 grid, cudaStream_t st, const float* qn, const float* kn, const void* qkv_conv,
+                        int v_off, int qkv_stride, const float* gexp, const float* beta, float* o, float* state,
+                        const int32_t* slot_idx, const int32_t* cu, int Hk, int Hv, int init_state) {
+  delta_scan_kernel<T, D, K><<<grid, 128, 0, st>>>(qn, kn, (const T*)qkv_conv, v_off, qkv_stride, gexp, beta, o,
+                                                   state, slot_idx, cu, Hk, Hv, init_state);
+}
+
+}  // namespace sn
+
+extern "C" {
+
+sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring, const void* conv_w, float* state,
+                        const int32_t* slot_idx, const int32_t* positions, const float* A_log,
+                        const float* dt_bias, const void* norm_w, void* out, int B, int Hk, int Hv, int D,
+                        int conv_width, float scale, float eps_l2, float eps_norm, int dtype, void* stream) {
+  SN_REQUIRE(B > 0 && Hk > 0 && Hv > 0 && Hv % Hk == 0, "sn_gdn_decode: bad heads B=%d Hk=%d Hv=%d", B, Hk, Hv);
+  SN_REQUIRE(conv_width >= 1 && conv_width <= 8, "sn_gdn_decode: conv width %d not in [1,8]", conv_width);
+  SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && norm_w && out,
+             "sn_gdn_decode: NULL pointer argument");
+  DeltaDecodeArgs a{};
+  a.proj = proj; a.proj_stride = proj_stride; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
+  a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.norm_w = norm_w;
+  a.out = out; a.Hk = Hk; a.Hv = Hv; a.rank = 0; a.W = conv_width;
+  a.conv_channels = 2 * Hk * D + Hv * D;
+  a.q_off = 0; a.k_off = Hk * D; a.v_off = 2 * Hk * D; a.z_off = 2 * Hk * D + Hv * D;
+  a.b_off = 2 * Hk * D + 2 * Hv * D; a.a_off = a.b_off + Hv;
+  a.scale = scale; a.eps_l2 = eps_l2; a.eps_norm = eps_norm;
+  SN_REQUIRE(proj_stride >= a.a_off + Hv, "sn_gdn_decode: proj_stride %d < %d", proj_stride, a.a_off + Hv);
+  return launch_delta_decode<false>(a, B, D, dtype, (cudaStream_t)stream);
+}
+
+sn_status sn_kda_decode(const void* proj, int proj_stride, void* conv_ring, const void* conv_w, float* state,
+                        const int32_t* slot_idx, const int32_t* positions, const float* A_log,
+                        const float* dt_bias, const void* f2_w, const void* g2_w, const void* g2_b,
+                        const void* norm_w, void* out, int B, int H, int D, int rank, int conv_width, float scale,
+                        float eps_l2, float eps_norm, int dtype, void* stream) {
+  SN_REQUIRE(B > 0 && H > 0, "sn_kda_decode: bad shape B=%d H=%d", B, H);
+  SN_REQUIRE(rank > 0 && rank <= 256 && rank % 8 == 0, "sn_kda_decode: rank %d must be a multiple of 8 <= 256", rank);
+  SN_REQUIRE(conv_width >= 1 && conv_width <= 8, "sn_kda_decode: conv width %d not in [1,8]", conv_width);
+  SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && f2_w && g2_w && g2_b &&
+                 norm_w && out,
+             "sn_kda_decode: NULL pointer argument");
+  DeltaDecodeArgs a{};
+  a.proj = proj; a.proj_stride = proj_stride; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
+  a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.f2_w = f2_w;
+  a.g2_w = g2_w; a.g2_b = g2_b; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank;
+  a.W = conv_width; a.conv_channels = 3 * H * D;
+  a.q_off = 0; a.k_off = H * D; a.v_off = 2 * H * D; a.f1_off = 3 * H * D; a.g1_off = 3 * H * D + rank;
+  a.b_off = 3 * H * D + 2 * rank;
+  a.scale = scale; a.eps_l2 = eps_l2; a.eps_norm = eps_norm;
+  SN_REQUIRE(proj_stride >= a.b_off + H, "sn_kda_decode: proj_stride %d < %d", proj_stride, a.b_off + H);
+  return launch_delta_decode<true>(a, B, D, dtype, (cudaStream_t)stream);
+}
+
+sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv_w, void* conv_ring,
+                          const int32_t* cu_seqlens, const int32_t* slot_idx, int num_seqs, int rows,
+                          int channels, int width, int dtype, void* stream) {
+  SN_REQUIRE(num_seqs > 0 && rows > 0 && channels > 0, "sn_conv_prefill: bad shape");
+  SN_REQUIRE(width >= 1 && width <= 8, "sn_conv_prefill: width %d not in [1,8]", width);
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    dim3 grid(ceil_div(channels, 128), ceil_div(rows, 64), num_seqs);
+    conv_prefill_kernel<T><<<grid, 128, 0, (cudaStream_t)stream>>>((const T*)x, x_stride, (T*)y, (const T*)conv_w,
+                                                                  (T*)conv_ring, cu_seqlens, slot_idx, channels,
+                                                                  width);
+    return check_launch("sn_conv_prefill");
+  });
+}
+
+sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int proj_stride, int b_off, int a_off,
+                        const void* f, const float* A_log, const float* dt_bias, float* qn, float* kn, float* gexp,
+                        float* beta, int rows, int Hk, int Hv, int D, float scale, float eps_l2, int dtype,
+                        void* stream) {
+  SN_REQUIRE(kind == 0 || kind == 1, "sn_delta_prep: kind %d", kind);
+  SN_REQUIRE(rows > 0 && Hk > 0 && Hv % Hk == 0, "sn_delta_prep: bad shape");
+  SN_REQUIRE(kind == 0 || f != nullptr, "sn_delta_prep: KDA needs f");
+  SN_REQUIRE(D == 64 || D == 128, "sn_delta_prep: D=%d unsupported", D);
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    dim3 grid(Hv, rows);
+    cudaStream_t st = (cudaStream_t)stream;
+    auto fn = D == 128 ? (kind ? launch_prep<T, 128, true> : launch_prep<T, 128, false>)
+                       : (kind ? launch_prep<T, 64, true> : launch_prep<T, 64, false>);
+    fn(grid, st, qkv_conv, proj, proj_stride, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, scale,
+       eps_l2);
+    return check_launch("sn_delta_prep");
+  });
+}
+
+sn_status sn_delta_scan(int kind, const float* qn, const float* kn, const void* qkv_conv, int v_off,
+                        int qkv_stride, const float* gexp, const float* beta, float* o, float* state,
+                        const int32_t* slot_idx, const int32_t* cu_seqlens, int num_seqs, int Hk, int Hv, int D,
+                        int init_state, int dtype, void* stream) {
+  SN_REQUIRE(kind == 0 || kind == 1, "sn_delta_scan: kind %d", kind);
+  SN_REQUIRE(num_seqs > 0 && Hk > 0 && Hv % Hk == 0, "sn_delta_scan: bad shape");
+  SN_REQUIRE(D == 64 || D == 128, "sn_delta_scan: D=%d unsupported", D);
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    dim3 grid(D / 32, Hv, num_seqs);
+    cudaStream_t st = (cudaStream_t)stream;
+    auto fn = D == 128 ? (kind ? launch_scan<T, 128, true> : launch_scan<T, 128, false>)
+                       : (kind ? launch_scan<T, 64, true> : launch_scan<T, 64, false>);
+    fn(grid, st, qn, kn, qkv_conv, v_off, qkv_stride, gexp, beta, o, state, slot_idx, cu_seqlens, Hk, Hv,
+       init_state);
+    return check_launch("sn_delta_scan");
+  });
+}
+
+sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride, const void* norm_w, void* out,
+                           int rows, int H, int D, float eps, int act, int dtype, void* stream) {
+  SN_REQUIRE(rows > 0 && H > 0, "sn_gated_rmsnorm: bad shape");
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    dim3 grid(H, rows);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (D == 128) gated_rmsnorm_kernel<T, 128><<<grid, 128, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, H, eps, act);
+    else if (D == 64) gated_rmsnorm_kernel<T, 64><<<grid, 64, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, H, eps, act);
+    else { set_error("sn_gated_rmsnorm: D=%d unsupported", D); return SN_EUNSUPPORTED; }
+    return check_launch("sn_gated_rmsnorm");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,345 @@
+"""Placement-driven supernet runtime: layer loop, heterogeneous state pools,
+prefill and decode — the host side of the mixer step.
+
+Paper mapping:
+  * one mixer per layer chosen by the placement (R/PAPER.md:860-865); the layer
+    loop launches only that mixer's kernels, keyed by the immutable table
+    `self.kinds` (no global mutable state, so several Supernet objects — one per
+    placement — can share a process and a GPU);
+  * heterogeneous state (R/PAPER.md:834-843): FA paged KV, SWA ring KV, GDN/KDA
+    fp32 recurrent state + conv ring — here separate pools per mixer kind, sized
+    exactly, instead of vLLM's unified page size padding (which the paper blames
+    for its hybrid overhead, R/PAPER.md:1797, 1804);
+  * dual execution path (R/PAPER.md:845-850): a parallel prefill over the whole
+    prompt, then one fused in-place decode step per token;
+  * CUDA graphs per placement (R/PAPER.md:831, 863): see graphs.py.
+
+All compute runs in libsn100.so kernels (ops.py) plus cuBLAS GEMMs for the
+projections / FFN / LM head; there is no CPU path.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import ops
+from ._lib import load as _load_lib
+from .config import SupernetConfig, attn_scale
+from .placement import FA, GDN, KDA, SWA, layer_kinds
+from .weights import cast_weights, init_weights
+
+
+def _ceil(a, b):
+    return (a + b - 1) // b
+
+
+def choose_split(max_pages: int, rows: int, sms: int = 148, cap: int = 32) -> tuple[int, int]:
+    """Split-KV decomposition for decode attention: aim for ~4 CTAs per SM over
+    (sequence x kv head x split); returns (split_pages, max_splits)."""
+    want = max(1, _ceil(4 * sms, max(rows, 1)))
+    split_pages = max(1, min(cap, _ceil(max_pages, want)))
+    return split_pages, _ceil(max_pages, split_pages)
+
+
+class Supernet:
+    """A loaded placement of the supernet with its state pools.
+
+    placement: code string ("ASKG..."), list of type names, or a
+    placeopt-compatible Placement.  weights: optional pre-built structure
+    (paper_2604_19877_b200.weights.init_weights); default is the seeded random
+    init generated directly on the device.
+    """
+
+    def __init__(self, cfg: SupernetConfig, placement, *, batch: int, max_len: int, dtype=torch.bfloat16,
+                 device="cuda", seed: int = 0, weights=None, fa_block_table=None):
+        _load_lib()  # fail loudly if the extension is missing
+        self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise ValueError("Supernet runs on CUDA only (no CPU fallback)")
+        self.kinds = layer_kinds(placement)
+        if len(self.kinds) != cfg.num_layers:
+            raise ValueError(f"placement has {len(self.kinds)} layers, config {cfg.name} has {cfg.num_layers}")
+        if weights is None:
+            weights = init_weights(cfg, self.kinds, seed=seed, device=self.device, dtype=dtype)
+        self.w = cast_weights(weights, self.device, dtype)
+        self.inv_freq = cfg.inv_freq().to(device=self.device, dtype=torch.float32)
+        self.scale_attn = attn_scale(cfg)
+        self._alloc_state(fa_block_table)
+        self._alloc_decode_buffers()
+
+    # ------------------------------------------------------------------ state pools
+    def _alloc_state(self, fa_block_table):
+        cfg, B, dev, dt = self.cfg, self.B, self.device, self.dtype
+        P, Hkv, D = cfg.page_size, cfg.n_kv_heads, cfg.head_dim
+        i32 = dict(device=dev, dtype=torch.int32)
+        self.seq_lens = torch.zeros(B, **i32)
+        self.positions = torch.zeros(B, **i32)
+        self.fa_blocks = _ceil(self.max_len, P)
+        if fa_block_table is None:
+            fa_block_table = torch.arange(B * self.fa_blocks, dtype=torch.int32).view(B, self.fa_blocks)
+        self.fa_block_table = fa_block_table.to(**i32).contiguous()
+        self.fa_pages = int(self.fa_block_table.max().item()) + 1 if self.fa_block_table.numel() else 0
+        if cfg.window % P:
+            raise ValueError("SWA window must be a multiple of the page size")
+        self.swa_blocks = cfg.window // P
+        self.swa_block_table = torch.arange(B * self.swa_blocks, **i32).view(B, self.swa_blocks)
+        self.state = []
+        for kind in self.kinds:
+            if kind == FA:
+                shape = (self.fa_pages, Hkv, P, D)
+                self.state.append({"k": torch.zeros(shape, device=dev, dtype=dt),
+                                   "v": torch.zeros(shape, device=dev, dtype=dt)})
+            elif kind == SWA:
+                shape = (B * self.swa_blocks, Hkv, P, D)
+                self.state.append({"k": torch.zeros(shape, device=dev, dtype=dt),
+                                   "v": torch.zeros(shape, device=dev, dtype=dt)})
+            elif kind == GDN:
+                Dg = cfg.gdn_head_dim
+                self.state.append({"S": torch.zeros(B, cfg.gdn_v_heads, Dg, Dg, device=dev, dtype=torch.float32),
+                                   "conv": torch.zeros(B, cfg.gdn_conv_channels, cfg.conv_width, device=dev, dtype=dt)})
+            else:
+                Dk = cfg.kda_head_dim
+                self.state.append({"S": torch.zeros(B, cfg.kda_heads, Dk, Dk, device=dev, dtype=torch.float32),
+                                   "conv": torch.zeros(B, cfg.kda_conv_channels, cfg.conv_width, device=dev, dtype=dt)})
+
+    def reset(self):
+        self.seq_lens.zero_()
+        for st in self.state:
+            for t in st.values():
+                t.zero_()
+
+    def state_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for st in self.state for t in st.values())
+
+    def weight_bytes(self) -> int:
+        def walk(o):
+            if isinstance(o, dict):
+                return sum(walk(v) for v in o.values())
+            if isinstance(o, list):
+                return sum(walk(v) for v in o)
+            return o.numel() * o.element_size() if torch.is_tensor(o) else 0
+        return walk(self.w)
+
+    # ------------------------------------------------------------------ decode buffers
+    def _alloc_decode_buffers(self):
+        cfg, B, dev, dt = self.cfg, self.B, self.device, self.dtype
+        e = lambda *s, d=dt: torch.empty(*s, device=dev, dtype=d)
+        self.step_tokens = torch.zeros(B, device=dev, dtype=torch.int32)
+        self.next_tokens = torch.zeros(B, device=dev, dtype=torch.int32)
+        self.residual = e(B, cfg.hidden, d=torch.float32)
+        self.h = e(B, cfg.hidden)
+        self.mix_out = e(B, cfg.hidden)
+        self.ffn_out = e(B, cfg.hidden)
+        self.gu = e(B, 2 * cfg.ffn)
+        self.act = e(B, cfg.ffn)
+        self.logits = e(B, cfg.vocab)
+        kinds = set(self.kinds)
+        self.dec = {}
+        if kinds & {FA, SWA}:
+            Hq, Hkv, D = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+            self.dec["qkv"] = e(B, cfg.attn_qkv_width)
+            self.dec["q"] = e(B, Hq, D)
+            self.dec["attn"] = e(B, Hq * D)
+            self.dec["counters"] = torch.zeros(B * Hkv, device=dev, dtype=torch.int32)
+            self.attn_split = {}
+            for kind, max_keys in ((FA, self.max_len), (SWA, cfg.window)):
+                if kind in kinds:
+                    sp, ms = choose_split(_ceil(max_keys, cfg.page_size), B * Hkv)
+                    self.attn_split[kind] = (sp, ms)
+            ms_max = max(ms for _, ms in self.attn_split.values())
+            nbytes = ops.attn_decode_workspace_bytes(B, Hq, Hkv, D, ms_max)
+            self.dec["ws"] = torch.empty(max(nbytes // 4, 1), device=dev, dtype=torch.float32)
+            self.ws_max_splits = ms_max
+        if GDN in kinds:
+            self.dec["gdn_proj"] = e(B, cfg.gdn_in_width)
+            self.dec["gdn_out"] = e(B, cfg.gdn_value_dim)
+        if KDA in kinds:
+            self.dec["kda_proj"] = e(B, cfg.kda_in_width)
+            self.dec["kda_out"] = e(B, cfg.kda_dim)
+
+    # ------------------------------------------------------------------ decode
+    def _attn_decode(self, l, kind, h, out):
+        cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
+        Hq, Hkv, D, P = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size
+        window = cfg.window if kind == SWA else 0
+        bt = self.swa_block_table if kind == SWA else self.fa_block_table
+        torch.mm(h, w["qkv"].t(), out=d["qkv"])
+        ops.rope_kv_append(d["qkv"], None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
+                           st["k"], st["v"], bt, Hq, Hkv, D, P, window)
+        sp, _ = self.attn_split[kind]
+        ops.attn_decode(d["q"], st["k"], st["v"], bt, self.seq_lens, d["attn"], d["ws"], d["counters"], Hq, Hkv, D,
+                        P, window, sp, self.ws_max_splits, self.scale_attn, force_simt=getattr(self, "force_simt", False))
+        torch.mm(d["attn"], w["o"].t(), out=out)
+
+    def _gdn_decode(self, l, h, out):
+        cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
+        D = cfg.gdn_head_dim
+        torch.mm(h, w["w_in"].t(), out=d["gdn_proj"])
+        ops.gdn_decode(d["gdn_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"], w["dt_bias"],
+                       w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D, cfg.conv_width,
+                       1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+        torch.mm(d["gdn_out"], w["o"].t(), out=out)
+
+    def _kda_decode(self, l, h, out):
+        cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
+        D = cfg.kda_head_dim
+        torch.mm(h, w["w_in"].t(), out=d["kda_proj"])
+        ops.kda_decode(d["kda_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
+                       w["dt_bias"], w["f2"], w["g2"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D,
+                       cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+        torch.mm(d["kda_out"], w["o"].t(), out=out)
+
+    def decode_body(self):
+        """One decode step on the current stream: step_tokens -> logits, next_tokens.
+        Graph-capturable: every size/position it needs is read from device buffers."""
+        cfg, w = self.cfg, self.w
+        ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
+        delta = None
+        for l, kind in enumerate(self.kinds):
+            lw = w["layers"][l]
+            ops.add_rmsnorm(delta, self.residual, lw["norm1"], self.h, cfg.norm_eps)
+            if kind == GDN:
+                self._gdn_decode(l, self.h, self.mix_out)
+            elif kind == KDA:
+                self._kda_decode(l, self.h, self.mix_out)
+            else:
+                self._attn_decode(l, kind, self.h, self.mix_out)
+            ops.add_rmsnorm(self.mix_out, self.residual, lw["norm2"], self.h, cfg.norm_eps)
+            torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
+            ops.silu_mul(self.gu, self.act)
+            torch.mm(self.act, lw["ffn_down"].t(), out=self.ffn_out)
+            delta = self.ffn_out
+        ops.add_rmsnorm(delta, self.residual, w["final_norm"], self.h, cfg.norm_eps)
+        torch.mm(self.h, w["lm_head"].t(), out=self.logits)
+        ops.argmax(self.logits, self.next_tokens)
+
+    def kernels_per_step(self) -> dict:
+        """Launch census of one decode step: {"sn": own kernels, "cublas": library GEMMs}."""
+        sn = 1 + 1 + 1  # embed, final norm, argmax
+        gemm = 1        # lm head
+        for kind in self.kinds:
+            sn += 2 + 1  # two add_rmsnorm + silu_mul
+            gemm += 2    # ffn
+            if kind in (FA, SWA):
+                sn += 2
+                gemm += 2
+            else:
+                sn += 1
+                gemm += 2
+        return {"sn": sn, "cublas": gemm}
+
+    @torch.no_grad()
+    def decode(self, tokens):
+        """Eager decode step.  tokens: [B] ints (any device) -> logits [B, V] (device buffer)."""
+        self.step_tokens.copy_(torch.as_tensor(tokens, dtype=torch.int32))
+        self.decode_body()
+        return self.logits
+
+    # ------------------------------------------------------------------ prefill
+    @torch.no_grad()
+    def prefill(self, tokens, return_all: bool = False):
+        """Parallel prefill of B prompts of equal length T from an empty state.
+        tokens [B, T] -> logits [B, T, V] (return_all) or [B, V] for the last position."""
+        cfg, w, dev, dt = self.cfg, self.w, self.device, self.dtype
+        tokens = torch.as_tensor(tokens).to(device=dev, dtype=torch.int32)
+        B, T = tokens.shape
+        if B != self.B:
+            raise ValueError(f"prefill batch {B} != engine batch {self.B}")
+        if T > self.max_len:
+            raise ValueError(f"prompt length {T} > max_len {self.max_len}")
+        rows = B * T
+        i32 = dict(device=dev, dtype=torch.int32)
+        cu = torch.arange(0, rows + 1, T, **i32)
+        row_seq = torch.arange(B, **i32).repeat_interleave(T)
+        row_pos = torch.arange(T, **i32).repeat(B)
+        self.reset()
+        self.seq_lens.fill_(T)
+        e = lambda *s, d=dt: torch.empty(*s, device=dev, dtype=d)
+        resid = e(rows, cfg.hidden, d=torch.float32)
+        h, mix, ffn_o = e(rows, cfg.hidden), e(rows, cfg.hidden), e(rows, cfg.hidden)
+        ops.embed(tokens.reshape(-1), w["embed"], resid)
+        delta = None
+        for l, kind in enumerate(self.kinds):
+            lw = w["layers"][l]
+            ops.add_rmsnorm(delta, resid, lw["norm1"], h, cfg.norm_eps)
+            if kind in (FA, SWA):
+                self._attn_prefill(l, kind, h, mix, cu, row_seq, row_pos)
+            elif kind == GDN:
+                self._gdn_prefill(l, h, mix, cu)
+            else:
+                self._kda_prefill(l, h, mix, cu)
+            ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
+            gu = h @ lw["ffn_gu"].t()
+            act = e(rows, cfg.ffn)
+            ops.silu_mul(gu, act)
+            torch.mm(act, lw["ffn_down"].t(), out=ffn_o)
+            delta = ffn_o
+        ops.add_rmsnorm(delta, resid, w["final_norm"], h, cfg.norm_eps)
+        if return_all:
+            return (h @ w["lm_head"].t()).view(B, T, cfg.vocab)
+        last = h.view(B, T, cfg.hidden)[:, -1]
+        return last @ w["lm_head"].t()
+
+    def _attn_prefill(self, l, kind, h, out, cu, row_seq, row_pos):
+        cfg, st, w = self.cfg, self.state[l], self.w["layers"][l]["mixer"]
+        Hq, Hkv, D, P = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size
+        rows = h.shape[0]
+        window = cfg.window if kind == SWA else 0
+        bt = self.swa_block_table if kind == SWA else self.fa_block_table
+        qkv = h @ w["qkv"].t()
+        q = torch.empty(rows, Hq, D, device=h.device, dtype=h.dtype)
+        k = torch.empty(rows, Hkv, D, device=h.device, dtype=h.dtype)
+        v = torch.empty_like(k)
+        ops.rope_kv_append(qkv, row_seq, row_pos, self.seq_lens, self.inv_freq, q, k, v, st["k"], st["v"], bt, Hq,
+                           Hkv, D, P, window)
+        o = torch.empty(rows, Hq * D, device=h.device, dtype=h.dtype)
+        ops.attn_prefill(q, k, v, cu, o, Hq, Hkv, D, window, self.scale_attn)
+        torch.mm(o, w["o"].t(), out=out)
+
+    def _delta_prefill(self, kind, l, h, out, cu):
+        cfg, st, w = self.cfg, self.state[l], self.w["layers"][l]["mixer"]
+        rows = h.shape[0]
+        dev = h.device
+        proj = h @ w["w_in"].t()
+        if kind == GDN:
+            Hk, Hv, D = cfg.gdn_k_heads, cfg.gdn_v_heads, cfg.gdn_head_dim
+            C = cfg.gdn_conv_channels
+            z_off, b_off = C, C + Hv * D
+            a_off = b_off + Hv
+            f = None
+            gate, gate_stride = proj[:, z_off:], proj.stride(0)
+        else:
+            Hk = Hv = cfg.kda_heads
+            D, R = cfg.kda_head_dim, cfg.kda_rank
+            C = cfg.kda_conv_channels
+            f1_off, g1_off, b_off, a_off = C, C + R, C + 2 * R, 0
+            f = (proj[:, f1_off:f1_off + R] @ w["f2"].t()).contiguous()
+            gate = (proj[:, g1_off:g1_off + R] @ w["g2"].t() + w["g2_b"]).contiguous()
+            gate_stride = gate.stride(0)
+        y = torch.empty(rows, C, device=dev, dtype=h.dtype)
+        ops.conv_prefill(proj, proj.stride(0), y, w["conv_w"], st["conv"], cu, None, C, cfg.conv_width)
+        f32 = dict(device=dev, dtype=torch.float32)
+        qn, kn = torch.empty(rows, Hk, D, **f32), torch.empty(rows, Hk, D, **f32)
+        gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
+        beta = torch.empty(rows, Hv, **f32)
+        k_code = 1 if kind == KDA else 0
+        ops.delta_prep(k_code, y, proj, b_off, a_off, f, w["A_log"], w["dt_bias"], qn, kn, gexp, beta, Hk, Hv, D,
+                       1.0 / math.sqrt(D), cfg.l2_eps)
+        o = torch.empty(rows, Hv, D, **f32)
+        ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], None, cu, Hk, Hv, D, init_state=False)
+        y_out = torch.empty(rows, Hv * D, device=dev, dtype=h.dtype)
+        ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
+        torch.mm(y_out, w["o"].t(), out=out)
+
+    def _gdn_prefill(self, l, h, out, cu):
+        self._delta_prefill(GDN, l, h, out, cu)
+
+    def _kda_prefill(self, l, h, out, cu):
+        self._delta_prefill(KDA, l, h, out, cu)
+
+    # ------------------------------------------------------------------ introspection for tests
+    def recurrent_state(self, layer):
+        """[B, Hv, K, V] view of a GDN/KDA state (stored [B, Hv, V, K])."""
+        return self.state[layer]["S"].transpose(-1, -2)

@@ -1,0 +1,118 @@
+"""Torch-facing wrappers over the C ABI (include/sn_abi.h).
+
+Each wrapper checks shapes/dtypes/devices, then passes raw device pointers and
+the current CUDA stream.  Nothing here computes on the CPU: a tensor that is
+not on a CUDA device is an error.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import SN_ATTN_FORCE_SIMT, SN_BF16, SN_F32, call
+
+_DT = {torch.bfloat16: SN_BF16, torch.float32: SN_F32}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DT[dt]
+    except KeyError:
+        raise TypeError(f"unsupported I/O dtype {dt}; use bfloat16 or float32") from None
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libsn100 ops need CUDA tensors (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def embed(tokens, table, residual, seq_lens=None, positions=None):
+    assert tokens.dtype == torch.int32 and residual.dtype == torch.float32
+    call("sn_embed", _p(tokens), _p(table), _p(residual), _p(seq_lens), _p(positions), tokens.numel(),
+         table.shape[1], dtype_code(table.dtype), _s())
+
+
+def add_rmsnorm(delta, residual, weight, out, eps):
+    rows, dim = residual.shape
+    call("sn_add_rmsnorm", _p(delta), _p(residual), _p(weight), _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
+
+
+def silu_mul(gate_up, out):
+    rows, ffn = out.shape
+    call("sn_silu_mul", _p(gate_up), _p(out), rows, ffn, dtype_code(out.dtype), _s())
+
+
+def argmax(logits, out_tokens):
+    rows, vocab = logits.shape
+    call("sn_argmax", _p(logits), rows, vocab, _p(out_tokens), dtype_code(logits.dtype), _s())
+
+
+def rope_kv_append(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,
+                   Hq, Hkv, D, page_size, window):
+    rows = qkv.shape[0]
+    call("sn_rope_kv_append", _p(qkv), _p(row_seq), _p(row_pos), _p(seq_lens), _p(inv_freq), _p(q_out), _p(k_out),
+         _p(v_out), _p(k_cache), _p(v_cache), _p(block_table), rows, Hq, Hkv, D, page_size, block_table.shape[1],
+         window, dtype_code(qkv.dtype), _s())
+
+
+def attn_decode_workspace_bytes(B, Hq, Hkv, D, max_splits):
+    return _lib.load().sn_attn_decode_workspace_bytes(B, Hq, Hkv, D, max_splits)
+
+
+def attn_decode(q, k_cache, v_cache, block_table, seq_lens, out, workspace, counters, Hq, Hkv, D, page_size, window,
+                split_pages, max_splits, scale, force_simt=False):
+    B = seq_lens.shape[0]
+    code = dtype_code(q.dtype) | (SN_ATTN_FORCE_SIMT if force_simt else 0)
+    call("sn_attn_decode", _p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_lens), _p(out), _p(workspace),
+         _p(counters), B, Hq, Hkv, D, page_size, block_table.shape[1], window, split_pages, max_splits, scale, code,
+         _s())
+
+
+def attn_prefill(q, k, v, cu_seqlens, out, Hq, Hkv, D, window, scale):
+    call("sn_attn_prefill", _p(q), _p(k), _p(v), _p(cu_seqlens), _p(out), cu_seqlens.numel() - 1, q.shape[0], Hq, Hkv,
+         D, window, scale, dtype_code(q.dtype), _s())
+
+
+def gdn_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, norm_w, out, Hk, Hv, D, width,
+               scale, eps_l2, eps_norm):
+    B = positions.shape[0]
+    call("sn_gdn_decode", _p(proj), proj.stride(0), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
+         _p(positions), _p(A_log), _p(dt_bias), _p(norm_w), _p(out), B, Hk, Hv, D, width, scale, eps_l2, eps_norm,
+         dtype_code(proj.dtype), _s())
+
+
+def kda_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, f2, g2, g2_b, norm_w, out, H, D,
+               rank, width, scale, eps_l2, eps_norm):
+    B = positions.shape[0]
+    call("sn_kda_decode", _p(proj), proj.stride(0), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
+         _p(positions), _p(A_log), _p(dt_bias), _p(f2), _p(g2), _p(g2_b), _p(norm_w), _p(out), B, H, D, rank, width,
+         scale, eps_l2, eps_norm, dtype_code(proj.dtype), _s())
+
+
+def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channels, width):
+    call("sn_conv_prefill", _p(x), x_stride, _p(y), _p(conv_w), _p(conv_ring), _p(cu_seqlens), _p(slot_idx),
+         cu_seqlens.numel() - 1, y.shape[0], channels, width, dtype_code(y.dtype), _s())
+
+
+def delta_prep(kind, qkv_conv, proj, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, D, scale, eps_l2):
+    call("sn_delta_prep", kind, _p(qkv_conv), _p(proj), proj.stride(0), b_off, a_off, _p(f), _p(A_log), _p(dt_bias),
+         _p(qn), _p(kn), _p(gexp), _p(beta), qkv_conv.shape[0], Hk, Hv, D, scale, eps_l2, dtype_code(qkv_conv.dtype),
+         _s())
+
+
+def delta_scan(kind, qn, kn, qkv_conv, v_off, gexp, beta, o, state, slot_idx, cu_seqlens, Hk, Hv, D, init_state):
+    call("sn_delta_scan", kind, _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(gexp), _p(beta), _p(o),
+         _p(state), _p(slot_idx), _p(cu_seqlens), cu_seqlens.numel() - 1, Hk, Hv, D, int(init_state),
+         dtype_code(qkv_conv.dtype), _s())
+
+
+def gated_rmsnorm(o, gate, gate_stride, norm_w, out, H, D, eps, act):
+    call("sn_gated_rmsnorm", _p(o), _p(gate), gate_stride, _p(norm_w), _p(out), o.shape[0], H, D, eps, act,
+         dtype_code(out.dtype), _s())
