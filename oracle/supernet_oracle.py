@@ -206,12 +206,14 @@ def kda_core(cfg, p, hist, S, w):
 
 
 def attention_ref(q, keys, vals, scale):
-    """softmax(q k^T * scale) v with GQA.  q [B, Hq, D]; keys/vals [B, S, Hkv, D] (post-RoPE)."""
-    G = q.shape[1] // keys.shape[2]
-    keys = keys.repeat_interleave(G, dim=2)
-    vals = vals.repeat_interleave(G, dim=2)
-    sc = torch.einsum("bhd,bshd->bhs", q, keys) * scale
-    return torch.einsum("bhs,bshd->bhd", sc.softmax(-1), vals)
+    """softmax(q k^T * scale) v with GQA (query head h reads kv head h // G).
+    q [B, Hq, D]; keys/vals [B, S, Hkv, D] (post-RoPE)."""
+    B, Hq, D = q.shape
+    Hkv = keys.shape[2]
+    qg = q.view(B, Hkv, Hq // Hkv, D)
+    sc = torch.einsum("bhgd,bshd->bhgs", qg, keys) * scale
+    return torch.einsum("bhgs,bshd->bhgd", sc.softmax(-1), vals).reshape(B, Hq, D)
+
 
 def _map_tensors(obj, fn):
     if isinstance(obj, dict):

@@ -68,6 +68,8 @@ class Supernet:
         self.scale_attn = attn_scale(cfg)
         self._alloc_state(fa_block_table)
         self._alloc_decode_buffers()
+        self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
+        self.force_simt = False
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -169,27 +171,42 @@ class Supernet:
         ops.rope_kv_append(d["qkv"], None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
                            st["k"], st["v"], bt, Hq, Hkv, D, P, window)
         sp, _ = self.attn_split[kind]
+        name = "swa_decode" if kind == SWA else "fa_decode"
+        self._probe_begin(name)
         ops.attn_decode(d["q"], st["k"], st["v"], bt, self.seq_lens, d["attn"], d["ws"], d["counters"], Hq, Hkv, D,
-                        P, window, sp, self.ws_max_splits, self.scale_attn, force_simt=getattr(self, "force_simt", False))
+                        P, window, sp, self.ws_max_splits, self.scale_attn, force_simt=self.force_simt)
+        self._probe_end(name)
         torch.mm(d["attn"], w["o"].t(), out=out)
 
     def _gdn_decode(self, l, h, out):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.gdn_head_dim
         torch.mm(h, w["w_in"].t(), out=d["gdn_proj"])
+        self._probe_begin("gdn_decode")
         ops.gdn_decode(d["gdn_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"], w["dt_bias"],
                        w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D, cfg.conv_width,
                        1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+        self._probe_end("gdn_decode")
         torch.mm(d["gdn_out"], w["o"].t(), out=out)
 
     def _kda_decode(self, l, h, out):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.kda_head_dim
         torch.mm(h, w["w_in"].t(), out=d["kda_proj"])
+        self._probe_begin("kda_decode")
         ops.kda_decode(d["kda_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
                        w["dt_bias"], w["f2"], w["g2"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D,
                        cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+        self._probe_end("kda_decode")
         torch.mm(d["kda_out"], w["o"].t(), out=out)
+
+    def _probe_begin(self, name):
+        if self.probe is not None:
+            self.probe.begin(name)
+
+    def _probe_end(self, name):
+        if self.probe is not None:
+            self.probe.end(name)
 
     def decode_body(self):
         """One decode step on the current stream: step_tokens -> logits, next_tokens.
@@ -343,3 +360,26 @@ class Supernet:
     def recurrent_state(self, layer):
         """[B, Hv, K, V] view of a GDN/KDA state (stored [B, Hv, V, K])."""
         return self.state[layer]["S"].transpose(-1, -2)
+
+
+class KernelProbe:
+    """Timing events around named kernels.  Created with external=True so that, when the decode
+    step is captured into a CUDA graph, the records become graph event nodes on the launching
+    stream; after each replay `collect()` returns {name: [ms per launch]}."""
+
+    def __init__(self):
+        self.pairs = {}
+        self._open = {}
+
+    def begin(self, name):
+        e = torch.cuda.Event(enable_timing=True, external=True)
+        e.record()
+        self._open[name] = e
+
+    def end(self, name):
+        e = torch.cuda.Event(enable_timing=True, external=True)
+        e.record()
+        self.pairs.setdefault(name, []).append((self._open.pop(name), e))
+
+    def collect(self):
+        return {n: [a.elapsed_time(b) for a, b in ps] for n, ps in self.pairs.items()}
