@@ -62,10 +62,12 @@ sn_status sn_embed(const int32_t* tokens, const void* table, float* residual,
                    int32_t* seq_lens, int32_t* positions, int rows, int dim,
                    int dtype, void* stream);
 
-/* if delta != NULL: residual += delta;  out = rmsnorm(residual) * weight.  */
-sn_status sn_add_rmsnorm(const void* delta, float* residual, const void* weight,
-                         void* out, int rows, int dim, float eps, int dtype,
-                         void* stream);
+/* residual += delta (if non-NULL) + sum_{s<nsplit} partials[s] (fp32 slabs
+ * [nsplit][rows][dim] from SN_GEMM_PARTIAL, added in slab order);
+ * out = rmsnorm(residual) * weight.                                          */
+sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit,
+                         float* residual, const void* weight, void* out, int rows,
+                         int dim, float eps, int dtype, void* stream);
 
 /* out[r,i] = silu(gate_up[r,i]) * gate_up[r,ffn+i]                         */
 sn_status sn_silu_mul(const void* gate_up, void* out, int rows, int ffn, int dtype,
@@ -181,6 +183,26 @@ sn_status sn_delta_scan(int kind, const float* qn, const float* kn,
 sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride,
                            const void* norm_w, void* out, int rows, int H, int D,
                            float eps, int act, int dtype, void* stream);
+
+/* ---------------------------------------------------------------- decode GEMM
+ * Weight-streaming projection GEMM for decode batches (M <= 128):
+ * C[m][n] = sum_k X[m][k] W[n][k], X [M][ldx] bf16, W [N][ldw] bf16 (nn.Linear
+ * layout), on tcgen05/TMEM/TMA.  Each CTA owns whole row blocks of W over the
+ * full K (block height chosen so ~all 148 SMs stream; no split-K, so results
+ * are deterministic); launched with programmatic dependent launch so W starts
+ * streaming while the previous kernel finishes.  Replaces the projection / FFN
+ * / LM-head GEMMs of the decode step (the trunk of R/PAPER.md:175-182 and each
+ * mixer's projections, R/PAPER.md:1540-1625).
+ *   SN_GEMM_STORE : out bf16 [M][ldo] = C
+ *   SN_GEMM_SWIGLU: W is [2N][K] = [gate; up]; out bf16 [M][ldo] = silu(C_g)*C_u
+ *   SN_GEMM_RESID : out fp32 [M][ldo] += C   (residual stream)
+ *   SN_GEMM_PARTIAL: split-K; out fp32 [S][M][ldo] gets one K-split partial per slab,
+ *                   S = sn_gemm_decode_splits(M, N, K, mode) (also returned in *splits_out);
+ *                   the consumer sums the slabs (sn_add_rmsnorm does, in slab order).   */
+typedef enum { SN_GEMM_STORE = 0, SN_GEMM_SWIGLU = 1, SN_GEMM_RESID = 2, SN_GEMM_PARTIAL = 3 } sn_gemm_mode;
+int sn_gemm_decode_splits(int M, int N, int K, int mode);
+sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw,
+                         void* out, int ldo, int mode, int* splits_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,9 @@
 namespace sn {
 
 // ------------------------------------------------------------------ RoPE + append
-// grid (rows), block: one thread per rotary pair of every head.
+// grid (rows, Hq + 2*Hkv): one CTA per (row, head); heads < Hq are query heads
+// (rotate, write q_out), the next Hkv are key heads (rotate, append to the cache),
+// the last Hkv are value heads (copy to the cache).  Thread i owns rotary pair i.
 template <typename T>
 __global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ row_seq,
                                       const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
@@ -20,49 +22,53 @@ __global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* 
                                       T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
                                       T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
                                       int Hkv, int D, int page_size, int max_blocks, int window) {
-  const int r = blockIdx.x;
+  sn::pdl_launch_dependents();
+  const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
+  const int half = D / 2;
+  if (i >= half) return;
   const int seq = row_seq ? row_seq[r] : r;
   const int pos = row_pos[r];
-  const int half = D / 2;
-  const int stride = (Hq + 2 * Hkv) * D;
-  const T* row = qkv + (size_t)r * stride;
-  // cache slot for this row (or -1 when an SWA row is already outside the window)
-  int slot = window > 0 ? pos % window : pos;
-  bool write = true;
-  if (window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window) write = false;
-  const int page = block_table[(size_t)seq * max_blocks + slot / page_size];
-  const int off = slot % page_size;
-  for (int idx = threadIdx.x; idx < (Hq + Hkv) * half; idx += blockDim.x) {
-    const int head = idx / half, i = idx - head * half;
-    const float ang = (float)pos * inv_freq[i];
-    float sn, cs;
-    sincosf(ang, &sn, &cs);
-    const T* src = row + head * D;  // q heads then k heads are contiguous in the row
-    const float x1 = io<T>::ld(src + i), x2 = io<T>::ld(src + i + half);
-    const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
-    if (head < Hq) {
-      T* dst = q_out + ((size_t)r * Hq + head) * D;
-      io<T>::st(dst + i, y1);
-      io<T>::st(dst + i + half, y2);
-    } else {
-      const int hk = head - Hq;
-      if (k_out) {
-        T* dst = k_out + ((size_t)r * Hkv + hk) * D;
-        io<T>::st(dst + i, y1);
-        io<T>::st(dst + i + half, y2);
-      }
-      if (write) {
-        T* dst = k_cache + (((size_t)page * Hkv + hk) * page_size + off) * D;
-        io<T>::st(dst + i, y1);
-        io<T>::st(dst + i + half, y2);
-      }
+  const T* src = qkv + (size_t)r * (Hq + 2 * Hkv) * D + (size_t)head * D;
+  // cache slot (FA: the position; SWA: ring slot), SWA rows older than the window are not stored
+  const int slot = window > 0 ? pos % window : pos;
+  const bool write = !(window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window);
+  if (head >= Hq + Hkv) {  // value head: plain copy
+    const int hk = head - Hq - Hkv;
+    const T v1 = src[i], v2 = src[i + half];
+    if (v_out) {
+      T* dst = v_out + ((size_t)r * Hkv + hk) * D;
+      dst[i] = v1;
+      dst[i + half] = v2;
     }
+    if (write) {
+      const int page = block_table[(size_t)seq * max_blocks + slot / page_size];
+      T* dst = v_cache + (((size_t)page * Hkv + hk) * page_size + slot % page_size) * D;
+      dst[i] = v1;
+      dst[i + half] = v2;
+    }
+    return;
   }
-  for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
-    const int hk = idx / D, d = idx - hk * D;
-    const T val = row[(Hq + Hkv) * D + idx];
-    if (v_out) v_out[((size_t)r * Hkv + hk) * D + d] = val;
-    if (write) v_cache[(((size_t)page * Hkv + hk) * page_size + off) * D + d] = val;
+  float sn, cs;
+  sincosf((float)pos * inv_freq[i], &sn, &cs);
+  const float x1 = io<T>::ld(src + i), x2 = io<T>::ld(src + i + half);
+  const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+  if (head < Hq) {
+    T* dst = q_out + ((size_t)r * Hq + head) * D;
+    io<T>::st(dst + i, y1);
+    io<T>::st(dst + i + half, y2);
+    return;
+  }
+  const int hk = head - Hq;
+  if (k_out) {
+    T* dst = k_out + ((size_t)r * Hkv + hk) * D;
+    io<T>::st(dst + i, y1);
+    io<T>::st(dst + i + half, y2);
+  }
+  if (write) {
+    const int page = block_table[(size_t)seq * max_blocks + slot / page_size];
+    T* dst = k_cache + (((size_t)page * Hkv + hk) * page_size + slot % page_size) * D;
+    io<T>::st(dst + i, y1);
+    io<T>::st(dst + i + half, y2);
   }
 }
 
@@ -71,6 +77,7 @@ __global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* 
 // keeps its own online-softmax state, the 4 states merge in smem.
 template <typename T, int D, int GMAX>
 __global__ void __launch_bounds__(128) attn_decode_simt_kernel(AttnDecodeArgs a) {
+  sn::pdl_launch_dependents();
   constexpr int EPL = D / 32;
   __shared__ float s_q[GMAX][D];
   __shared__ float s_m[4][GMAX], s_l[4][GMAX];
@@ -236,7 +243,8 @@ sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq, const int32
   SN_REQUIRE(qkv && row_pos && inv_freq && q_out && k_cache && v_cache && block_table,
              "sn_rope_kv_append: NULL pointer argument");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    rope_kv_append_kernel<T><<<rows, 256, 0, (cudaStream_t)stream>>>(
+    dim3 grid(rows, Hq + 2 * Hkv);
+    rope_kv_append_kernel<T><<<grid, ((D / 2 + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(
         (const T*)qkv, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache,
         (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
     return check_launch("sn_rope_kv_append");

@@ -92,6 +92,7 @@ template <int D>
 __global__ void __launch_bounds__(NW * 32, 1)
     attn_decode_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                           const AttnDecodeArgs a) {
+  sn::pdl_launch_dependents();
   constexpr int TILE_BYTES = KT * D * 2;        // one of K or V
   constexpr int STAGE_BYTES = 2 * TILE_BYTES;   // K then V
   constexpr int NKS = D / 16;                   // k-steps of Q.K^T

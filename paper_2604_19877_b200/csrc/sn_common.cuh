@@ -97,6 +97,13 @@ __device__ __forceinline__ float block_sum(float v, float* scratch) {
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch: lets the next kernel in the stream (if it was
+// launched with the PDL attribute — the decode GEMMs are) start its prologue and
+// its weight prefetch while this kernel is still running.  No-op otherwise.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace sn
 
 #define SN_DISPATCH_DTYPE(dtype, T, ...)                                  \

@@ -85,6 +85,7 @@ constexpr int kDecodeThreads = 256;
 
 template <typename T, int D, bool KDA>
 __global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const DeltaDecodeArgs a) {
+  sn::pdl_launch_dependents();
   constexpr int NW = kDecodeThreads / 32;
   constexpr int EPL = D / 32;     // key entries per lane
   constexpr int CPW = D / NW;     // value columns per warp
@@ -101,11 +102,30 @@ __global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const Delt
   __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
   __shared__ float s_red[NW];
   __shared__ float s_beta;
+  __shared__ __align__(8) uint64_t s_bar;
+  extern __shared__ __align__(16) float s_state[];  // [D][D]: the (seq, head) state, bulk-copied in
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = blockIdx.x, b = blockIdx.y;
   const int G = a.Hv / a.Hk, kh = h / G;
+  // The state is written only by this layer's previous decode step, so it can be
+  // fetched before griddepcontrol.wait: the 2*D*D*4-byte HBM read overlaps both the
+  // producer kernel's tail (PDL) and this CTA's conv / norm / gate prologue.
   const int slot = a.slot_idx ? a.slot_idx[b] : b;
+  float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
+  if (tid == 0) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    constexpr uint32_t kBytes = D * D * 4, kChunk = kBytes < 16384 ? kBytes : 16384;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBytes) : "memory");
+    for (uint32_t off = 0; off < kBytes; off += kChunk)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(reinterpret_cast<char*>(s_state) + off)),
+                   "l"(reinterpret_cast<const char*>(S) + off), "r"(kChunk), "r"(bar)
+                   : "memory");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pos = a.positions[b];
   const int W = a.W;
   const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
@@ -187,12 +207,18 @@ __global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const Delt
     kg[e] = s_k[i] * eg[e];
     qg[e] = s_q[i] * eg[e];
   }
-  float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
+  {
+    uint32_t ok = 0;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(ok) : "r"(bar) : "memory");
+  }
 #pragma unroll 1
   for (int c0 = warp * CPW; c0 < (warp + 1) * CPW; c0 += NB) {
     float s[NB][EPL];
 #pragma unroll
-    for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
+    for (int n = 0; n < NB; ++n) vecf<EPL>::ld(s_state + (c0 + n) * D + lane * EPL, s[n]);
     float kd[NB], qd[NB];
 #pragma unroll
     for (int n = 0; n < NB; ++n) {
@@ -386,14 +412,39 @@ __global__ void __launch_bounds__(D) gated_rmsnorm_kernel(const float* __restric
   io<T>::st(out + ((size_t)r * H + h) * D + j, v * rstd * io<T>::ld(w + j) * a);
 }
 
+template <typename T, int D, bool KDA>
+static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStream_t st) {
+  const int smem = D * D * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(delta_decode_kernel<T, D, KDA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.Hv, B);
+  cfg.blockDim = dim3(kDecodeThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // state prefetch overlaps the in-proj tail
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA>, a);
+  if (e != cudaSuccess) {
+    set_error("%s launch: %s", KDA ? "sn_kda_decode" : "sn_gdn_decode", cudaGetErrorString(e));
+    return SN_ECUDA;
+  }
+  return check_launch(KDA ? "sn_kda_decode" : "sn_gdn_decode");
+}
+
 template <bool KDA>
 static sn_status launch_delta_decode(const DeltaDecodeArgs& a, int B, int D, int dtype, cudaStream_t st) {
-  dim3 grid(a.Hv, B);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    if (D == 128) delta_decode_kernel<T, 128, KDA><<<grid, kDecodeThreads, 0, st>>>(a);
-    else if (D == 64) delta_decode_kernel<T, 64, KDA><<<grid, kDecodeThreads, 0, st>>>(a);
-    else { set_error("delta decode: head dim %d unsupported (64 or 128)", D); return SN_EUNSUPPORTED; }
-    return check_launch(KDA ? "sn_kda_decode" : "sn_gdn_decode");
+    if (D == 128) return launch_delta_decode_t<T, 128, KDA>(a, B, st);
+    if (D == 64) return launch_delta_decode_t<T, 64, KDA>(a, B, st);
+    set_error("delta decode: head dim %d unsupported (64 or 128)", D);
+    return SN_EUNSUPPORTED;
   });
 }
 

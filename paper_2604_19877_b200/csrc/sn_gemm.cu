@@ -1,0 +1,449 @@
+// Weight-streaming decode GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Decode projections/FFN/LM head are  C[m][n] = sum_k X[m][k] * W[n][k]  with a
+// tiny batch M (<= 128 sequences) and big weights W [N x K] (58% of the bytes of
+// a fastest-preset decode step).  The kernel is therefore an
+// HBM stream of W: each CTA owns a 128-row block of W (and optionally a K slice),
+// TMA streams [128 x 64] W tiles and the matching [BN x 64] X tiles through an
+// mbarrier ring in shared memory (128B swizzle), one elected thread issues
+// tcgen05.mma (M=128 weight rows x N=BN batch columns x K=16) into a TMEM
+// accumulator, and the 4 warps drain TMEM with tcgen05.ld in the epilogue.
+// "Swap-AB": W is the UMMA A operand so the tiny batch sits in the N dimension.
+//
+// Work split: measured on B200, one SM pulls only ~45-60 GB/s of TMA tiles, so a
+// decode GEMM must keep (nearly) every one of the 148 SMs streaming, and split-K
+// fix-ups cost more than they save (all partials finish together at the end).
+// Instead each CTA owns whole row blocks over the full K: the host picks the
+// block height BR (a multiple of 8 <= 128; the UMMA still runs M=128, rows >= BR
+// of the smem tile are ignored) that minimises waves x BR, e.g. BR=40 for
+// N=5120 (128 CTAs), BR=72 for N=10304 (144 CTAs), BR=128 for the LM head
+// (persistent: ~7 blocks per CTA).  No reduction, no workspace, deterministic.
+// TMEM holds two accumulators so the epilogue of one block overlaps the MMAs of
+// the next; warp roles: 0 = TMA producer, 1 = MMA issuer, 4-7 = epilogue.
+// Programmatic dependent launch lets the first stages of W stream in while the
+// previous kernel of the decode step is still running.
+//
+// Epilogues (fused to remove separate elementwise kernels from the step):
+//   SN_GEMM_STORE   out[m][n] = acc                         (bf16)
+//   SN_GEMM_SWIGLU  W = [gate; up] (2N rows): out[m][n] = silu(g) * u  (bf16)
+//   SN_GEMM_RESID   resid[m][n] += acc                      (fp32 residual stream)
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "sn_common.cuh"
+
+namespace sn {
+namespace gemm {
+
+constexpr int BM = 128;     // weight rows per CTA (UMMA M)
+constexpr int BK = 64;      // K per stage (one 128-B swizzle row of bf16)
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_noarrive(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// UMMA shared-memory descriptor: K-major operand, 128B swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+  d |= (uint64_t)1 << 46;              // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: kind::f16, bf16 x bf16 -> f32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct GemmArgs {
+  void* out;       // bf16 [M][ldo] | fp32 residual [M][ldo] | fp32 partial slabs [splits][M][ldo]
+  int M, N, K, ldo, mode, kblocks;
+  int br;          // weight rows per block (multiple of 8, <= BM)
+  int nblocks;     // ceil(N / br)
+  int splits;      // K splits per block (PARTIAL mode only, else 1)
+  int ns;          // pipeline stages (runtime: as many as fit, so small blocks keep W in flight)
+  int stage_bytes; // NA * br * 128 + BN * 128 (1024-aligned)
+};
+
+constexpr int kMaxStages = 32;
+
+constexpr int kGemmThreads = 256;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// smem: [stages][ A (NA x 16 KB) | B (BN x 128 B) ].  NA = 2 for SwiGLU.
+template <int BN, int NA>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_decode_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap,
+                       const GemmArgs g) {
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int ACC = NA * BN;  // TMEM columns per accumulator buffer
+  constexpr int TMEM_COLS = (2 * ACC) <= 32 ? 32 : (2 * ACC) <= 64 ? 64 : (2 * ACC) <= 128 ? 128 : (2 * ACC) <= 256 ? 256 : 512;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int BR = g.br, S = g.splits;
+  const int KB = g.kblocks / S;  // k-blocks per item (the host makes splits divide kblocks)
+  const int items = g.nblocks * S;
+  const int my_blocks = items > c ? (items - c + G - 1) / G : 0;  // work items c, c+G, c+2G, ...
+  const int my_units = my_blocks * KB;
+  const uint32_t a_bytes = (uint32_t)BR * BK * 2;  // one A tile: BR rows (the UMMA reads 128; extra rows ignored)
+  const int NS = g.ns, STAGE = g.stage_bytes;
+  const int A_BYTES = (int)a_bytes;
+  pdl_launch_dependents();
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    for (int i = 0; i < NS; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer: one continuous ring over the CTA's blocks
+      // PDL: W does not depend on the previous kernel, so the first NS stages of W are
+      // requested before griddepcontrol.wait; the stage's single arrival comes with its
+      // X half, so a stage can never complete on its W bytes alone.
+      const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+      const int npre = min(NS, my_units);
+      for (int i = 0; i < npre; ++i) {
+        const int item = c + (i / KB) * G, blk = item / S, kc = ((item % S) * KB + i % KB) * BK;
+        uint8_t* st = smem + i * STAGE;
+        mbar_expect_tx_noarrive(&full_bar[i], NA * a_bytes);
+        tma_load_2d(st, &wmap, kc, blk * BR, &full_bar[i], pw);
+        if (NA == 2) tma_load_2d(st + A_BYTES, &wmap, kc, g.N + blk * BR, &full_bar[i], pw);
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int i = 0; i < npre; ++i) {
+        const int item = c + (i / KB) * G, kc = ((item % S) * KB + i % KB) * BK;
+        mbar_expect_tx(&full_bar[i], B_BYTES);
+        tma_load_2d(smem + i * STAGE + NA * A_BYTES, &xmap, kc, 0, &full_bar[i], px);
+      }
+      for (int i = npre; i < my_units; ++i) {
+        const int s = i % NS, r = i / NS;
+        mbar_wait(&empty_bar[s], (r - 1) & 1);
+        uint8_t* st = smem + s * STAGE;
+        mbar_expect_tx(&full_bar[s], NA * a_bytes + B_BYTES);
+        const int item = c + (i / KB) * G, blk = item / S, kc = ((item % S) * KB + i % KB) * BK;
+        tma_load_2d(st, &wmap, kc, blk * BR, &full_bar[s], pw);
+        if (NA == 2) tma_load_2d(st + A_BYTES, &wmap, kc, g.N + blk * BR, &full_bar[s], pw);
+        tma_load_2d(st + NA * A_BYTES, &xmap, kc, 0, &full_bar[s], px);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      for (int blk_i = 0, i = 0; blk_i < my_blocks; ++blk_i) {
+        const int buf = blk_i & 1;
+        if (blk_i >= 2) mbar_wait(&tempty_bar[buf], ((blk_i >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + buf * ACC;
+        for (int kb = 0; kb < KB; ++kb, ++i) {
+          const int s = i % NS, r = i / NS;
+          mbar_wait(&full_bar[s], r & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * STAGE);
+          const uint32_t sb = sa + NA * A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t bdesc = desc_sw128(sb + k * 32);
+            const uint32_t accum = (kb == 0 && k == 0) ? 0u : 1u;
+            umma(acc, desc_sw128(sa + k * 32), bdesc, idesc, accum);
+            if (NA == 2) umma(acc + BN, desc_sw128(sa + A_BYTES + k * 32), bdesc, idesc, accum);
+          }
+          umma_commit(&empty_bar[s]);
+        }
+        umma_commit(&tfull_bar[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue warps: thread t <-> TMEM lane t <-> weight row blk*BR + t
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int t = threadIdx.x - 128;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int mode = g.mode;
+    for (int blk_i = 0; blk_i < my_blocks; ++blk_i) {
+      const int buf = blk_i & 1;
+      const int item = c + blk_i * G;
+      const int n = (item / S) * BR + t;
+      const bool row_ok = t < BR && n < g.N;
+      mbar_wait(&tfull_bar[buf], (blk_i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t acc = tmem + lane_off + buf * ACC;
+#pragma unroll 1
+      for (int col = 0; col < BN; col += 16) {
+        float v[16], w2[16], old[16];
+        if (mode == SN_GEMM_RESID && row_ok) {
+          const float* o = reinterpret_cast<const float*>(g.out) + n;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) old[j] = (col + j < g.M) ? __ldcg(o + (size_t)(col + j) * g.ldo) : 0.f;
+        }
+        tmem_ld16(acc + col, v);
+        if (NA == 2) tmem_ld16(acc + BN + col, w2);
+        if (row_ok) {
+          if (mode == SN_GEMM_PARTIAL) {
+            float* o = reinterpret_cast<float*>(g.out) + (size_t)(item % S) * g.M * g.ldo + n;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (col + j < g.M) __stcg(o + (size_t)(col + j) * g.ldo, v[j]);
+          } else if (mode == SN_GEMM_RESID) {
+            float* o = reinterpret_cast<float*>(g.out) + n;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (col + j < g.M) o[(size_t)(col + j) * g.ldo] = old[j] + v[j];
+          } else {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + n;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (col + j < g.M)
+                o[(size_t)(col + j) * g.ldo] =
+                    __float2bfloat16_rn(mode == SN_GEMM_SWIGLU ? silu_f(v[j]) * w2[j] : v[j]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      named_bar(1, 128);
+      if (t == 0) mbar_arrive_local(&tempty_bar[buf]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static bool map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                   uint32_t box_rows) {
+  // (box_rows <= 256; for W it is the block height BR, for X the batch tile BN)
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Work decomposition.  Per-CTA time ~ waves x k-blocks-per-item x (NA*BR + BN) bytes;
+// BR >= 48 keeps >= 1.5 KB of W per UMMA (tcgen05.mma issues at ~45 cycles minimum,
+// measured), split-K (PARTIAL mode only: the consumer sums the slabs) lets a narrow N
+// fill the SMs with tall blocks.  Ties -> fewer splits, then taller blocks.
+static void pick_tiling(int N, int kblocks, int sms, int na, int bn, int max_splits, int* br_out,
+                        int* splits_out) {
+  long best_cost = -1;
+  for (int s = 1; s <= max_splits; ++s) {
+    if (kblocks % s) continue;
+    for (int br = BM; br >= 48; br -= 8) {
+      const long items = (long)((N + br - 1) / br) * s;
+      const long waves = (items + sms - 1) / sms;
+      const long cost = waves * (kblocks / s) * (long)(na * br + bn);
+      if (best_cost < 0 || cost < best_cost) { best_cost = cost; *br_out = br; *splits_out = s; }
+    }
+  }
+}
+
+static int batch_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128; }
+
+template <int BN, int NA>
+static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, GemmArgs g, int grid, cudaStream_t st) {
+  constexpr int kSmemMax = 227 * 1024;          // per-CTA opt-in maximum on sm_100
+  const int stage = NA * g.br * BK * 2 + BN * BK * 2;
+  const int tail = BM * BK * 2;  // the M=128 UMMA of the last stage may read 128 rows past its A tile
+  int ns = (kSmemMax - 2048 - tail) / stage;     // 1 KB alignment slack + static barriers
+  if (ns > kMaxStages) ns = kMaxStages;
+  g.ns = ns;
+  g.stage_bytes = stage;
+  const int smem = ns * stage + tail + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_decode_kernel<BN, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax - 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the producer's tail
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_decode_kernel<BN, NA>, wm, xm, g);
+  if (e != cudaSuccess) {
+    set_error("sn_gemm_decode launch: %s", cudaGetErrorString(e));
+    return SN_ECUDA;
+  }
+  return check_launch("sn_gemm_decode");
+}
+
+}  // namespace gemm
+}  // namespace sn
+
+using namespace sn;
+using namespace sn::gemm;
+
+extern "C" {
+
+int sn_gemm_decode_splits(int M, int N, int K, int mode) {
+  int br = BM, splits = 1;
+  if (mode != SN_GEMM_PARTIAL || K % BK) return 1;
+  pick_tiling(N, K / BK, num_sms(), 1, batch_tile(M), 8, &br, &splits);
+  return splits;
+}
+
+sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw, void* out, int ldo,
+                         int mode, int* splits_out, void* stream) {
+  SN_REQUIRE(x && w && out, "sn_gemm_decode: NULL pointer");
+  SN_REQUIRE(M >= 1 && M <= 128, "sn_gemm_decode: M=%d must be in [1, 128] (decode batch)", M);
+  SN_REQUIRE(K % BK == 0 && K >= BK, "sn_gemm_decode: K=%d must be a multiple of %d", K, BK);
+  SN_REQUIRE(N >= 1 && ldw >= K && ldx >= K, "sn_gemm_decode: bad N/ld");
+  SN_REQUIRE(mode == SN_GEMM_STORE || mode == SN_GEMM_SWIGLU || mode == SN_GEMM_RESID || mode == SN_GEMM_PARTIAL,
+             "sn_gemm_decode: mode %d", mode);
+  SN_REQUIRE(((uintptr_t)x % 16) == 0 && ((uintptr_t)w % 16) == 0 && (ldx % 8) == 0 && (ldw % 8) == 0,
+             "sn_gemm_decode: operands must be 16-byte aligned");
+  const int BN = batch_tile(M);
+  const int sms = num_sms();
+  int br = BM, splits = 1;
+  pick_tiling(N, K / BK, sms, mode == SN_GEMM_SWIGLU ? 2 : 1, BN, mode == SN_GEMM_PARTIAL ? 8 : 1, &br, &splits);
+  CUtensorMap wm, xm;
+  const uint64_t wrows = mode == SN_GEMM_SWIGLU ? 2ull * N : (uint64_t)N;
+  if (!map_2d(&wm, w, wrows, K, ldw, br) || !map_2d(&xm, x, M, K, ldx, BN)) {
+    set_error("sn_gemm_decode: cuTensorMapEncodeTiled failed");
+    return SN_ECUDA;
+  }
+  const int nblocks = (N + br - 1) / br;
+  const int items = nblocks * splits;
+  const int grid = items < sms ? items : sms;
+  if (splits_out) *splits_out = splits;
+  GemmArgs g{out, M, N, K, ldo, mode, K / BK, br, nblocks, splits, 0, 0};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mode == SN_GEMM_SWIGLU) {
+    switch (BN) {
+      case 16: return launch<16, 2>(wm, xm, g, grid, st);
+      case 32: return launch<32, 2>(wm, xm, g, grid, st);
+      case 64: return launch<64, 2>(wm, xm, g, grid, st);
+      default: return launch<128, 2>(wm, xm, g, grid, st);
+    }
+  }
+  switch (BN) {
+    case 16: return launch<16, 1>(wm, xm, g, grid, st);
+    case 32: return launch<32, 1>(wm, xm, g, grid, st);
+    case 64: return launch<64, 1>(wm, xm, g, grid, st);
+    default: return launch<128, 1>(wm, xm, g, grid, st);
+  }
+}
+
+}  // extern "C"

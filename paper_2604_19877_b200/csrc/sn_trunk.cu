@@ -7,7 +7,11 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <cooperative_groups.h>
+
 #include "sn_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sn {
 
@@ -34,6 +38,7 @@ template <typename T>
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __restrict__ table,
                              float* __restrict__ residual, int32_t* seq_lens, int32_t* positions,
                              int rows, int dim) {
+  sn::pdl_launch_dependents();
   const int r = blockIdx.x;
   if (seq_lens != nullptr && r == 0) {
     for (int b = threadIdx.x; b < rows; b += blockDim.x) {
@@ -53,55 +58,82 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __rest
 }
 
 // ------------------------------------------------------------------ add + rmsnorm
-// One CTA per row; the row (dim <= 8*256*MAXV floats) stays in registers between
-// the sum-of-squares pass and the normalise pass.
-template <typename T, int MAXV>
+// A row is split across a thread-block cluster of CS CTAs (CS = 4 for d = 5120), each
+// thread owning one 8-element chunk, so a 64-row decode batch runs as 256 CTAs instead
+// of 64 long ones.  All of a chunk's inputs (residual, bf16 delta, up to 8 fp32 split-K
+// slabs) are loaded in one batch before they are summed in a fixed order, the
+// sum of squares is combined through distributed shared memory, and the chunk is
+// normalised from registers.
+constexpr int kNormMaxSplit = 8;
+
+template <typename T>
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const T* __restrict__ delta,
+                                                          const float* __restrict__ partials, int nsplit,
                                                           float* __restrict__ residual,
                                                           const T* __restrict__ weight,
-                                                          T* __restrict__ out, int dim, float eps) {
+                                                          T* __restrict__ out, int rows, int dim, float eps) {
+  sn::pdl_launch_dependents();
   __shared__ float scratch[32];
-  const int r = blockIdx.x;
-  float* res = residual + (size_t)r * dim;
-  float v[MAXV][8];
+  __shared__ float cta_sum;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int part = (int)cluster.block_rank();
+  const int r = blockIdx.x / CS;
+  const int per_cta = dim / CS;
+  const int i = part * per_cta + threadIdx.x * 8;
+  const bool active = threadIdx.x * 8 < per_cta;
+  float v[8];
   float ss = 0.f;
+  if (active) {
+    float* res = residual + (size_t)r * dim + i;
+    float4 a = *reinterpret_cast<const float4*>(res);
+    float4 b = *reinterpret_cast<const float4*>(res + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    if (delta != nullptr || nsplit > 0) {
+      float d[8], p[kNormMaxSplit][8];
+      if (delta != nullptr) load8<T>(delta + (size_t)r * dim + i, d);
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c) {
-    const int i = (c * blockDim.x + threadIdx.x) * 8;
-    if (i < dim) {
-      float4 a = *reinterpret_cast<const float4*>(res + i);
-      float4 b = *reinterpret_cast<const float4*>(res + i + 4);
-      v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
-      v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+      for (int s = 0; s < kNormMaxSplit; ++s)
+        if (s < nsplit) load8<float>(partials + ((size_t)s * rows + r) * dim + i, p[s]);
       if (delta != nullptr) {
-        float d[8];
-        load8<T>(delta + (size_t)r * dim + i, d);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[c][k] += d[k];
-        *reinterpret_cast<float4*>(res + i) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
-        *reinterpret_cast<float4*>(res + i + 4) = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+        for (int k = 0; k < 8; ++k) v[k] += d[k];
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) ss += v[c][k] * v[c][k];
+      for (int s = 0; s < kNormMaxSplit; ++s) {
+        if (s < nsplit) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] += p[s][k];
+        }
+      }
+      *reinterpret_cast<float4*>(res) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(res + 4) = make_float4(v[4], v[5], v[6], v[7]);
     }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss += v[k] * v[k];
   }
   ss = block_sum(ss, scratch);
+  if (CS > 1) {
+    if (threadIdx.x == 0) cta_sum = ss;
+    cluster.sync();
+    ss = 0.f;
+    for (int q = 0; q < CS; ++q) ss += *cluster.map_shared_rank(&cta_sum, q);
+    cluster.sync();  // keep every CTA's cta_sum alive until all ranks have read it
+  }
   const float rstd = rsqrtf(ss / (float)dim + eps);
+  if (active) {
+    float w[8];
+    load8<T>(weight + i, w);
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c) {
-    const int i = (c * blockDim.x + threadIdx.x) * 8;
-    if (i < dim) {
-      float w[8];
-      load8<T>(weight + i, w);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) io<T>::st(out + (size_t)r * dim + i + k, v[c][k] * rstd * w[k]);
-    }
+    for (int k = 0; k < 8; ++k) io<T>::st(out + (size_t)r * dim + i + k, v[k] * rstd * w[k]);
   }
 }
 
 // ------------------------------------------------------------------ silu * mul
 template <typename T>
 __global__ void silu_mul_kernel(const T* __restrict__ gu, T* __restrict__ out, int rows, int ffn) {
+  sn::pdl_launch_dependents();
   const size_t n8 = (size_t)rows * ffn / 8;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n8;
        q += (size_t)gridDim.x * blockDim.x) {
@@ -119,6 +151,7 @@ __global__ void silu_mul_kernel(const T* __restrict__ gu, T* __restrict__ out, i
 template <typename T>
 __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logits, int vocab,
                                                       int32_t* __restrict__ out) {
+  sn::pdl_launch_dependents();
   __shared__ float sv[32];
   __shared__ int si[32];
   const T* row = logits + (size_t)blockIdx.x * vocab;
@@ -167,14 +200,35 @@ sn_status sn_embed(const int32_t* tokens, const void* table, float* residual, in
   });
 }
 
-sn_status sn_add_rmsnorm(const void* delta, float* residual, const void* weight, void* out, int rows,
-                         int dim, float eps, int dtype, void* stream) {
+sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit, float* residual, const void* weight,
+                         void* out, int rows, int dim, float eps, int dtype, void* stream) {
+  SN_REQUIRE(nsplit >= 0 && nsplit <= kNormMaxSplit && (nsplit == 0 || partials != nullptr),
+             "sn_add_rmsnorm: bad partials (nsplit %d)", nsplit);
   SN_REQUIRE(rows > 0 && dim > 0 && dim % 8 == 0, "sn_add_rmsnorm: bad shape rows=%d dim=%d", rows, dim);
-  SN_REQUIRE(dim <= 8 * 256 * 4, "sn_add_rmsnorm: dim %d > 8192 unsupported", dim);
+  // cluster size: each CTA owns <= 256 chunks of 8 (and >= 4-way split once rows are long)
+  int cs = 1;
+  while (cs < 8 && (dim / 8 / cs > 256 || (dim / 8 / cs > 64 && cs < 4)) && dim % (16 * cs) == 0) cs *= 2;
+  SN_REQUIRE(dim / 8 / cs <= 256 && dim % (8 * cs) == 0, "sn_add_rmsnorm: dim %d unsupported", dim);
+  const int per_cta = dim / cs;
+  const int threads = ((per_cta / 8 + 31) / 32) * 32;
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    const int threads = dim / 8 >= 256 ? 256 : ((dim / 8 + 31) / 32) * 32;
-    add_rmsnorm_kernel<T, 4><<<rows, threads, 0, (cudaStream_t)stream>>>(
-        (const T*)delta, residual, (const T*)weight, (T*)out, dim, eps);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(rows * cs);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = cs;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, add_rmsnorm_kernel<T>, (const T*)delta, partials, nsplit, residual,
+                                       (const T*)weight, (T*)out, rows, dim, eps);
+    if (e != cudaSuccess) {
+      set_error("sn_add_rmsnorm launch: %s", cudaGetErrorString(e));
+      return SN_ECUDA;
+    }
     return check_launch("sn_add_rmsnorm");
   });
 }

@@ -70,6 +70,15 @@ class Supernet:
         self._alloc_decode_buffers()
         self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
         self.force_simt = False
+        # Which decode projections run on the tcgen05 weight-streaming GEMM (libsn100) and which
+        # on cuBLAS.  Chosen per shape from B200 measurements at B=64 (tools/bench_gemm.py,
+        # profiles/): ours wins for the LM head and the split-K FFN down-projection (its
+        # partial slabs are summed inside the next add_rmsnorm, removing cuBLAS's split-K
+        # reduce kernel); cuBLAS is still faster on the 42-130 MB in/out projections and the
+        # gate/up GEMM.  fp32 I/O (the 1e-4 parity mode) always uses cuBLAS fp32.
+        tc_ok = dtype == torch.bfloat16 and batch <= 128
+        self.sn_gemm = {"lm_head": tc_ok, "ffn_down": tc_ok, "ffn_gate_up": False, "in_proj": False,
+                        "out_proj": False}
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -137,6 +146,10 @@ class Supernet:
         self.gu = e(B, 2 * cfg.ffn)
         self.act = e(B, cfg.ffn)
         self.logits = e(B, cfg.vocab)
+        # fp32 K-split partial slabs of the residual-updating projections (o-proj, FFN down),
+        # summed into the residual by the next add_rmsnorm
+        self.slab_mix = e(8, B, cfg.hidden, d=torch.float32)
+        self.slab_ffn = e(8, B, cfg.hidden, d=torch.float32)
         kinds = set(self.kinds)
         self.dec = {}
         if kinds & {FA, SWA}:
@@ -167,7 +180,7 @@ class Supernet:
         Hq, Hkv, D, P = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
-        torch.mm(h, w["qkv"].t(), out=d["qkv"])
+        self._gemm_store(h, w["qkv"], d["qkv"], "in_proj")
         ops.rope_kv_append(d["qkv"], None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
                            st["k"], st["v"], bt, Hq, Hkv, D, P, window)
         sp, _ = self.attn_split[kind]
@@ -176,29 +189,29 @@ class Supernet:
         ops.attn_decode(d["q"], st["k"], st["v"], bt, self.seq_lens, d["attn"], d["ws"], d["counters"], Hq, Hkv, D,
                         P, window, sp, self.ws_max_splits, self.scale_attn, force_simt=self.force_simt)
         self._probe_end(name)
-        torch.mm(d["attn"], w["o"].t(), out=out)
+        return self._gemm_residual(d["attn"], w["o"], self.slab_mix, out, "out_proj")
 
     def _gdn_decode(self, l, h, out):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.gdn_head_dim
-        torch.mm(h, w["w_in"].t(), out=d["gdn_proj"])
+        self._gemm_store(h, w["w_in"], d["gdn_proj"], "in_proj")
         self._probe_begin("gdn_decode")
         ops.gdn_decode(d["gdn_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"], w["dt_bias"],
                        w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D, cfg.conv_width,
                        1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
         self._probe_end("gdn_decode")
-        torch.mm(d["gdn_out"], w["o"].t(), out=out)
+        return self._gemm_residual(d["gdn_out"], w["o"], self.slab_mix, out, "out_proj")
 
     def _kda_decode(self, l, h, out):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.kda_head_dim
-        torch.mm(h, w["w_in"].t(), out=d["kda_proj"])
+        self._gemm_store(h, w["w_in"], d["kda_proj"], "in_proj")
         self._probe_begin("kda_decode")
         ops.kda_decode(d["kda_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
                        w["dt_bias"], w["f2"], w["g2"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D,
                        cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
         self._probe_end("kda_decode")
-        torch.mm(d["kda_out"], w["o"].t(), out=out)
+        return self._gemm_residual(d["kda_out"], w["o"], self.slab_mix, out, "out_proj")
 
     def _probe_begin(self, name):
         if self.probe is not None:
@@ -208,44 +221,64 @@ class Supernet:
         if self.probe is not None:
             self.probe.end(name)
 
+    def _gemm_store(self, x, w, out, role):
+        if self.sn_gemm[role]:
+            ops.gemm_decode(x, w, out, "store")
+        else:
+            torch.mm(x, w.t(), out=out)
+
+    def _gemm_residual(self, x, w, slab, out_bf16, role):
+        """Projection whose result is added to the residual stream.  Returns the pending
+        update (delta, partials, nsplit) that the next add_rmsnorm applies."""
+        if self.sn_gemm[role]:
+            ns = ops.gemm_decode(x, w, slab, "partial")
+            return (None, slab, ns)
+        torch.mm(x, w.t(), out=out_bf16)
+        return (out_bf16, None, 0)
+
+    def _norm(self, pending, weight):
+        delta, part, ns = pending
+        ops.add_rmsnorm(delta, self.residual, weight, self.h, self.cfg.norm_eps, partials=part, nsplit=ns)
+
     def decode_body(self):
         """One decode step on the current stream: step_tokens -> logits, next_tokens.
         Graph-capturable: every size/position it needs is read from device buffers."""
         cfg, w = self.cfg, self.w
         ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
-        delta = None
+        pending = (None, None, 0)
         for l, kind in enumerate(self.kinds):
             lw = w["layers"][l]
-            ops.add_rmsnorm(delta, self.residual, lw["norm1"], self.h, cfg.norm_eps)
+            self._norm(pending, lw["norm1"])
             if kind == GDN:
-                self._gdn_decode(l, self.h, self.mix_out)
+                pending = self._gdn_decode(l, self.h, self.mix_out)
             elif kind == KDA:
-                self._kda_decode(l, self.h, self.mix_out)
+                pending = self._kda_decode(l, self.h, self.mix_out)
             else:
-                self._attn_decode(l, kind, self.h, self.mix_out)
-            ops.add_rmsnorm(self.mix_out, self.residual, lw["norm2"], self.h, cfg.norm_eps)
-            torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
-            ops.silu_mul(self.gu, self.act)
-            torch.mm(self.act, lw["ffn_down"].t(), out=self.ffn_out)
-            delta = self.ffn_out
-        ops.add_rmsnorm(delta, self.residual, w["final_norm"], self.h, cfg.norm_eps)
-        torch.mm(self.h, w["lm_head"].t(), out=self.logits)
+                pending = self._attn_decode(l, kind, self.h, self.mix_out)
+            self._norm(pending, lw["norm2"])
+            if self.sn_gemm["ffn_gate_up"]:
+                ops.gemm_decode(self.h, lw["ffn_gu"], self.act, "swiglu")
+            else:
+                torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
+                ops.silu_mul(self.gu, self.act)
+            pending = self._gemm_residual(self.act, lw["ffn_down"], self.slab_ffn, self.ffn_out, "ffn_down")
+        self._norm(pending, w["final_norm"])
+        self._gemm_store(self.h, w["lm_head"], self.logits, "lm_head")
         ops.argmax(self.logits, self.next_tokens)
 
     def kernels_per_step(self) -> dict:
-        """Launch census of one decode step: {"sn": own kernels, "cublas": library GEMMs}."""
-        sn = 1 + 1 + 1  # embed, final norm, argmax
-        gemm = 1        # lm head
+        """Launch census of one decode step: {"sn": libsn100 kernels, "cublas": library GEMMs}."""
+        g = self.sn_gemm
+        sn = 3                                 # embed, final norm, argmax
+        lib = 0
+        sn, lib = (sn + 1, lib) if g["lm_head"] else (sn, lib + 1)
         for kind in self.kinds:
-            sn += 2 + 1  # two add_rmsnorm + silu_mul
-            gemm += 2    # ffn
-            if kind in (FA, SWA):
-                sn += 2
-                gemm += 2
-            else:
-                sn += 1
-                gemm += 2
-        return {"sn": sn, "cublas": gemm}
+            sn += 2                            # two add_rmsnorm
+            sn += 2 if kind in (FA, SWA) else 1    # rope+attention | fused delta-rule decode
+            for role in ("in_proj", "out_proj", "ffn_down"):
+                sn, lib = (sn + 1, lib) if g[role] else (sn, lib + 1)
+            sn, lib = (sn + 1, lib) if g["ffn_gate_up"] else (sn + 1, lib + 1)  # fused SwiGLU | GEMM + silu_mul
+        return {"sn": sn, "cublas": lib}
 
     @torch.no_grad()
     def decode(self, tokens):

@@ -6,10 +6,13 @@ not on a CUDA device is an error.
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _lib
-from ._lib import SN_ATTN_FORCE_SIMT, SN_BF16, SN_F32, call
+from ._lib import (SN_ATTN_FORCE_SIMT, SN_BF16, SN_F32, SN_GEMM_PARTIAL, SN_GEMM_RESID, SN_GEMM_STORE, SN_GEMM_SWIGLU,
+                   call)
 
 _DT = {torch.bfloat16: SN_BF16, torch.float32: SN_F32}
 
@@ -39,9 +42,13 @@ def embed(tokens, table, residual, seq_lens=None, positions=None):
          table.shape[1], dtype_code(table.dtype), _s())
 
 
-def add_rmsnorm(delta, residual, weight, out, eps):
+def add_rmsnorm(delta, residual, weight, out, eps, partials=None, nsplit=0):
+    """residual += delta + sum(partials[:nsplit]); out = rmsnorm(residual) * weight."""
     rows, dim = residual.shape
-    call("sn_add_rmsnorm", _p(delta), _p(residual), _p(weight), _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
+    if nsplit:
+        assert partials is not None and partials.dtype == torch.float32 and partials.numel() >= nsplit * rows * dim
+    call("sn_add_rmsnorm", _p(delta), _p(partials) if nsplit else None, int(nsplit), _p(residual), _p(weight),
+         _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
 
 
 def silu_mul(gate_up, out):
@@ -116,3 +123,34 @@ def delta_scan(kind, qn, kn, qkv_conv, v_off, gexp, beta, o, state, slot_idx, cu
 def gated_rmsnorm(o, gate, gate_stride, norm_w, out, H, D, eps, act):
     call("sn_gated_rmsnorm", _p(o), _p(gate), gate_stride, _p(norm_w), _p(out), o.shape[0], H, D, eps, act,
          dtype_code(out.dtype), _s())
+
+
+GEMM_MODES = {"store": SN_GEMM_STORE, "swiglu": SN_GEMM_SWIGLU, "resid": SN_GEMM_RESID, "partial": SN_GEMM_PARTIAL}
+
+
+def gemm_decode_splits(M, N, K, mode="partial"):
+    return _lib.load().sn_gemm_decode_splits(M, N, K, GEMM_MODES[mode])
+
+
+def gemm_decode(x, w, out, mode="store"):
+    """out (+)= x @ w.T on tensor cores (tcgen05).  x [M, K] bf16 (M <= 128), w [N(or 2N), K] bf16.
+    mode "store": out bf16 [M, N]; "swiglu": w = [gate; up], out bf16 [M, N] = silu(g) * u;
+    "resid": out fp32 [M, N] += x @ w.T; "partial": out fp32 [S, M, N] K-split partial slabs
+    (S = gemm_decode_splits(M, N, K)), returned."""
+    M, K = x.shape
+    code = GEMM_MODES[mode]
+    N = out.shape[-1] if mode not in ("store",) else w.shape[0]
+    if mode == "swiglu":
+        assert w.shape[0] == 2 * N
+    if mode in ("resid", "partial"):
+        assert out.dtype == torch.float32
+    else:
+        assert out.dtype == torch.bfloat16
+    if mode == "partial":
+        S = gemm_decode_splits(M, N, K)
+        assert out.dim() == 3 and out.shape[0] >= S and out.shape[1] == M and out.is_contiguous()
+    assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and x.stride(1) == 1 and w.stride(1) == 1
+    s_out = ctypes.c_int(1)
+    call("sn_gemm_decode", _p(x), M, K, x.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(-2), code,
+         ctypes.byref(s_out), _s())
+    return s_out.value
