@@ -84,7 +84,7 @@ __device__ __forceinline__ float row_dot(const T* __restrict__ row, const float*
 constexpr int kDecodeThreads = 256;
 
 template <typename T, int D, bool KDA>
-__global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const DeltaDecodeArgs a) {
+__global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kernel(const DeltaDecodeArgs a) {
   sn::pdl_launch_dependents();
   constexpr int NW = kDecodeThreads / 32;
   constexpr int EPL = D / 32;     // key entries per lane
@@ -102,29 +102,19 @@ __global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const Delt
   __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
   __shared__ float s_red[NW];
   __shared__ float s_beta;
-  __shared__ __align__(8) uint64_t s_bar;
-  extern __shared__ __align__(16) float s_state[];  // [D][D]: the (seq, head) state, bulk-copied in
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = blockIdx.x, b = blockIdx.y;
   const int G = a.Hv / a.Hk, kh = h / G;
-  // The state is written only by this layer's previous decode step, so it can be
-  // fetched before griddepcontrol.wait: the 2*D*D*4-byte HBM read overlaps both the
-  // producer kernel's tail (PDL) and this CTA's conv / norm / gate prologue.
+  // The state is written only by this layer's previous decode step, so its first column
+  // batch is requested before griddepcontrol.wait: the HBM latency overlaps the producer
+  // kernel's tail (PDL) and this CTA's conv / norm / gate prologue.  Afterwards the
+  // stream is software-pipelined (batch j+1 in flight while batch j is updated).
   const int slot = a.slot_idx ? a.slot_idx[b] : b;
   float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
-  if (tid == 0) {
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    constexpr uint32_t kBytes = D * D * 4, kChunk = kBytes < 16384 ? kBytes : 16384;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBytes) : "memory");
-    for (uint32_t off = 0; off < kBytes; off += kChunk)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       (uint32_t)__cvta_generic_to_shared(reinterpret_cast<char*>(s_state) + off)),
-                   "l"(reinterpret_cast<const char*>(S) + off), "r"(kChunk), "r"(bar)
-                   : "memory");
-  }
+  float s_nx[NB][EPL];
+#pragma unroll
+  for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pos = a.positions[b];
   const int W = a.W;
@@ -207,18 +197,17 @@ __global__ void __launch_bounds__(kDecodeThreads) delta_decode_kernel(const Delt
     kg[e] = s_k[i] * eg[e];
     qg[e] = s_q[i] * eg[e];
   }
-  {
-    uint32_t ok = 0;
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
-    while (!ok)
-      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                   : "=r"(ok) : "r"(bar) : "memory");
-  }
 #pragma unroll 1
   for (int c0 = warp * CPW; c0 < (warp + 1) * CPW; c0 += NB) {
     float s[NB][EPL];
 #pragma unroll
-    for (int n = 0; n < NB; ++n) vecf<EPL>::ld(s_state + (c0 + n) * D + lane * EPL, s[n]);
+    for (int n = 0; n < NB; ++n)
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) s[n][e] = s_nx[n][e];
+    if (c0 + NB < (warp + 1) * CPW) {
+#pragma unroll
+      for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + NB + n) * D + lane * EPL, s_nx[n]);
+    }
     float kd[NB], qd[NB];
 #pragma unroll
     for (int n = 0; n < NB; ++n) {
@@ -414,12 +403,7 @@ __global__ void __launch_bounds__(D) gated_rmsnorm_kernel(const float* __restric
 
 template <typename T, int D, bool KDA>
 static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStream_t st) {
-  const int smem = D * D * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(delta_decode_kernel<T, D, KDA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  const int smem = 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.Hv, B);
   cfg.blockDim = dim3(kDecodeThreads);

@@ -181,8 +181,10 @@ class Supernet:
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
         self._gemm_store(h, w["qkv"], d["qkv"], "in_proj")
+        self._probe_begin("rope_kv_append", fine=True)
         ops.rope_kv_append(d["qkv"], None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
                            st["k"], st["v"], bt, Hq, Hkv, D, P, window)
+        self._probe_end("rope_kv_append", fine=True)
         sp, _ = self.attn_split[kind]
         name = "swa_decode" if kind == SWA else "fa_decode"
         self._probe_begin(name)
@@ -213,38 +215,47 @@ class Supernet:
         self._probe_end("kda_decode")
         return self._gemm_residual(d["kda_out"], w["o"], self.slab_mix, out, "out_proj")
 
-    def _probe_begin(self, name):
-        if self.probe is not None:
+    def _probe_begin(self, name, fine=False):
+        if self.probe is not None and (self.probe.fine or not fine):
             self.probe.begin(name)
 
-    def _probe_end(self, name):
-        if self.probe is not None:
+    def _probe_end(self, name, fine=False):
+        if self.probe is not None and (self.probe.fine or not fine):
             self.probe.end(name)
 
     def _gemm_store(self, x, w, out, role):
+        self._probe_begin("gemm_" + role, fine=True)
         if self.sn_gemm[role]:
             ops.gemm_decode(x, w, out, "store")
         else:
             torch.mm(x, w.t(), out=out)
+        self._probe_end("gemm_" + role, fine=True)
 
     def _gemm_residual(self, x, w, slab, out_bf16, role):
         """Projection whose result is added to the residual stream.  Returns the pending
         update (delta, partials, nsplit) that the next add_rmsnorm applies."""
+        self._probe_begin("gemm_" + role, fine=True)
         if self.sn_gemm[role]:
             ns = ops.gemm_decode(x, w, slab, "partial")
+            self._probe_end("gemm_" + role, fine=True)
             return (None, slab, ns)
         torch.mm(x, w.t(), out=out_bf16)
+        self._probe_end("gemm_" + role, fine=True)
         return (out_bf16, None, 0)
 
     def _norm(self, pending, weight):
         delta, part, ns = pending
+        self._probe_begin("add_rmsnorm", fine=True)
         ops.add_rmsnorm(delta, self.residual, weight, self.h, self.cfg.norm_eps, partials=part, nsplit=ns)
+        self._probe_end("add_rmsnorm", fine=True)
 
     def decode_body(self):
         """One decode step on the current stream: step_tokens -> logits, next_tokens.
         Graph-capturable: every size/position it needs is read from device buffers."""
         cfg, w = self.cfg, self.w
+        self._probe_begin("embed", fine=True)
         ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
+        self._probe_end("embed", fine=True)
         pending = (None, None, 0)
         for l, kind in enumerate(self.kinds):
             lw = w["layers"][l]
@@ -256,15 +267,21 @@ class Supernet:
             else:
                 pending = self._attn_decode(l, kind, self.h, self.mix_out)
             self._norm(pending, lw["norm2"])
+            self._probe_begin("gemm_ffn_gate_up", fine=True)
             if self.sn_gemm["ffn_gate_up"]:
                 ops.gemm_decode(self.h, lw["ffn_gu"], self.act, "swiglu")
             else:
                 torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
+                self._probe_end("gemm_ffn_gate_up", fine=True)
+                self._probe_begin("silu_mul", fine=True)
                 ops.silu_mul(self.gu, self.act)
+            self._probe_end("silu_mul" if not self.sn_gemm["ffn_gate_up"] else "gemm_ffn_gate_up", fine=True)
             pending = self._gemm_residual(self.act, lw["ffn_down"], self.slab_ffn, self.ffn_out, "ffn_down")
         self._norm(pending, w["final_norm"])
         self._gemm_store(self.h, w["lm_head"], self.logits, "lm_head")
+        self._probe_begin("argmax", fine=True)
         ops.argmax(self.logits, self.next_tokens)
+        self._probe_end("argmax", fine=True)
 
     def kernels_per_step(self) -> dict:
         """Launch census of one decode step: {"sn": libsn100 kernels, "cublas": library GEMMs}."""
@@ -400,9 +417,10 @@ class KernelProbe:
     step is captured into a CUDA graph, the records become graph event nodes on the launching
     stream; after each replay `collect()` returns {name: [ms per launch]}."""
 
-    def __init__(self):
+    def __init__(self, fine: bool = False):
         self.pairs = {}
         self._open = {}
+        self.fine = fine  # also time norms / GEMMs / elementwise kernels (step breakdown)
 
     def begin(self, name):
         e = torch.cuda.Event(enable_timing=True, external=True)
