@@ -80,6 +80,9 @@ class OracleSupernet:
         self.w = _map_tensors(weights, f32)
         self.inv_freq = cfg.inv_freq().to(torch.float32)
         self.pos = 0
+        # tensor-parallel emulation hook: applied to every row-parallel output (mixer out-proj,
+        # FFN down) before the residual add; identity for the single-device oracle
+        self.reduce = lambda t: t
         B, Hkv, D = batch, cfg.n_kv_heads, cfg.head_dim
         self.state = []
         for k in self.kinds:
@@ -130,14 +133,14 @@ class OracleSupernet:
             lw = w["layers"][l]
             xn = rmsnorm(x, lw["norm1"], cfg.norm_eps)
             if kind in (FA, SWA):
-                x = x + self._attention(l, xn, kind)
+                x = x + self.reduce(self._attention(l, xn, kind))
             elif kind == GDN:
-                x = x + self._gdn(l, xn)
+                x = x + self.reduce(self._gdn(l, xn))
             else:
-                x = x + self._kda(l, xn)
+                x = x + self.reduce(self._kda(l, xn))
             xn = rmsnorm(x, lw["norm2"], cfg.norm_eps)
             gu = xn @ lw["ffn_gu"].T
-            x = x + (F.silu(gu[:, : cfg.ffn]) * gu[:, cfg.ffn:]) @ lw["ffn_down"].T
+            x = x + self.reduce((F.silu(gu[:, : cfg.ffn]) * gu[:, cfg.ffn:]) @ lw["ffn_down"].T)
         self.pos += 1
         return rmsnorm(x, w["final_norm"], cfg.norm_eps) @ w["lm_head"].T
 
@@ -154,6 +157,33 @@ class OracleSupernet:
     def conv_history(self, layer):
         return self.state[layer]["hist"]
 
+
+
+def delta_step(S, q, k, v, beta, g):
+    """One gated delta-rule step for all heads (the recurrence of R/PAPER.md:1575-1578 / 1606-1609).
+    S [B, H, K, V]; q (already scaled), k [B, H, K]; v [B, H, V]; beta [B, H];
+    g: log-decay, [B, H] (GDN, scalar per head) or [B, H, K] (KDA, per key channel).
+    Returns (o [B, H, V], new S):  S <- diag(e^g) S;  S += k (beta (v - k^T S))^T;  o = S^T q."""
+    decay = g.exp()[..., None] if g.dim() == 3 else g.exp()[:, :, None, None]
+    S = S * decay
+    u = beta[:, :, None] * (v - torch.einsum("bhk,bhkv->bhv", k, S))
+    S = S + k[:, :, :, None] * u[:, :, None, :]
+    return torch.einsum("bhk,bhkv->bhv", q, S), S
+
+
+def delta_rule_recurrent(q, k, v, beta, g, initial_state=None, scale=None):
+    """Token-by-token gated delta rule in FLA's calling convention (3P-FLA/ops/gated_delta_rule/
+    naive.py:13-64 for g [B,T,H], 3P-FLA/ops/kda/naive.py:12-66 for g [B,T,H,K]):
+    q,k [B,T,H,K], v [B,T,H,V], beta [B,T,H] -> (o [B,T,H,V], S [B,H,K,V]); q is scaled by K^-1/2."""
+    B, T, H, K = q.shape
+    scale = K ** -0.5 if scale is None else scale
+    S = torch.zeros(B, H, K, v.shape[-1]) if initial_state is None else initial_state.float().clone()
+    outs = []
+    for t in range(T):
+        o, S = delta_step(S, q[:, t].float() * scale, k[:, t].float(), v[:, t].float(), beta[:, t].float(),
+                          g[:, t].float())
+        outs.append(o)
+    return torch.stack(outs, dim=1), S
 
 
 def gdn_core(cfg, p, hist, S, w):
@@ -174,10 +204,7 @@ def gdn_core(cfg, p, hist, S, w):
     k = l2norm(k, cfg.l2_eps).repeat_interleave(G, dim=1)
     g = -w["A_log"].exp() * F.softplus(a_raw + w["dt_bias"])  # [B, Hv]
     beta = torch.sigmoid(b_raw)
-    S = S * g.exp()[:, :, None, None]
-    u = beta[:, :, None] * (v - torch.einsum("bhk,bhkv->bhv", k, S))
-    S = S + k[:, :, :, None] * u[:, :, None, :]
-    o = torch.einsum("bhk,bhkv->bhv", q, S)
+    o, S = delta_step(S, q, k, v, beta, g)
     o = rmsnorm(o, w["norm_w"], cfg.mixer_norm_eps) * F.silu(z)
     return o.reshape(B, Hv * D), hist, S
 
@@ -197,10 +224,7 @@ def kda_core(cfg, p, hist, S, w):
     q = l2norm(q, cfg.l2_eps) / math.sqrt(D)
     k = l2norm(k, cfg.l2_eps)
     beta = torch.sigmoid(b_raw)
-    S = S * g.exp()[:, :, :, None]
-    u = beta[:, :, None] * (v - torch.einsum("bhk,bhkv->bhv", k, S))
-    S = S + k[:, :, :, None] * u[:, :, None, :]
-    o = torch.einsum("bhk,bhkv->bhv", q, S)
+    o, S = delta_step(S, q, k, v, beta, g)
     o = rmsnorm(o, w["norm_w"], cfg.mixer_norm_eps) * torch.sigmoid(gate)
     return o.reshape(B, HD), hist, S
 

@@ -52,9 +52,9 @@ class Supernet:
     """
 
     def __init__(self, cfg: SupernetConfig, placement, *, batch: int, max_len: int, dtype=torch.bfloat16,
-                 device="cuda", seed: int = 0, weights=None, fa_block_table=None):
+                 device="cuda", seed: int = 0, weights=None, fa_block_table=None, tp_group=None):
         _load_lib()  # fail loudly if the extension is missing
-        self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
+        self.B, self.max_len, self.dtype = batch, max_len, dtype
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise ValueError("Supernet runs on CUDA only (no CPU fallback)")
@@ -63,6 +63,17 @@ class Supernet:
             raise ValueError(f"placement has {len(self.kinds)} layers, config {cfg.name} has {cfg.num_layers}")
         if weights is None:
             weights = init_weights(cfg, self.kinds, seed=seed, device=self.device, dtype=dtype)
+        # head-parallel tensor parallelism (dist.py): local head counts, sharded weights, one
+        # all-reduce after each mixer out-projection and after each FFN down-projection
+        self.tp_group, self.tp = tp_group, 1
+        if tp_group is not None:
+            import torch.distributed as tdist
+            from .dist import shard_weights, tp_config
+            self.tp, rank = tdist.get_world_size(tp_group), tdist.get_rank(tp_group)
+            if self.tp > 1:
+                weights = shard_weights(cfg, self.kinds, weights, self.tp, rank)
+                cfg = tp_config(cfg, self.tp)
+        self.cfg = cfg
         self.w = cast_weights(weights, self.device, dtype)
         self.inv_freq = cfg.inv_freq().to(device=self.device, dtype=torch.float32)
         self.scale_attn = attn_scale(cfg)
@@ -234,6 +245,16 @@ class Supernet:
     def _gemm_residual(self, x, w, slab, out_bf16, role):
         """Projection whose result is added to the residual stream.  Returns the pending
         update (delta, partials, nsplit) that the next add_rmsnorm applies."""
+        if self.tp > 1:  # row-parallel: fp32 partial of this rank, summed over the TP group
+            from .dist import allreduce_sum_
+            buf = slab[0]
+            if self.dtype == torch.bfloat16:
+                buf.zero_()
+                ops.gemm_decode(x, w, buf, "resid")
+            else:
+                torch.mm(x, w.t(), out=buf)
+            allreduce_sum_(buf, self.tp_group)
+            return (None, slab, 1)
         self._probe_begin("gemm_" + role, fine=True)
         if self.sn_gemm[role]:
             ns = ops.gemm_decode(x, w, slab, "partial")
@@ -337,17 +358,30 @@ class Supernet:
                 self._gdn_prefill(l, h, mix, cu)
             else:
                 self._kda_prefill(l, h, mix, cu)
+            self._tp_sum(mix)
             ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
             gu = h @ lw["ffn_gu"].t()
             act = e(rows, cfg.ffn)
             ops.silu_mul(gu, act)
             torch.mm(act, lw["ffn_down"].t(), out=ffn_o)
+            self._tp_sum(ffn_o)
             delta = ffn_o
         ops.add_rmsnorm(delta, resid, w["final_norm"], h, cfg.norm_eps)
         if return_all:
             return (h @ w["lm_head"].t()).view(B, T, cfg.vocab)
         last = h.view(B, T, cfg.hidden)[:, -1]
         return last @ w["lm_head"].t()
+
+    def _tp_sum(self, t):
+        """Prefill: sum a row-parallel projection output over the TP group (in fp32)."""
+        if self.tp > 1:
+            from .dist import allreduce_sum_
+            if t.dtype == torch.float32:
+                allreduce_sum_(t, self.tp_group)
+            else:
+                t32 = t.float()
+                allreduce_sum_(t32, self.tp_group)
+                t.copy_(t32)
 
     def _attn_prefill(self, l, kind, h, out, cu, row_seq, row_pos):
         cfg, st, w = self.cfg, self.state[l], self.w["layers"][l]["mixer"]
