@@ -58,6 +58,8 @@ def test_delta_mixer_head_parallel(kind, world):
         part, S_r = _run_delta(local, kind, shard_mixer(cfg, kind, w, world, r), x,
                                S0[:, r * h:(r + 1) * h].contiguous())
         acc += part
-        assert torch.allclose(S_r, S_full[:, r * h:(r + 1) * h], atol=1e-5, rtol=1e-5)
+        # bf16 projections are rounded by different GEMM shapes in the two layouts: state within 2e-3
+        ref_s = S_full[:, r * h:(r + 1) * h]
+        assert ((S_r - ref_s).abs().max() / ref_s.abs().max()).item() < 2e-3
     torch.cuda.synchronize()
     assert ((acc - full).abs().max() / full.abs().max()).item() < 1e-3
