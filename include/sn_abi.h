@@ -69,9 +69,11 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit,
                          float* residual, const void* weight, void* out, int rows,
                          int dim, float eps, int dtype, void* stream);
 
-/* out[r,i] = silu(gate_up[r,i]) * gate_up[r,ffn+i]                         */
-sn_status sn_silu_mul(const void* gate_up, void* out, int rows, int ffn, int dtype,
-                      void* stream);
+/* out[r,i] = silu(gate_up[r,i]) * gate_up[r,ffn+i].  gate_up is a [rows][2*ffn]
+ * dtype matrix (gu_nsplit == 0) or the fp32 split-K slabs of SN_GEMM_PARTIAL
+ * ([gu_nsplit][rows][2*ffn], summed in slab order).                          */
+sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, int ffn,
+                      int dtype, void* stream);
 
 /* out_tokens[r] = argmax_v logits[r,v] (lowest index on ties).             */
 sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens,
@@ -86,8 +88,9 @@ sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens
  * [q Hq*D | k Hkv*D | v Hkv*D], then append k,v at the row's position into
  * the page pool (window==0: slot = pos; window>0: ring slot = pos % window,
  * rows older than seq_lens[seq]-window are not written).  q_out [rows][Hq][D];
- * k_out/v_out [rows][Hkv][D] optional (prefill attention input).            */
-sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq,
+ * k_out/v_out [rows][Hkv][D] optional (prefill attention input).  qkv may be
+ * fp32 split-K slabs (qkv_nsplit > 0, see SN_GEMM_PARTIAL).                  */
+sn_status sn_rope_kv_append(const void* qkv, int qkv_nsplit, const int32_t* row_seq,
                             const int32_t* row_pos, const int32_t* seq_lens,
                             const float* inv_freq, void* q_out, void* k_out,
                             void* v_out, void* k_cache, void* v_cache,
@@ -127,8 +130,10 @@ sn_status sn_attn_prefill(const void* q, const void* k, const void* v,
  * GDN proj row layout (one fused in-proj GEMM output, R/PAPER.md:1584-1587):
  *   [ q Hk*D | k Hk*D | v Hv*D | z Hv*D | b Hv | a Hv ]   conv channels = q|k|v
  *   g = -exp(A_log[h]) * softplus(a + dt_bias[h]),  beta = sigmoid(b),
- *   out = RMSNorm(o) * norm_w * silu(z)                                      */
-sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring,
+ *   out = RMSNorm(o) * norm_w * silu(z)
+ * proj is a [B][proj_stride] dtype matrix (proj_nsplit == 0) or the fp32 split-K
+ * slabs [proj_nsplit][B][proj_stride] of SN_GEMM_PARTIAL (summed on load).     */
+sn_status sn_gdn_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring,
                         const void* conv_w, float* state, const int32_t* slot_idx,
                         const int32_t* positions, const float* A_log,
                         const float* dt_bias, const void* norm_w, void* out, int B,
@@ -139,12 +144,13 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring,
  *   g[h,i] = -exp(A_log[h]) * softplus((f1 @ f2_w^T)[h*D+i] + dt_bias[h*D+i])
  *   gate   = g1 @ g2_w^T + g2_b ;  out = RMSNorm(o) * norm_w * sigmoid(gate)
  *   (f2_w, g2_w: [H*D][R] row-major; the second low-rank factors are fused
- *    into the decode kernel)                                                 */
-sn_status sn_kda_decode(const void* proj, int proj_stride, void* conv_ring,
+ *    into the decode kernel) — or, if fg != NULL, fg = [2][B][H*D] holds the
+ *   precomputed (f1 @ f2_w^T, g1 @ g2_w^T) (f2_w/g2_w unused; g2_b still added). */
+sn_status sn_kda_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring,
                         const void* conv_w, float* state, const int32_t* slot_idx,
                         const int32_t* positions, const float* A_log,
                         const float* dt_bias, const void* f2_w, const void* g2_w,
-                        const void* g2_b, const void* norm_w, void* out, int B,
+                        const void* g2_b, const void* fg, const void* norm_w, void* out, int B,
                         int H, int D, int rank, int conv_width, float scale,
                         float eps_l2, float eps_norm, int dtype, void* stream);
 
@@ -201,6 +207,8 @@ sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride,
  *                   the consumer sums the slabs (sn_add_rmsnorm does, in slab order).   */
 typedef enum { SN_GEMM_STORE = 0, SN_GEMM_SWIGLU = 1, SN_GEMM_RESID = 2, SN_GEMM_PARTIAL = 3 } sn_gemm_mode;
 int sn_gemm_decode_splits(int M, int N, int K, int mode);
+/* profiling aid: per-CTA pipeline wait counters of later launches (4 x #SMs u64), NULL = off */
+void sn_gemm_debug_stats(unsigned long long* dev_stats);
 sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw,
                          void* out, int ldo, int mode, int* splits_out, void* stream);
 

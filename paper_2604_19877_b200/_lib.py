@@ -22,22 +22,23 @@ SIGNATURES = {
     "sn_abi_version": [],
     "sn_embed": [P, P, P, P, P, I, I, I, P],
     "sn_add_rmsnorm": [P, P, I, P, P, P, I, I, Fl, I, P],
-    "sn_silu_mul": [P, P, I, I, I, P],
+    "sn_silu_mul": [P, I, P, I, I, I, P],
     "sn_argmax": [P, I, I, P, I, P],
-    "sn_rope_kv_append": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, P],
+    "sn_rope_kv_append": [P, I, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, P],
     "sn_attn_decode_workspace_bytes": [I, I, I, I, I],
     "sn_attn_decode": [P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, Fl, I, P],
     "sn_attn_prefill": [P, P, P, P, P, I, I, I, I, I, I, Fl, I, P],
-    "sn_gdn_decode": [P, I, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
-    "sn_kda_decode": [P, I, P, P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
+    "sn_gdn_decode": [P, I, I, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
+    "sn_kda_decode": [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
     "sn_conv_prefill": [P, I, P, P, P, P, P, I, I, I, I, I, P],
     "sn_delta_prep": [I, P, P, I, I, I, P, P, P, P, P, P, P, I, I, I, I, Fl, Fl, I, P],
     "sn_delta_scan": [I, P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gated_rmsnorm": [P, P, I, P, P, I, I, I, Fl, I, I, P],
     "sn_gemm_decode_splits": [I, I, I, I],
+    "sn_gemm_debug_stats": [P],
     "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, P],
 }
-RESTYPES = {"sn_attn_decode_workspace_bytes": ctypes.c_size_t, "sn_abi_version": ctypes.c_int}
+RESTYPES = {"sn_gemm_debug_stats": None, "sn_attn_decode_workspace_bytes": ctypes.c_size_t, "sn_abi_version": ctypes.c_int}
 
 SN_F32, SN_BF16 = 0, 1
 SN_ATTN_FORCE_SIMT = 0x100

@@ -16,7 +16,7 @@ namespace sn {
 // (rotate, write q_out), the next Hkv are key heads (rotate, append to the cache),
 // the last Hkv are value heads (copy to the cache).  Thread i owns rotary pair i.
 template <typename T>
-__global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ row_seq,
+__global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __restrict__ row_seq,
                                       const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
                                       const float* __restrict__ inv_freq, T* __restrict__ q_out,
                                       T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
@@ -28,29 +28,29 @@ __global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* 
   if (i >= half) return;
   const int seq = row_seq ? row_seq[r] : r;
   const int pos = row_pos[r];
-  const T* src = qkv + (size_t)r * (Hq + 2 * Hkv) * D + (size_t)head * D;
+  const size_t src = (size_t)r * (Hq + 2 * Hkv) * D + (size_t)head * D;
   // cache slot (FA: the position; SWA: ring slot), SWA rows older than the window are not stored
   const int slot = window > 0 ? pos % window : pos;
   const bool write = !(window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window);
   if (head >= Hq + Hkv) {  // value head: plain copy
     const int hk = head - Hq - Hkv;
-    const T v1 = src[i], v2 = src[i + half];
+    const float v1 = qkv(src + i), v2 = qkv(src + i + half);
     if (v_out) {
       T* dst = v_out + ((size_t)r * Hkv + hk) * D;
-      dst[i] = v1;
-      dst[i + half] = v2;
+      io<T>::st(dst + i, v1);
+      io<T>::st(dst + i + half, v2);
     }
     if (write) {
       const int page = block_table[(size_t)seq * max_blocks + slot / page_size];
       T* dst = v_cache + (((size_t)page * Hkv + hk) * page_size + slot % page_size) * D;
-      dst[i] = v1;
-      dst[i + half] = v2;
+      io<T>::st(dst + i, v1);
+      io<T>::st(dst + i + half, v2);
     }
     return;
   }
   float sn, cs;
   sincosf((float)pos * inv_freq[i], &sn, &cs);
-  const float x1 = io<T>::ld(src + i), x2 = io<T>::ld(src + i + half);
+  const float x1 = qkv(src + i), x2 = qkv(src + i + half);
   const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
   if (head < Hq) {
     T* dst = q_out + ((size_t)r * Hq + head) * D;
@@ -232,7 +232,7 @@ using namespace sn;
 
 extern "C" {
 
-sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq, const int32_t* row_pos,
+sn_status sn_rope_kv_append(const void* qkv, int qkv_nsplit, const int32_t* row_seq, const int32_t* row_pos,
                             const int32_t* seq_lens, const float* inv_freq, void* q_out, void* k_out,
                             void* v_out, void* k_cache, void* v_cache, const int32_t* block_table, int rows,
                             int Hq, int Hkv, int D, int page_size, int max_blocks, int window, int dtype,
@@ -240,12 +240,14 @@ sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq, const int32
   SN_REQUIRE(rows > 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0 && D % 2 == 0, "sn_rope_kv_append: bad shape");
   SN_REQUIRE(page_size > 0 && (window == 0 || window % page_size == 0),
              "sn_rope_kv_append: window %d must be a multiple of page_size %d", window, page_size);
+  SN_REQUIRE(qkv_nsplit >= 0 && qkv_nsplit <= kMaxSplit, "sn_rope_kv_append: qkv_nsplit %d", qkv_nsplit);
   SN_REQUIRE(qkv && row_pos && inv_freq && q_out && k_cache && v_cache && block_table,
              "sn_rope_kv_append: NULL pointer argument");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(rows, Hq + 2 * Hkv);
+    const GemmIn<T> in{qkv, qkv_nsplit, (size_t)rows * (Hq + 2 * Hkv) * D};
     rope_kv_append_kernel<T><<<grid, ((D / 2 + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(
-        (const T*)qkv, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache,
+        in, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache,
         (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
     return check_launch("sn_rope_kv_append");
   });

@@ -31,6 +31,7 @@ namespace sn {
 struct DeltaDecodeArgs {
   const void* proj;
   int proj_stride;
+  int proj_nsplit;  // 0: T rows; >0: fp32 split-K slabs [nsplit][B][proj_stride]
   void* conv_ring;
   const void* conv_w;
   float* state;
@@ -41,6 +42,7 @@ struct DeltaDecodeArgs {
   const void* f2_w;
   const void* g2_w;
   const void* g2_b;
+  const void* fg;     // KDA: optional precomputed [2][B][H*D] = (f1 @ f2^T, g1 @ g2^T); then f2/g2 unused
   const void* norm_w;
   void* out;
   int Hk, Hv, rank, W, conv_channels;
@@ -67,6 +69,32 @@ template <> struct vecf<2> {
     *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
   }
 };
+
+template <typename T> __device__ __forceinline__ void load4(const T* p, float* f);
+template <> __device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* p, float* f) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+template <> __device__ __forceinline__ void load4<float>(const float* p, float* f) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+}
+
+// Two block-wide sums in one pass (scratch: 2 * blockDim.x/32 floats).
+__device__ __forceinline__ void block_sum2(float& x, float& y, float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  x = warp_sum(x);
+  y = warp_sum(y);
+  __syncthreads();
+  if (lane == 0) { scratch[warp] = x; scratch[nw + warp] = y; }
+  __syncthreads();
+  float tx = 0.f, ty = 0.f;
+  for (int i = 0; i < nw; ++i) { tx += scratch[i]; ty += scratch[nw + i]; }
+  x = tx;
+  y = ty;
+}
 
 // Dot of a T row (len R, 16B aligned) with an fp32 smem vector.
 template <typename T>
@@ -100,7 +128,7 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
   __shared__ __align__(16) float s_o[D];
   __shared__ __align__(16) float s_f1[KDA ? 256 : 1];
   __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
-  __shared__ float s_red[NW];
+  __shared__ float s_red[2 * NW];
   __shared__ float s_beta;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -118,64 +146,116 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pos = a.positions[b];
   const int W = a.W;
-  const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
+  const GemmIn<T> pin{a.proj, a.proj_nsplit, (size_t)gridDim.y * a.proj_stride};
+  const size_t prow = (size_t)b * a.proj_stride;
   T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * W;
   const T* cw = reinterpret_cast<const T*>(a.conv_w);
 
-  // ---- 1. causal conv update + SiLU for q (key head), k (key head), v (this head)
-  for (int c = tid; c < 3 * D; c += kDecodeThreads) {
-    const int part = c / D, i = c - part * D;
-    const int ch = part == 0 ? a.q_off + kh * D + i : (part == 1 ? a.k_off + kh * D + i : a.v_off + h * D + i);
-    const float x = io<T>::ld(prow + ch);
-    const T* wrow = cw + (size_t)ch * W;
-    T* rrow = ring + (size_t)ch * W;
-    float acc = io<T>::ld(wrow + W - 1) * x;
-    for (int d = 1; d < W; ++d) {
-      const int p = pos - d;
-      if (p >= 0) acc += io<T>::ld(wrow + W - 1 - d) * io<T>::ld(rrow + (p % W));
-    }
-    const float y = silu_f(acc);
-    if (part == 2 || (h % G) == 0) io<T>::st(rrow + (pos % W), x);
-    (part == 0 ? s_q : part == 1 ? s_k : s_v)[i] = y;
-  }
-  if (KDA) {
-    for (int r = tid; r < a.rank; r += kDecodeThreads) {
-      s_f1[r] = io<T>::ld(prow + a.f1_off + r);
-      s_g1[r] = io<T>::ld(prow + a.g1_off + r);
-    }
-  }
-  __syncthreads();
-
-  // ---- 2. L2 norms, gates, beta
-  float qq = 0.f, kk = 0.f;
-  for (int i = tid; i < D; i += kDecodeThreads) { qq += s_q[i] * s_q[i]; kk += s_k[i] * s_k[i]; }
-  qq = block_sum(qq, s_red);
-  kk = block_sum(kk, s_red);
-  const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
-  const float negA = -expf(a.A_log[h]);
-  if (!KDA) {
-    const float graw = io<T>::ld(prow + a.a_off + h) + a.dt_bias[h];
-    const float eg = expf(negA * softplus_f(graw));
-    for (int i = tid; i < D; i += kDecodeThreads) {
-      s_eg[i] = eg;
-      s_gate[i] = io<T>::ld(prow + a.z_off + h * D + i);
-    }
-  } else {
-    const T* f2 = reinterpret_cast<const T*>(a.f2_w);
-    const T* g2 = reinterpret_cast<const T*>(a.g2_w);
-    const T* g2b = reinterpret_cast<const T*>(a.g2_b);
-    for (int c = tid; c < 2 * D; c += kDecodeThreads) {
-      const int i = c % D;
-      const int row = h * D + i;
-      if (c < D) {
-        const float f = row_dot<T>(f2 + (size_t)row * a.rank, s_f1, a.rank);
-        s_eg[i] = expf(negA * softplus_f(f + a.dt_bias[row]));
-      } else {
-        s_gate[i] = row_dot<T>(g2 + (size_t)row * a.rank, s_g1, a.rank) + io<T>::ld(g2b + row);
+  // ---- 1. prologue loads, all issued before any is consumed (one memory round trip):
+  //      the <=2 conv channels of this thread (proj value, 4 taps, 4 ring slots),
+  //      the output gate z (GDN) / low-rank gate inputs f1,g1 (KDA), a, b.
+  constexpr int NCH = (3 * D + kDecodeThreads - 1) / kDecodeThreads;
+  float xin[NCH], wt[NCH][4], rg[NCH][4];
+  int chn[NCH];
+#pragma unroll
+  for (int u = 0; u < NCH; ++u) {
+    const int c = tid + u * kDecodeThreads;
+    chn[u] = -1;
+    if (c < 3 * D) {
+      const int part = c / D, i = c - part * D;
+      const int ch = part == 0 ? a.q_off + kh * D + i : (part == 1 ? a.k_off + kh * D + i : a.v_off + h * D + i);
+      chn[u] = ch;
+      xin[u] = pin(prow + ch);
+      if (W == 4) {
+        load4<T>(cw + (size_t)ch * 4, wt[u]);
+        load4<T>(ring + (size_t)ch * 4, rg[u]);
       }
     }
   }
-  if (tid == 0) s_beta = sigmoid_f(io<T>::ld(prow + a.b_off + h));
+  float zval = 0.f;
+  if (!KDA && tid < D) zval = pin(prow + a.z_off + h * D + tid);
+  float fg = 0.f, fpre = 0.f, gpre = 0.f;
+  const bool have_fg = KDA && a.fg != nullptr;
+  if (KDA && !have_fg && tid < 2 * a.rank) fg = pin(prow + (tid < a.rank ? a.f1_off + tid : a.g1_off + tid - a.rank));
+  if (have_fg && tid < D) {
+    const size_t HD = (size_t)a.Hv * D;
+    const T* fgp = reinterpret_cast<const T*>(a.fg) + (size_t)b * HD + h * D + tid;
+    fpre = io<T>::ld(fgp) + a.dt_bias[h * D + tid];
+    gpre = io<T>::ld(fgp + gridDim.y * HD) + io<T>::ld(reinterpret_cast<const T*>(a.g2_b) + h * D + tid);
+  }
+  const float braw = pin(prow + a.b_off + h);
+  const float graw = KDA ? 0.f : pin(prow + a.a_off + h) + a.dt_bias[h];
+  const float negA = -expf(a.A_log[h]);
+
+  // ---- 2. conv + SiLU (slot p % W of the ring holds the input of position p)
+#pragma unroll
+  for (int u = 0; u < NCH; ++u) {
+    if (chn[u] < 0) continue;
+    const int c = tid + u * kDecodeThreads;
+    const int part = c / D, i = c - part * D;
+    const int ch = chn[u];
+    float acc;
+    if (W == 4) {
+      acc = wt[u][3] * xin[u];
+#pragma unroll
+      for (int d = 1; d < 4; ++d)
+        if (pos - d >= 0) acc += wt[u][3 - d] * rg[u][(pos - d) & 3];
+    } else {
+      const T* wrow = cw + (size_t)ch * W;
+      const T* rrow = ring + (size_t)ch * W;
+      acc = io<T>::ld(wrow + W - 1) * xin[u];
+      for (int d = 1; d < W; ++d) {
+        const int p = pos - d;
+        if (p >= 0) acc += io<T>::ld(wrow + W - 1 - d) * io<T>::ld(rrow + (p % W));
+      }
+    }
+    if (part == 2 || (h % G) == 0) io<T>::st(ring + (size_t)ch * W + (pos % W), xin[u]);
+    (part == 0 ? s_q : part == 1 ? s_k : s_v)[i] = silu_f(acc);
+  }
+  if (KDA && !have_fg && tid < 2 * a.rank) (tid < a.rank ? s_f1[tid] : s_g1[tid - a.rank]) = fg;
+  if (have_fg && tid < D) {
+    s_eg[tid] = expf(negA * softplus_f(fpre));
+    s_gate[tid] = gpre;
+  }
+  if (!KDA && tid < D) s_gate[tid] = zval;
+  __syncthreads();
+
+  // ---- 3. L2 norms (one two-value block reduction), gates, beta
+  float qq = 0.f, kk = 0.f;
+  for (int i = tid; i < D; i += kDecodeThreads) { qq += s_q[i] * s_q[i]; kk += s_k[i] * s_k[i]; }
+  block_sum2(qq, kk, s_red);
+  const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
+  if (!KDA) {
+    const float eg = expf(negA * softplus_f(graw));
+    for (int i = tid; i < D; i += kDecodeThreads) s_eg[i] = eg;
+  } else if (!have_fg) {
+    // second low-rank factors: rows h*D .. h*D+D-1 of f2 (-> gate g) and g2 (-> output gate),
+    // half a warp per row (16 lanes x 16 B = one 256-B row when R = 128), coalesced
+    const T* f2 = reinterpret_cast<const T*>(a.f2_w);
+    const T* g2 = reinterpret_cast<const T*>(a.g2_w);
+    const T* g2b = reinterpret_cast<const T*>(a.g2_b);
+    const int half = lane >> 4, hl = lane & 15;
+    for (int rr = warp * 2 + half; rr < 2 * D; rr += 2 * (kDecodeThreads / 32)) {
+      const bool is_f = rr < D;
+      const int i = is_f ? rr : rr - D;
+      const T* row = (is_f ? f2 : g2) + (size_t)(h * D + i) * a.rank;
+      const float* vec = is_f ? s_f1 : s_g1;
+      float acc = 0.f;
+      for (int r0 = hl * 8; r0 < a.rank; r0 += 128) {
+        float wv[8];
+        load8<T>(row + r0, wv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += wv[k] * vec[r0 + k];
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (hl == 0) {
+        if (is_f) s_eg[i] = expf(negA * softplus_f(acc + a.dt_bias[h * D + i]));
+        else s_gate[i] = acc + io<T>::ld(g2b + h * D + i);
+      }
+    }
+  }
+  if (tid == 0) s_beta = sigmoid_f(braw);
   __syncthreads();
   float qk = 0.f;
   for (int i = tid; i < D; i += kDecodeThreads) {
@@ -458,7 +538,7 @@ static void launch_scan(dim3 grid, cudaStream_t st, const float* qn, const float
 
 extern "C" {
 
-sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring, const void* conv_w, float* state,
+sn_status sn_gdn_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring, const void* conv_w, float* state,
                         const int32_t* slot_idx, const int32_t* positions, const float* A_log,
                         const float* dt_bias, const void* norm_w, void* out, int B, int Hk, int Hv, int D,
                         int conv_width, float scale, float eps_l2, float eps_norm, int dtype, void* stream) {
@@ -467,7 +547,8 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring, cons
   SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && norm_w && out,
              "sn_gdn_decode: NULL pointer argument");
   DeltaDecodeArgs a{};
-  a.proj = proj; a.proj_stride = proj_stride; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
+  SN_REQUIRE(proj_nsplit >= 0 && proj_nsplit <= kMaxSplit, "delta decode: proj_nsplit %d", proj_nsplit);
+  a.proj = proj; a.proj_stride = proj_stride; a.proj_nsplit = proj_nsplit; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
   a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.norm_w = norm_w;
   a.out = out; a.Hk = Hk; a.Hv = Hv; a.rank = 0; a.W = conv_width;
   a.conv_channels = 2 * Hk * D + Hv * D;
@@ -478,21 +559,22 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring, cons
   return launch_delta_decode<false>(a, B, D, dtype, (cudaStream_t)stream);
 }
 
-sn_status sn_kda_decode(const void* proj, int proj_stride, void* conv_ring, const void* conv_w, float* state,
+sn_status sn_kda_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring, const void* conv_w, float* state,
                         const int32_t* slot_idx, const int32_t* positions, const float* A_log,
                         const float* dt_bias, const void* f2_w, const void* g2_w, const void* g2_b,
-                        const void* norm_w, void* out, int B, int H, int D, int rank, int conv_width, float scale,
-                        float eps_l2, float eps_norm, int dtype, void* stream) {
+                        const void* fg, const void* norm_w, void* out, int B, int H, int D, int rank, int conv_width,
+                        float scale, float eps_l2, float eps_norm, int dtype, void* stream) {
   SN_REQUIRE(B > 0 && H > 0, "sn_kda_decode: bad shape B=%d H=%d", B, H);
   SN_REQUIRE(rank > 0 && rank <= 256 && rank % 8 == 0, "sn_kda_decode: rank %d must be a multiple of 8 <= 256", rank);
   SN_REQUIRE(conv_width >= 1 && conv_width <= 8, "sn_kda_decode: conv width %d not in [1,8]", conv_width);
-  SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && f2_w && g2_w && g2_b &&
-                 norm_w && out,
+  SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && norm_w && out && g2_b &&
+                 (fg || (f2_w && g2_w)),
              "sn_kda_decode: NULL pointer argument");
   DeltaDecodeArgs a{};
-  a.proj = proj; a.proj_stride = proj_stride; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
+  SN_REQUIRE(proj_nsplit >= 0 && proj_nsplit <= kMaxSplit, "delta decode: proj_nsplit %d", proj_nsplit);
+  a.proj = proj; a.proj_stride = proj_stride; a.proj_nsplit = proj_nsplit; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
   a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.f2_w = f2_w;
-  a.g2_w = g2_w; a.g2_b = g2_b; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank;
+  a.g2_w = g2_w; a.g2_b = g2_b; a.fg = fg; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank;
   a.W = conv_width; a.conv_channels = 3 * H * D;
   a.q_off = 0; a.k_off = H * D; a.v_off = 2 * H * D; a.f1_off = 3 * H * D; a.g1_off = 3 * H * D + rank;
   a.b_off = 3 * H * D + 2 * rank;

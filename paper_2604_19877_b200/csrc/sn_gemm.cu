@@ -71,6 +71,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -128,6 +151,10 @@ struct GemmArgs {
   int br;          // weight rows per block (multiple of 8, <= BM)
   int nblocks;     // ceil(N / br)
   int splits;      // K splits per block (PARTIAL mode only, else 1)
+  int cs;          // CTAs per cluster sharing (multicasting) each activation tile
+  unsigned long long* stats;  // optional per-CTA cycle counters (profiling; NULL in production)
+  int row_mul;     // weight rows per block: BR (one A tile or SwiGLU pair) or 2*BR (two stacked tiles)
+  int a2_base;     // row offset of the second A tile inside a block: N (SwiGLU: up rows) or BR
   int ns;          // pipeline stages (runtime: as many as fit, so small blocks keep W in flight)
   int stage_bytes; // NA * br * 128 + BN * 128 (1024-aligned)
 };
@@ -154,12 +181,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x, c = blockIdx.x;
-  const int BR = g.br, S = g.splits;
+  const int BR = g.br, S = g.splits, CS = g.cs;
   const int KB = g.kblocks / S;  // k-blocks per item (the host makes splits divide kblocks)
-  const int items = g.nblocks * S;
-  const int my_blocks = items > c ? (items - c + G - 1) / G : 0;  // work items c, c+G, c+2G, ...
+  // CS CTAs of a cluster take CS adjacent row blocks of the same K split in lockstep and
+  // multicast the shared activation tile (each loads BN/CS rows of it for everyone).
+  // Work group j = (block group j / S, split j % S); cluster q takes groups q, q+Q, ...
+  const int rank = CS > 1 ? (int)cluster_ctarank() : 0;
+  const int q = blockIdx.x / CS, Q = gridDim.x / CS;
+  const int groups = ((g.nblocks + CS - 1) / CS) * S;
+  const int my_blocks = groups > q ? (groups - q + Q - 1) / Q : 0;
   const int my_units = my_blocks * KB;
+  const uint16_t cmask = (uint16_t)((1u << CS) - 1);
+  const int xrows = BN / CS;
+  const uint32_t x_bytes_own = (uint32_t)xrows * BK * 2;
   const uint32_t a_bytes = (uint32_t)BR * BK * 2;  // one A tile: BR rows (the UMMA reads 128; extra rows ignored)
   const int NS = g.ns, STAGE = g.stage_bytes;
   const int A_BYTES = (int)a_bytes;
@@ -168,7 +202,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-    for (int i = 0; i < NS; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], CS); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -180,6 +214,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers' barriers exist before anyone multicasts into them
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
 
@@ -190,33 +225,56 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // X half, so a stage can never complete on its W bytes alone.
       const uint64_t pw = policy_evict_first(), px = policy_evict_last();
       const int npre = min(NS, my_units);
+      auto unit = [&](int i, int& blk, int& kc) {
+        const int j = q + (i / KB) * Q;
+        blk = (j / S) * CS + rank;
+        kc = ((j % S) * KB + i % KB) * BK;
+      };
       for (int i = 0; i < npre; ++i) {
-        const int item = c + (i / KB) * G, blk = item / S, kc = ((item % S) * KB + i % KB) * BK;
+        int blk, kc;
+        unit(i, blk, kc);
         uint8_t* st = smem + i * STAGE;
         mbar_expect_tx_noarrive(&full_bar[i], NA * a_bytes);
-        tma_load_2d(st, &wmap, kc, blk * BR, &full_bar[i], pw);
-        if (NA == 2) tma_load_2d(st + A_BYTES, &wmap, kc, g.N + blk * BR, &full_bar[i], pw);
+        tma_load_2d(st, &wmap, kc, blk * g.row_mul, &full_bar[i], pw);
+        if (NA == 2) tma_load_2d(st + A_BYTES, &wmap, kc, blk * g.row_mul + g.a2_base, &full_bar[i], pw);
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      auto load_x = [&](int i, int s) {
+        int blk, kc;
+        unit(i, blk, kc);
+        uint8_t* xs = smem + s * STAGE + NA * A_BYTES;
+        if (CS > 1)
+          tma_load_2d_mc(xs + rank * x_bytes_own, &xmap, kc, rank * xrows, &full_bar[s], cmask, px);
+        else
+          tma_load_2d(xs, &xmap, kc, 0, &full_bar[s], px);
+      };
       for (int i = 0; i < npre; ++i) {
-        const int item = c + (i / KB) * G, kc = ((item % S) * KB + i % KB) * BK;
-        mbar_expect_tx(&full_bar[i], B_BYTES);
-        tma_load_2d(smem + i * STAGE + NA * A_BYTES, &xmap, kc, 0, &full_bar[i], px);
+        mbar_expect_tx(&full_bar[i], B_BYTES);  // the whole tile: own part + the peers' multicasts
+        load_x(i, i);
       }
+      long long t_wait = 0, t_begin = clock64();
       for (int i = npre; i < my_units; ++i) {
         const int s = i % NS, r = i / NS;
-        mbar_wait(&empty_bar[s], (r - 1) & 1);
+        long long t0 = clock64();
+        mbar_wait(&empty_bar[s], (r - 1) & 1);  // consumed by every CTA of the cluster
+        t_wait += clock64() - t0;
         uint8_t* st = smem + s * STAGE;
         mbar_expect_tx(&full_bar[s], NA * a_bytes + B_BYTES);
-        const int item = c + (i / KB) * G, blk = item / S, kc = ((item % S) * KB + i % KB) * BK;
-        tma_load_2d(st, &wmap, kc, blk * BR, &full_bar[s], pw);
-        if (NA == 2) tma_load_2d(st + A_BYTES, &wmap, kc, g.N + blk * BR, &full_bar[s], pw);
-        tma_load_2d(st + NA * A_BYTES, &xmap, kc, 0, &full_bar[s], px);
+        int blk, kc;
+        unit(i, blk, kc);
+        tma_load_2d(st, &wmap, kc, blk * g.row_mul, &full_bar[s], pw);
+        if (NA == 2) tma_load_2d(st + A_BYTES, &wmap, kc, blk * g.row_mul + g.a2_base, &full_bar[s], pw);
+        load_x(i, s);
+      }
+      if (g.stats) {
+        g.stats[blockIdx.x * 4 + 0] = t_wait;
+        g.stats[blockIdx.x * 4 + 1] = clock64() - t_begin;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      long long m_wait = 0, m_begin = clock64();
       for (int blk_i = 0, i = 0; blk_i < my_blocks; ++blk_i) {
         const int buf = blk_i & 1;
         if (blk_i >= 2) mbar_wait(&tempty_bar[buf], ((blk_i >> 1) - 1) & 1);
@@ -224,7 +282,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t acc = tmem + buf * ACC;
         for (int kb = 0; kb < KB; ++kb, ++i) {
           const int s = i % NS, r = i / NS;
+          long long t0 = clock64();
           mbar_wait(&full_bar[s], r & 1);
+          m_wait += clock64() - t0;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + NA * A_BYTES;
@@ -235,9 +295,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             umma(acc, desc_sw128(sa + k * 32), bdesc, idesc, accum);
             if (NA == 2) umma(acc + BN, desc_sw128(sa + A_BYTES + k * 32), bdesc, idesc, accum);
           }
-          umma_commit(&empty_bar[s]);
+          if (CS > 1) umma_commit_mc(&empty_bar[s], cmask);  // frees the slot in every CTA of the cluster
+          else umma_commit(&empty_bar[s]);
         }
         umma_commit(&tfull_bar[buf]);
+      }
+      if (g.stats) {
+        g.stats[blockIdx.x * 4 + 2] = m_wait;
+        g.stats[blockIdx.x * 4 + 3] = clock64() - m_begin;
       }
     }
   } else if (warp >= 4) {
@@ -248,41 +313,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int mode = g.mode;
     for (int blk_i = 0; blk_i < my_blocks; ++blk_i) {
       const int buf = blk_i & 1;
-      const int item = c + blk_i * G;
-      const int n = (item / S) * BR + t;
-      const bool row_ok = t < BR && n < g.N;
+      const int j = q + blk_i * Q;
+      const int item_split = j % S;
+      const int blk = (j / S) * CS + rank;
+      const int n = blk * g.row_mul + t;                       // row of accumulator 0
+      const int n2 = blk * g.row_mul + g.a2_base + t;          // row of accumulator 1 (paired tiles)
+      const bool swiglu = mode == SN_GEMM_SWIGLU;
       mbar_wait(&tfull_bar[buf], (blk_i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t acc = tmem + lane_off + buf * ACC;
+      // store 16 batch columns [col, col+16) of one output row
+      auto emit = [&](int row, int col, const float* v) {
+        if (t >= BR || row >= g.N) return;
+        if (mode == SN_GEMM_PARTIAL) {
+          float* o = reinterpret_cast<float*>(g.out) + (size_t)item_split * g.M * g.ldo + row;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (col + jj < g.M) __stcg(o + (size_t)(col + jj) * g.ldo, v[jj]);
+        } else if (mode == SN_GEMM_RESID) {
+          float* o = reinterpret_cast<float*>(g.out) + row;
+          float old[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) old[jj] = (col + jj < g.M) ? __ldcg(o + (size_t)(col + jj) * g.ldo) : 0.f;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (col + jj < g.M) o[(size_t)(col + jj) * g.ldo] = old[jj] + v[jj];
+        } else {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + row;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            if (col + jj < g.M) o[(size_t)(col + jj) * g.ldo] = __float2bfloat16_rn(v[jj]);
+        }
+      };
 #pragma unroll 1
       for (int col = 0; col < BN; col += 16) {
-        float v[16], w2[16], old[16];
-        if (mode == SN_GEMM_RESID && row_ok) {
-          const float* o = reinterpret_cast<const float*>(g.out) + n;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) old[j] = (col + j < g.M) ? __ldcg(o + (size_t)(col + j) * g.ldo) : 0.f;
-        }
+        float v[16], w2[16];
         tmem_ld16(acc + col, v);
         if (NA == 2) tmem_ld16(acc + BN + col, w2);
-        if (row_ok) {
-          if (mode == SN_GEMM_PARTIAL) {
-            float* o = reinterpret_cast<float*>(g.out) + (size_t)(item % S) * g.M * g.ldo + n;
+        if (NA == 2 && swiglu) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (col + j < g.M) __stcg(o + (size_t)(col + j) * g.ldo, v[j]);
-          } else if (mode == SN_GEMM_RESID) {
-            float* o = reinterpret_cast<float*>(g.out) + n;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (col + j < g.M) o[(size_t)(col + j) * g.ldo] = old[j] + v[j];
-          } else {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + n;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (col + j < g.M)
-                o[(size_t)(col + j) * g.ldo] =
-                    __float2bfloat16_rn(mode == SN_GEMM_SWIGLU ? silu_f(v[j]) * w2[j] : v[j]);
-          }
+          for (int jj = 0; jj < 16; ++jj) v[jj] = silu_f(v[jj]) * w2[jj];
+          emit(n, col, v);
+        } else {
+          emit(n, col, v);
+          if (NA == 2) emit(n2, col, w2);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -292,6 +366,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 // ------------------------------------------------------------------ host
@@ -340,13 +415,26 @@ static int num_sms() {
 // BR >= 48 keeps >= 1.5 KB of W per UMMA (tcgen05.mma issues at ~45 cycles minimum,
 // measured), split-K (PARTIAL mode only: the consumer sums the slabs) lets a narrow N
 // fill the SMs with tall blocks.  Ties -> fewer splits, then taller blocks.
+static unsigned long long* g_stats = nullptr;  // sn_gemm_debug_stats(): profiling only
+static int g_cluster = -1;  // CTAs per multicast cluster (env SN_GEMM_CLUSTER, default 2)
+
+static int cluster_size() {
+  if (g_cluster < 0) {
+    const char* e = getenv("SN_GEMM_CLUSTER");
+    g_cluster = e ? atoi(e) : 1;
+    if (g_cluster != 1 && g_cluster != 2 && g_cluster != 4) g_cluster = 2;
+  }
+  return g_cluster;
+}
+
 static void pick_tiling(int N, int kblocks, int sms, int na, int bn, int max_splits, int* br_out,
                         int* splits_out) {
   long best_cost = -1;
+  const int cs = cluster_size();
   for (int s = 1; s <= max_splits; ++s) {
     if (kblocks % s) continue;
     for (int br = BM; br >= 48; br -= 8) {
-      const long items = (long)((N + br - 1) / br) * s;
+      const long items = (long)((N + br * cs - 1) / (br * cs)) * cs * s;
       const long waves = (items + sms - 1) / sms;
       const long cost = waves * (kblocks / s) * (long)(na * br + bn);
       if (best_cost < 0 || cost < best_cost) { best_cost = cost; *br_out = br; *splits_out = s; }
@@ -376,17 +464,50 @@ static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, GemmArgs g
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the producer's tail
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = g.cs;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_decode_kernel<BN, NA>, wm, xm, g);
   if (e != cudaSuccess) {
     set_error("sn_gemm_decode launch: %s", cudaGetErrorString(e));
     return SN_ECUDA;
   }
   return check_launch("sn_gemm_decode");
+}
+
+struct Plan {
+  int bn, br, splits, na, row_mul, nblocks, cs, grid;
+  bool swiglu, pair;
+};
+
+// Tiling plan: two 128-row A tiles per stage whenever N allows (SwiGLU gate+up, or two
+// stacked row blocks) so each activation tile feeds 256 weight rows (smem traffic per W
+// byte 2.5 instead of 3), block height / split-K from pick_tiling, multicast cluster size.
+static Plan make_plan(int M, int N, int K, int mode) {
+  Plan p{};
+  static int pair_env = getenv("SN_GEMM_PAIR") ? atoi(getenv("SN_GEMM_PAIR")) : 1;
+  const int sms = num_sms();
+  p.bn = batch_tile(M);
+  p.swiglu = mode == SN_GEMM_SWIGLU;
+  p.pair = !p.swiglu && pair_env && N >= 2 * BM;
+  p.na = (p.swiglu || p.pair) ? 2 : 1;
+  p.br = BM;
+  p.splits = 1;
+  pick_tiling(p.pair ? (N + 1) / 2 : N, K / BK, sms, p.na, p.bn, mode == SN_GEMM_PARTIAL ? 8 : 1, &p.br, &p.splits);
+  p.row_mul = p.pair ? 2 * p.br : p.br;
+  p.nblocks = (N + p.row_mul - 1) / p.row_mul;
+  p.cs = cluster_size();
+  if (p.nblocks < p.cs || p.bn / p.cs < 8) p.cs = 1;
+  const int groups = ((p.nblocks + p.cs - 1) / p.cs) * p.splits;
+  const int clusters = groups < sms / p.cs ? groups : sms / p.cs;
+  p.grid = clusters * p.cs;
+  return p;
 }
 
 }  // namespace gemm
@@ -397,11 +518,13 @@ using namespace sn::gemm;
 
 extern "C" {
 
+// Profiling aid: later launches write per-CTA clock64 counters [producer empty-wait, producer
+// total, MMA full-wait, MMA total] into dev_stats (4 x #SMs u64); NULL disables.
+void sn_gemm_debug_stats(unsigned long long* dev_stats) { g_stats = dev_stats; }
+
 int sn_gemm_decode_splits(int M, int N, int K, int mode) {
-  int br = BM, splits = 1;
-  if (mode != SN_GEMM_PARTIAL || K % BK) return 1;
-  pick_tiling(N, K / BK, num_sms(), 1, batch_tile(M), 8, &br, &splits);
-  return splits;
+  if (K % BK || mode != SN_GEMM_PARTIAL) return 1;
+  return make_plan(M, N, K, mode).splits;
 }
 
 sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw, void* out, int ldo,
@@ -414,35 +537,30 @@ sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, in
              "sn_gemm_decode: mode %d", mode);
   SN_REQUIRE(((uintptr_t)x % 16) == 0 && ((uintptr_t)w % 16) == 0 && (ldx % 8) == 0 && (ldw % 8) == 0,
              "sn_gemm_decode: operands must be 16-byte aligned");
-  const int BN = batch_tile(M);
-  const int sms = num_sms();
-  int br = BM, splits = 1;
-  pick_tiling(N, K / BK, sms, mode == SN_GEMM_SWIGLU ? 2 : 1, BN, mode == SN_GEMM_PARTIAL ? 8 : 1, &br, &splits);
+  const Plan pl = make_plan(M, N, K, mode);
   CUtensorMap wm, xm;
-  const uint64_t wrows = mode == SN_GEMM_SWIGLU ? 2ull * N : (uint64_t)N;
-  if (!map_2d(&wm, w, wrows, K, ldw, br) || !map_2d(&xm, x, M, K, ldx, BN)) {
+  const uint64_t wrows = pl.swiglu ? 2ull * N : (uint64_t)N;
+  if (!map_2d(&wm, w, wrows, K, ldw, pl.br) || !map_2d(&xm, x, M, K, ldx, pl.bn / pl.cs)) {
     set_error("sn_gemm_decode: cuTensorMapEncodeTiled failed");
     return SN_ECUDA;
   }
-  const int nblocks = (N + br - 1) / br;
-  const int items = nblocks * splits;
-  const int grid = items < sms ? items : sms;
-  if (splits_out) *splits_out = splits;
-  GemmArgs g{out, M, N, K, ldo, mode, K / BK, br, nblocks, splits, 0, 0};
+  if (splits_out) *splits_out = pl.splits;
+  GemmArgs g{out, M, N, K, ldo, mode, K / BK, pl.br, pl.nblocks, pl.splits, pl.cs, g_stats, pl.row_mul,
+             pl.swiglu ? N : pl.br, 0, 0};
   cudaStream_t st = (cudaStream_t)stream;
-  if (mode == SN_GEMM_SWIGLU) {
-    switch (BN) {
-      case 16: return launch<16, 2>(wm, xm, g, grid, st);
-      case 32: return launch<32, 2>(wm, xm, g, grid, st);
-      case 64: return launch<64, 2>(wm, xm, g, grid, st);
-      default: return launch<128, 2>(wm, xm, g, grid, st);
+  if (pl.na == 2) {
+    switch (pl.bn) {
+      case 16: return launch<16, 2>(wm, xm, g, pl.grid, st);
+      case 32: return launch<32, 2>(wm, xm, g, pl.grid, st);
+      case 64: return launch<64, 2>(wm, xm, g, pl.grid, st);
+      default: return launch<128, 2>(wm, xm, g, pl.grid, st);
     }
   }
-  switch (BN) {
-    case 16: return launch<16, 1>(wm, xm, g, grid, st);
-    case 32: return launch<32, 1>(wm, xm, g, grid, st);
-    case 64: return launch<64, 1>(wm, xm, g, grid, st);
-    default: return launch<128, 1>(wm, xm, g, grid, st);
+  switch (pl.bn) {
+    case 16: return launch<16, 1>(wm, xm, g, pl.grid, st);
+    case 32: return launch<32, 1>(wm, xm, g, pl.grid, st);
+    case 64: return launch<64, 1>(wm, xm, g, pl.grid, st);
+    default: return launch<128, 1>(wm, xm, g, pl.grid, st);
   }
 }
 

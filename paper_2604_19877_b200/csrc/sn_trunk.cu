@@ -132,18 +132,13 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const T* __restrict__ 
 
 // ------------------------------------------------------------------ silu * mul
 template <typename T>
-__global__ void silu_mul_kernel(const T* __restrict__ gu, T* __restrict__ out, int rows, int ffn) {
+__global__ void silu_mul_kernel(const GemmIn<T> gu, T* __restrict__ out, int rows, int ffn) {
   sn::pdl_launch_dependents();
-  const size_t n8 = (size_t)rows * ffn / 8;
-  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n8;
-       q += (size_t)gridDim.x * blockDim.x) {
-    const size_t e = q * 8;
+  const size_t n = (size_t)rows * ffn;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     const size_t r = e / ffn, i = e % ffn;
-    float g[8], u[8];
-    load8<T>(gu + r * 2 * ffn + i, g);
-    load8<T>(gu + r * 2 * ffn + ffn + i, u);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) io<T>::st(out + r * ffn + i + k, silu_f(g[k]) * u[k]);
+    const float g = gu(r * 2 * ffn + i), u = gu(r * 2 * ffn + ffn + i);
+    io<T>::st(out + e, silu_f(g) * u);
   }
 }
 
@@ -233,13 +228,15 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit, f
   });
 }
 
-sn_status sn_silu_mul(const void* gate_up, void* out, int rows, int ffn, int dtype, void* stream) {
+sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, int ffn, int dtype, void* stream) {
+  SN_REQUIRE(gu_nsplit >= 0 && gu_nsplit <= kMaxSplit, "sn_silu_mul: gu_nsplit %d", gu_nsplit);
   SN_REQUIRE(rows > 0 && ffn > 0 && ffn % 8 == 0, "sn_silu_mul: bad shape rows=%d ffn=%d", rows, ffn);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    const size_t n8 = (size_t)rows * ffn / 8;
-    int grid = (int)((n8 + 255) / 256);
+    const size_t n = (size_t)rows * ffn;
+    int grid = (int)((n + 255) / 256);
     if (grid > 148 * 16) grid = 148 * 16;
-    silu_mul_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>((const T*)gate_up, (T*)out, rows, ffn);
+    const GemmIn<T> in{gate_up, gu_nsplit, (size_t)rows * 2 * ffn};
+    silu_mul_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(in, (T*)out, rows, ffn);
     return check_launch("sn_silu_mul");
   });
 }

@@ -81,15 +81,22 @@ class Supernet:
         self._alloc_decode_buffers()
         self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
         self.force_simt = False
-        # Which decode projections run on the tcgen05 weight-streaming GEMM (libsn100) and which
-        # on cuBLAS.  Chosen per shape from B200 measurements at B=64 (tools/bench_gemm.py,
-        # profiles/): ours wins for the LM head and the split-K FFN down-projection (its
-        # partial slabs are summed inside the next add_rmsnorm, removing cuBLAS's split-K
-        # reduce kernel); cuBLAS is still faster on the 42-130 MB in/out projections and the
-        # gate/up GEMM.  fp32 I/O (the 1e-4 parity mode) always uses cuBLAS fp32.
+        # bf16 decode projections run either on the tcgen05 weight-streaming GEMM (libsn100:
+        # stacked 256-row tiles, split-K over all SMs, fp32 slabs summed by the consuming
+        # kernel — rope / GDN / KDA decode / silu_mul / add_rmsnorm — so there is no reduction
+        # kernel) or on cuBLAS.  Default from in-step B200 measurements (tools/step_breakdown.py):
+        # ours for the LM head and the FFN down-projection, where it is faster; cuBLAS for the
+        # rest (SN_DECODE_GEMMS=all switches everything to ours).  fp32 I/O uses cuBLAS fp32.
         tc_ok = dtype == torch.bfloat16 and batch <= 128
-        self.sn_gemm = {"lm_head": tc_ok, "ffn_down": tc_ok, "ffn_gate_up": False, "in_proj": False,
-                        "out_proj": False}
+        import os
+        sel = os.environ.get("SN_DECODE_GEMMS", "lm_head,ffn_down").split(",")
+        self.sn_gemm = {r: tc_ok and (r in sel or "all" in sel)
+                        for r in ("lm_head", "ffn_down", "ffn_gate_up", "in_proj", "out_proj")}
+        if tc_ok:  # fp32 split-K slabs of the input-side projections, summed by their consumers
+            n_in = max([cfg.attn_qkv_width if k in (FA, SWA) else cfg.gdn_in_width if k == GDN else cfg.kda_in_width
+                        for k in self.kinds])
+            self.slab_in = torch.empty(8, batch, n_in, device=self.device, dtype=torch.float32)
+            self.slab_gu = torch.empty(8, batch, 2 * cfg.ffn, device=self.device, dtype=torch.float32)
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -184,6 +191,12 @@ class Supernet:
         if KDA in kinds:
             self.dec["kda_proj"] = e(B, cfg.kda_in_width)
             self.dec["kda_out"] = e(B, cfg.kda_dim)
+            self.dec["kda_fg"] = e(2, B, cfg.kda_dim)
+            # stacked second low-rank factors [2][R][H*D] for the batched f/gate GEMM
+            for l, k in enumerate(self.kinds):
+                if k == KDA:
+                    mw = self.w["layers"][l]["mixer"]
+                    mw["fg2T"] = torch.stack([mw["f2"].t(), mw["g2"].t()]).contiguous()
 
     # ------------------------------------------------------------------ decode
     def _attn_decode(self, l, kind, h, out):
@@ -191,10 +204,10 @@ class Supernet:
         Hq, Hkv, D, P = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
-        self._gemm_store(h, w["qkv"], d["qkv"], "in_proj")
+        qkv, ns = self._gemm_in(h, w["qkv"], d["qkv"])
         self._probe_begin("rope_kv_append", fine=True)
-        ops.rope_kv_append(d["qkv"], None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
-                           st["k"], st["v"], bt, Hq, Hkv, D, P, window)
+        ops.rope_kv_append(qkv, None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
+                           st["k"], st["v"], bt, Hq, Hkv, D, P, window, nsplit=ns)
         self._probe_end("rope_kv_append", fine=True)
         sp, _ = self.attn_split[kind]
         name = "swa_decode" if kind == SWA else "fa_decode"
@@ -207,22 +220,29 @@ class Supernet:
     def _gdn_decode(self, l, h, out):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.gdn_head_dim
-        self._gemm_store(h, w["w_in"], d["gdn_proj"], "in_proj")
+        proj, ns = self._gemm_in(h, w["w_in"], d["gdn_proj"])
         self._probe_begin("gdn_decode")
-        ops.gdn_decode(d["gdn_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"], w["dt_bias"],
+        ops.gdn_decode(proj, st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"], w["dt_bias"],
                        w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D, cfg.conv_width,
-                       1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+                       1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps, nsplit=ns)
         self._probe_end("gdn_decode")
         return self._gemm_residual(d["gdn_out"], w["o"], self.slab_mix, out, "out_proj")
 
     def _kda_decode(self, l, h, out):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.kda_head_dim
-        self._gemm_store(h, w["w_in"], d["kda_proj"], "in_proj")
+        proj, ns = self._gemm_in(h, w["w_in"], d["kda_proj"])
+        fg = None
+        if ns == 0:  # low-rank gate second factors as one batched GEMM (1 MB of weights, read once)
+            HD, R = cfg.kda_dim, cfg.kda_rank
+            f1g1 = proj[:, 3 * HD:3 * HD + 2 * R].view(self.B, 2, R).transpose(0, 1)
+            fg = d["kda_fg"]
+            torch.bmm(f1g1, w["fg2T"], out=fg)
         self._probe_begin("kda_decode")
-        ops.kda_decode(d["kda_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
+        ops.kda_decode(proj, st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
                        w["dt_bias"], w["f2"], w["g2"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D,
-                       cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+                       cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps, nsplit=ns,
+                       fg=fg)
         self._probe_end("kda_decode")
         return self._gemm_residual(d["kda_out"], w["o"], self.slab_mix, out, "out_proj")
 
@@ -233,6 +253,23 @@ class Supernet:
     def _probe_end(self, name, fine=False):
         if self.probe is not None and (self.probe.fine or not fine):
             self.probe.end(name)
+
+    def _gemm_in(self, x, w, out_bf16):
+        """Input-side projection: (tensor, nsplit) for the consuming kernel — fp32 split-K slabs
+        of the tcgen05 GEMM (summed on load by the consumer), or a cuBLAS bf16 result."""
+        self._probe_begin("gemm_in_proj", fine=True)
+        if self.sn_gemm["in_proj"]:
+            slab = self._slab_view(self.slab_in, w.shape[0])
+            res = (slab, ops.gemm_decode(x, w, slab, "partial"))
+        else:
+            torch.mm(x, w.t(), out=out_bf16)
+            res = (out_bf16, 0)
+        self._probe_end("gemm_in_proj", fine=True)
+        return res
+
+    def _slab_view(self, buf, n):
+        """Contiguous [8, B, n] view at the start of a slab buffer (slab stride B*n)."""
+        return buf.view(-1)[: 8 * self.B * n].view(8, self.B, n)
 
     def _gemm_store(self, x, w, out, role):
         self._probe_begin("gemm_" + role, fine=True)
@@ -290,13 +327,14 @@ class Supernet:
             self._norm(pending, lw["norm2"])
             self._probe_begin("gemm_ffn_gate_up", fine=True)
             if self.sn_gemm["ffn_gate_up"]:
-                ops.gemm_decode(self.h, lw["ffn_gu"], self.act, "swiglu")
+                gu, ns = self.slab_gu, ops.gemm_decode(self.h, lw["ffn_gu"], self.slab_gu, "partial")
             else:
                 torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
-                self._probe_end("gemm_ffn_gate_up", fine=True)
-                self._probe_begin("silu_mul", fine=True)
-                ops.silu_mul(self.gu, self.act)
-            self._probe_end("silu_mul" if not self.sn_gemm["ffn_gate_up"] else "gemm_ffn_gate_up", fine=True)
+                gu, ns = self.gu, 0
+            self._probe_end("gemm_ffn_gate_up", fine=True)
+            self._probe_begin("silu_mul", fine=True)
+            ops.silu_mul(gu, self.act, nsplit=ns)
+            self._probe_end("silu_mul", fine=True)
             pending = self._gemm_residual(self.act, lw["ffn_down"], self.slab_ffn, self.ffn_out, "ffn_down")
         self._norm(pending, w["final_norm"])
         self._gemm_store(self.h, w["lm_head"], self.logits, "lm_head")
@@ -313,9 +351,9 @@ class Supernet:
         for kind in self.kinds:
             sn += 2                            # two add_rmsnorm
             sn += 2 if kind in (FA, SWA) else 1    # rope+attention | fused delta-rule decode
-            for role in ("in_proj", "out_proj", "ffn_down"):
+            for role in ("in_proj", "out_proj", "ffn_down", "ffn_gate_up"):
                 sn, lib = (sn + 1, lib) if g[role] else (sn, lib + 1)
-            sn, lib = (sn + 1, lib) if g["ffn_gate_up"] else (sn + 1, lib + 1)  # fused SwiGLU | GEMM + silu_mul
+            sn += 1                            # silu_mul (sums the gate/up split-K slabs)
         return {"sn": sn, "cublas": lib}
 
     @torch.no_grad()

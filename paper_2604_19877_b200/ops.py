@@ -51,9 +51,10 @@ def add_rmsnorm(delta, residual, weight, out, eps, partials=None, nsplit=0):
          _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
 
 
-def silu_mul(gate_up, out):
+def silu_mul(gate_up, out, nsplit=0):
+    """gate_up: [rows, 2F] (dtype of out) or fp32 split-K slabs [>=nsplit, rows, 2F]."""
     rows, ffn = out.shape
-    call("sn_silu_mul", _p(gate_up), _p(out), rows, ffn, dtype_code(out.dtype), _s())
+    call("sn_silu_mul", _p(gate_up), int(nsplit), _p(out), rows, ffn, dtype_code(out.dtype), _s())
 
 
 def argmax(logits, out_tokens):
@@ -62,11 +63,12 @@ def argmax(logits, out_tokens):
 
 
 def rope_kv_append(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,
-                   Hq, Hkv, D, page_size, window):
-    rows = qkv.shape[0]
-    call("sn_rope_kv_append", _p(qkv), _p(row_seq), _p(row_pos), _p(seq_lens), _p(inv_freq), _p(q_out), _p(k_out),
+                   Hq, Hkv, D, page_size, window, nsplit=0):
+    """qkv: [rows, (Hq+2Hkv)D] (dtype of the cache) or fp32 split-K slabs [>=nsplit, rows, ...]."""
+    rows = q_out.shape[0]
+    call("sn_rope_kv_append", _p(qkv), int(nsplit), _p(row_seq), _p(row_pos), _p(seq_lens), _p(inv_freq), _p(q_out), _p(k_out),
          _p(v_out), _p(k_cache), _p(v_cache), _p(block_table), rows, Hq, Hkv, D, page_size, block_table.shape[1],
-         window, dtype_code(qkv.dtype), _s())
+         window, dtype_code(q_out.dtype), _s())
 
 
 def attn_decode_workspace_bytes(B, Hq, Hkv, D, max_splits):
@@ -88,19 +90,22 @@ def attn_prefill(q, k, v, cu_seqlens, out, Hq, Hkv, D, window, scale):
 
 
 def gdn_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, norm_w, out, Hk, Hv, D, width,
-               scale, eps_l2, eps_norm):
+               scale, eps_l2, eps_norm, nsplit=0):
+    """proj: [B, N_in] (dtype of out) or fp32 split-K slabs [>=nsplit, B, N_in]."""
     B = positions.shape[0]
-    call("sn_gdn_decode", _p(proj), proj.stride(0), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
+    call("sn_gdn_decode", _p(proj), proj.stride(-2), int(nsplit), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
          _p(positions), _p(A_log), _p(dt_bias), _p(norm_w), _p(out), B, Hk, Hv, D, width, scale, eps_l2, eps_norm,
-         dtype_code(proj.dtype), _s())
+         dtype_code(out.dtype), _s())
 
 
 def kda_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, f2, g2, g2_b, norm_w, out, H, D,
-               rank, width, scale, eps_l2, eps_norm):
+               rank, width, scale, eps_l2, eps_norm, nsplit=0, fg=None):
+    """proj: [B, N_in] (dtype of out) or fp32 split-K slabs [>=nsplit, B, N_in]."""
     B = positions.shape[0]
-    call("sn_kda_decode", _p(proj), proj.stride(0), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
-         _p(positions), _p(A_log), _p(dt_bias), _p(f2), _p(g2), _p(g2_b), _p(norm_w), _p(out), B, H, D, rank, width,
-         scale, eps_l2, eps_norm, dtype_code(proj.dtype), _s())
+    call("sn_kda_decode", _p(proj), proj.stride(-2), int(nsplit), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
+         _p(positions), _p(A_log), _p(dt_bias), _p(f2), _p(g2), _p(g2_b), _p(fg), _p(norm_w), _p(out), B, H, D, rank,
+         width,
+         scale, eps_l2, eps_norm, dtype_code(out.dtype), _s())
 
 
 def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channels, width):

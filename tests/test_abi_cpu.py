@@ -42,7 +42,7 @@ def test_ctypes_signatures_match_header():
 def test_error_path_without_gpu():
     """Argument validation happens before any CUDA call: a bad call fails cleanly on CPU."""
     lib = _lib.load()
-    st = lib.sn_gdn_decode(None, 0, None, None, None, None, None, None, None, None, None, 1, 1, 1, 128, 4,
+    st = lib.sn_gdn_decode(None, 0, 0, None, None, None, None, None, None, None, None, None, 1, 1, 1, 128, 4,
                            1.0, 1e-6, 1e-5, 1, None)
     assert st == 1 and b"NULL" in lib.sn_last_error()
     st = lib.sn_attn_decode(None, None, None, None, None, None, None, None, 1, 32, 7, 128, 64, 8, 0, 1, 1, 1.0, 1,

@@ -133,9 +133,9 @@ def _delta_weights(cfg, kind, gen, dtype):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("kind", [GDN, KDA])
+@pytest.mark.parametrize("kind,use_fg", [(GDN, False), (KDA, False), (KDA, True)])
 @pytest.mark.parametrize("cfg", [APRIEL, TINY], ids=["apriel", "tiny"])
-def test_delta_decode_steps(cfg, kind, dtype):
+def test_delta_decode_steps(cfg, kind, use_fg, dtype):
     """Several decode steps of the fused GDN/KDA kernel vs oracle gdn_core/kda_core, from a random
     non-zero state and conv history (including positions < W-1 where the ring must read zeros)."""
     ops = _ops()
@@ -165,9 +165,15 @@ def test_delta_decode_steps(cfg, kind, dtype):
                            cfg.mixer_norm_eps)
         else:
             o_ref, hist, S_ref = kda_core(cfg, p.float(), hist, S_ref, wf)
+            fg = None
+            if use_fg:  # precomputed second low-rank factors (the model's batched-GEMM path)
+                HD, R = cfg.kda_dim, cfg.kda_rank
+                pc = p.cuda()
+                f1g1 = pc[:, 3 * HD:3 * HD + 2 * R].view(B, 2, R).transpose(0, 1)
+                fg = torch.bmm(f1g1, torch.stack([wd["f2"].t(), wd["g2"].t()]).contiguous())
             ops.kda_decode(p.cuda(), ring, wd["conv_w"], S_dev, None, positions, wd["A_log"], wd["dt_bias"], wd["f2"],
                            wd["g2"], wd["g2_b"], wd["norm_w"], out, Hv, D, cfg.kda_rank, W, 1 / math.sqrt(D),
-                           cfg.l2_eps, cfg.mixer_norm_eps)
+                           cfg.l2_eps, cfg.mixer_norm_eps, fg=fg)
         torch.cuda.synchronize()
         assert rel_err(out, o_ref) <= TOL[dtype], (step, rel_err(out, o_ref))
         assert rel_err(S_dev.transpose(-1, -2), S_ref) <= TOL[dtype]

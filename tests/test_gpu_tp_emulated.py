@@ -44,9 +44,11 @@ def _run_delta(cfg, kind, w, x, S0):
 def test_delta_mixer_head_parallel(kind, world):
     cfg = APRIEL
     torch.manual_seed(0)
-    w = {k: (v if k in ("A_log", "dt_bias") else v.to(torch.bfloat16)) for k, v in init_mixer(cfg, 0, kind).items()}
+    # fp32 I/O: the sharded and unsharded in-projections then produce the same per-column values
+    # (bf16 rounding would differ between GEMM shapes and blur the comparison)
+    w = init_mixer(cfg, 0, kind)
     B = 4
-    x = (torch.randn(B, cfg.hidden) * 0.5).to(torch.bfloat16).cuda()
+    x = (torch.randn(B, cfg.hidden) * 0.5).cuda()
     H = cfg.gdn_v_heads if kind == GDN else cfg.kda_heads
     D = cfg.gdn_head_dim if kind == GDN else cfg.kda_head_dim
     S0 = (torch.randn(B, H, D, D) * 0.05).cuda()
@@ -58,8 +60,7 @@ def test_delta_mixer_head_parallel(kind, world):
         part, S_r = _run_delta(local, kind, shard_mixer(cfg, kind, w, world, r), x,
                                S0[:, r * h:(r + 1) * h].contiguous())
         acc += part
-        # bf16 projections are rounded by different GEMM shapes in the two layouts: state within 2e-3
         ref_s = S_full[:, r * h:(r + 1) * h]
-        assert ((S_r - ref_s).abs().max() / ref_s.abs().max()).item() < 2e-3
+        assert ((S_r - ref_s).abs().max() / ref_s.abs().max()).item() < 1e-4
     torch.cuda.synchronize()
-    assert ((acc - full).abs().max() / full.abs().max()).item() < 1e-3
+    assert ((acc - full).abs().max() / full.abs().max()).item() < 1e-4
