@@ -52,11 +52,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
   }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// KV pages are read exactly once per decode step: evict-first so they do not displace the
+// L2-resident activations / block tables.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -122,6 +125,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   __syncthreads();
 
+  uint64_t evict_first;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
   uint8_t* my_stages = smem + (size_t)warp * NST * STAGE_BYTES;
   uint64_t* my_bars = bars + warp * NST;
   auto issue = [&](int j) {
@@ -134,8 +139,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     mbar_expect_tx(bar, STAGE_BYTES);
 #pragma unroll
     for (int box = 0; box < D / 64; ++box) {
-      tma_load_2d(st + box * KT * 128, &kmap, box * 64, row, bar);
-      tma_load_2d(st + TILE_BYTES + box * KT * 128, &vmap, box * 64, row, bar);
+      tma_load_2d(st + box * KT * 128, &kmap, box * 64, row, bar, evict_first);
+      tma_load_2d(st + TILE_BYTES + box * KT * 128, &vmap, box * 64, row, bar, evict_first);
     }
   };
   if (lane == 0)

@@ -51,22 +51,22 @@ struct DeltaDecodeArgs {
 };
 
 template <int EPL> struct vecf;
-template <> struct vecf<4> {
+template <> struct vecf<4> {  // the recurrent state is streamed: evict-first loads and stores
   static __device__ __forceinline__ void ld(const float* p, float* v) {
-    float4 t = *reinterpret_cast<const float4*>(p);
+    float4 t = __ldcs(reinterpret_cast<const float4*>(p));
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   }
   static __device__ __forceinline__ void st(float* p, const float* v) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
   }
 };
 template <> struct vecf<2> {
   static __device__ __forceinline__ void ld(const float* p, float* v) {
-    float2 t = *reinterpret_cast<const float2*>(p);
+    float2 t = __ldcs(reinterpret_cast<const float2*>(p));
     v[0] = t.x; v[1] = t.y;
   }
   static __device__ __forceinline__ void st(float* p, const float* v) {
-    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
   }
 };
 
