@@ -171,9 +171,10 @@ sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv
 sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj,
                         int proj_stride, int b_off, int a_off, const void* f,
                         const float* A_log, const float* dt_bias, float* qn,
-                        float* kn, float* gexp, float* beta, int rows, int Hk,
-                        int Hv, int D, float scale, float eps_l2, int dtype,
+                        float* kn, float* gexp, float* glog, float* beta, int rows,
+                        int Hk, int Hv, int D, float scale, float eps_l2, int dtype,
                         void* stream);
+/* (glog, optional, GDN only: the log decay g per [row][Hv], for the chunked prefill) */
 
 /* Recurrent scan over each sequence: o[t] (fp32 [rows][Hv][D]) and the final
  * state written to state[slot_idx[s]] (read first if init_state != 0).      */
@@ -183,6 +184,32 @@ sn_status sn_delta_scan(int kind, const float* qn, const float* kn,
                         float* state, const int32_t* slot_idx,
                         const int32_t* cu_seqlens, int num_seqs, int Hk, int Hv,
                         int D, int init_state, int dtype, void* stream);
+
+/* Chunked (WY, C = 64) GDN prefill on tensor cores, bf16 only: same inputs/outputs
+ * as sn_delta_scan (kind 0) plus glog from sn_delta_prep; one CTA per
+ * (sequence, value head, 64-wide value tile), chunks in order, state in registers.
+ * R/PAPER.md:1599 (WY representation), 845-848 (prefill path).                  */
+sn_status sn_gdn_chunk_prefill(const float* qn, const float* kn, const void* qkv_conv,
+                               int v_off, int qkv_stride, const float* glog,
+                               const float* beta, float* o, float* state,
+                               const int32_t* slot_idx, const int32_t* cu_seqlens,
+                               int num_seqs, int Hk, int Hv, int D, int init_state,
+                               int dtype, void* stream);
+
+/* Two-phase chunked GDN prefill (long prompts): phase 1 computes every chunk's
+ * local WY tiles in parallel (one CTA per (chunk, value head)), phase 2 runs the
+ * sequential state pass over precomputed bf16 tiles streamed through
+ * double-buffered shared memory.  chunks: int32 [num_chunks][2] = (first token,
+ * length <= 64) in sequence order; seq_chunk0: int32 [num_seqs+1] chunk offsets.
+ * workspace: sn_gdn_chunk_workspace_bytes(num_chunks, Hv, D).                     */
+size_t sn_gdn_chunk_workspace_bytes(int num_chunks, int Hv, int D);
+sn_status sn_gdn_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv,
+                                int v_off, int qkv_stride, const float* glog,
+                                const float* beta, const int32_t* chunks,
+                                const int32_t* seq_chunk0, int num_chunks, void* workspace,
+                                float* o, float* state, const int32_t* slot_idx,
+                                int num_seqs, int Hk, int Hv, int D, int init_state,
+                                int dtype, void* stream);
 
 /* out[r,h,:] = RMSNorm(o[r,h,:]) * norm_w * act(gate[r, h*D + :]),
  * act: 0 = silu (GDN), 1 = sigmoid (KDA).  gate row stride gate_stride.    */

@@ -382,8 +382,8 @@ __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv
                                                        const T* __restrict__ f, const float* __restrict__ A_log,
                                                        const float* __restrict__ dt_bias, float* __restrict__ qn,
                                                        float* __restrict__ kn, float* __restrict__ gexp,
-                                                       float* __restrict__ beta, int Hk, int Hv, float scale,
-                                                       float eps_l2) {
+                                                       float* __restrict__ glog, float* __restrict__ beta, int Hk,
+                                                       int Hv, float scale, float eps_l2) {
   __shared__ float red[D / 32];
   const int r = blockIdx.y, h = blockIdx.x, i = threadIdx.x;
   const int G = Hv / Hk, kh = h / G;
@@ -402,7 +402,9 @@ __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv
     const float fv = io<T>::ld(f + (size_t)r * Hv * D + h * D + i);
     gexp[((size_t)r * Hv + h) * D + i] = expf(negA * softplus_f(fv + dt_bias[h * D + i]));
   } else if (i == 0) {
-    gexp[(size_t)r * Hv + h] = expf(negA * softplus_f(io<T>::ld(prow + a_off + h) + dt_bias[h]));
+    const float g = negA * softplus_f(io<T>::ld(prow + a_off + h) + dt_bias[h]);
+    gexp[(size_t)r * Hv + h] = expf(g);
+    if (glog) glog[(size_t)r * Hv + h] = g;
   }
   if (i == 0) beta[(size_t)r * Hv + h] = sigmoid_f(io<T>::ld(prow + b_off + h));
 }
@@ -520,10 +522,10 @@ namespace sn {
 template <typename T, int D, bool K>
 static void launch_prep(dim3 grid, cudaStream_t st, const void* qkv_conv, const void* proj, int proj_stride,
                         int b_off, int a_off, const void* f, const float* A_log, const float* dt_bias, float* qn,
-                        float* kn, float* gexp, float* beta, int Hk, int Hv, float scale, float eps_l2) {
+                        float* kn, float* gexp, float* glog, float* beta, int Hk, int Hv, float scale, float eps_l2) {
   delta_prep_kernel<T, D, K><<<grid, D, 0, st>>>((const T*)qkv_conv, (const T*)proj, proj_stride, b_off, a_off,
-                                                 (const T*)f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, scale,
-                                                 eps_l2);
+                                                 (const T*)f, A_log, dt_bias, qn, kn, gexp, glog, beta, Hk, Hv,
+                                                 scale, eps_l2);
 }
 
 template <typename T, int D, bool K>
@@ -599,8 +601,8 @@ sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv
 
 sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int proj_stride, int b_off, int a_off,
                         const void* f, const float* A_log, const float* dt_bias, float* qn, float* kn, float* gexp,
-                        float* beta, int rows, int Hk, int Hv, int D, float scale, float eps_l2, int dtype,
-                        void* stream) {
+                        float* glog, float* beta, int rows, int Hk, int Hv, int D, float scale, float eps_l2,
+                        int dtype, void* stream) {
   SN_REQUIRE(kind == 0 || kind == 1, "sn_delta_prep: kind %d", kind);
   SN_REQUIRE(rows > 0 && Hk > 0 && Hv % Hk == 0, "sn_delta_prep: bad shape");
   SN_REQUIRE(kind == 0 || f != nullptr, "sn_delta_prep: KDA needs f");
@@ -610,8 +612,8 @@ sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int pr
     cudaStream_t st = (cudaStream_t)stream;
     auto fn = D == 128 ? (kind ? launch_prep<T, 128, true> : launch_prep<T, 128, false>)
                        : (kind ? launch_prep<T, 64, true> : launch_prep<T, 64, false>);
-    fn(grid, st, qkv_conv, proj, proj_stride, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, scale,
-       eps_l2);
+    fn(grid, st, qkv_conv, proj, proj_stride, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, glog, beta, Hk, Hv,
+       scale, eps_l2);
     return check_launch("sn_delta_prep");
   });
 }

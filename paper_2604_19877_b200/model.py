@@ -464,10 +464,18 @@ class Supernet:
         gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
         beta = torch.empty(rows, Hv, **f32)
         k_code = 1 if kind == KDA else 0
+        # bf16 GDN: chunked WY prefill on tensor cores; fp32 I/O (1e-4 parity mode) and KDA: the
+        # recurrent scan (same outputs, token-sequential)
+        chunked = kind == GDN and h.dtype == torch.bfloat16 and getattr(self, "chunked_prefill", True)
+        glog = torch.empty(rows, Hv, **f32) if chunked else None
         ops.delta_prep(k_code, y, proj, b_off, a_off, f, w["A_log"], w["dt_bias"], qn, kn, gexp, beta, Hk, Hv, D,
-                       1.0 / math.sqrt(D), cfg.l2_eps)
+                       1.0 / math.sqrt(D), cfg.l2_eps, glog=glog)
         o = torch.empty(rows, Hv, D, **f32)
-        ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], None, cu, Hk, Hv, D, init_state=False)
+        if chunked:
+            ops.gdn_chunk_prefill(qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], None, cu, Hk, Hv, D, init_state=False)
+        else:
+            ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], None, cu, Hk, Hv, D,
+                           init_state=False)
         y_out = torch.empty(rows, Hv * D, device=dev, dtype=h.dtype)
         ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
         torch.mm(y_out, w["o"].t(), out=out)

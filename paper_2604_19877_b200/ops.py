@@ -113,10 +113,17 @@ def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channe
          cu_seqlens.numel() - 1, y.shape[0], channels, width, dtype_code(y.dtype), _s())
 
 
-def delta_prep(kind, qkv_conv, proj, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, D, scale, eps_l2):
+def delta_prep(kind, qkv_conv, proj, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, D, scale, eps_l2,
+               glog=None):
     call("sn_delta_prep", kind, _p(qkv_conv), _p(proj), proj.stride(0), b_off, a_off, _p(f), _p(A_log), _p(dt_bias),
-         _p(qn), _p(kn), _p(gexp), _p(beta), qkv_conv.shape[0], Hk, Hv, D, scale, eps_l2, dtype_code(qkv_conv.dtype),
-         _s())
+         _p(qn), _p(kn), _p(gexp), _p(glog), _p(beta), qkv_conv.shape[0], Hk, Hv, D, scale, eps_l2,
+         dtype_code(qkv_conv.dtype), _s())
+
+
+def gdn_chunk_prefill(qn, kn, qkv_conv, v_off, glog, beta, o, state, slot_idx, cu_seqlens, Hk, Hv, D, init_state):
+    call("sn_gdn_chunk_prefill", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(glog), _p(beta), _p(o),
+         _p(state), _p(slot_idx), _p(cu_seqlens), cu_seqlens.numel() - 1, Hk, Hv, D, int(init_state),
+         dtype_code(qkv_conv.dtype), _s())
 
 
 def delta_scan(kind, qn, kn, qkv_conv, v_off, gexp, beta, o, state, slot_idx, cu_seqlens, Hk, Hv, D, init_state):
@@ -159,3 +166,26 @@ def gemm_decode(x, w, out, mode="store"):
     call("sn_gemm_decode", _p(x), M, K, x.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(-2), code,
          ctypes.byref(s_out), _s())
     return s_out.value
+
+
+def chunk_plan(cu_seqlens_host, chunk=64, device="cuda"):
+    """(chunks int32 [n, 2] = (first token, length), seq_chunk0 int32 [S+1]) for the two-phase prefill."""
+    chunks, starts = [], [0]
+    for s0, s1 in zip(cu_seqlens_host[:-1], cu_seqlens_host[1:]):
+        for t in range(int(s0), int(s1), chunk):
+            chunks.append((t, min(chunk, int(s1) - t)))
+        starts.append(len(chunks))
+    return (torch.tensor(chunks, dtype=torch.int32, device=device).view(-1, 2),
+            torch.tensor(starts, dtype=torch.int32, device=device))
+
+
+def gdn_chunk_prefill2(qn, kn, qkv_conv, v_off, glog, beta, chunks, seq_chunk0, o, state, slot_idx, Hk, Hv, D,
+                       init_state, workspace=None):
+    n = chunks.shape[0]
+    nbytes = _lib.load().sn_gdn_chunk_workspace_bytes(n, Hv, D)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=qn.device)
+    call("sn_gdn_chunk_prefill2", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(glog), _p(beta),
+         _p(chunks), _p(seq_chunk0), n, _p(workspace), _p(o), _p(state), _p(slot_idx), seq_chunk0.numel() - 1, Hk, Hv,
+         D, int(init_state), dtype_code(qkv_conv.dtype), _s())
+    return workspace

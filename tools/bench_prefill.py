@@ -1,0 +1,41 @@
+"""GDN prefill core (after prep): chunked WY on tensor cores vs the token-sequential scan,
+Apriel head shapes, one sequence of T tokens, all 32 value heads."""
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2604_19877_b200 import ops  # noqa: E402
+
+D, Hk, Hv = 128, 8, 32
+for T in (512, 4096, 16384):
+    qn = torch.nn.functional.normalize(torch.randn(T, Hk, D, device="cuda"), dim=-1) / math.sqrt(D)
+    kn = torch.nn.functional.normalize(torch.randn(T, Hk, D, device="cuda"), dim=-1)
+    qkv = torch.randn(T, (2 * Hk + Hv) * D, device="cuda").to(torch.bfloat16)
+    glog = -torch.rand(T, Hv, device="cuda") * 0.3
+    beta = torch.rand(T, Hv, device="cuda")
+    cu = torch.tensor([0, T], dtype=torch.int32, device="cuda")
+    S = torch.zeros(1, Hv, D, D, device="cuda")
+    o = torch.empty(T, Hv, D, device="cuda")
+    gexp = glog.exp()
+    res = {}
+    for name in ("chunk", "scan"):
+        def run():
+            if name == "chunk":
+                ops.gdn_chunk_prefill(qn, kn, qkv, 2 * Hk * D, glog, beta, o, S, None, cu, Hk, Hv, D, init_state=False)
+            else:
+                ops.delta_scan(0, qn, kn, qkv, 2 * Hk * D, gexp, beta, o, S, None, cu, Hk, Hv, D, init_state=False)
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / 3
+    flops = T / 64 * Hv * 2 * (64 * 64 * 128 * 2 + 64 * 128 * 64 + 64 * 64 * 64 + 64 * 128 * 64 * 3 + 64 * 64 * 64)
+    print(f"T={T:6d}: chunk {res['chunk']:8.3f} ms ({flops / res['chunk'] / 1e9:6.1f} TFLOP/s)   scan {res['scan']:8.3f} ms"
+          f"   speed-up {res['scan'] / res['chunk']:5.1f}x")
