@@ -23,6 +23,7 @@ __global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __rest
                                       T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
                                       int Hkv, int D, int page_size, int max_blocks, int window) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
   const int half = D / 2;
   if (i >= half) return;
@@ -78,6 +79,7 @@ __global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __rest
 template <typename T, int D, int GMAX>
 __global__ void __launch_bounds__(128) attn_decode_simt_kernel(AttnDecodeArgs a) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   constexpr int EPL = D / 32;
   __shared__ float s_q[GMAX][D];
   __shared__ float s_m[4][GMAX], s_l[4][GMAX];
@@ -246,7 +248,7 @@ sn_status sn_rope_kv_append(const void* qkv, int qkv_nsplit, const int32_t* row_
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(rows, Hq + 2 * Hkv);
     const GemmIn<T> in{qkv, qkv_nsplit, (size_t)rows * (Hq + 2 * Hkv) * D};
-    rope_kv_append_kernel<T><<<grid, ((D / 2 + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(
+    launch_pdl(rope_kv_append_kernel<T>, grid, dim3(((D / 2 + 31) / 32) * 32), 0, (cudaStream_t)stream,
         in, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache,
         (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
     return check_launch("sn_rope_kv_append");
@@ -276,8 +278,8 @@ sn_status sn_attn_decode(const void* q, const void* k_cache, const void* v_cache
     return attn_decode_tc_bf16(a, D, st);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(max_splits, Hkv, B);
-    if (D == 128) attn_decode_simt_kernel<T, 128, 8><<<grid, 128, 0, st>>>(a);
-    else if (D == 64) attn_decode_simt_kernel<T, 64, 8><<<grid, 128, 0, st>>>(a);
+    if (D == 128) launch_pdl(attn_decode_simt_kernel<T, 128, 8>, grid, dim3(128), 0, st, a);
+    else if (D == 64) launch_pdl(attn_decode_simt_kernel<T, 64, 8>, grid, dim3(128), 0, st, a);
     else { set_error("sn_attn_decode: D=%d unsupported", D); return SN_EUNSUPPORTED; }
     return check_launch("sn_attn_decode");
   });

@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     attn_decode_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                           const AttnDecodeArgs a) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   constexpr int TILE_BYTES = KT * D * 2;        // one of K or V
   constexpr int STAGE_BYTES = 2 * TILE_BYTES;   // K then V
   constexpr int NKS = D / 16;                   // k-steps of Q.K^T
@@ -329,11 +330,11 @@ sn_status attn_decode_tc_bf16(const AttnDecodeArgs& a, int D, cudaStream_t st) {
   if (D == 128) {
     static bool attr = false;
     if (!attr) { cudaFuncSetAttribute(attn_decode_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn); attr = true; }
-    attn_decode_tc_kernel<128><<<grid, NW * 32, dyn, st>>>(kmap, vmap, a);
+    launch_pdl(attn_decode_tc_kernel<128>, grid, dim3(NW * 32), dyn, st, kmap, vmap, a);
   } else if (D == 64) {
     static bool attr = false;
     if (!attr) { cudaFuncSetAttribute(attn_decode_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn); attr = true; }
-    attn_decode_tc_kernel<64><<<grid, NW * 32, dyn, st>>>(kmap, vmap, a);
+    launch_pdl(attn_decode_tc_kernel<64>, grid, dim3(NW * 32), dyn, st, kmap, vmap, a);
   } else {
     set_error("attn_decode_tc: D=%d unsupported", D);
     return SN_EUNSUPPORTED;

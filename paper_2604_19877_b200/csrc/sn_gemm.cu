@@ -163,6 +163,11 @@ constexpr int kMaxStages = 32;
 
 constexpr int kGemmThreads = 256;
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int NS = g.ns, STAGE = g.stage_bytes;
   const int A_BYTES = (int)a_bytes;
   pdl_launch_dependents();
+  if (g.stats && threadIdx.x == 0) g.stats[blockIdx.x * 8 + 4] = clock64();
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (CS > 1) cluster_sync_all();  // peers' barriers exist before anyone multicasts into them
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
+  if (g.stats && threadIdx.x == 32) g.stats[blockIdx.x * 8 + 1] = clock64();  // setup done
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer: one continuous ring over the CTA's blocks
@@ -267,8 +274,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         load_x(i, s);
       }
       if (g.stats) {
-        g.stats[blockIdx.x * 4 + 0] = t_wait;
-        g.stats[blockIdx.x * 4 + 1] = clock64() - t_begin;
+        g.stats[blockIdx.x * 8 + 0] = t_wait;
       }
     }
   } else if (warp == 1) {
@@ -285,6 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           long long t0 = clock64();
           mbar_wait(&full_bar[s], r & 1);
           m_wait += clock64() - t0;
+          if (g.stats && i == 0) g.stats[blockIdx.x * 8 + 5] = clock64();
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + NA * A_BYTES;
@@ -301,8 +308,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         umma_commit(&tfull_bar[buf]);
       }
       if (g.stats) {
-        g.stats[blockIdx.x * 4 + 2] = m_wait;
-        g.stats[blockIdx.x * 4 + 3] = clock64() - m_begin;
+        g.stats[blockIdx.x * 8 + 2] = m_wait;
+        g.stats[blockIdx.x * 8 + 3] = clock64() - m_begin;
+        g.stats[blockIdx.x * 8 + 6] = clock64();
       }
     }
   } else if (warp >= 4) {
@@ -365,7 +373,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
 
+  __syncwarp();  // warps 0/1 diverged (one elected lane each): reconverge before the CTA barrier
   __syncthreads();
+  if (g.stats && threadIdx.x == 0) g.stats[blockIdx.x * 8 + 7] = clock64();
   if (CS > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
@@ -449,7 +459,9 @@ static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, GemmArgs g
   constexpr int kSmemMax = 227 * 1024;          // per-CTA opt-in maximum on sm_100
   const int stage = NA * g.br * BK * 2 + BN * BK * 2;
   const int tail = BM * BK * 2;  // the M=128 UMMA of the last stage may read 128 rows past its A tile
-  int ns = (kSmemMax - 2048 - tail) / stage;     // 1 KB alignment slack + static barriers
+  static int budget = getenv("SN_GEMM_SMEM_KB") ? atoi(getenv("SN_GEMM_SMEM_KB")) * 1024 : kSmemMax;
+  int ns = ((budget < kSmemMax ? budget : kSmemMax) - 2048 - tail) / stage;  // 1 KB alignment slack + barriers
+  if (ns < 2) ns = 2;
   if (ns > kMaxStages) ns = kMaxStages;
   g.ns = ns;
   g.stage_bytes = stage;
@@ -518,8 +530,9 @@ using namespace sn::gemm;
 
 extern "C" {
 
-// Profiling aid: later launches write per-CTA clock64 counters [producer empty-wait, producer
-// total, MMA full-wait, MMA total] into dev_stats (4 x #SMs u64); NULL disables.
+// Profiling aid: later launches write per-CTA counters [producer empty-wait, producer total,
+// MMA full-wait, MMA total (clock64); entry, first stage landed, last MMA issued, exit
+// (%globaltimer ns)] into dev_stats (8 x #SMs u64); NULL disables.
 void sn_gemm_debug_stats(unsigned long long* dev_stats) { g_stats = dev_stats; }
 
 int sn_gemm_decode_splits(int M, int N, int K, int mode) {

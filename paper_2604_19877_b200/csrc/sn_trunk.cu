@@ -39,6 +39,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __rest
                              float* __restrict__ residual, int32_t* seq_lens, int32_t* positions,
                              int rows, int dim) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   const int r = blockIdx.x;
   if (seq_lens != nullptr && r == 0) {
     for (int b = threadIdx.x; b < rows; b += blockDim.x) {
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const T* __restrict__ 
                                                           const T* __restrict__ weight,
                                                           T* __restrict__ out, int rows, int dim, float eps) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   __shared__ float scratch[32];
   __shared__ float cta_sum;
   cg::cluster_group cluster = cg::this_cluster();
@@ -134,6 +136,7 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const T* __restrict__ 
 template <typename T>
 __global__ void silu_mul_kernel(const GemmIn<T> gu, T* __restrict__ out, int rows, int ffn) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   const size_t n = (size_t)rows * ffn;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     const size_t r = e / ffn, i = e % ffn;
@@ -147,6 +150,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logits, int vocab,
                                                       int32_t* __restrict__ out) {
   sn::pdl_launch_dependents();
+  sn::pdl_wait();
   __shared__ float sv[32];
   __shared__ int si[32];
   const T* row = logits + (size_t)blockIdx.x * vocab;
@@ -189,8 +193,8 @@ sn_status sn_embed(const int32_t* tokens, const void* table, float* residual, in
   SN_REQUIRE(rows > 0 && dim > 0 && dim % 8 == 0, "sn_embed: bad shape rows=%d dim=%d", rows, dim);
   SN_REQUIRE((seq_lens == nullptr) == (positions == nullptr), "sn_embed: seq_lens/positions must be both set or both NULL");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    embed_kernel<T><<<rows, 128, 0, (cudaStream_t)stream>>>(tokens, (const T*)table, residual, seq_lens,
-                                                            positions, rows, dim);
+    launch_pdl(embed_kernel<T>, dim3(rows), dim3(128), 0, (cudaStream_t)stream, tokens, (const T*)table, residual,
+               seq_lens, positions, rows, dim);
     return check_launch("sn_embed");
   });
 }
@@ -211,13 +215,15 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit, f
     cfg.gridDim = dim3(rows * cs);
     cfg.blockDim = dim3(threads);
     cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = cs;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, add_rmsnorm_kernel<T>, (const T*)delta, partials, nsplit, residual,
                                        (const T*)weight, (T*)out, rows, dim, eps);
     if (e != cudaSuccess) {
@@ -236,7 +242,7 @@ sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, i
     int grid = (int)((n + 255) / 256);
     if (grid > 148 * 16) grid = 148 * 16;
     const GemmIn<T> in{gate_up, gu_nsplit, (size_t)rows * 2 * ffn};
-    silu_mul_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(in, (T*)out, rows, ffn);
+    launch_pdl(silu_mul_kernel<T>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, in, (T*)out, rows, ffn);
     return check_launch("sn_silu_mul");
   });
 }
@@ -244,7 +250,8 @@ sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, i
 sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens, int dtype, void* stream) {
   SN_REQUIRE(rows > 0 && vocab > 0 && vocab % 8 == 0, "sn_argmax: bad shape rows=%d vocab=%d", rows, vocab);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    argmax_kernel<T><<<rows, 1024, 0, (cudaStream_t)stream>>>((const T*)logits, vocab, out_tokens);
+    launch_pdl(argmax_kernel<T>, dim3(rows), dim3(1024), 0, (cudaStream_t)stream, (const T*)logits, vocab,
+               out_tokens);
     return check_launch("sn_argmax");
   });
 }

@@ -472,13 +472,35 @@ class Supernet:
                        1.0 / math.sqrt(D), cfg.l2_eps, glog=glog)
         o = torch.empty(rows, Hv, D, **f32)
         if chunked:
-            ops.gdn_chunk_prefill(qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], None, cu, Hk, Hv, D, init_state=False)
+            self._chunked_gdn(qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], cu, Hk, Hv, D)
         else:
             ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], None, cu, Hk, Hv, D,
                            init_state=False)
         y_out = torch.empty(rows, Hv * D, device=dev, dtype=h.dtype)
         ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
         torch.mm(y_out, w["o"].t(), out=out)
+
+    def _chunked_gdn(self, qn, kn, y, v_off, glog, beta, o, S, cu, Hk, Hv, D, ws_cap=2 << 30):
+        """Two-phase chunked prefill over groups of sequences whose chunk workspace fits ws_cap bytes
+        (B equal-length prompts: one chunk plan serves every group)."""
+        B, rows = S.shape[0], qn.shape[0]
+        T = rows // B
+        per_seq = ops._lib.load().sn_gdn_chunk_workspace_bytes(-(-T // 64), Hv, D)
+        grp = max(1, min(B, ws_cap // max(per_seq, 1)))
+        key = (T, grp)
+        if getattr(self, "_chunk_key", None) != key:
+            self._chunk_key = key
+            self._chunk_plan = ops.chunk_plan(list(range(0, grp * T + 1, T)), device=qn.device)
+            self._chunk_ws = None
+        for b0 in range(0, B, grp):
+            b1 = min(B, b0 + grp)
+            r0, r1 = b0 * T, b1 * T
+            chunks, c0 = self._chunk_plan
+            if b1 - b0 != grp:
+                chunks, c0 = ops.chunk_plan(list(range(0, (b1 - b0) * T + 1, T)), device=qn.device)
+            self._chunk_ws = ops.gdn_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1], beta[r0:r1],
+                                                    chunks, c0, o[r0:r1], S[b0:b1], None, Hk, Hv, D,
+                                                    init_state=False, workspace=self._chunk_ws)
 
     def _gdn_prefill(self, l, h, out, cu):
         self._delta_prefill(GDN, l, h, out, cu)

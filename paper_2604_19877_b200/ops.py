@@ -189,3 +189,4 @@ def gdn_chunk_prefill2(qn, kn, qkv_conv, v_off, glog, beta, chunks, seq_chunk0, 
          _p(chunks), _p(seq_chunk0), n, _p(workspace), _p(o), _p(state), _p(slot_idx), seq_chunk0.numel() - 1, Hk, Hv,
          D, int(init_state), dtype_code(qkv_conv.dtype), _s())
     return workspace
+

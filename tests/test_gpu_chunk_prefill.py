@@ -40,12 +40,16 @@ def test_chunked_matches_scan(D, Hk, Hv, lens, init):
     dev = {k: v.cuda() for k, v in dict(qn=qn, kn=kn, qkv=qkv, glog=glog, beta=beta, cu=cu).items()}
     gexp = dev["glog"].exp()
     outs = {}
-    for name in ("scan", "chunk"):
+    for name in ("scan", "chunk", "chunk2"):
         S = S0.clone().cuda()
         o = torch.zeros(sum(lens), Hv, D, device="cuda")
         if name == "scan":
             ops.delta_scan(0, dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, gexp, dev["beta"], o, S, None, dev["cu"],
                            Hk, Hv, D, init_state=init)
+        elif name == "chunk2":
+            chunks, c0 = ops.chunk_plan(cu.tolist())
+            ops.gdn_chunk_prefill2(dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, dev["glog"], dev["beta"], chunks, c0,
+                                   o, S, None, Hk, Hv, D, init_state=init)
         else:
             ops.gdn_chunk_prefill(dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, dev["glog"], dev["beta"], o, S, None,
                                   dev["cu"], Hk, Hv, D, init_state=init)
@@ -53,6 +57,8 @@ def test_chunked_matches_scan(D, Hk, Hv, lens, init):
         outs[name] = (o.cpu(), S.cpu())
     assert rel(outs["chunk"][0], outs["scan"][0]) < TOL
     assert rel(outs["chunk"][1], outs["scan"][1]) < TOL
+    assert rel(outs["chunk2"][0], outs["scan"][0]) < TOL
+    assert rel(outs["chunk2"][1], outs["scan"][1]) < TOL
     # and the scan itself against the oracle recurrence (first sequence)
     L0 = lens[0]
     G = Hv // Hk
@@ -62,3 +68,24 @@ def test_chunked_matches_scan(D, Hk, Hv, lens, init):
                                         scale=1.0)
     assert rel(outs["scan"][0][:L0], o_ref[0]) < 1e-4
     assert rel(outs["scan"][1][0].transpose(-1, -2), S_ref[0]) < 1e-4
+
+
+@pytest.mark.gpu
+def test_grouped_two_phase_matches_scan():
+    """The model's grouped driver (workspace capped so sequences run in several groups, last one short)."""
+    from types import SimpleNamespace
+
+    from paper_2604_19877_b200 import ops
+    from paper_2604_19877_b200.model import Supernet
+    D, Hk, Hv, B, T = 64, 1, 4, 5, 130
+    qn, kn, qkv, glog, beta, cu = _inputs([T] * B, Hk, Hv, D, seed=5)
+    dev = {k: v.cuda() for k, v in dict(qn=qn, kn=kn, qkv=qkv, glog=glog, beta=beta, cu=cu).items()}
+    S_ref, S = torch.zeros(B, Hv, D, D, device="cuda"), torch.zeros(B, Hv, D, D, device="cuda")
+    o_ref, o = torch.zeros(B * T, Hv, D, device="cuda"), torch.zeros(B * T, Hv, D, device="cuda")
+    ops.delta_scan(0, dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, dev["glog"].exp(), dev["beta"], o_ref, S_ref, None,
+                   dev["cu"], Hk, Hv, D, init_state=False)
+    per_seq = ops._lib.load().sn_gdn_chunk_workspace_bytes(3, Hv, D)
+    Supernet._chunked_gdn(SimpleNamespace(), dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, dev["glog"], dev["beta"],
+                          o, S, dev["cu"], Hk, Hv, D, ws_cap=2 * per_seq)
+    torch.cuda.synchronize()
+    assert rel(o, o_ref) < TOL and rel(S, S_ref) < TOL

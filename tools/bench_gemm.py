@@ -5,9 +5,11 @@ import torch
 from paper_2604_19877_b200 import ops
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-shapes = [("ffn_gu(swiglu)", 14336, 5120, "swiglu"), ("ffn_down(partial)", 5120, 14336, "partial"),
-          ("gdn_in", 10304, 5120, "store"), ("gdn_out(partial)", 5120, 4096, "partial"),
-          ("attn_qkv", 6144, 5120, "store"), ("kda_in", 12576, 5120, "store"), ("lm_head", 131072, 5120, "store")]
+shapes = [("ffn_gu(swiglu)", 14336, 5120, "swiglu"), ("ffn_gu(partial)", 28672, 5120, "partial"),
+          ("ffn_down(partial)", 5120, 14336, "partial"),
+          ("gdn_in(partial)", 10304, 5120, "partial"), ("gdn_out(partial)", 5120, 4096, "partial"),
+          ("attn_qkv(partial)", 6144, 5120, "partial"), ("kda_in(partial)", 12576, 5120, "partial"),
+          ("lm_head", 131072, 5120, "store")]
 for name, N, K, mode in shapes:
     rows = 2 * N if mode == "swiglu" else N
     nbuf = max(2, min(8, int(3e9 // (rows * K * 2))))
@@ -18,6 +20,7 @@ for name, N, K, mode in shapes:
     else:
         out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if mode == "resid" else torch.bfloat16)
     res = {}
+    splits = ops.gemm_decode_splits(M, N if mode != "swiglu" else 2 * N, K, mode) if mode == "partial" else 1
     for impl in ("sn", "cublas"):
         def run(i):
             if impl == "sn":
@@ -46,6 +49,6 @@ for name, N, K, mode in shapes:
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / it * 1e3
         res[impl] = (us, rows * K * 2 / us / 1e3)
-    print(f"{name:16s} N={N:6d} K={K:5d}  "
+    print(f"{name:18s} N={N:6d} K={K:5d} splits={splits}  "
           f"sn {res['sn'][0]:7.1f}us {res['sn'][1]:6.0f}GB/s   cublas {res['cublas'][0]:7.1f}us {res['cublas'][1]:6.0f}GB/s")
     del Ws

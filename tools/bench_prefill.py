@@ -21,9 +21,15 @@ for T in (512, 4096, 16384):
     o = torch.empty(T, Hv, D, device="cuda")
     gexp = glog.exp()
     res = {}
-    for name in ("chunk", "scan"):
+    chunks, c0 = ops.chunk_plan([0, T])
+    ws = None
+    for name in ("chunk2", "chunk", "scan"):
         def run():
-            if name == "chunk":
+            global ws
+            if name == "chunk2":
+                ws = ops.gdn_chunk_prefill2(qn, kn, qkv, 2 * Hk * D, glog, beta, chunks, c0, o, S, None, Hk, Hv, D,
+                                            init_state=False, workspace=ws)
+            elif name == "chunk":
                 ops.gdn_chunk_prefill(qn, kn, qkv, 2 * Hk * D, glog, beta, o, S, None, cu, Hk, Hv, D, init_state=False)
             else:
                 ops.delta_scan(0, qn, kn, qkv, 2 * Hk * D, gexp, beta, o, S, None, cu, Hk, Hv, D, init_state=False)
@@ -37,5 +43,6 @@ for T in (512, 4096, 16384):
         torch.cuda.synchronize()
         res[name] = e0.elapsed_time(e1) / 3
     flops = T / 64 * Hv * 2 * (64 * 64 * 128 * 2 + 64 * 128 * 64 + 64 * 64 * 64 + 64 * 128 * 64 * 3 + 64 * 64 * 64)
-    print(f"T={T:6d}: chunk {res['chunk']:8.3f} ms ({flops / res['chunk'] / 1e9:6.1f} TFLOP/s)   scan {res['scan']:8.3f} ms"
+    print(f"T={T:6d}: two-phase {res['chunk2']:8.3f} ms ({flops / res['chunk2'] / 1e9:6.1f} TFLOP/s)", end="  ")
+    print(f"chunk {res['chunk']:8.3f} ms ({flops / res['chunk'] / 1e9:6.1f} TFLOP/s)   scan {res['scan']:8.3f} ms"
           f"   speed-up {res['scan'] / res['chunk']:5.1f}x")

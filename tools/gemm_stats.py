@@ -16,7 +16,7 @@ for spec in sys.argv[1:]:
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     out = torch.zeros(8, M, N, device="cuda", dtype=torch.float32) if mode == "partial" else \
         torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-    st = torch.zeros(148 * 4, dtype=torch.int64, device="cuda")
+    st = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
     for i in range(2):
         ops.gemm_decode(x, ws[i], out, mode)
     torch.cuda.synchronize()
@@ -27,9 +27,16 @@ for spec in sys.argv[1:]:
     e1.record()
     torch.cuda.synchronize()
     lib.sn_gemm_debug_stats(None)
-    s = st.view(148, 4).double().cpu()
+    s = st.view(148, 8).double().cpu()
     act = s[:, 3] > 0
     s = s[act]
+    t0 = s[:, 4:5]
+    rel = torch.cat([s[:, 1:2], s[:, 5:]], 1)
+    rel = (rel - t0) / 1.9e3  # clock64 cycles -> us at ~1.9 GHz, relative to the CTA's own entry
+    print(f"  timeline us from CTA entry (min/mean/max): setup {rel[:,0].min():.2f}/{rel[:,0].mean():.2f}/{rel[:,0].max():.2f}"
+          f"  first-stage {rel[:,1].min():.2f}/{rel[:,1].mean():.2f}/{rel[:,1].max():.2f}"
+          f"  mma-done {rel[:,2].min():.2f}/{rel[:,2].mean():.2f}/{rel[:,2].max():.2f}"
+          f"  exit {rel[:,3].min():.2f}/{rel[:,3].mean():.2f}/{rel[:,3].max():.2f}")
     print(f"{N}x{K} {mode}: {e0.elapsed_time(e1)*1e3:.1f} us event; CTAs {int(act.sum())}; "
-          f"producer wait/total {s[:,0].mean()/1e3:.1f}k/{s[:,1].mean()/1e3:.1f}k cyc; "
+          f"producer wait {s[:,0].mean()/1e3:.1f}k cyc; "
           f"MMA full-wait/total {s[:,2].mean()/1e3:.1f}k/{s[:,3].mean()/1e3:.1f}k cyc")
