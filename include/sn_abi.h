@@ -220,21 +220,31 @@ sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride,
 /* ---------------------------------------------------------------- decode GEMM
  * Weight-streaming projection GEMM for decode batches (M <= 128):
  * C[m][n] = sum_k X[m][k] W[n][k], X [M][ldx] bf16, W [N][ldw] bf16 (nn.Linear
- * layout), on tcgen05/TMEM/TMA.  Each CTA owns whole row blocks of W over the
- * full K (block height chosen so ~all 148 SMs stream; no split-K, so results
- * are deterministic); launched with programmatic dependent launch so W starts
- * streaming while the previous kernel finishes.  Replaces the projection / FFN
- * / LM-head GEMMs of the decode step (the trunk of R/PAPER.md:175-182 and each
- * mixer's projections, R/PAPER.md:1540-1625).
+ * layout), on tcgen05/TMEM/TMA: the batch tile is the UMMA M operand (64 or 128
+ * rows) and blocks of up to 256 weight rows the N operand, streamed once from HBM
+ * by a persistent grid (block height / split-K chosen to balance the SMs); launched
+ * with programmatic dependent launch so W starts streaming while the previous kernel
+ * finishes.  Replaces the projection / FFN / LM-head GEMMs of the decode step (the
+ * trunk of R/PAPER.md:175-182 and each mixer's projections, R/PAPER.md:1540-1625).
  *   SN_GEMM_STORE : out bf16 [M][ldo] = C
  *   SN_GEMM_SWIGLU: W is [2N][K] = [gate; up]; out bf16 [M][ldo] = silu(C_g)*C_u
+ *   SN_GEMM_SWIGLU_IL: same result, W pre-interleaved in blocks of h gate rows followed
+ *                   by the same h up rows (h = sn_gemm_swiglu_block(M, N, K); the last
+ *                   block zero-padded to 2h rows): one contiguous weight stream
  *   SN_GEMM_RESID : out fp32 [M][ldo] += C   (residual stream)
  *   SN_GEMM_PARTIAL: split-K; out fp32 [S][M][ldo] gets one K-split partial per slab,
  *                   S = sn_gemm_decode_splits(M, N, K, mode) (also returned in *splits_out);
  *                   the consumer sums the slabs (sn_add_rmsnorm does, in slab order).   */
-typedef enum { SN_GEMM_STORE = 0, SN_GEMM_SWIGLU = 1, SN_GEMM_RESID = 2, SN_GEMM_PARTIAL = 3 } sn_gemm_mode;
+typedef enum {
+  SN_GEMM_STORE = 0,
+  SN_GEMM_SWIGLU = 1,
+  SN_GEMM_RESID = 2,
+  SN_GEMM_PARTIAL = 3,
+  SN_GEMM_SWIGLU_IL = 4
+} sn_gemm_mode;
 int sn_gemm_decode_splits(int M, int N, int K, int mode);
-/* profiling aid: per-CTA pipeline wait counters of later launches (4 x #SMs u64), NULL = off */
+int sn_gemm_swiglu_block(int M, int N, int K);
+/* profiling aid: per-CTA pipeline counters of later launches (8 x #SMs u64), NULL = off */
 void sn_gemm_debug_stats(unsigned long long* dev_stats);
 sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw,
                          void* out, int ldo, int mode, int* splits_out, void* stream);

@@ -38,6 +38,7 @@ SIGNATURES = {
     "sn_delta_scan": [I, P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gated_rmsnorm": [P, P, I, P, P, I, I, I, Fl, I, I, P],
     "sn_gemm_decode_splits": [I, I, I, I],
+    "sn_gemm_swiglu_block": [I, I, I],
     "sn_gemm_debug_stats": [P],
     "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, P],
 }
@@ -45,7 +46,7 @@ RESTYPES = {"sn_gdn_chunk_workspace_bytes": ctypes.c_size_t, "sn_gemm_debug_stat
 
 SN_F32, SN_BF16 = 0, 1
 SN_ATTN_FORCE_SIMT = 0x100
-SN_GEMM_STORE, SN_GEMM_SWIGLU, SN_GEMM_RESID, SN_GEMM_PARTIAL = 0, 1, 2, 3
+SN_GEMM_STORE, SN_GEMM_SWIGLU, SN_GEMM_RESID, SN_GEMM_PARTIAL, SN_GEMM_SWIGLU_IL = 0, 1, 2, 3, 4
 ABI_VERSION = 1
 
 _lib = None

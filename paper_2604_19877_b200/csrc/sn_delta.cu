@@ -493,7 +493,7 @@ static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStre
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // state prefetch overlaps the in-proj tail
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA>, a);

@@ -157,6 +157,7 @@ struct GemmArgs {
   int a2_base;     // row offset of the second A tile inside a block: N (SwiGLU: up rows) or BR
   int ns;          // pipeline stages (runtime: as many as fit, so small blocks keep W in flight)
   int stage_bytes; // NA * br * 128 + BN * 128 (1024-aligned)
+  int dbg;         // experiments (env SN_GEMM_DBG): 1 = no TMA after the prologue (MMA-rate probe)
 };
 
 constexpr int kMaxStages = 32;
@@ -266,6 +267,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&empty_bar[s], (r - 1) & 1);  // consumed by every CTA of the cluster
         t_wait += clock64() - t0;
         uint8_t* st = smem + s * STAGE;
+        if (g.dbg & 1) {
+          mbar_arrive_local(&full_bar[s]);
+          continue;
+        }
         mbar_expect_tx(&full_bar[s], NA * a_bytes + B_BYTES);
         int blk, kc;
         unit(i, blk, kc);
@@ -465,6 +470,8 @@ static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, GemmArgs g
   if (ns > kMaxStages) ns = kMaxStages;
   g.ns = ns;
   g.stage_bytes = stage;
+  static int dbg = getenv("SN_GEMM_DBG") ? atoi(getenv("SN_GEMM_DBG")) : 0;
+  g.dbg = dbg;
   const int smem = ns * stage + tail + 1024;
   static bool attr = false;
   if (!attr) {
@@ -478,7 +485,7 @@ static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, GemmArgs g
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: overlap with the producer's tail
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   attrs[1].id = cudaLaunchAttributeClusterDimension;
   attrs[1].val.clusterDim.x = g.cs;
   attrs[1].val.clusterDim.y = 1;
@@ -512,6 +519,14 @@ static Plan make_plan(int M, int N, int K, int mode) {
   p.br = BM;
   p.splits = 1;
   pick_tiling(p.pair ? (N + 1) / 2 : N, K / BK, sms, p.na, p.bn, mode == SN_GEMM_PARTIAL ? 8 : 1, &p.br, &p.splits);
+  if (const char* f = getenv("SN_GEMM_FORCE")) {  // experiments: "br,splits"
+    int br = 0, sp = 0;
+    if (sscanf(f, "%d,%d", &br, &sp) == 2 && br >= 8 && br <= BM && br % 8 == 0 && sp >= 1 &&
+        (K / BK) % sp == 0 && (sp == 1 || mode == SN_GEMM_PARTIAL)) {
+      p.br = br;
+      p.splits = sp;
+    }
+  }
   p.row_mul = p.pair ? 2 * p.br : p.br;
   p.nblocks = (N + p.row_mul - 1) / p.row_mul;
   p.cs = cluster_size();
@@ -525,17 +540,37 @@ static Plan make_plan(int M, int N, int K, int mode) {
 }  // namespace gemm
 }  // namespace sn
 
+namespace sn {
+int gemm2_splits(int M, int N, int K, int mode);
+int gemm2_swiglu_block(int M, int N, int K);
+void gemm2_debug_stats(unsigned long long* s);
+sn_status gemm2_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw, void* out, int ldo,
+                       int mode, int* splits_out, cudaStream_t st);
+}  // namespace sn
+
 using namespace sn;
 using namespace sn::gemm;
+
+// Kernel generation: 2 = batch-as-M (sn_gemm2.cu, default), 1 = weights-as-M (this file).
+static int gemm_version() {
+  static int v = getenv("SN_GEMM_V") ? atoi(getenv("SN_GEMM_V")) : 2;
+  return v;
+}
 
 extern "C" {
 
 // Profiling aid: later launches write per-CTA counters [producer empty-wait, producer total,
 // MMA full-wait, MMA total (clock64); entry, first stage landed, last MMA issued, exit
 // (%globaltimer ns)] into dev_stats (8 x #SMs u64); NULL disables.
-void sn_gemm_debug_stats(unsigned long long* dev_stats) { g_stats = dev_stats; }
+void sn_gemm_debug_stats(unsigned long long* dev_stats) {
+  g_stats = dev_stats;
+  gemm2_debug_stats(dev_stats);
+}
+
+int sn_gemm_swiglu_block(int M, int N, int K) { return gemm_version() == 2 ? gemm2_swiglu_block(M, N, K) : 0; }
 
 int sn_gemm_decode_splits(int M, int N, int K, int mode) {
+  if (gemm_version() == 2) return gemm2_splits(M, N, K, mode);
   if (K % BK || mode != SN_GEMM_PARTIAL) return 1;
   return make_plan(M, N, K, mode).splits;
 }
@@ -546,10 +581,12 @@ sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, in
   SN_REQUIRE(M >= 1 && M <= 128, "sn_gemm_decode: M=%d must be in [1, 128] (decode batch)", M);
   SN_REQUIRE(K % BK == 0 && K >= BK, "sn_gemm_decode: K=%d must be a multiple of %d", K, BK);
   SN_REQUIRE(N >= 1 && ldw >= K && ldx >= K, "sn_gemm_decode: bad N/ld");
-  SN_REQUIRE(mode == SN_GEMM_STORE || mode == SN_GEMM_SWIGLU || mode == SN_GEMM_RESID || mode == SN_GEMM_PARTIAL,
+  SN_REQUIRE(mode == SN_GEMM_STORE || mode == SN_GEMM_SWIGLU || mode == SN_GEMM_RESID || mode == SN_GEMM_PARTIAL ||
+                 (mode == SN_GEMM_SWIGLU_IL && gemm_version() == 2),
              "sn_gemm_decode: mode %d", mode);
   SN_REQUIRE(((uintptr_t)x % 16) == 0 && ((uintptr_t)w % 16) == 0 && (ldx % 8) == 0 && (ldw % 8) == 0,
              "sn_gemm_decode: operands must be 16-byte aligned");
+  if (gemm_version() == 2) return gemm2_decode(x, M, K, ldx, w, N, ldw, out, ldo, mode, splits_out, (cudaStream_t)stream);
   const Plan pl = make_plan(M, N, K, mode);
   CUtensorMap wm, xm;
   const uint64_t wrows = pl.swiglu ? 2ull * N : (uint64_t)N;

@@ -1,0 +1,542 @@
+// Decode GEMM, batch-as-M formulation (tcgen05 + TMEM + TMA).
+//
+// C[m][n] = sum_k X[m][k] * W[n][k] with a decode batch M <= 128 and a weight W [N x K]
+// streamed from HBM once.  The activation tile X [M x 64] is the UMMA A operand (M = 64 or
+// 128 rows, zero-filled past the batch) and a block of up to 256 weight rows is the B
+// operand, so one tcgen05.mma (M=64, N=256, K=16) covers a 256-row weight block.
+//
+// Why not weights-as-M: with W as the M=128 operand every 128 weight rows need their own
+// UMMA per k-step and each re-reads the activation tile; measured on B200
+// (tools/umma_bench.cu, tools/gemm_force.py) the single issuing thread then spends
+// ~120 cycles per M=128 x N=64 UMMA once the stage barrier waits and commits are in the
+// loop, which caps a CTA at ~55 GB/s of weights.  An M=64 x N=256 UMMA runs 128 cycles
+// of tensor time for 4x the weight bytes, so the issue overhead hides under it and the
+// activation tile is read once per k-step.
+//
+// Work: units (row block, K split) are dealt round-robin to a persistent grid (<= #SMs);
+// the host picks the block height and split count that balance 148 SMs (make_plan).
+// Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 4-7 = epilogue
+// (TMEM -> registers -> global).  Two TMEM accumulators so a block's epilogue overlaps
+// the next block's MMAs.  PDL: the first stages of W are requested before
+// griddepcontrol.wait (weights do not depend on the previous kernel).
+//
+// Epilogues: STORE (bf16), SWIGLU (W = [gate; up], block = half gate rows + half up rows,
+// out = silu(g) * u), RESID (fp32 residual += acc), PARTIAL (fp32 split-K slab per split,
+// summed by the consumer in a fixed order -> deterministic).
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "sn_common.cuh"
+
+namespace sn {
+namespace gemm2 {
+
+constexpr int BK = 64;            // K per stage: one 128-byte swizzle row of bf16
+constexpr int kThreads = 256;
+constexpr int kMaxStages = 16;
+constexpr int kMaxRows = 256;     // UMMA N limit
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_noarrive(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, A and B K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// Same load without the wait: several in flight, then one tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// After tmem_wait_ld(): ties the loaded registers to this point so no use of them can be
+// scheduled between the asynchronous load and its wait.
+__device__ __forceinline__ void reg_fence16(float* v) {
+  asm volatile(""
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                 "+f"(v[15]));
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct Args {
+  void* out;     // bf16 [M][ldo] | fp32 residual [M][ldo] | fp32 slabs [splits][M][ldo]
+  int M, N, K, ldo, mode, kblocks;
+  int br;        // weight rows per block = UMMA N (multiple of 16, <= 256); SWIGLU: br/2 gate + br/2 up
+  int nblocks;   // row blocks
+  int splits;    // K splits per block (PARTIAL only)
+  int ns;        // pipeline stages
+  int stage_bytes;
+  int acc_cols;  // TMEM columns per accumulator buffer
+  unsigned long long* stats;
+  int dbg;       // experiments (env SN_GEMM_DBG): 2 = no epilogue stores
+  int pre;       // W stages requested before griddepcontrol.wait
+  int ks;        // 64-column K atoms per pipeline stage (amortises the per-stage barrier cost)
+};
+
+// smem stage: [ KS X atoms: UM rows x 128 B | KS W atoms: br rows x 128 B ]
+template <int UM>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap, const Args g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = g.splits, KB = g.kblocks / S, BR = g.br, NS = g.ns, STAGE = g.stage_bytes;
+  const int KS = g.ks, KU = KB / KS;  // 64-column atoms per stage, stages per item
+  const bool swiglu = g.mode == SN_GEMM_SWIGLU || g.mode == SN_GEMM_SWIGLU_IL;
+  const bool interleaved = g.mode == SN_GEMM_SWIGLU_IL;
+  const int half = BR >> 1;
+  const int q = blockIdx.x, Q = gridDim.x;
+  const int items = g.nblocks * S;
+  const int my_items = items > q ? (items - q + Q - 1) / Q : 0;
+  const int my_units = my_items * KU;
+  constexpr uint32_t X_BYTES = UM * BK * 2;
+  const uint32_t w_bytes = (uint32_t)BR * BK * 2;  // one 64-column atom of the weight block
+  const int w_atom = (int)w_bytes;
+  const int tmem_cols = 2 * g.acc_cols;
+  pdl_launch_dependents();
+  if (g.stats && threadIdx.x == 0) g.stats[blockIdx.x * 8 + 4] = clock64();
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    for (int i = 0; i < NS; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+      // unit = (item, k-step of KS 64-column atoms); walked with incremental counters
+      int it = 0, ku = 0, s = 0;
+      uint32_t ph = 0;
+      auto load = [&](bool w_part, bool x_part) {
+        const int j = q + it * Q;
+        const int blk = j / S;
+        const int kc0 = ((j % S) * KB + ku * KS) * BK;
+        uint8_t* st = smem + s * STAGE;
+#pragma unroll 1
+        for (int a = 0; a < KS; ++a) {
+          const int kc = kc0 + a * BK;
+          if (w_part) {
+            uint8_t* wt = st + KS * X_BYTES + a * w_atom;
+            if (swiglu && !interleaved) {
+              tma_load_2d(wt, &wmap, kc, blk * half, &full_bar[s], pw);
+              tma_load_2d(wt + half * 128, &wmap, kc, g.N + blk * half, &full_bar[s], pw);
+            } else {
+              tma_load_2d(wt, &wmap, kc, blk * BR, &full_bar[s], pw);
+            }
+          }
+          if (x_part) tma_load_2d(st + a * X_BYTES, &xmap, kc, 0, &full_bar[s], px);
+        }
+      };
+      auto advance = [&]() {
+        if (++ku == KU) { ku = 0; ++it; }
+        if (++s == NS) { s = 0; ph ^= 1; }
+      };
+      // Only the first g.pre stages of W are requested before griddepcontrol.wait: the
+      // activation tile of stage 0 queues behind them, so a deep W burst delays the first MMA.
+      const int npre = min(min(NS, g.pre), my_units);
+      for (int u = 0; u < npre; ++u) {
+        mbar_expect_tx_noarrive(&full_bar[s], KS * w_bytes);
+        load(true, false);
+        advance();
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      it = 0; ku = 0; s = 0; ph = 0;
+      for (int u = 0; u < npre; ++u) {
+        mbar_expect_tx(&full_bar[s], KS * X_BYTES);
+        load(false, true);
+        advance();
+      }
+      for (int u = npre; u < my_units; ++u) {
+        if (u >= NS) mbar_wait(&empty_bar[s], ph ^ 1);
+        mbar_expect_tx(&full_bar[s], KS * (w_bytes + X_BYTES));
+        load(true, true);
+        advance();
+      }
+      if (g.stats) g.stats[blockIdx.x * 8 + 1] = clock64();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = idesc_bf16(UM, BR);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < my_items; ++it) {
+        const int buf = it & 1;
+        if (it >= 2) mbar_wait(&tempty_bar[buf], ((it >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + buf * g.acc_cols;
+        for (int ku = 0; ku < KU; ++ku) {
+          mbar_wait(&full_bar[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sx = smem_u32(smem + s * STAGE);
+          const uint32_t sw = sx + KS * X_BYTES;
+#pragma unroll 1
+          for (int a = 0; a < KS; ++a) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma(acc, desc_sw128(sx + a * X_BYTES + k * 32), desc_sw128(sw + a * w_atom + k * 32), idesc,
+                   (ku | a | k) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[s]);
+          if (++s == NS) { s = 0; ph ^= 1; }
+        }
+        umma_commit(&tfull_bar[buf]);
+      }
+      if (g.stats) g.stats[blockIdx.x * 8 + 6] = clock64();
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp w drains TMEM lanes [32*(w%4), +32); lane <-> batch row
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int sp = warp & 3;
+    // UM=64: the accumulator occupies lanes 0-15 of each 32-lane subpartition (row 16*sp + t)
+    const int m = UM == 64 ? 16 * sp + lane : 32 * sp + lane;
+    const bool row_ok = (UM == 64 ? lane < 16 : true) && m < g.M;
+    const uint32_t lane_addr = (uint32_t)(32 * sp) << 16;
+    const int mode = g.mode;
+    const bool vec = (g.ldo & 7) == 0;
+    // store 16 consecutive output columns [n, n+16) of batch row m
+    auto emit = [&](float* v, int n, int split) {
+      const bool full = vec && n + 16 <= g.N;
+      if (mode == SN_GEMM_PARTIAL || mode == SN_GEMM_RESID) {
+        float* o = reinterpret_cast<float*>(g.out) + ((size_t)(mode == SN_GEMM_PARTIAL ? split : 0) * g.M + m) * g.ldo + n;
+        if (full) {
+          if (mode == SN_GEMM_RESID) {
+#pragma unroll
+            for (int e = 0; e < 16; e += 4) {
+              const float4 old = __ldcg(reinterpret_cast<const float4*>(o + e));
+              v[e] += old.x; v[e + 1] += old.y; v[e + 2] += old.z; v[e + 3] += old.w;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            __stcg(reinterpret_cast<float4*>(o + e), make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (n + e < g.N) o[e] = v[e] + (mode == SN_GEMM_RESID ? o[e] : 0.f);
+        }
+      } else {  // STORE / SWIGLU: bf16
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.out) + (size_t)m * g.ldo + n;
+        if (full) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            pk[e] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          reinterpret_cast<uint4*>(o)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          reinterpret_cast<uint4*>(o)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (n + e < g.N) o[e] = __float2bfloat16_rn(v[e]);
+        }
+      }
+    };
+    for (int it = 0; it < my_items; ++it) {
+      const int buf = it & 1;
+      const int j = q + it * Q;
+      const int blk = j / S, split = j % S;
+      mbar_wait(&tfull_bar[buf], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t acc = tmem + lane_addr + buf * g.acc_cols;
+      const int ncols = swiglu ? half : BR;
+      const int n_base = swiglu ? blk * half : blk * BR;
+      // 64 columns per round: up to 4 (SwiGLU: 8) TMEM loads in flight, one wait
+#pragma unroll 1
+      for (int c0 = 0; c0 < ncols; c0 += 64) {
+        float v[4][16], u[4][16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          if (c0 + 16 * q4 < ncols) {
+            tmem_ld16_async(acc + c0 + 16 * q4, v[q4]);
+            if (swiglu) tmem_ld16_async(acc + half + c0 + 16 * q4, u[q4]);
+          }
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          reg_fence16(v[q4]);
+          if (swiglu) reg_fence16(u[q4]);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int c = c0 + 16 * q4;
+          const int n = n_base + c;
+          if (c >= ncols || !row_ok || n >= g.N || (g.dbg & 2)) continue;
+          float* vv = v[q4];
+          if (swiglu) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) vv[e] = silu_f(vv[e]) * u[q4][e];
+          }
+          emit(vv, n, split);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[buf]);  // 4 epilogue warps -> count 4
+    }
+    if (g.stats && threadIdx.x == 128) g.stats[blockIdx.x * 8 + 7] = clock64();
+  }
+  __syncwarp();
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 map [rows][cols] (row stride ld elements), box {64 cols, box_rows}, 128B swizzle;
+// rows past the end are zero-filled (the batch tile past M).
+static bool map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                   uint32_t box_rows) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct Plan {
+  int um, br, splits, nblocks, grid;
+};
+
+// Per-CTA time ~ waves x k-blocks per unit x (weight rows + half the batch tile: the
+// activation tile comes from L2) + the split-K slab traffic the consumer pays.  Ties ->
+// fewer splits, then taller blocks.
+static Plan make_plan(int M, int N, int K, int mode) {
+  Plan p{};
+  const int sms = num_sms();
+  const int kblocks = K / BK;
+  p.um = M <= 64 ? 64 : 128;
+  const bool swiglu = mode == SN_GEMM_SWIGLU || mode == SN_GEMM_SWIGLU_IL;
+  const int max_splits = mode == SN_GEMM_PARTIAL ? 8 : 1;
+  double best = -1;
+  for (int s = 1; s <= max_splits; ++s) {
+    if (kblocks % s) continue;
+    // SwiGLU blocks hold br/2 gate + br/2 up rows; the epilogue drains 16 columns at a time
+    for (int br = kMaxRows; br >= 32; br -= swiglu ? 32 : 16) {
+      const long blocks = swiglu ? (N + br / 2 - 1) / (br / 2) : (N + br - 1) / br;
+      const long items = blocks * s;
+      const long waves = (items + sms - 1) / sms;
+      const double cost = (double)waves * (kblocks / s) * (br + p.um / 2) * 128.0 +
+                          (s > 1 ? (double)s * M * N * 8.0 / sms : 0.0);
+      if (best < 0 || cost < best * 0.999) { best = cost; p.br = br; p.splits = s; }
+    }
+  }
+  if (const char* f = getenv("SN_GEMM_FORCE")) {  // experiments: "br,splits"
+    int br = 0, sp = 0;
+    if (sscanf(f, "%d,%d", &br, &sp) == 2 && br >= 16 && br <= kMaxRows && br % (swiglu ? 32 : 16) == 0 && sp >= 1 &&
+        kblocks % sp == 0 && (sp == 1 || mode == SN_GEMM_PARTIAL)) {
+      p.br = br;
+      p.splits = sp;
+    }
+  }
+  p.nblocks = swiglu ? (N + p.br / 2 - 1) / (p.br / 2) : (N + p.br - 1) / p.br;
+  const int items = p.nblocks * p.splits;
+  p.grid = items < sms ? items : sms;
+  return p;
+}
+
+static unsigned long long* g_stats2 = nullptr;
+
+template <int UM>
+static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, Args g, int grid, cudaStream_t st) {
+  constexpr int kSmemMax = 227 * 1024;
+  // K atoms per stage: >= 32 KB of weights per stage barrier round trip (the issuing
+  // thread pays ~500 cycles per stage for the wait/commit/descriptors), >= 3 stages.
+  static int ks_env = getenv("SN_GEMM_KS") ? atoi(getenv("SN_GEMM_KS")) : 0;
+  const int kb_item = g.kblocks / g.splits;
+  int ks = 1;
+  if (ks_env > 0) {
+    ks = ks_env;
+    while (ks > 1 && kb_item % ks) ks >>= 1;
+  } else {
+    while (ks < 4 && g.br * BK * 2 * ks < 32768 && kb_item % (2 * ks) == 0 &&
+           (kSmemMax - 2048) / (2 * ks * (UM + g.br) * BK * 2) >= 3)
+      ks *= 2;
+  }
+  g.ks = ks;
+  const int stage = ks * (UM * BK * 2 + g.br * BK * 2);
+  int ns = (kSmemMax - 2048) / stage;
+  if (ns > kMaxStages) ns = kMaxStages;
+  g.ns = ns;
+  g.stage_bytes = stage;
+  int cols = 32;
+  while (cols < g.br) cols <<= 1;
+  g.acc_cols = cols;
+  const int smem = ns * stage + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm2_kernel<UM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax - 1024);
+    attr = true;
+  }
+  cudaError_t e = launch_pdl(gemm2_kernel<UM>, dim3(grid), dim3(kThreads), (size_t)smem, st, wm, xm, g);
+  if (e != cudaSuccess) {
+    set_error("sn_gemm_decode launch: %s", cudaGetErrorString(e));
+    return SN_ECUDA;
+  }
+  return check_launch("sn_gemm_decode");
+}
+
+}  // namespace gemm2
+
+// Entry used by sn_gemm_decode (sn_gemm.cu).
+int gemm2_swiglu_block(int M, int N, int K) {
+  if (K % gemm2::BK) return 0;
+  return gemm2::make_plan(M, N, K, SN_GEMM_SWIGLU_IL).br / 2;
+}
+
+int gemm2_splits(int M, int N, int K, int mode) {
+  if (K % gemm2::BK || mode != SN_GEMM_PARTIAL) return 1;
+  return gemm2::make_plan(M, N, K, mode).splits;
+}
+
+void gemm2_debug_stats(unsigned long long* s) { gemm2::g_stats2 = s; }
+
+sn_status gemm2_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw, void* out, int ldo,
+                       int mode, int* splits_out, cudaStream_t st) {
+  using namespace gemm2;
+  const Plan pl = make_plan(M, N, K, mode);
+  CUtensorMap wm, xm;
+  const bool swiglu = mode == SN_GEMM_SWIGLU;
+  // SWIGLU_IL: W pre-interleaved in blocks of [h gate rows; h up rows] (h = sn_gemm_swiglu_block)
+  const uint64_t wrows = mode == SN_GEMM_SWIGLU_IL ? (uint64_t)pl.nblocks * pl.br : swiglu ? 2ull * N : (uint64_t)N;
+  if (!map_2d(&wm, w, wrows, K, ldw, swiglu ? pl.br / 2 : pl.br) || !map_2d(&xm, x, M, K, ldx, pl.um)) {
+    set_error("sn_gemm_decode: cuTensorMapEncodeTiled failed");
+    return SN_ECUDA;
+  }
+  if (splits_out) *splits_out = pl.splits;
+  static int dbg = getenv("SN_GEMM_DBG") ? atoi(getenv("SN_GEMM_DBG")) : 0;
+  static int pre = getenv("SN_GEMM_PRE") ? atoi(getenv("SN_GEMM_PRE")) : 2;
+  Args g{out, M, N, K, ldo, mode, K / BK, pl.br, pl.nblocks, pl.splits, 0, 0, 0, g_stats2, dbg, pre};
+  return pl.um == 64 ? launch<64>(wm, xm, g, pl.grid, st) : launch<128>(wm, xm, g, pl.grid, st);
+}
+
+}  // namespace sn

@@ -81,22 +81,30 @@ class Supernet:
         self._alloc_decode_buffers()
         self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
         self.force_simt = False
-        # bf16 decode projections run either on the tcgen05 weight-streaming GEMM (libsn100:
-        # stacked 256-row tiles, split-K over all SMs, fp32 slabs summed by the consuming
-        # kernel — rope / GDN / KDA decode / silu_mul / add_rmsnorm — so there is no reduction
-        # kernel) or on cuBLAS.  Default from in-step B200 measurements (tools/step_breakdown.py):
-        # ours for the LM head and the FFN down-projection, where it is faster; cuBLAS for the
-        # rest (SN_DECODE_GEMMS=all switches everything to ours).  fp32 I/O uses cuBLAS fp32.
+        # bf16 decode projections run on the tcgen05 weight-streaming GEMM (libsn100, batch-as-M
+        # UMMA, persistent balanced grid; fp32 split-K slabs are summed by the consuming kernel,
+        # the gate/up projection fuses SiLU-mul) or on cuBLAS.  Default from in-step B200 A/B
+        # runs (tools/step_time.py): ours for the LM head, the fused FFN gate/up and the FFN
+        # down-projection; cuBLAS for the mixer in/out projections, where ours is ~par alone but
+        # slower inside the step.  SN_DECODE_GEMMS=all switches every role to ours.
         tc_ok = dtype == torch.bfloat16 and batch <= 128
         import os
-        sel = os.environ.get("SN_DECODE_GEMMS", "lm_head,ffn_down").split(",")
+        sel = os.environ.get("SN_DECODE_GEMMS", "lm_head,ffn_down,ffn_gate_up").split(",")
         self.sn_gemm = {r: tc_ok and (r in sel or "all" in sel)
-                        for r in ("lm_head", "ffn_down", "ffn_gate_up", "in_proj", "out_proj")}
+                        for r in ("lm_head", "ffn_down", "ffn_gate_up", "in_proj", "attn_qkv", "out_proj")}
         if tc_ok:  # fp32 split-K slabs of the input-side projections, summed by their consumers
             n_in = max([cfg.attn_qkv_width if k in (FA, SWA) else cfg.gdn_in_width if k == GDN else cfg.kda_in_width
                         for k in self.kinds])
             self.slab_in = torch.empty(8, batch, n_in, device=self.device, dtype=torch.float32)
             self.slab_gu = torch.empty(8, batch, 2 * cfg.ffn, device=self.device, dtype=torch.float32)
+        self.gu_mode = os.environ.get("SN_GU_MODE", "swiglu_il")
+        self.in_mode = os.environ.get("SN_IN_MODE", "store")
+        if self.sn_gemm["ffn_gate_up"] and self.gu_mode == "swiglu_il":
+            # fused gate/up + SiLU-mul: gate and up rows interleaved in the GEMM's block height
+            ffn = self.w["layers"][0]["ffn_gu"].shape[0] // 2
+            hb = ops.gemm_swiglu_block(batch, ffn, cfg.hidden)
+            for lw in self.w["layers"]:
+                lw["ffn_gu_il"] = ops.interleave_swiglu(lw["ffn_gu"], hb)
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -204,7 +212,7 @@ class Supernet:
         Hq, Hkv, D, P = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
-        qkv, ns = self._gemm_in(h, w["qkv"], d["qkv"])
+        qkv, ns = self._gemm_in(h, w["qkv"], d["qkv"], attn=True)
         self._probe_begin("rope_kv_append", fine=True)
         ops.rope_kv_append(qkv, None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
                            st["k"], st["v"], bt, Hq, Hkv, D, P, window, nsplit=ns)
@@ -254,11 +262,17 @@ class Supernet:
         if self.probe is not None and (self.probe.fine or not fine):
             self.probe.end(name)
 
-    def _gemm_in(self, x, w, out_bf16):
-        """Input-side projection: (tensor, nsplit) for the consuming kernel — fp32 split-K slabs
-        of the tcgen05 GEMM (summed on load by the consumer), or a cuBLAS bf16 result."""
+    def _gemm_in(self, x, w, out_bf16, attn=False):
+        """Input-side projection: (tensor, nsplit) for the consuming kernel — bf16 (tcgen05 GEMM
+        or cuBLAS), or fp32 split-K slabs of the tcgen05 GEMM summed on load by the consumer.
+        Role "in_proj" covers the delta-rule mixers, "attn_qkv" the attention projection (6144
+        rows: too few for a balanced unsplit weight stream, cuBLAS by default)."""
         self._probe_begin("gemm_in_proj", fine=True)
-        if self.sn_gemm["in_proj"]:
+        role = "attn_qkv" if attn else "in_proj"
+        if self.sn_gemm[role] and self.in_mode == "store":
+            ops.gemm_decode(x, w, out_bf16, "store")
+            res = (out_bf16, 0)
+        elif self.sn_gemm[role]:
             slab = self._slab_view(self.slab_in, w.shape[0])
             res = (slab, ops.gemm_decode(x, w, slab, "partial"))
         else:
@@ -326,15 +340,19 @@ class Supernet:
                 pending = self._attn_decode(l, kind, self.h, self.mix_out)
             self._norm(pending, lw["norm2"])
             self._probe_begin("gemm_ffn_gate_up", fine=True)
-            if self.sn_gemm["ffn_gate_up"]:
-                gu, ns = self.slab_gu, ops.gemm_decode(self.h, lw["ffn_gu"], self.slab_gu, "partial")
+            if self.sn_gemm["ffn_gate_up"] and self.gu_mode == "swiglu_il":
+                ops.gemm_decode(self.h, lw["ffn_gu_il"], self.act, "swiglu_il")
+                self._probe_end("gemm_ffn_gate_up", fine=True)
             else:
-                torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
-                gu, ns = self.gu, 0
-            self._probe_end("gemm_ffn_gate_up", fine=True)
-            self._probe_begin("silu_mul", fine=True)
-            ops.silu_mul(gu, self.act, nsplit=ns)
-            self._probe_end("silu_mul", fine=True)
+                if self.sn_gemm["ffn_gate_up"]:
+                    gu, ns = self.slab_gu, ops.gemm_decode(self.h, lw["ffn_gu"], self.slab_gu, "partial")
+                else:
+                    torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
+                    gu, ns = self.gu, 0
+                self._probe_end("gemm_ffn_gate_up", fine=True)
+                self._probe_begin("silu_mul", fine=True)
+                ops.silu_mul(gu, self.act, nsplit=ns)
+                self._probe_end("silu_mul", fine=True)
             pending = self._gemm_residual(self.act, lw["ffn_down"], self.slab_ffn, self.ffn_out, "ffn_down")
         self._norm(pending, w["final_norm"])
         self._gemm_store(self.h, w["lm_head"], self.logits, "lm_head")
@@ -351,9 +369,12 @@ class Supernet:
         for kind in self.kinds:
             sn += 2                            # two add_rmsnorm
             sn += 2 if kind in (FA, SWA) else 1    # rope+attention | fused delta-rule decode
-            for role in ("in_proj", "out_proj", "ffn_down", "ffn_gate_up"):
+            for role in ("attn_qkv" if kind in (FA, SWA) else "in_proj", "out_proj", "ffn_down", "ffn_gate_up"):
                 sn, lib = (sn + 1, lib) if g[role] else (sn, lib + 1)
-            sn += 1                            # silu_mul (sums the gate/up split-K slabs)
+            if kind == KDA and not g["in_proj"]:
+                lib += 1                       # low-rank gate second factors (batched GEMM)
+            if not (g["ffn_gate_up"] and self.gu_mode == "swiglu_il"):
+                sn += 1                        # silu_mul (fused into the gate/up GEMM otherwise)
         return {"sn": sn, "cublas": lib}
 
     @torch.no_grad()

@@ -12,6 +12,7 @@ import torch
 
 from . import _lib
 from ._lib import (SN_ATTN_FORCE_SIMT, SN_BF16, SN_F32, SN_GEMM_PARTIAL, SN_GEMM_RESID, SN_GEMM_STORE, SN_GEMM_SWIGLU,
+                   SN_GEMM_SWIGLU_IL,
                    call)
 
 _DT = {torch.bfloat16: SN_BF16, torch.float32: SN_F32}
@@ -137,7 +138,27 @@ def gated_rmsnorm(o, gate, gate_stride, norm_w, out, H, D, eps, act):
          dtype_code(out.dtype), _s())
 
 
-GEMM_MODES = {"store": SN_GEMM_STORE, "swiglu": SN_GEMM_SWIGLU, "resid": SN_GEMM_RESID, "partial": SN_GEMM_PARTIAL}
+GEMM_MODES = {"store": SN_GEMM_STORE, "swiglu": SN_GEMM_SWIGLU, "resid": SN_GEMM_RESID, "partial": SN_GEMM_PARTIAL,
+              "swiglu_il": SN_GEMM_SWIGLU_IL}
+
+
+def gemm_swiglu_block(M, N, K):
+    """Block half-height h of the interleaved SwiGLU weight layout (mode "swiglu_il")."""
+    return _lib.load().sn_gemm_swiglu_block(M, N, K)
+
+
+def interleave_swiglu(w_gu, h):
+    """[gate; up] ([2N, K]) -> blocks of h gate rows then the same h up rows, zero-padded to
+    ceil(N / h) blocks of 2h rows: the weight layout of mode "swiglu_il"."""
+    N2, K = w_gu.shape
+    N = N2 // 2
+    nb = -(-N // h)
+    out = torch.zeros(nb, 2, h, K, dtype=w_gu.dtype, device=w_gu.device)
+    g = torch.zeros(nb * h, K, dtype=w_gu.dtype, device=w_gu.device)
+    u = torch.zeros_like(g)
+    g[:N], u[:N] = w_gu[:N], w_gu[N:]
+    out[:, 0], out[:, 1] = g.view(nb, h, K), u.view(nb, h, K)
+    return out.view(nb * 2 * h, K)
 
 
 def gemm_decode_splits(M, N, K, mode="partial"):
@@ -152,6 +173,9 @@ def gemm_decode(x, w, out, mode="store"):
     M, K = x.shape
     code = GEMM_MODES[mode]
     N = out.shape[-1] if mode not in ("store",) else w.shape[0]
+    if mode == "swiglu_il":
+        h = gemm_swiglu_block(M, N, K)
+        assert h > 0 and w.shape[0] == -(-N // h) * 2 * h, "weight not in the interleaved layout for this shape"
     if mode == "swiglu":
         assert w.shape[0] == 2 * N
     if mode in ("resid", "partial"):

@@ -29,13 +29,15 @@ def test_gemm_store(M, N, K):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("M", [1, 64, 128])
-def test_gemm_swiglu(M):
-    F, K = 768, 512
+@pytest.mark.parametrize("F,K", [(768, 512), (14336, 5120), (1000, 256)])
+@pytest.mark.parametrize("mode", ["swiglu", "swiglu_il"])
+def test_gemm_swiglu(M, F, K, mode):
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(2 * F, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
     out = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
-    ops.gemm_decode(x, w, out, "swiglu")
+    wk = w if mode == "swiglu" else ops.interleave_swiglu(w, ops.gemm_swiglu_block(M, F, K))
+    ops.gemm_decode(x, wk, out, mode)
     torch.cuda.synchronize()
     gu = _ref(x, w)
     ref = torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]

@@ -5,22 +5,24 @@ import torch
 from paper_2604_19877_b200 import ops
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-shapes = [("ffn_gu(swiglu)", 14336, 5120, "swiglu"), ("ffn_gu(partial)", 28672, 5120, "partial"),
+shapes = [("ffn_gu(swiglu_il)", 14336, 5120, "swiglu_il"), ("ffn_gu(swiglu)", 14336, 5120, "swiglu"), ("ffn_gu(partial)", 28672, 5120, "partial"),
           ("ffn_down(partial)", 5120, 14336, "partial"),
           ("gdn_in(partial)", 10304, 5120, "partial"), ("gdn_out(partial)", 5120, 4096, "partial"),
           ("attn_qkv(partial)", 6144, 5120, "partial"), ("kda_in(partial)", 12576, 5120, "partial"),
           ("lm_head", 131072, 5120, "store")]
 for name, N, K, mode in shapes:
-    rows = 2 * N if mode == "swiglu" else N
+    rows = 2 * N if mode.startswith("swiglu") else N
     nbuf = max(2, min(8, int(3e9 // (rows * K * 2))))
     Ws = [torch.randn(rows, K, device="cuda").to(torch.bfloat16) for _ in range(nbuf)]
+    if mode == "swiglu_il":
+        Ws = [ops.interleave_swiglu(w_, ops.gemm_swiglu_block(M, N, K)) for w_ in Ws]
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     if mode == "partial":
         out = torch.zeros(8, M, N, device="cuda", dtype=torch.float32)
     else:
         out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if mode == "resid" else torch.bfloat16)
     res = {}
-    splits = ops.gemm_decode_splits(M, N if mode != "swiglu" else 2 * N, K, mode) if mode == "partial" else 1
+    splits = ops.gemm_decode_splits(M, N, K, mode) if mode == "partial" else 1
     for impl in ("sn", "cublas"):
         def run(i):
             if impl == "sn":
