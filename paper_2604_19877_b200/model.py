@@ -75,6 +75,7 @@ class Supernet:
                 cfg = tp_config(cfg, self.tp)
         self.cfg = cfg
         self.w = cast_weights(weights, self.device, dtype)
+        del weights  # self.w may alias it; the FFN interleave below must free the original rows
         self.inv_freq = cfg.inv_freq().to(device=self.device, dtype=torch.float32)
         self.scale_attn = attn_scale(cfg)
         self._alloc_state(fa_block_table)
@@ -101,10 +102,15 @@ class Supernet:
         self.in_mode = os.environ.get("SN_IN_MODE", "store")
         if self.sn_gemm["ffn_gate_up"] and self.gu_mode == "swiglu_il":
             # fused gate/up + SiLU-mul: gate and up rows interleaved in the GEMM's block height
+            # the interleaved copy replaces [gate; up] (no doubled FFN weights in HBM); prefill
+            # de-interleaves its GEMM output (deinterleave_swiglu)
             ffn = self.w["layers"][0]["ffn_gu"].shape[0] // 2
             hb = ops.gemm_swiglu_block(batch, ffn, cfg.hidden)
+            self.gu_il = (ffn, hb)
             for lw in self.w["layers"]:
-                lw["ffn_gu_il"] = ops.interleave_swiglu(lw["ffn_gu"], hb)
+                lw["ffn_gu_il"] = ops.interleave_swiglu(lw.pop("ffn_gu"), hb)
+        else:
+            self.gu_il = None
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -419,7 +425,10 @@ class Supernet:
                 self._kda_prefill(l, h, mix, cu)
             self._tp_sum(mix)
             ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
-            gu = h @ lw["ffn_gu"].t()
+            if self.gu_il is not None:
+                gu = ops.deinterleave_swiglu(h @ lw["ffn_gu_il"].t(), *self.gu_il)
+            else:
+                gu = h @ lw["ffn_gu"].t()
             act = e(rows, cfg.ffn)
             ops.silu_mul(gu, act)
             torch.mm(act, lw["ffn_down"].t(), out=ffn_o)

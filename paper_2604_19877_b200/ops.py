@@ -153,12 +153,19 @@ def interleave_swiglu(w_gu, h):
     N2, K = w_gu.shape
     N = N2 // 2
     nb = -(-N // h)
-    out = torch.zeros(nb, 2, h, K, dtype=w_gu.dtype, device=w_gu.device)
-    g = torch.zeros(nb * h, K, dtype=w_gu.dtype, device=w_gu.device)
-    u = torch.zeros_like(g)
-    g[:N], u[:N] = w_gu[:N], w_gu[N:]
-    out[:, 0], out[:, 1] = g.view(nb, h, K), u.view(nb, h, K)
-    return out.view(nb * 2 * h, K)
+    out = torch.zeros(nb * 2 * h, K, dtype=w_gu.dtype, device=w_gu.device)
+    i = torch.arange(N, device=w_gu.device)
+    dst = (i // h) * (2 * h) + i % h
+    out.index_copy_(0, dst, w_gu[:N])
+    out.index_copy_(0, dst + h, w_gu[N:])
+    return out
+
+
+def deinterleave_swiglu(gu_il, N, h):
+    """Inverse of interleave_swiglu on GEMM outputs: [rows, nb*2h] -> [rows, 2N] = [gate | up]."""
+    rows = gu_il.shape[0]
+    v = gu_il.view(rows, -1, 2, h)
+    return torch.cat([v[:, :, 0].reshape(rows, -1)[:, :N], v[:, :, 1].reshape(rows, -1)[:, :N]], 1)
 
 
 def gemm_decode_splits(M, N, K, mode="partial"):

@@ -38,3 +38,17 @@ def test_kernel_launch_bytes():
     assert gd == 64 * (2 * 32 * 128 * 128 * 4 + 2 * 6144 * 3 * 2 + (10304 + 4096) * 2)
     sw = roofline.kernel_launch_bytes(APRIEL, "swa_decode", 64, 32768)
     assert sw == 64 * (4096 * 4096 + 2 * 32 * 128 * 2)
+
+
+def test_swiglu_interleave_roundtrip():
+    """The fused gate/up weight layout (mode swiglu_il) and its prefill inverse are exact."""
+    import torch
+    from paper_2604_19877_b200 import ops
+    N, K, h = 100, 8, 48
+    w = torch.randn(2 * N, K)
+    il = ops.interleave_swiglu(w, h)
+    assert il.shape == (3 * 2 * h, K)
+    x = torch.randn(5, K)
+    assert torch.equal(ops.deinterleave_swiglu(x @ il.t(), N, h), x @ w.t())
+    assert torch.equal(il.view(3, 2, h, K)[:, 0].reshape(-1, K)[:N], w[:N])
+    assert not il.view(3, 2, h, K)[-1, :, N - 2 * h:].any()
