@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsn100.so")
+# SN_LIB: A/B experiments against another build of the same ABI (tools/); default in-tree
+LIB_PATH = os.environ.get("SN_LIB") or os.path.join(_HERE, "libsn100.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int
