@@ -211,6 +211,20 @@ sn_status sn_gdn_chunk_prefill2(const float* qn, const float* kn, const void* qk
                                 int num_seqs, int Hk, int Hv, int D, int init_state,
                                 int dtype, void* stream);
 
+/* Two-phase chunked KDA prefill: the same WY chunk form with a per-key-channel
+ * gate (FLA naive_chunk_kda, 3P-FLA/ops/kda/naive.py:69-166).  Hk = Hv = H;
+ * glog: fp32 [rows][H][D] per-channel log gates (sn_delta_prep kind 1 with glog);
+ * workspace: sn_kda_chunk_workspace_bytes(num_chunks, H, D).  Replaces the
+ * token-sequential sn_delta_scan(kind=1) for bf16 prompts.                      */
+size_t sn_kda_chunk_workspace_bytes(int num_chunks, int H, int D);
+sn_status sn_kda_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv,
+                                int v_off, int qkv_stride, const float* glog,
+                                const float* beta, const int32_t* chunks,
+                                const int32_t* seq_chunk0, int num_chunks, void* workspace,
+                                float* o, float* state, const int32_t* slot_idx,
+                                int num_seqs, int H, int D, int init_state,
+                                int dtype, void* stream);
+
 /* out[r,h,:] = RMSNorm(o[r,h,:]) * norm_w * act(gate[r, h*D + :]),
  * act: 0 = silu (GDN), 1 = sigmoid (KDA).  gate row stride gate_stride.    */
 sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride,

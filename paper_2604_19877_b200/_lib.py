@@ -36,6 +36,8 @@ SIGNATURES = {
     "sn_gdn_chunk_prefill": [P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gdn_chunk_workspace_bytes": [I, I, I],
     "sn_gdn_chunk_prefill2": [P, P, P, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, I, P],
+    "sn_kda_chunk_workspace_bytes": [I, I, I],
+    "sn_kda_chunk_prefill2": [P, P, P, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, P],
     "sn_delta_scan": [I, P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gated_rmsnorm": [P, P, I, P, P, I, I, I, Fl, I, I, P],
     "sn_gemm_decode_splits": [I, I, I, I],
@@ -43,7 +45,7 @@ SIGNATURES = {
     "sn_gemm_debug_stats": [P],
     "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, P],
 }
-RESTYPES = {"sn_gdn_chunk_workspace_bytes": ctypes.c_size_t, "sn_gemm_debug_stats": None, "sn_attn_decode_workspace_bytes": ctypes.c_size_t, "sn_abi_version": ctypes.c_int}
+RESTYPES = {"sn_gdn_chunk_workspace_bytes": ctypes.c_size_t, "sn_kda_chunk_workspace_bytes": ctypes.c_size_t, "sn_gemm_debug_stats": None, "sn_attn_decode_workspace_bytes": ctypes.c_size_t, "sn_abi_version": ctypes.c_int}
 
 SN_F32, SN_BF16 = 0, 1
 SN_ATTN_FORCE_SIMT = 0x100

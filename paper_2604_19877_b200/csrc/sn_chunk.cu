@@ -569,7 +569,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int D>
+// PERCH (KDA): glast holds the chunk's per-key-channel cumulative log decay [D] per (chunk,
+// head) and S is decayed row-wise, diag(e^{G_C}) S; otherwise one scalar per (chunk, head).
+template <int D, bool PERCH = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gdn_chunk_state_kernel(const __nv_bfloat16* __restrict__ ws, const float* __restrict__ glast,
                            const int32_t* __restrict__ chunks, const int32_t* __restrict__ seq_chunk0,
@@ -708,15 +710,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<float2*>(o + ((size_t)(c0 + r) * Hv + h) * D + cc) = make_float2(oc[nt][e], oc[nt][e + 1]);
         }
     }
-    // S = e^{G_C} S + Kd^T V'
+    // S = e^{G_C} S + Kd^T V'   (KDA: diag(e^{G_C}) S, one factor per key row)
     {
-      const float dec = expf(glast[(size_t)n * Hv + h]);
+      if (PERCH) {
+        const float* gl = glast + ((size_t)n * Hv + h) * D;
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const float dec = expf(gl[(warp * MT + mt) * 16 + g4 + (e2 << 3)]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sf[mt][nt][e] *= dec;
+            for (int nt = 0; nt < 8; ++nt) {
+              sf[mt][nt][2 * e2] *= dec;
+              sf[mt][nt][2 * e2 + 1] *= dec;
+            }
+          }
+      } else {
+        const float dec = expf(glast[(size_t)n * Hv + h]);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) sf[mt][nt][e] *= dec;
+      }
 #pragma unroll
       for (int ks = 0; ks < C; ks += 16) {
 #pragma unroll
@@ -769,6 +786,237 @@ static sn_status launch_two_phase(const float* qn, const float* kn, const void* 
   return check_launch("sn_gdn_chunk_prefill(state)");
 }
 
+// =====================================================================================
+// KDA (per-key-channel gate) chunk-local phase.  Oracle: the token recurrence
+// S_t = (I - b k k^T) diag(e^{g_t}) S_{t-1} + b k v^T (oracle/supernet_oracle.py), pinned to
+// FLA's naive_chunk_kda (3P-FLA/ops/kda/naive.py:69-166), whose chunk form this follows with
+// G = in-chunk cumulative log decay per channel:
+//   A_kk[i][j] = b_i sum_d k_id k_jd e^{G_id - G_jd} (i > j),  A_qk[i][j] = sum_d q_id k_jd e^{G_id - G_jd} (i >= j)
+//   T = (I + A_kk)^{-1},  W = T (b o e^G o K),  U = T (b o V),  Qg = e^G o Q,  Kd = e^{G_C - G} o K
+// The state pass is the GDN one with a per-channel decay (gdn_chunk_state_kernel<D, true>).
+// Per-channel decay factors cannot be pulled out of a plain K K^T product (G spans up to
+// ~100 in a 64-token chunk: e^{-G} overflows fp32), so warp w (rows 16w..16w+15, one
+// 16-token sub-chunk) factorises around its own reference row r = 16w:
+//   e^{G_i - G_j} = e^{G_i - G_r} . e^{G_r - G_j}
+// with e^{G_i - G_r} <= 1 for i >= r and e^{G_r - G_j} <= 1 for j < r; only the diagonal
+// 16x16 block has factors > 1 (at most the decay of 15 tokens, far from overflow).  The
+// left operand is the warp's own 16 rows; the right operand (16(w+1) rows of K scaled to
+// reference r) is a per-warp shared-memory tile, and both products run on mma.sync.
+
+template <int D>
+struct KdaIntraSmem {
+  static constexpr int LDK = D + 8, LDC = C + 8;
+  static constexpr int KR_ROWS = 16 * (1 + 2 + 3 + 4);  // per-warp right operands
+  __nv_bfloat16 q[C * LDK];
+  __nv_bfloat16 k[C * LDK];
+  union {
+    struct { __nv_bfloat16 ql[C * LDK]; __nv_bfloat16 kl[C * LDK]; } a;  // A step: left operands
+    struct { __nv_bfloat16 kb[C * LDK]; __nv_bfloat16 vb[C * LDK]; } w;  // W/U step
+  } u1;
+  union {
+    __nv_bfloat16 kr[KR_ROWS * LDK];
+    struct { float l[C][C + 1]; float x[C][C + 1]; } lx;
+  } u2;
+  __nv_bfloat16 t[C * LDC];
+  float g[C * D];  // G[r][d]: cumulative log decay
+  float beta[C];
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads)
+    kda_chunk_intra_kernel(const float* __restrict__ qn, const float* __restrict__ kn, const T* __restrict__ qkv,
+                           int v_off, int qkv_stride, const float* __restrict__ glog, const float* __restrict__ beta,
+                           const int32_t* __restrict__ chunks, __nv_bfloat16* __restrict__ ws,
+                           float* __restrict__ glast, int H) {
+  pdl_launch_dependents();
+  using SM = KdaIntraSmem<D>;
+  constexpr int LDK = SM::LDK, LDC = SM::LDC;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int n = blockIdx.x, h = blockIdx.y;
+  const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
+  for (int idx = tid; idx < C * D / 4; idx += kThreads) {
+    const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
+    float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), kv = qv, gv = qv;
+    if (r < len) {
+      const size_t off = ((size_t)(c0 + r) * H + h) * D + c4;
+      qv = *reinterpret_cast<const float4*>(qn + off);
+      kv = *reinterpret_cast<const float4*>(kn + off);
+      gv = *reinterpret_cast<const float4*>(glog + off);
+    }
+    *reinterpret_cast<uint2*>(&sm.q[r * LDK + c4]) = make_uint2(pack_bf16(qv.x, qv.y), pack_bf16(qv.z, qv.w));
+    *reinterpret_cast<uint2*>(&sm.k[r * LDK + c4]) = make_uint2(pack_bf16(kv.x, kv.y), pack_bf16(kv.z, kv.w));
+    *reinterpret_cast<float4*>(&sm.g[r * D + c4]) = gv;
+  }
+  if (tid < C) sm.beta[tid] = tid < len ? beta[(size_t)(c0 + tid) * H + h] : 0.f;
+  __syncthreads();
+  for (int d = tid; d < D; d += kThreads) {  // per-channel prefix sum over the chunk
+    float acc = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < C; ++r) {
+      acc += sm.g[r * D + d];
+      sm.g[r * D + d] = acc;
+    }
+  }
+  __syncthreads();
+  // ---- per-warp operands around reference row r0 = 16 * warp
+  const int r0 = 16 * warp, nrows = 16 * (warp + 1);
+  __nv_bfloat16* kr = sm.u2.kr + 16 * (warp * (warp + 1) / 2) * LDK;
+  for (int idx = lane; idx < 16 * D / 2; idx += 32) {
+    const int r = r0 + idx / (D / 2), cc = (idx % (D / 2)) * 2;
+    const float e0 = expf(sm.g[r * D + cc] - sm.g[r0 * D + cc]), e1 = expf(sm.g[r * D + cc + 1] - sm.g[r0 * D + cc + 1]);
+    const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[r * LDK + cc]));
+    const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[r * LDK + cc]));
+    *reinterpret_cast<uint32_t*>(&sm.u1.a.ql[r * LDK + cc]) = pack_bf16(qv.x * e0, qv.y * e1);
+    *reinterpret_cast<uint32_t*>(&sm.u1.a.kl[r * LDK + cc]) = pack_bf16(kv.x * e0, kv.y * e1);
+  }
+  for (int idx = lane; idx < nrows * D / 2; idx += 32) {
+    const int j = idx / (D / 2), cc = (idx % (D / 2)) * 2;
+    const float e0 = expf(sm.g[r0 * D + cc] - sm.g[j * D + cc]), e1 = expf(sm.g[r0 * D + cc + 1] - sm.g[j * D + cc + 1]);
+    const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[j * LDK + cc]));
+    *reinterpret_cast<uint32_t*>(&kr[j * LDK + cc]) = pack_bf16(kv.x * e0, kv.y * e1);
+  }
+  __syncwarp();
+  float kk[8][4], qk[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) kk[nt][e] = qk[nt][e] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < D; ks += 16) {
+    uint32_t ak[4], aq[4];
+    lda(sm.u1.a.kl, LDK, r0, ks, ak);
+    lda(sm.u1.a.ql, LDK, r0, ks, aq);
+#pragma unroll
+    for (int nt = 0; nt < 8; nt += 2) {
+      if (nt * 8 < nrows) {  // warp-uniform: only column blocks at or left of the diagonal
+        uint32_t b0, b1, b2, b3;
+        ldb_nk(kr, LDK, nt * 8, ks, b0, b1, b2, b3);
+        mma_bf16(kk[nt], ak, b0, b1);
+        mma_bf16(kk[nt + 1], ak, b2, b3);
+        mma_bf16(qk[nt], aq, b0, b1);
+        mma_bf16(qk[nt + 1], aq, b2, b3);
+      }
+    }
+  }
+  __syncthreads();  // every warp is done with kr before l / x (aliased) are written
+  __nv_bfloat16* rec = ws + ws_tile<D>(n, h, H);
+  __nv_bfloat16* wW = rec;
+  __nv_bfloat16* wQg = rec + C * D;
+  __nv_bfloat16* wKd = rec + 2 * C * D;
+  __nv_bfloat16* wU = rec + 3 * C * D;
+  __nv_bfloat16* wP = rec + 4 * C * D;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; e += 2) {
+      const int i = r0 + g4 + ((e >> 1) << 3), j = nt * 8 + t4 * 2;
+      float pv[2];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const bool in = j + d < nrows;
+        sm.u2.lx.l[i][j + d] = in && i > j + d ? -sm.beta[i] * kk[nt][e + d] : 0.f;
+        pv[d] = in && i >= j + d ? qk[nt][e + d] : 0.f;
+      }
+      *reinterpret_cast<uint32_t*>(wP + i * C + j) = pack_bf16(pv[0], pv[1]);
+    }
+  if (tid < C) sm.u2.lx.x[0][tid] = tid == 0 ? 1.f : 0.f;
+  // chunk-global operands: b e^G K, b V (W/U step), e^G Q and e^{G_C - G} K (state pass)
+  for (int idx = tid; idx < C * D / 2; idx += kThreads) {
+    const int r = idx / (D / 2), cc = (idx % (D / 2)) * 2;
+    const float g0 = sm.g[r * D + cc], g1 = sm.g[r * D + cc + 1];
+    const float gl0 = sm.g[(C - 1) * D + cc], gl1 = sm.g[(C - 1) * D + cc + 1];
+    const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[r * LDK + cc]));
+    const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[r * LDK + cc]));
+    const float b = sm.beta[r];
+    *reinterpret_cast<uint32_t*>(&sm.u1.w.kb[r * LDK + cc]) = pack_bf16(kv.x * b * expf(g0), kv.y * b * expf(g1));
+    *reinterpret_cast<uint32_t*>(wKd + r * D + cc) = pack_bf16(kv.x * expf(gl0 - g0), kv.y * expf(gl1 - g1));
+    *reinterpret_cast<uint32_t*>(wQg + r * D + cc) = pack_bf16(qv.x * expf(g0), qv.y * expf(g1));
+  }
+  for (int idx = tid; idx < C * D; idx += kThreads) {
+    const int r = idx / D, cc = idx % D;
+    const float v = r < len ? io<T>::ld(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + cc) : 0.f;
+    sm.u1.w.vb[r * LDK + cc] = __float2bfloat16_rn(v * sm.beta[r]);
+  }
+  for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.g[(C - 1) * D + d];
+  __syncthreads();
+  // T = (I - L)^{-1} by forward substitution (row i depends on rows < i)
+  for (int i = 1; i < C; ++i) {
+    if (tid < C) {
+      const int j = tid;
+      float acc = 0.f;
+      if (j < i) {
+        acc = sm.u2.lx.l[i][j];
+        for (int m = j + 1; m < i; ++m) acc += sm.u2.lx.l[i][m] * sm.u2.lx.x[m][j];
+      } else if (j == i) {
+        acc = 1.f;
+      }
+      sm.u2.lx.x[i][j] = acc;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < C * C; idx += kThreads) {
+    const int i = idx / C, j = idx % C;
+    sm.t[i * LDC + j] = __float2bfloat16_rn(sm.u2.lx.x[i][j]);
+  }
+  __syncthreads();
+  // W = T Kb, U = T Vb -> workspace
+  {
+    float wacc[D / 8][4], uacc[D / 8][4];
+#pragma unroll
+    for (int nt = 0; nt < D / 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) wacc[nt][e] = uacc[nt][e] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < C; ks += 16) {
+      uint32_t a[4];
+      lda(sm.t, LDC, warp * 16, ks, a);
+#pragma unroll
+      for (int nt = 0; nt < D / 8; nt += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldb_kn(sm.u1.w.kb, LDK, nt * 8, ks, b0, b1, b2, b3);
+        mma_bf16(wacc[nt], a, b0, b1);
+        mma_bf16(wacc[nt + 1], a, b2, b3);
+        ldb_kn(sm.u1.w.vb, LDK, nt * 8, ks, b0, b1, b2, b3);
+        mma_bf16(uacc[nt], a, b0, b1);
+        mma_bf16(uacc[nt + 1], a, b2, b3);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < D / 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; e += 2) {
+        const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = nt * 8 + t4 * 2;
+        *reinterpret_cast<uint32_t*>(wW + r * D + cc) = pack_bf16(wacc[nt][e], wacc[nt][e + 1]);
+        *reinterpret_cast<uint32_t*>(wU + r * D + cc) = pack_bf16(uacc[nt][e], uacc[nt][e + 1]);
+      }
+  }
+}
+
+template <typename T, int D>
+static sn_status launch_kda_two_phase(const float* qn, const float* kn, const void* qkv, int v_off, int qkv_stride,
+                                      const float* glog, const float* beta, const int32_t* chunks,
+                                      const int32_t* seq_chunk0, int num_chunks, void* ws, float* glast, float* o,
+                                      float* state, const int32_t* slot_idx, int num_seqs, int H, int init_state,
+                                      cudaStream_t st) {
+  const int smem_a = (int)sizeof(KdaIntraSmem<D>), smem_b = (int)sizeof(StateSmem<D>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kda_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
+    attr = true;
+  }
+  kda_chunk_intra_kernel<T, D><<<dim3(num_chunks, H), kThreads, smem_a, st>>>(
+      qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, H);
+  sn_status e = check_launch("sn_kda_chunk_prefill(intra)");
+  if (e != SN_OK) return e;
+  gdn_chunk_state_kernel<D, true><<<dim3(D / VT, H, num_seqs), kThreads, smem_b, st>>>(
+      (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
+  return check_launch("sn_kda_chunk_prefill(state)");
+}
+
 }  // namespace chunk
 }  // namespace sn
 
@@ -790,6 +1038,33 @@ sn_status sn_gdn_chunk_prefill(const float* qn, const float* kn, const void* qkv
                                               cu_seqlens, num_seqs, Hk, Hv, init_state, st);
   return chunk::launch<__nv_bfloat16, 64>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, o, state, slot_idx,
                                            cu_seqlens, num_seqs, Hk, Hv, init_state, st);
+}
+
+size_t sn_kda_chunk_workspace_bytes(int num_chunks, int H, int D) {
+  return (size_t)num_chunks * H * (4 * (size_t)chunk::C * D + (size_t)chunk::C * chunk::C) * 2 +
+         (size_t)num_chunks * H * D * sizeof(float);
+}
+
+sn_status sn_kda_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv, int v_off, int qkv_stride,
+                                const float* glog, const float* beta, const int32_t* chunks,
+                                const int32_t* seq_chunk0, int num_chunks, void* workspace, float* o, float* state,
+                                const int32_t* slot_idx, int num_seqs, int H, int D, int init_state, int dtype,
+                                void* stream) {
+  SN_REQUIRE(qn && kn && qkv_conv && glog && beta && chunks && seq_chunk0 && workspace && o && state,
+             "sn_kda_chunk_prefill2: NULL pointer");
+  SN_REQUIRE(num_seqs > 0 && num_chunks > 0 && H > 0, "sn_kda_chunk_prefill2: bad shape");
+  SN_REQUIRE(D == 64 || D == 128, "sn_kda_chunk_prefill2: D=%d unsupported", D);
+  SN_REQUIRE(dtype == SN_BF16, "sn_kda_chunk_prefill2: bf16 only");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* glast = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                          (size_t)num_chunks * H * (4 * (size_t)chunk::C * D + (size_t)chunk::C * chunk::C) * 2);
+  if (D == 128)
+    return chunk::launch_kda_two_phase<__nv_bfloat16, 128>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, chunks,
+                                                            seq_chunk0, num_chunks, workspace, glast, o, state,
+                                                            slot_idx, num_seqs, H, init_state, st);
+  return chunk::launch_kda_two_phase<__nv_bfloat16, 64>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, chunks,
+                                                         seq_chunk0, num_chunks, workspace, glast, o, state, slot_idx,
+                                                         num_seqs, H, init_state, st);
 }
 
 size_t sn_gdn_chunk_workspace_bytes(int num_chunks, int Hv, int D) {

@@ -400,7 +400,9 @@ __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv
   const float negA = -expf(A_log[h]);
   if (KDA) {
     const float fv = io<T>::ld(f + (size_t)r * Hv * D + h * D + i);
-    gexp[((size_t)r * Hv + h) * D + i] = expf(negA * softplus_f(fv + dt_bias[h * D + i]));
+    const float gl = negA * softplus_f(fv + dt_bias[h * D + i]);
+    gexp[((size_t)r * Hv + h) * D + i] = expf(gl);
+    if (glog) glog[((size_t)r * Hv + h) * D + i] = gl;  // per-channel log gate (chunked KDA prefill)
   } else if (i == 0) {
     const float g = negA * softplus_f(io<T>::ld(prow + a_off + h) + dt_bias[h]);
     gexp[(size_t)r * Hv + h] = expf(g);

@@ -494,15 +494,15 @@ class Supernet:
         gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
         beta = torch.empty(rows, Hv, **f32)
         k_code = 1 if kind == KDA else 0
-        # bf16 GDN: chunked WY prefill on tensor cores; fp32 I/O (1e-4 parity mode) and KDA: the
-        # recurrent scan (same outputs, token-sequential)
-        chunked = kind == GDN and h.dtype == torch.bfloat16 and getattr(self, "chunked_prefill", True)
-        glog = torch.empty(rows, Hv, **f32) if chunked else None
+        # bf16: chunked WY prefill on tensor cores (GDN scalar gate / KDA per-channel gate);
+        # fp32 I/O (1e-4 parity mode): the recurrent scan (same outputs, token-sequential)
+        chunked = h.dtype == torch.bfloat16 and getattr(self, "chunked_prefill", True)
+        glog = (torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)) if chunked else None
         ops.delta_prep(k_code, y, proj, b_off, a_off, f, w["A_log"], w["dt_bias"], qn, kn, gexp, beta, Hk, Hv, D,
                        1.0 / math.sqrt(D), cfg.l2_eps, glog=glog)
         o = torch.empty(rows, Hv, D, **f32)
         if chunked:
-            self._chunked_gdn(qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], cu, Hk, Hv, D)
+            self._chunked_delta(kind, qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], cu, Hk, Hv, D)
         else:
             ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], None, cu, Hk, Hv, D,
                            init_state=False)
@@ -510,12 +510,14 @@ class Supernet:
         ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
         torch.mm(y_out, w["o"].t(), out=out)
 
-    def _chunked_gdn(self, qn, kn, y, v_off, glog, beta, o, S, cu, Hk, Hv, D, ws_cap=2 << 30):
+    def _chunked_delta(self, kind, qn, kn, y, v_off, glog, beta, o, S, cu, Hk, Hv, D, ws_cap=2 << 30):
         """Two-phase chunked prefill over groups of sequences whose chunk workspace fits ws_cap bytes
         (B equal-length prompts: one chunk plan serves every group)."""
         B, rows = S.shape[0], qn.shape[0]
         T = rows // B
-        per_seq = ops._lib.load().sn_gdn_chunk_workspace_bytes(-(-T // 64), Hv, D)
+        lib = ops._lib.load()
+        ws_fn = lib.sn_kda_chunk_workspace_bytes if kind == KDA else lib.sn_gdn_chunk_workspace_bytes
+        per_seq = ws_fn(-(-T // 64), Hv, D)
         grp = max(1, min(B, ws_cap // max(per_seq, 1)))
         key = (T, grp)
         if getattr(self, "_chunk_key", None) != key:
@@ -528,9 +530,14 @@ class Supernet:
             chunks, c0 = self._chunk_plan
             if b1 - b0 != grp:
                 chunks, c0 = ops.chunk_plan(list(range(0, (b1 - b0) * T + 1, T)), device=qn.device)
-            self._chunk_ws = ops.gdn_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1], beta[r0:r1],
-                                                    chunks, c0, o[r0:r1], S[b0:b1], None, Hk, Hv, D,
-                                                    init_state=False, workspace=self._chunk_ws)
+            if kind == KDA:
+                self._chunk_ws = ops.kda_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
+                                                        beta[r0:r1], chunks, c0, o[r0:r1], S[b0:b1], None, Hv, D,
+                                                        init_state=False, workspace=self._chunk_ws)
+            else:
+                self._chunk_ws = ops.gdn_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
+                                                        beta[r0:r1], chunks, c0, o[r0:r1], S[b0:b1], None, Hk, Hv,
+                                                        D, init_state=False, workspace=self._chunk_ws)
 
     def _gdn_prefill(self, l, h, out, cu):
         self._delta_prefill(GDN, l, h, out, cu)

@@ -56,3 +56,31 @@ def kernel_launch_bytes(cfg: SupernetConfig, name: str, B: int, ctx: int, elt: i
         keys = ctx + 1 if name == "fa_decode" else min(ctx + 1, cfg.window)
         return B * (keys * kv_token_bytes(cfg, elt) + 2 * cfg.n_q_heads * cfg.head_dim * elt)
     raise ValueError(name)
+
+
+def role_step_bytes(cfg: SupernetConfig, kinds, role: str, B: int, ctx: int, elt: int = 2):
+    """Algorithmic bytes per decode step of one kernel role of the step (the names the
+    bench's KernelProbe records): mixer kernels as kernel_launch_bytes x layers of that kind;
+    GEMM roles as weight bytes + bf16 activations in and out.  None for latency-bound glue
+    (norms, RoPE/append, embed, argmax)."""
+    d, F = cfg.hidden, cfg.ffn
+    mixer = {"gdn_decode": [GDN], "kda_decode": [KDA], "fa_decode": [FA], "swa_decode": [SWA]}
+    if role in mixer:
+        n = sum(1 for k in kinds if k in mixer[role])
+        return n * kernel_launch_bytes(cfg, role, B, ctx, elt)
+
+    def gemm(N, K):
+        return (N * K + B * (N + K)) * elt
+    if role == "gemm_ffn_gate_up":
+        return len(kinds) * gemm(2 * F, d)
+    if role == "gemm_ffn_down":
+        return len(kinds) * gemm(d, F)
+    if role == "gemm_lm_head":
+        return gemm(cfg.vocab, d)
+    if role == "gemm_in_proj":
+        width = {FA: cfg.attn_qkv_width, SWA: cfg.attn_qkv_width, GDN: cfg.gdn_in_width, KDA: cfg.kda_in_width}
+        return sum(gemm(width[k], d) for k in kinds)
+    if role == "gemm_out_proj":
+        o_in = {FA: cfg.attn_o_in, SWA: cfg.attn_o_in, GDN: cfg.gdn_value_dim, KDA: cfg.kda_dim}
+        return sum(gemm(d, o_in[k]) for k in kinds)
+    return None
