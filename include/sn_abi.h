@@ -75,6 +75,12 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit,
 sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, int ffn,
                       int dtype, void* stream);
 
+/* out[r, i] = silu(g) * u for the interleaved gate/up layout of GEMM mode
+ * SN_GEMM_SWIGLU_IL (row of ceil(ffn/h) blocks of [h gate | h up] columns, row
+ * stride ld); used on the prefill gate/up GEMM output.                       */
+sn_status sn_swiglu_il(const void* gate_up, int ld, void* out, int rows, int ffn,
+                       int h, int dtype, void* stream);
+
 /* out_tokens[r] = argmax_v logits[r,v] (lowest index on ties).             */
 sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens,
                     int dtype, void* stream);

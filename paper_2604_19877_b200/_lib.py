@@ -25,6 +25,7 @@ SIGNATURES = {
     "sn_add_rmsnorm": [P, P, I, P, P, P, I, I, Fl, I, P],
     "sn_silu_mul": [P, I, P, I, I, I, P],
     "sn_argmax": [P, I, I, P, I, P],
+    "sn_swiglu_il": [P, I, P, I, I, I, I, P],
     "sn_rope_kv_append": [P, I, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, P],
     "sn_attn_decode_workspace_bytes": [I, I, I, I, I],
     "sn_attn_decode": [P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, Fl, I, P],

@@ -227,6 +227,9 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const T* __restrict__
 }
 
 sn_status attn_decode_tc_bf16(const AttnDecodeArgs& a, int D, cudaStream_t st);  // sn_attn_tc.cu
+sn_status attn_prefill_tc_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
+                               int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale,
+                               cudaStream_t st);  // sn_attn_prefill.cu
 
 }  // namespace sn
 
@@ -289,6 +292,9 @@ sn_status sn_attn_prefill(const void* q, const void* k, const void* v, const int
                           int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale, int dtype,
                           void* stream) {
   SN_REQUIRE(num_seqs > 0 && rows > 0 && Hkv > 0 && Hq % Hkv == 0, "sn_attn_prefill: bad shape");
+  if (dtype == SN_BF16)  // tensor-core flash attention (sn_attn_prefill.cu); fp32 I/O below
+    return attn_prefill_tc_bf16(q, k, v, cu_seqlens, out, num_seqs, rows, Hq, Hkv, D, window, scale,
+                                (cudaStream_t)stream);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(ceil_div(rows, 4), Hq);
     cudaStream_t st = (cudaStream_t)stream;

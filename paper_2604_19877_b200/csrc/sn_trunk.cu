@@ -132,7 +132,84 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(const T* __restrict__ 
   }
 }
 
+// Long-row-count variant (prefill): one CTA of 256 threads per row, each thread owning up to
+// 4 chunks of 8 (dim <= 8192), no cluster; delta only (prefill has no split-K slabs).
+template <typename T>
+__global__ void __launch_bounds__(256) add_rmsnorm_rows_kernel(const T* __restrict__ delta,
+                                                               float* __restrict__ residual,
+                                                               const T* __restrict__ weight, T* __restrict__ out,
+                                                               int dim, float eps) {
+  sn::pdl_launch_dependents();
+  sn::pdl_wait();
+  __shared__ float scratch[32];
+  const int r = blockIdx.x;
+  const int nch = dim / 8;
+  float v[4][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int ch = threadIdx.x + c * 256;
+    if (ch < nch) {
+      float* res = residual + (size_t)r * dim + ch * 8;
+      load8<float>(res, v[c]);
+      if (delta != nullptr) {
+        float d[8];
+        load8<T>(delta + (size_t)r * dim + ch * 8, d);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[c][k] += d[k];
+        *reinterpret_cast<float4*>(res) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+        *reinterpret_cast<float4*>(res + 4) = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss += v[c][k] * v[c][k];
+    }
+  }
+  ss = block_sum(ss, scratch);
+  const float rstd = rsqrtf(ss / (float)dim + eps);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int ch = threadIdx.x + c * 256;
+    if (ch < nch) {
+      float w[8];
+      load8<T>(weight + ch * 8, w);
+      uint4 pk;
+      uint32_t* pp = reinterpret_cast<uint32_t*>(&pk);
+      if (sizeof(T) == 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(v[c][2 * k] * rstd * w[2 * k], v[c][2 * k + 1] * rstd * w[2 * k + 1]);
+          pp[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(out + (size_t)r * dim + ch * 8) = pk;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) io<T>::st(out + (size_t)r * dim + ch * 8 + k, v[c][k] * rstd * w[k]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ silu * mul
+// Interleaved gate/up layout (GEMM mode SWIGLU_IL weights, prefill GEMM output): row of
+// ceil(ffn/h) blocks of [h gate | h up] columns.
+template <typename T>
+__global__ void swiglu_il_kernel(const T* __restrict__ gu, T* __restrict__ out, int rows, int ffn, int h, int ld) {
+  sn::pdl_launch_dependents();
+  sn::pdl_wait();
+  const size_t n8 = (size_t)rows * (ffn / 8);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n8; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = e / (ffn / 8);
+    const int i = (int)(e % (ffn / 8)) * 8;
+    const int b = i / h, o = i % h;  // h % 8 == 0: a chunk of 8 stays inside one block
+    const T* row = gu + r * ld + (size_t)b * 2 * h + o;
+    float g[8], u[8];
+    load8<T>(row, g);
+    load8<T>(row + h, u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) io<T>::st(out + r * ffn + i + k, silu_f(g[k]) * u[k]);
+  }
+}
+
 template <typename T>
 __global__ void silu_mul_kernel(const GemmIn<T> gu, T* __restrict__ out, int rows, int ffn) {
   sn::pdl_launch_dependents();
@@ -204,6 +281,12 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit, f
   SN_REQUIRE(nsplit >= 0 && nsplit <= kNormMaxSplit && (nsplit == 0 || partials != nullptr),
              "sn_add_rmsnorm: bad partials (nsplit %d)", nsplit);
   SN_REQUIRE(rows > 0 && dim > 0 && dim % 8 == 0, "sn_add_rmsnorm: bad shape rows=%d dim=%d", rows, dim);
+  if (rows > 512 && nsplit == 0 && dim <= 8192)  // prefill: a CTA per row, no cluster round trips
+    return SN_DISPATCH_DTYPE(dtype, T, [&] {
+      launch_pdl(add_rmsnorm_rows_kernel<T>, dim3(rows), dim3(256), 0, (cudaStream_t)stream, (const T*)delta,
+                 residual, (const T*)weight, (T*)out, dim, eps);
+      return check_launch("sn_add_rmsnorm");
+    });
   // cluster size: each CTA owns <= 256 chunks of 8 (and >= 4-way split once rows are long)
   int cs = 1;
   while (cs < 8 && (dim / 8 / cs > 256 || (dim / 8 / cs > 64 && cs < 4)) && dim % (16 * cs) == 0) cs *= 2;
@@ -244,6 +327,20 @@ sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, i
     const GemmIn<T> in{gate_up, gu_nsplit, (size_t)rows * 2 * ffn};
     launch_pdl(silu_mul_kernel<T>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, in, (T*)out, rows, ffn);
     return check_launch("sn_silu_mul");
+  });
+}
+
+sn_status sn_swiglu_il(const void* gate_up, int ld, void* out, int rows, int ffn, int h, int dtype, void* stream) {
+  SN_REQUIRE(rows > 0 && ffn > 0 && ffn % 8 == 0 && h > 0 && h % 8 == 0, "sn_swiglu_il: bad shape ffn=%d h=%d",
+             ffn, h);
+  SN_REQUIRE(ld >= ((ffn + h - 1) / h) * 2 * h && ld % 8 == 0, "sn_swiglu_il: ld %d too small", ld);
+  return SN_DISPATCH_DTYPE(dtype, T, [&] {
+    const size_t n8 = (size_t)rows * (ffn / 8);
+    int grid = (int)((n8 + 255) / 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    launch_pdl(swiglu_il_kernel<T>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const T*)gate_up, (T*)out, rows,
+               ffn, h, ld);
+    return check_launch("sn_swiglu_il");
   });
 }
 

@@ -425,12 +425,11 @@ class Supernet:
                 self._kda_prefill(l, h, mix, cu)
             self._tp_sum(mix)
             ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
-            if self.gu_il is not None:
-                gu = ops.deinterleave_swiglu(h @ lw["ffn_gu_il"].t(), *self.gu_il)
-            else:
-                gu = h @ lw["ffn_gu"].t()
             act = e(rows, cfg.ffn)
-            ops.silu_mul(gu, act)
+            if self.gu_il is not None:
+                ops.swiglu_il(h @ lw["ffn_gu_il"].t(), act, *self.gu_il)
+            else:
+                ops.silu_mul(h @ lw["ffn_gu"].t(), act)
             torch.mm(act, lw["ffn_down"].t(), out=ffn_o)
             self._tp_sum(ffn_o)
             delta = ffn_o

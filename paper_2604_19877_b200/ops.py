@@ -234,3 +234,8 @@ def kda_chunk_prefill2(qn, kn, qkv_conv, v_off, glog, beta, chunks, seq_chunk0, 
          _p(chunks), _p(seq_chunk0), n, _p(workspace), _p(o), _p(state), _p(slot_idx), seq_chunk0.numel() - 1, H, D,
          int(init_state), dtype_code(qkv_conv.dtype), _s())
     return workspace
+
+
+def swiglu_il(gu_il, out, ffn, h):
+    """out [rows, ffn] = silu(gate) * up from the interleaved gate/up GEMM output [rows, nb*2h]."""
+    call("sn_swiglu_il", _p(gu_il), gu_il.stride(0), _p(out), gu_il.shape[0], ffn, h, dtype_code(out.dtype), _s())
