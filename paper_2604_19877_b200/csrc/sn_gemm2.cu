@@ -427,8 +427,8 @@ struct Plan {
   int um, br, splits, nblocks, grid;
 };
 
-// Per-CTA time ~ waves x k-blocks per unit x (weight rows + half the batch tile: the
-// activation tile comes from L2) + the split-K slab traffic the consumer pays.  Ties ->
+// Per-CTA time ~ waves x k-blocks per unit x weight rows (+ a small activation-tile term)
+// + the split-K slab traffic the consumer pays.  Ties ->
 // fewer splits, then taller blocks.
 static Plan make_plan(int M, int N, int K, int mode) {
   Plan p{};
@@ -445,7 +445,8 @@ static Plan make_plan(int M, int N, int K, int mode) {
       const long blocks = swiglu ? (N + br / 2 - 1) / (br / 2) : (N + br - 1) / br;
       const long items = blocks * s;
       const long waves = (items + sms - 1) / sms;
-      const double cost = (double)waves * (kblocks / s) * (br + p.um / 2) * 128.0 +
+      // the activation tile is an L2 hit and measured free (SN_GEMM_DBG=4): weigh it lightly
+      const double cost = (double)waves * (kblocks / s) * (br + p.um / 8) * 128.0 +
                           (s > 1 ? (double)s * M * N * 8.0 / sms : 0.0);
       if (best < 0 || cost < best * 0.999) { best = cost; p.br = br; p.splits = s; }
     }
