@@ -795,18 +795,20 @@ static sn_status launch_two_phase(const float* qn, const float* kn, const void* 
 //   T = (I + A_kk)^{-1},  W = T (b o e^G o K),  U = T (b o V),  Qg = e^G o Q,  Kd = e^{G_C - G} o K
 // The state pass is the GDN one with a per-channel decay (gdn_chunk_state_kernel<D, true>).
 // Per-channel decay factors cannot be pulled out of a plain K K^T product (G spans up to
-// ~100 in a 64-token chunk: e^{-G} overflows fp32), so warp w (rows 16w..16w+15, one
-// 16-token sub-chunk) factorises around its own reference row r = 16w:
-//   e^{G_i - G_j} = e^{G_i - G_r} . e^{G_r - G_j}
-// with e^{G_i - G_r} <= 1 for i >= r and e^{G_r - G_j} <= 1 for j < r; only the diagonal
-// 16x16 block has factors > 1 (at most the decay of 15 tokens, far from overflow).  The
-// left operand is the warp's own 16 rows; the right operand (16(w+1) rows of K scaled to
-// reference r) is a per-warp shared-memory tile, and both products run on mma.sync.
+// hundreds in a 64-token chunk: e^{-G} overflows fp32), so warp w (rows 16w..16w+15, one
+// 16-token sub-chunk) factorises the blocks left of its diagonal around its own
+// reference row r = 16w:
+//   e^{G_i - G_j} = e^{G_i - G_r} . e^{G_r - G_j},   e^{G_i - G_r} <= 1 (i >= r), e^{G_r - G_j} <= 1 (j < r)
+// — the left operand is the warp's own 16 rows, the right operand (the 16w rows j < r of K
+// scaled to reference r) a per-warp shared-memory tile, both products on mma.sync.  The
+// diagonal 16x16 block (r <= j <= i) is computed exactly in fp32 with e^{G_i - G_j} <= 1
+// per term (a factorised form would need e^{G_r - G_j} > 1, which overflows for strong
+// gates).
 
 template <int D>
 struct KdaIntraSmem {
   static constexpr int LDK = D + 8, LDC = C + 8;
-  static constexpr int KR_ROWS = 16 * (1 + 2 + 3 + 4);  // per-warp right operands
+  static constexpr int KR_ROWS = 16 * (0 + 1 + 2 + 3);  // per-warp right operands (rows j < 16w)
   __nv_bfloat16 q[C * LDK];
   __nv_bfloat16 k[C * LDK];
   union {
@@ -861,9 +863,9 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   __syncthreads();
-  // ---- per-warp operands around reference row r0 = 16 * warp
-  const int r0 = 16 * warp, nrows = 16 * (warp + 1);
-  __nv_bfloat16* kr = sm.u2.kr + 16 * (warp * (warp + 1) / 2) * LDK;
+  // ---- per-warp operands around reference row r0 = 16 * warp (off-diagonal blocks j < r0)
+  const int r0 = 16 * warp, nrows = 16 * warp;
+  __nv_bfloat16* kr = sm.u2.kr + 16 * (warp * (warp - 1) / 2) * LDK;
   for (int idx = lane; idx < 16 * D / 2; idx += 32) {
     const int r = r0 + idx / (D / 2), cc = (idx % (D / 2)) * 2;
     const float e0 = expf(sm.g[r * D + cc] - sm.g[r0 * D + cc]), e1 = expf(sm.g[r * D + cc + 1] - sm.g[r0 * D + cc + 1]);
@@ -891,7 +893,7 @@ __global__ void __launch_bounds__(kThreads)
     lda(sm.u1.a.ql, LDK, r0, ks, aq);
 #pragma unroll
     for (int nt = 0; nt < 8; nt += 2) {
-      if (nt * 8 < nrows) {  // warp-uniform: only column blocks at or left of the diagonal
+      if (nt * 8 < nrows) {  // warp-uniform: only the column blocks left of the diagonal block
         uint32_t b0, b1, b2, b3;
         ldb_nk(kr, LDK, nt * 8, ks, b0, b1, b2, b3);
         mma_bf16(kk[nt], ak, b0, b1);
@@ -899,6 +901,35 @@ __global__ void __launch_bounds__(kThreads)
         mma_bf16(qk[nt], aq, b0, b1);
         mma_bf16(qk[nt + 1], aq, b2, b3);
       }
+    }
+  }
+  // diagonal block, exact: pairs (i, j) = (r0 + a, r0 + b), 0 <= b <= a < 16, 136 per warp
+  constexpr int kPairs = 136, kPerLane = (kPairs + 31) / 32;
+  float dkk[kPerLane], dqk[kPerLane];
+#pragma unroll
+  for (int u = 0; u < kPerLane; ++u) {
+    const int p = lane + 32 * u;
+    dkk[u] = dqk[u] = 0.f;
+    if (p < kPairs) {
+      int a = (int)((sqrtf(8.f * p + 1.f) - 1.f) * 0.5f);
+      if ((a + 1) * (a + 2) / 2 <= p) ++a;
+      if (a * (a + 1) / 2 > p) --a;
+      const int b = p - a * (a + 1) / 2;
+      const int i = r0 + a, j = r0 + b;
+      const float* gi = sm.g + i * D;
+      const float* gj = sm.g + j * D;
+      float sk = 0.f, sq = 0.f;
+#pragma unroll 4
+      for (int d = 0; d < D; d += 2) {
+        const float2 ki = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[i * LDK + d]));
+        const float2 qi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[i * LDK + d]));
+        const float2 kj = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[j * LDK + d]));
+        const float e0 = expf(gi[d] - gj[d]) * kj.x, e1 = expf(gi[d + 1] - gj[d + 1]) * kj.y;
+        sk += ki.x * e0 + ki.y * e1;
+        sq += qi.x * e0 + qi.y * e1;
+      }
+      dkk[u] = sk;
+      dqk[u] = sq;
     }
   }
   __syncthreads();  // every warp is done with kr before l / x (aliased) are written
@@ -922,6 +953,20 @@ __global__ void __launch_bounds__(kThreads)
       }
       *reinterpret_cast<uint32_t*>(wP + i * C + j) = pack_bf16(pv[0], pv[1]);
     }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < kPerLane; ++u) {
+    const int p = lane + 32 * u;
+    if (p < kPairs) {
+      int a = (int)((sqrtf(8.f * p + 1.f) - 1.f) * 0.5f);
+      if ((a + 1) * (a + 2) / 2 <= p) ++a;
+      if (a * (a + 1) / 2 > p) --a;
+      const int b = p - a * (a + 1) / 2;
+      const int i = r0 + a, j = r0 + b;
+      if (a > b) sm.u2.lx.l[i][j] = -sm.beta[i] * dkk[u];
+      wP[i * C + j] = __float2bfloat16_rn(dqk[u]);
+    }
+  }
   if (tid < C) sm.u2.lx.x[0][tid] = tid == 0 ? 1.f : 0.f;
   // chunk-global operands: b e^G K, b V (W/U step), e^G Q and e^{G_C - G} K (state pass)
   for (int idx = tid; idx < C * D / 2; idx += kThreads) {

@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv
                                                        float* __restrict__ glog, float* __restrict__ beta, int Hk,
                                                        int Hv, float scale, float eps_l2) {
   __shared__ float red[D / 32];
-  const int r = blockIdx.y, h = blockIdx.x, i = threadIdx.x;
+  const int r = blockIdx.x, h = blockIdx.y, i = threadIdx.x;  // rows on x: > 65535 tokens
   const int G = Hv / Hk, kh = h / G;
   const int qkv_stride = 2 * Hk * D + Hv * D;
   const T* row = qkv + (size_t)r * qkv_stride;
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(D) gated_rmsnorm_kernel(const float* __restric
                                                           int gate_stride, const T* __restrict__ w,
                                                           T* __restrict__ out, int H, float eps, int act) {
   __shared__ float red[D / 32];
-  const int r = blockIdx.y, h = blockIdx.x, j = threadIdx.x;
+  const int r = blockIdx.x, h = blockIdx.y, j = threadIdx.x;
   const float v = o[((size_t)r * H + h) * D + j];
   const float ss = block_sum(v * v, red);
   const float rstd = rsqrtf(ss / (float)D + eps);
@@ -610,7 +610,7 @@ sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int pr
   SN_REQUIRE(kind == 0 || f != nullptr, "sn_delta_prep: KDA needs f");
   SN_REQUIRE(D == 64 || D == 128, "sn_delta_prep: D=%d unsupported", D);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    dim3 grid(Hv, rows);
+    dim3 grid(rows, Hv);
     cudaStream_t st = (cudaStream_t)stream;
     auto fn = D == 128 ? (kind ? launch_prep<T, 128, true> : launch_prep<T, 128, false>)
                        : (kind ? launch_prep<T, 64, true> : launch_prep<T, 64, false>);
@@ -642,7 +642,7 @@ sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride, co
                            int rows, int H, int D, float eps, int act, int dtype, void* stream) {
   SN_REQUIRE(rows > 0 && H > 0, "sn_gated_rmsnorm: bad shape");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    dim3 grid(H, rows);
+    dim3 grid(rows, H);
     cudaStream_t st = (cudaStream_t)stream;
     if (D == 128) gated_rmsnorm_kernel<T, 128><<<grid, 128, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, H, eps, act);
     else if (D == 64) gated_rmsnorm_kernel<T, 64><<<grid, 64, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, H, eps, act);
