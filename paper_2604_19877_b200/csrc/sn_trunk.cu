@@ -252,7 +252,9 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logi
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
       if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
-    out[blockIdx.x] = bi;
+    // an all-NaN row never beats -inf: return token 0, never an out-of-range id that the
+    // graph's token feedback would hand to the embedding gather
+    out[blockIdx.x] = bi < vocab ? bi : 0;
   }
 }
 
