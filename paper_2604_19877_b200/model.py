@@ -104,13 +104,19 @@ class Supernet:
             # fused gate/up + SiLU-mul: gate and up rows interleaved in the GEMM's block height
             # the interleaved copy replaces [gate; up] (no doubled FFN weights in HBM); prefill
             # de-interleaves its GEMM output (deinterleave_swiglu)
-            ffn = self.w["layers"][0]["ffn_gu"].shape[0] // 2
-            hb = ops.gemm_swiglu_block(batch, ffn, cfg.hidden)
+            ffn = self.cfg.ffn
+            hb = ops.gemm_swiglu_block(batch, ffn, self.cfg.hidden)
             self.gu_il = (ffn, hb)
             for lw in self.w["layers"]:
-                lw["ffn_gu_il"] = ops.interleave_swiglu(lw.pop("ffn_gu"), hb)
+                if "ffn_gu_il" in lw:  # prebuilt and shared (serving.SupernetStore)
+                    if lw["ffn_gu_il"].shape[0] != -(-ffn // hb) * 2 * hb:
+                        raise ValueError("prebuilt SwiGLU-interleaved FFN weights do not match this batch's block")
+                else:
+                    lw["ffn_gu_il"] = ops.interleave_swiglu(lw.pop("ffn_gu"), hb)
         else:
             self.gu_il = None
+            if any("ffn_gu" not in lw for lw in self.w["layers"]):
+                raise ValueError("this engine needs the [gate; up] FFN weights (ffn_gu)")
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
