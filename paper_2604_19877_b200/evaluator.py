@@ -81,6 +81,7 @@ def main(argv=None) -> int:
     ap.add_argument("--trace-len", type=int, default=256)
     ap.add_argument("--batch", type=int, default=4, help="traces per prefill")
     ap.add_argument("--seed", type=int, default=0, help="weight seed")
+    ap.add_argument("--init-device", default="cuda", help="where the seeded weight draws run (cpu = the oracle's weights)")
     ap.add_argument("--trace-seed", type=int, default=1)
     ap.add_argument("--normalize", default="", help="lo,hi: print (ll - lo) / (hi - lo) (R/PAPER.md:921)")
     a = ap.parse_args(argv)
@@ -97,7 +98,7 @@ def main(argv=None) -> int:
     from . import ops
     from .model import Supernet
     from .serving import SupernetStore
-    store = SupernetStore(cfg, seed=a.seed)
+    store = SupernetStore(cfg, seed=a.seed, init_device=a.init_device)
     B = min(a.batch, traces.shape[0])
     block = ops.gemm_swiglu_block(B, cfg.ffn, cfg.hidden)  # the FFN decode layout, shared by every placement
     for code in codes:

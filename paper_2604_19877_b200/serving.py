@@ -28,6 +28,14 @@ from .placement import DEFAULT_CATALOG, coerce_placement, layer_kinds
 from .weights import init_mixer, init_trunk
 
 
+def _to(obj, device):
+    if isinstance(obj, dict):
+        return {k: _to(v, device) for k, v in obj.items()}
+    if isinstance(obj, list):
+        return [_to(v, device) for v in obj]
+    return obj.to(device) if torch.is_tensor(obj) else obj
+
+
 def placement_code(placement) -> str:
     return coerce_placement(placement).to_codes(DEFAULT_CATALOG)
 
@@ -35,17 +43,22 @@ def placement_code(placement) -> str:
 class SupernetStore:
     """Resident supernet weights: the trunk once, each (layer, mixer kind) on first use."""
 
-    def __init__(self, cfg: SupernetConfig, seed: int = 0, device="cuda", dtype=torch.bfloat16):
+    def __init__(self, cfg: SupernetConfig, seed: int = 0, device="cuda", dtype=torch.bfloat16, init_device=None):
+        """init_device: where the seeded draws happen (default: device).  The CPU and CUDA
+        generators give different numbers for one seed; init_device="cpu" reproduces the
+        weights the CPU oracle / tests draw (slow for Apriel-size supernets)."""
         self.cfg, self.seed, self.device, self.dtype = cfg, seed, torch.device(device), dtype
-        self.trunk = init_trunk(cfg, seed, self.device, dtype)
+        self.init_device = torch.device(init_device) if init_device is not None else self.device
+        self.trunk = _to(init_trunk(cfg, seed, self.init_device, dtype), self.device)
         self._mixers: dict[tuple[int, int], dict] = {}
         self._gu_il: dict[tuple[int, int], torch.Tensor] = {}
 
     def mixer(self, layer: int, kind: int) -> dict:
         key = (layer, kind)
         if key not in self._mixers:
-            m = init_mixer(self.cfg, layer, kind, self.seed, self.device, self.dtype)
-            self._mixers[key] = {k: (v if k in ("A_log", "dt_bias") else v.to(self.dtype)) for k, v in m.items()}
+            m = init_mixer(self.cfg, layer, kind, self.seed, self.init_device, self.dtype)
+            self._mixers[key] = {k: (v if k in ("A_log", "dt_bias") else v.to(self.dtype)).to(self.device)
+                                 for k, v in m.items()}
         return self._mixers[key]
 
     def swiglu_interleaved(self, layer: int, block: int) -> torch.Tensor:

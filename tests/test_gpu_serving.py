@@ -23,7 +23,7 @@ def test_evaluator_line_protocol_matches_oracle_loglik():
     placements = ["ASKG", "AAAA", "GGKS"]
     N, T = 2, 96
     p = subprocess.run([sys.executable, "-m", "paper_2604_19877_b200.evaluator", "--config", "tiny", "--num-traces",
-                        str(N), "--trace-len", str(T), "--batch", "2"], input="\n".join(placements) + "\n",
+                        str(N), "--trace-len", str(T), "--batch", "2", "--init-device", "cpu"], input="\n".join(placements) + "\n",
                        capture_output=True, text=True, cwd=ROOT)
     assert p.returncode == 0, p.stderr[-2000:]
     scores = [float(x) for x in p.stdout.split()]
@@ -34,14 +34,14 @@ def test_evaluator_line_protocol_matches_oracle_loglik():
         w = cast_weights(init_weights(TINY, kinds, seed=0), "cpu", torch.bfloat16)
         logits = OracleSupernet(TINY, kinds, w, batch=N, max_len=T).run(traces)
         ref = float(loglik_from_logits(logits, traces).mean())
-        assert abs(got - ref) < 2e-2 * abs(ref), (code, got, ref)
+        assert abs(got - ref) < 5e-3, (code, got, ref)
     assert len(set(scores)) == len(scores)  # placements are distinguishable
 
 
 @pytest.mark.gpu
 def test_router_matches_standalone_placements():
     from paper_2604_19877_b200.serving import PlacementRouter, SupernetStore
-    store = SupernetStore(TINY, seed=0)
+    store = SupernetStore(TINY, seed=0, init_device="cpu")
     g = torch.Generator().manual_seed(5)
     prompts = [torch.randint(0, TINY.vocab, (40,), generator=g) for _ in range(5)]
     reqs = [("ASKG", prompts[0]), ("GGGG", prompts[1]), ("ASKG", prompts[2]), ("AAAA", prompts[3]),
@@ -61,3 +61,27 @@ def test_router_matches_standalone_placements():
     # the mixers of every placement share one trunk: resident bytes well under 3 full copies
     full = sum(t.numel() * t.element_size() for t in [store.trunk["embed"], store.trunk["lm_head"]])
     assert store.resident_bytes() < 3 * full + 3 * 10**8
+
+
+@pytest.mark.gpu
+def test_speculative_traces_match_oracle_logprobs():
+    from paper_2604_19877_b200.serving import SupernetStore
+    from paper_2604_19877_b200.speculative import acceptance_traces
+    store = SupernetStore(TINY, seed=0, init_device="cpu")  # the oracle's (CPU-drawn) weights
+    prompts = torch.randint(0, TINY.vocab, (2, 24), generator=torch.Generator().manual_seed(3))
+    rows = acceptance_traces(store, "GGGG", "AAAA", prompts, completion_len=16)
+    assert len(rows) == 2 and all(len(r["log_q"]) == len(r["log_p"]) == 16 for r in rows)
+    # the completion is the target's greedy continuation: recompute both log-prob sets on the oracle
+    from paper_2604_19877_b200.serving import PlacementRouter
+    gen = PlacementRouter(store, max_len=40).generate([("AAAA", prompts[b]) for b in range(2)], 16)
+    seqs = torch.cat([prompts, torch.stack(gen).long()], 1)
+    for key, code in (("log_p", "AAAA"), ("log_q", "GGGG")):
+        kinds = layer_kinds(code)
+        w = cast_weights(init_weights(TINY, kinds, seed=0), "cpu", torch.bfloat16)
+        logits = OracleSupernet(TINY, kinds, w, batch=2, max_len=40).run(seqs)
+        lp = torch.log_softmax(logits[:, 23:-1].float(), -1).gather(-1, seqs[:, 24:, None])[..., 0]
+        got = torch.tensor([r[key] for r in rows])
+        assert (got - lp).abs().max() < 5e-2, key
+    # draft == target: every ratio is 1, so every drafted token is accepted
+    same = acceptance_traces(store, "AAAA", "AAAA", prompts, completion_len=8)
+    assert all(r["log_q"] == r["log_p"] for r in same)

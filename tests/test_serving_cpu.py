@@ -91,3 +91,19 @@ def test_store_hands_out_the_standalone_tensors():
     assert store.weights("ASKG")["layers"][0]["ffn_gu"] is store.weights("GGKA")["layers"][0]["ffn_gu"]
     with pytest.raises(ValueError, match="layers"):
         store.weights("ASK")
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference sources not present")
+def test_speculative_trace_schema_feeds_reference_estimator():
+    """Our JSONL rows construct the reference's TraceTokenLogProbs and estimate_acceptance
+    (speculative.py:62-94) accepts them."""
+    sys.path.insert(0, REF_SRC)
+    try:
+        from placeopt.speculative import TraceTokenLogProbs, estimate_acceptance
+    finally:
+        sys.path.remove(REF_SRC)
+    rows = [{"prompt_id": "prompt-0", "log_q": [-1.0] * 16, "log_p": [-1.0] * 16},
+            {"prompt_id": "prompt-1", "log_q": [-2.0] * 16, "log_p": [-1.0] * 16}]
+    est = estimate_acceptance([TraceTokenLogProbs(r["prompt_id"], tuple(r["log_q"]), tuple(r["log_p"])) for r in rows],
+                              gamma=8)
+    assert est.n_steps == 4 and 0 < est.acceptance_rate <= 1
