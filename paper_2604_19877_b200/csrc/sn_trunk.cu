@@ -205,8 +205,19 @@ __global__ void swiglu_il_kernel(const T* __restrict__ gu, T* __restrict__ out, 
     float g[8], u[8];
     load8<T>(row, g);
     load8<T>(row + h, u);
+    if (sizeof(T) == 2) {  // one 16-byte store per 8 outputs
+      uint4 pk;
+      uint32_t* pp = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) io<T>::st(out + r * ffn + i + k, silu_f(g[k]) * u[k]);
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(silu_f(g[2 * k]) * u[2 * k], silu_f(g[2 * k + 1]) * u[2 * k + 1]);
+        pp[k] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(out + r * ffn + i) = pk;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) io<T>::st(out + r * ffn + i + k, silu_f(g[k]) * u[k]);
+    }
   }
 }
 
