@@ -22,6 +22,72 @@ constexpr int C = 64;      // chunk length
 constexpr int VT = 64;     // value columns per CTA
 constexpr int kThreads = 128;
 
+
+// T = (I - L)^{-1} for a strictly lower-triangular 64x64 L (fp32 rows of stride C + 1).
+// Blocked: each warp inverts one 16x16 diagonal block by warp-synchronous substitution
+// (lane j < 16 owns column j in registers: T_ii = I + L_ii T_ii), then the three block rows
+// below the diagonal, T_ij = T_ii sum_{k=j}^{i-1} L_ik T_kj, one warp per block — 3 block
+// barriers instead of one per row.  Same fp32 arithmetic as row-by-row substitution, only
+// reassociated.  All 128 threads must call; l must be complete (caller synchronises);
+// x is complete on return.  scr: 4 x 16 x 17 floats.
+__device__ __forceinline__ void invert_unit_lower(const float (*l)[C + 1], float (*x)[C + 1], float* scr) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {  // diagonal blocks
+    const int b0 = 16 * warp, j = lane;
+    if (lane < 16) {
+      float xc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float acc = 0.f;
+#pragma unroll
+        for (int m = 0; m < i; ++m) acc += l[b0 + i][b0 + m] * xc[m];
+        xc[i] = i < j ? 0.f : (i == j ? 1.f : acc);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[b0 + i][b0 + j] = xc[i];
+    }
+  }
+  for (int idx = tid; idx < 6 * 256; idx += kThreads) {  // blocks above the diagonal are zero
+    const int blk = idx >> 8, e = idx & 255;
+    const int bi = blk < 3 ? 0 : (blk < 5 ? 1 : 2), bj = blk < 3 ? blk + 1 : (blk < 5 ? blk - 1 : 3);
+    x[16 * bi + (e >> 4)][16 * bj + (e & 15)] = 0.f;
+  }
+  __syncthreads();
+  const int r = lane >> 1, c0 = (lane & 1) * 8;
+  float* M = scr + warp * 16 * 17;
+  for (int bi = 1; bi < 4; ++bi) {
+    if (warp < bi) {
+      const int bj = warp;
+      float acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+      for (int k = bj; k < bi; ++k)
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const float a = l[16 * bi + r][16 * k + m];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] += a * x[16 * k + m][16 * bj + c0 + c];
+        }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) M[r * 17 + c0 + c] = acc[c];
+      __syncwarp();
+      float res[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) res[c] = 0.f;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const float a = x[16 * bi + r][16 * bi + m];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) res[c] += a * M[m * 17 + c0 + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) x[16 * bi + r][16 * bj + c0 + c] = res[c];
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
 template <int D>
 struct Smem {
   static constexpr int LDK = D + 8, LDV = VT + 8, LDC = C + 8;
@@ -35,7 +101,8 @@ struct Smem {
   __nv_bfloat16 t[C * LDC];    // T = (I - L)^{-1}
   __nv_bfloat16 p[C * LDC];    // P
   float l[C][C + 1];           // L (fp32)
-  float x[C][C + 1];           // forward-substitution result
+  float x[C][C + 1];           // T = (I - L)^{-1}
+  float scr[4 * 16 * 17];      // invert_unit_lower scratch
   float g[C], beta[C];
 };
 
@@ -145,12 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
 
-    // ---- T = (I - L)^{-1} by forward substitution (threads 0..63 own a column each),
-    //      meanwhile the other warps scale the operands.
-    if (tid < C) {
-      const int j = tid;
-      sm.x[0][j] = j == 0 ? 1.f : 0.f;
-    }
+    // ---- operand scaling, then T = (I - L)^{-1} (invert_unit_lower)
     // operand scaling: Kb = b e^G K, Kd = e^{G_C - G} K (in place of K), Qg = e^G Q (in place of Q)
     {
       const float gl = sm.g[C - 1];
@@ -164,20 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
-    for (int i = 1; i < C; ++i) {
-      if (tid < C) {
-        const int j = tid;
-        float acc = 0.f;
-        if (j < i) {
-          acc = sm.l[i][j];
-          for (int m = j + 1; m < i; ++m) acc += sm.l[i][m] * sm.x[m][j];
-        } else if (j == i) {
-          acc = 1.f;
-        }
-        sm.x[i][j] = acc;
-      }
-      __syncthreads();
-    }
+    invert_unit_lower(sm.l, sm.x, sm.scr);
     for (int idx = tid; idx < C * C; idx += kThreads) {
       const int i = idx / C, j = idx % C;
       sm.t[i * LDC + j] = __float2bfloat16_rn(sm.x[i][j]);
@@ -371,15 +420,20 @@ static sn_status launch(const float* qn, const float* kn, const void* qkv, int v
 // Workspace per (chunk, head), bf16: W, Qg, Kd, U [64][D] and P [64][64]; glast fp32.
 
 template <int D>
-struct IntraSmem {
+struct IntraSmem {  // ~90 KB at D = 128: two CTAs per SM
   static constexpr int LDK = D + 8, LDC = C + 8;
-  __nv_bfloat16 q[C * LDK];
+  union {
+    __nv_bfloat16 q[C * LDK];   // Q until e^G o Q is written out
+    __nv_bfloat16 vb[C * LDK];  // then b o V
+  } qv;
   __nv_bfloat16 k[C * LDK];
   __nv_bfloat16 kb[C * LDK];
-  __nv_bfloat16 vb[C * LDK];
-  __nv_bfloat16 t[C * LDC];
-  float l[C][C + 1];
+  union {
+    float l[C][C + 1];            // L until inverted
+    __nv_bfloat16 t[C * LDC];     // then T (bf16 operand)
+  } lt;
   float x[C][C + 1];
+  float scr[4 * 16 * 17];
   float g[C], beta[C];
 };
 
@@ -411,7 +465,7 @@ __global__ void __launch_bounds__(kThreads)
       qv = *reinterpret_cast<const float4*>(qn + ((size_t)(c0 + r) * Hk + kh) * D + c4);
       kv = *reinterpret_cast<const float4*>(kn + ((size_t)(c0 + r) * Hk + kh) * D + c4);
     }
-    *reinterpret_cast<uint2*>(&sm.q[r * LDK + c4]) = make_uint2(pack_bf16(qv.x, qv.y), pack_bf16(qv.z, qv.w));
+    *reinterpret_cast<uint2*>(&sm.qv.q[r * LDK + c4]) = make_uint2(pack_bf16(qv.x, qv.y), pack_bf16(qv.z, qv.w));
     *reinterpret_cast<uint2*>(&sm.k[r * LDK + c4]) = make_uint2(pack_bf16(kv.x, kv.y), pack_bf16(kv.z, kv.w));
   }
   if (tid < C) {
@@ -429,11 +483,6 @@ __global__ void __launch_bounds__(kThreads)
     a1 += __shfl_sync(0xffffffffu, a0, 31);
     sm.g[lane] = a0;
     sm.g[32 + lane] = a1;
-  }
-  for (int idx = tid; idx < C * D; idx += kThreads) {
-    const int r = idx / D, cc = idx % D;
-    const float v = r < len ? io<T>::ld(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + cc) : 0.f;
-    sm.vb[r * LDK + cc] = __float2bfloat16_rn(v * sm.beta[r]);
   }
   __syncthreads();
   __nv_bfloat16* rec = ws + ws_tile<D>(n, h, Hv);
@@ -453,7 +502,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int ks = 0; ks < D; ks += 16) {
       uint32_t ak[4], aq[4];
       lda(sm.k, LDK, warp * 16, ks, ak);
-      lda(sm.q, LDK, warp * 16, ks, aq);
+      lda(sm.qv.q, LDK, warp * 16, ks, aq);
 #pragma unroll
       for (int nt = 0; nt < 8; nt += 2) {
         uint32_t b0, b1, b2, b3;
@@ -473,20 +522,19 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
           const float gam = i >= j + d ? expf(sm.g[i] - sm.g[j + d]) : 0.f;
-          sm.l[i][j + d] = i > j + d ? -sm.beta[i] * kk[nt][e + d] * gam : 0.f;
+          sm.lt.l[i][j + d] = i > j + d ? -sm.beta[i] * kk[nt][e + d] * gam : 0.f;
           pv[d] = qk[nt][e + d] * gam;
         }
         *reinterpret_cast<uint32_t*>(wP + i * C + j) = pack_bf16(pv[0], pv[1]);
       }
   }
-  if (tid < C) sm.x[0][tid] = tid == 0 ? 1.f : 0.f;
   {
     const float gl = sm.g[C - 1];
     for (int idx = tid; idx < C * D / 2; idx += kThreads) {
       const int r = idx / (D / 2), cc = (idx % (D / 2)) * 2;
       const float eg = expf(sm.g[r]), ed = expf(gl - sm.g[r]);
       const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[r * LDK + cc]));
-      const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[r * LDK + cc]));
+      const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.qv.q[r * LDK + cc]));
       *reinterpret_cast<uint32_t*>(&sm.kb[r * LDK + cc]) = pack_bf16(kv.x * sm.beta[r] * eg, kv.y * sm.beta[r] * eg);
       *reinterpret_cast<uint32_t*>(wKd + r * D + cc) = pack_bf16(kv.x * ed, kv.y * ed);
       *reinterpret_cast<uint32_t*>(wQg + r * D + cc) = pack_bf16(qv.x * eg, qv.y * eg);
@@ -494,25 +542,17 @@ __global__ void __launch_bounds__(kThreads)
     if (tid == 0) glast[(size_t)n * Hv + h] = gl;
   }
   __syncthreads();
-  // T = (I - L)^{-1}: 16x16 diagonal blocks first (each warp one block, rows in sequence),
-  // then the block rows below the diagonal by forward substitution over blocks.
-  for (int i = 1; i < C; ++i) {
-    if (tid < C) {
-      const int j = tid;
-      float acc = 0.f;
-      if (j < i) {
-        acc = sm.l[i][j];
-        for (int m = j + 1; m < i; ++m) acc += sm.l[i][m] * sm.x[m][j];
-      } else if (j == i) {
-        acc = 1.f;
-      }
-      sm.x[i][j] = acc;
-    }
-    __syncthreads();
+  // T = (I - L)^{-1}: 16x16 diagonal blocks, then the block rows below them
+  // Q is dead (e^G o Q went out): its tile takes b o V
+  for (int idx = tid; idx < C * D; idx += kThreads) {
+    const int r = idx / D, cc = idx % D;
+    const float v = r < len ? io<T>::ld(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + cc) : 0.f;
+    sm.qv.vb[r * LDK + cc] = __float2bfloat16_rn(v * sm.beta[r]);
   }
+  invert_unit_lower(sm.lt.l, sm.x, sm.scr);
   for (int idx = tid; idx < C * C; idx += kThreads) {
     const int i = idx / C, j = idx % C;
-    sm.t[i * LDC + j] = __float2bfloat16_rn(sm.x[i][j]);
+    sm.lt.t[i * LDC + j] = __float2bfloat16_rn(sm.x[i][j]);
   }
   __syncthreads();
   // W = T Kb, U = T Vb  (both [64][D]) -> workspace
@@ -525,14 +565,14 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int ks = 0; ks < C; ks += 16) {
       uint32_t a[4];
-      lda(sm.t, LDC, warp * 16, ks, a);
+      lda(sm.lt.t, LDC, warp * 16, ks, a);
 #pragma unroll
       for (int nt = 0; nt < D / 8; nt += 2) {
         uint32_t b0, b1, b2, b3;
         ldb_kn(sm.kb, LDK, nt * 8, ks, b0, b1, b2, b3);
         mma_bf16(wacc[nt], a, b0, b1);
         mma_bf16(wacc[nt + 1], a, b2, b3);
-        ldb_kn(sm.vb, LDK, nt * 8, ks, b0, b1, b2, b3);
+        ldb_kn(sm.qv.vb, LDK, nt * 8, ks, b0, b1, b2, b3);
         mma_bf16(uacc[nt], a, b0, b1);
         mma_bf16(uacc[nt + 1], a, b2, b3);
       }
@@ -820,6 +860,7 @@ struct KdaIntraSmem {
     struct { float l[C][C + 1]; float x[C][C + 1]; } lx;
   } u2;
   __nv_bfloat16 t[C * LDC];
+  float scr[4 * 16 * 17];
   float g[C * D];  // G[r][d]: cumulative log decay
   float beta[C];
 };
@@ -967,7 +1008,6 @@ __global__ void __launch_bounds__(kThreads)
       wP[i * C + j] = __float2bfloat16_rn(dqk[u]);
     }
   }
-  if (tid < C) sm.u2.lx.x[0][tid] = tid == 0 ? 1.f : 0.f;
   // chunk-global operands: b e^G K, b V (W/U step), e^G Q and e^{G_C - G} K (state pass)
   for (int idx = tid; idx < C * D / 2; idx += kThreads) {
     const int r = idx / (D / 2), cc = (idx % (D / 2)) * 2;
@@ -987,21 +1027,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.g[(C - 1) * D + d];
   __syncthreads();
-  // T = (I - L)^{-1} by forward substitution (row i depends on rows < i)
-  for (int i = 1; i < C; ++i) {
-    if (tid < C) {
-      const int j = tid;
-      float acc = 0.f;
-      if (j < i) {
-        acc = sm.u2.lx.l[i][j];
-        for (int m = j + 1; m < i; ++m) acc += sm.u2.lx.l[i][m] * sm.u2.lx.x[m][j];
-      } else if (j == i) {
-        acc = 1.f;
-      }
-      sm.u2.lx.x[i][j] = acc;
-    }
-    __syncthreads();
-  }
+  // T = (I - L)^{-1}
+  invert_unit_lower(sm.u2.lx.l, sm.u2.lx.x, sm.scr);
   for (int idx = tid; idx < C * C; idx += kThreads) {
     const int i = idx / C, j = idx % C;
     sm.t[i * LDC + j] = __float2bfloat16_rn(sm.u2.lx.x[i][j]);
