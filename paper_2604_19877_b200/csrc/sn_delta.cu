@@ -143,17 +143,13 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
   float s_nx[NB][EPL];
 #pragma unroll
   for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int pos = a.positions[b];
+  // Conv taps and the 4 ring slots of this thread's channels do not depend on the previous
+  // kernel either (weights; the ring is written by this layer's previous step and all 4
+  // slots are loaded, so the position is not needed yet): requested before the wait too,
+  // leaving only the in-projection values for after it.
   const int W = a.W;
-  const GemmIn<T> pin{a.proj, a.proj_nsplit, (size_t)gridDim.y * a.proj_stride};
-  const size_t prow = (size_t)b * a.proj_stride;
   T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * W;
   const T* cw = reinterpret_cast<const T*>(a.conv_w);
-
-  // ---- 1. prologue loads, all issued before any is consumed (one memory round trip):
-  //      the <=2 conv channels of this thread (proj value, 4 taps, 4 ring slots),
-  //      the output gate z (GDN) / low-rank gate inputs f1,g1 (KDA), a, b.
   constexpr int NCH = (3 * D + kDecodeThreads - 1) / kDecodeThreads;
   float xin[NCH], wt[NCH][4], rg[NCH][4];
   int chn[NCH];
@@ -165,13 +161,25 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
       const int part = c / D, i = c - part * D;
       const int ch = part == 0 ? a.q_off + kh * D + i : (part == 1 ? a.k_off + kh * D + i : a.v_off + h * D + i);
       chn[u] = ch;
-      xin[u] = pin(prow + ch);
       if (W == 4) {
         load4<T>(cw + (size_t)ch * 4, wt[u]);
         load4<T>(ring + (size_t)ch * 4, rg[u]);
       }
     }
   }
+  const float negA = -expf(a.A_log[h]);
+  const float dtb = KDA ? 0.f : a.dt_bias[h];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int pos = a.positions[b];
+  const GemmIn<T> pin{a.proj, a.proj_nsplit, (size_t)gridDim.y * a.proj_stride};
+  const size_t prow = (size_t)b * a.proj_stride;
+
+  // ---- 1. prologue loads of the in-projection row, all issued before any is consumed:
+  //      this thread's conv inputs, the output gate z (GDN) / low-rank gate inputs f1,g1
+  //      (KDA), a, b.
+#pragma unroll
+  for (int u = 0; u < NCH; ++u)
+    if (chn[u] >= 0) xin[u] = pin(prow + chn[u]);
   float zval = 0.f;
   if (!KDA && tid < D) zval = pin(prow + a.z_off + h * D + tid);
   float fg = 0.f, fpre = 0.f, gpre = 0.f;
@@ -184,8 +192,7 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
     gpre = io<T>::ld(fgp + gridDim.y * HD) + io<T>::ld(reinterpret_cast<const T*>(a.g2_b) + h * D + tid);
   }
   const float braw = pin(prow + a.b_off + h);
-  const float graw = KDA ? 0.f : pin(prow + a.a_off + h) + a.dt_bias[h];
-  const float negA = -expf(a.A_log[h]);
+  const float graw = KDA ? 0.f : pin(prow + a.a_off + h) + dtb;
 
   // ---- 2. conv + SiLU (slot p % W of the ring holds the input of position p)
 #pragma unroll
