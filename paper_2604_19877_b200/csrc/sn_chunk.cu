@@ -88,6 +88,72 @@ __device__ __forceinline__ void invert_unit_lower(const float (*l)[C + 1], float
   }
 }
 
+
+// Chunk-tile loaders with the global loads batched ahead of their conversions (one
+// dependent memory round trip per batch instead of one per element: the loops were the
+// top long-scoreboard stall of the intra kernels).
+// b o V tile [64][D] (bf16, row stride LDK) from the conv output rows c0.. (rows >= len zero).
+template <typename T, int D>
+__device__ __forceinline__ void load_vb_tile(const T* __restrict__ qkv, int qkv_stride, int v_off, int h, int c0,
+                                             int len, const float* beta_s, __nv_bfloat16* dst, int ldk) {
+  constexpr int IT = C * D / 8 / kThreads, BATCH = IT < 4 ? IT : 4;
+#pragma unroll
+  for (int i0 = 0; i0 < IT; i0 += BATCH) {
+    float v[BATCH][8];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int idx = threadIdx.x + (i0 + u) * kThreads;
+      const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
+      if (r < len) load8<T>(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + c8, v[u]);
+      else
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int idx = threadIdx.x + (i0 + u) * kThreads;
+      const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
+      const float b = beta_s[r];
+      uint4 pk;
+      pk.x = pack_bf16(v[u][0] * b, v[u][1] * b);
+      pk.y = pack_bf16(v[u][2] * b, v[u][3] * b);
+      pk.z = pack_bf16(v[u][4] * b, v[u][5] * b);
+      pk.w = pack_bf16(v[u][6] * b, v[u][7] * b);
+      *reinterpret_cast<uint4*>(dst + r * ldk + c8) = pk;
+    }
+  }
+}
+
+// fp32 [rows][heads][D] row slices (head hh, rows c0.. < len, else zero) -> bf16 tile [64][D]
+// (row stride ldk); NSRC tensors loaded together.
+template <int D, int NSRC>
+__device__ __forceinline__ void load_f32_tiles(const float* const* src, int heads, int hh, int c0, int len,
+                                               __nv_bfloat16* const* dst, int ldk) {
+  constexpr int IT = C * D / 4 / kThreads, BATCH = IT < 4 ? IT : 4;
+#pragma unroll
+  for (int i0 = 0; i0 < IT; i0 += BATCH) {
+    float4 v[NSRC][BATCH];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int idx = threadIdx.x + (i0 + u) * kThreads;
+      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
+#pragma unroll
+      for (int t = 0; t < NSRC; ++t)
+        v[t][u] = r < len ? *reinterpret_cast<const float4*>(src[t] + ((size_t)(c0 + r) * heads + hh) * D + c4)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int idx = threadIdx.x + (i0 + u) * kThreads;
+      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
+#pragma unroll
+      for (int t = 0; t < NSRC; ++t)
+        *reinterpret_cast<uint2*>(dst[t] + r * ldk + c4) =
+            make_uint2(pack_bf16(v[t][u].x, v[t][u].y), pack_bf16(v[t][u].z, v[t][u].w));
+    }
+  }
+}
+
 template <int D>
 struct Smem {
   static constexpr int LDK = D + 8, LDV = VT + 8, LDC = C + 8;
@@ -458,15 +524,10 @@ __global__ void __launch_bounds__(kThreads)
   const int n = blockIdx.x, h = blockIdx.y;
   const int G = Hv / Hk, kh = h / G;
   const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
-  for (int idx = tid; idx < C * D / 4; idx += kThreads) {
-    const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
-    float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), kv = qv;
-    if (r < len) {
-      qv = *reinterpret_cast<const float4*>(qn + ((size_t)(c0 + r) * Hk + kh) * D + c4);
-      kv = *reinterpret_cast<const float4*>(kn + ((size_t)(c0 + r) * Hk + kh) * D + c4);
-    }
-    *reinterpret_cast<uint2*>(&sm.qv.q[r * LDK + c4]) = make_uint2(pack_bf16(qv.x, qv.y), pack_bf16(qv.z, qv.w));
-    *reinterpret_cast<uint2*>(&sm.k[r * LDK + c4]) = make_uint2(pack_bf16(kv.x, kv.y), pack_bf16(kv.z, kv.w));
+  {
+    const float* src[2] = {qn, kn};
+    __nv_bfloat16* dst[2] = {sm.qv.q, sm.k};
+    load_f32_tiles<D, 2>(src, Hk, kh, c0, len, dst, LDK);
   }
   if (tid < C) {
     sm.g[tid] = tid < len ? glog[(size_t)(c0 + tid) * Hv + h] : 0.f;
@@ -544,11 +605,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   // T = (I - L)^{-1}: 16x16 diagonal blocks, then the block rows below them
   // Q is dead (e^G o Q went out): its tile takes b o V
-  for (int idx = tid; idx < C * D; idx += kThreads) {
-    const int r = idx / D, cc = idx % D;
-    const float v = r < len ? io<T>::ld(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + cc) : 0.f;
-    sm.qv.vb[r * LDK + cc] = __float2bfloat16_rn(v * sm.beta[r]);
-  }
+  load_vb_tile<T, D>(qkv, qkv_stride, v_off, h, c0, len, sm.beta, sm.qv.vb, LDK);
   invert_unit_lower(sm.lt.l, sm.x, sm.scr);
   for (int idx = tid; idx < C * C; idx += kThreads) {
     const int i = idx / C, j = idx % C;
@@ -880,18 +937,24 @@ __global__ void __launch_bounds__(kThreads)
   const int g4 = lane >> 2, t4 = lane & 3;
   const int n = blockIdx.x, h = blockIdx.y;
   const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
-  for (int idx = tid; idx < C * D / 4; idx += kThreads) {
-    const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
-    float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), kv = qv, gv = qv;
-    if (r < len) {
-      const size_t off = ((size_t)(c0 + r) * H + h) * D + c4;
-      qv = *reinterpret_cast<const float4*>(qn + off);
-      kv = *reinterpret_cast<const float4*>(kn + off);
-      gv = *reinterpret_cast<const float4*>(glog + off);
+  {
+    const float* src[2] = {qn, kn};
+    __nv_bfloat16* dst[2] = {sm.q, sm.k};
+    load_f32_tiles<D, 2>(src, H, h, c0, len, dst, LDK);
+    constexpr int IT = C * D / 4 / kThreads;
+    float4 gv[IT];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int idx = tid + u * kThreads;
+      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
+      gv[u] = r < len ? *reinterpret_cast<const float4*>(glog + ((size_t)(c0 + r) * H + h) * D + c4)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    *reinterpret_cast<uint2*>(&sm.q[r * LDK + c4]) = make_uint2(pack_bf16(qv.x, qv.y), pack_bf16(qv.z, qv.w));
-    *reinterpret_cast<uint2*>(&sm.k[r * LDK + c4]) = make_uint2(pack_bf16(kv.x, kv.y), pack_bf16(kv.z, kv.w));
-    *reinterpret_cast<float4*>(&sm.g[r * D + c4]) = gv;
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int idx = tid + u * kThreads;
+      *reinterpret_cast<float4*>(&sm.g[(idx / (D / 4)) * D + (idx % (D / 4)) * 4]) = gv[u];
+    }
   }
   if (tid < C) sm.beta[tid] = tid < len ? beta[(size_t)(c0 + tid) * H + h] : 0.f;
   __syncthreads();
@@ -1020,11 +1083,7 @@ __global__ void __launch_bounds__(kThreads)
     *reinterpret_cast<uint32_t*>(wKd + r * D + cc) = pack_bf16(kv.x * expf(gl0 - g0), kv.y * expf(gl1 - g1));
     *reinterpret_cast<uint32_t*>(wQg + r * D + cc) = pack_bf16(qv.x * expf(g0), qv.y * expf(g1));
   }
-  for (int idx = tid; idx < C * D; idx += kThreads) {
-    const int r = idx / D, cc = idx % D;
-    const float v = r < len ? io<T>::ld(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + cc) : 0.f;
-    sm.u1.w.vb[r * LDK + cc] = __float2bfloat16_rn(v * sm.beta[r]);
-  }
+  load_vb_tile<T, D>(qkv, qkv_stride, v_off, h, c0, len, sm.beta, sm.u1.w.vb, LDK);
   for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.g[(C - 1) * D + d];
   __syncthreads();
   // T = (I - L)^{-1}
