@@ -645,9 +645,9 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-template <int D>
+template <int D, int VTT = VT>
 struct StateSmem {
-  static constexpr int LDK = D + 8, LDV = VT + 8, LDC = C + 8;
+  static constexpr int LDK = D + 8, LDV = VTT + 8, LDC = C + 8;
   struct Stage {
     __nv_bfloat16 w[C * LDK];
     __nv_bfloat16 qg[C * LDK];
@@ -668,14 +668,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // PERCH (KDA): glast holds the chunk's per-key-channel cumulative log decay [D] per (chunk,
 // head) and S is decayed row-wise, diag(e^{G_C}) S; otherwise one scalar per (chunk, head).
-template <int D, bool PERCH = false>
+template <int D, bool PERCH = false, int VTT = VT>
 __global__ void __launch_bounds__(kThreads, 1)
     gdn_chunk_state_kernel(const __nv_bfloat16* __restrict__ ws, const float* __restrict__ glast,
                            const int32_t* __restrict__ chunks, const int32_t* __restrict__ seq_chunk0,
                            float* __restrict__ o, float* __restrict__ state, const int32_t* __restrict__ slot_idx,
                            int Hv, int init_state) {
   pdl_launch_dependents();
-  using SM = StateSmem<D>;
+  using SM = StateSmem<D, VTT>;
+  constexpr int NTV = VTT / 8;  // n8 tiles of this CTA's value columns
   constexpr int LDK = SM::LDK, LDV = SM::LDV, LDC = SM::LDC;
   constexpr int MT = D / 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -686,15 +687,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int slot = slot_idx ? slot_idx[seq] : seq;
   const int n0 = seq_chunk0[seq], n1 = seq_chunk0[seq + 1];
   float* Sg = state + ((size_t)slot * Hv + h) * D * D;
-  float sf[MT][8][4];
+  float sf[MT][NTV][4];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int kr = (warp * MT + mt) * 16 + g4 + ((e >> 1) << 3);
-        const int vc = vt * VT + nt * 8 + t4 * 2 + (e & 1);
+        const int vc = vt * VTT + nt * 8 + t4 * 2 + (e & 1);
         sf[mt][nt][e] = init_state ? Sg[(size_t)vc * D + kr] : 0.f;
       }
   auto load_stage = [&](int n, int b) {
@@ -706,9 +707,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       cp_async16(&S.qg[r * LDK + c8], rec + C * D + r * D + c8);
       cp_async16(&S.kd[r * LDK + c8], rec + 2 * C * D + r * D + c8);
     }
-    for (int idx = tid; idx < C * VT / 8; idx += kThreads) {  // U tile (this CTA's value columns), P
-      const int r = idx / (VT / 8), c8 = (idx % (VT / 8)) * 8;
-      cp_async16(&S.u[r * LDV + c8], rec + 3 * C * D + r * D + vt * VT + c8);
+    for (int idx = tid; idx < C * VTT / 8; idx += kThreads) {  // U tile (this CTA's value columns)
+      const int r = idx / (VTT / 8), c8 = (idx % (VTT / 8)) * 8;
+      cp_async16(&S.u[r * LDV + c8], rec + 3 * C * D + r * D + vt * VTT + c8);
+    }
+    for (int idx = tid; idx < C * C / 8; idx += kThreads) {  // P
+      const int r = idx / (C / 8), c8 = (idx % (C / 8)) * 8;
       cp_async16(&S.p[r * LDC + c8], rec + 4 * C * D + r * C + c8);
     }
     cp_async_commit();
@@ -726,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; e += 2) {
           const int kr = (warp * MT + mt) * 16 + g4 + ((e >> 1) << 3);
@@ -736,9 +740,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     typename SM::Stage& St = sm.st[b];
     const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
     // V' = U - W S
-    float vpc[8][4];
+    float vpc[NTV][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = nt * 8 + t4 * 2 + (e & 1);
@@ -749,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t a[4];
       lda(St.w, LDK, warp * 16, ks, a);
 #pragma unroll
-      for (int nt = 0; nt < 8; nt += 2) {
+      for (int nt = 0; nt < NTV; nt += 2) {
         uint32_t b0, b1, b2, b3;
         ldb_kn(sm.s, LDV, nt * 8, ks, b0, b1, b2, b3);
         float ws0[4] = {0.f, 0.f, 0.f, 0.f}, ws1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -760,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; e += 2) {
         const int r = warp * 16 + g4 + ((e >> 1) << 3);
@@ -769,9 +773,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     // O = Qg S + P V'
     {
-      float oc[8][4];
+      float oc[NTV][4];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) oc[nt][e] = 0.f;
 #pragma unroll
@@ -779,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t a[4];
         lda(St.qg, LDK, warp * 16, ks, a);
 #pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
+        for (int nt = 0; nt < NTV; nt += 2) {
           uint32_t b0, b1, b2, b3;
           ldb_kn(sm.s, LDV, nt * 8, ks, b0, b1, b2, b3);
           mma_bf16(oc[nt], a, b0, b1);
@@ -791,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t a[4];
         lda(St.p, LDC, warp * 16, ks, a);
 #pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
+        for (int nt = 0; nt < NTV; nt += 2) {
           uint32_t b0, b1, b2, b3;
           ldb_kn(sm.vp, LDV, nt * 8, ks, b0, b1, b2, b3);
           mma_bf16(oc[nt], a, b0, b1);
@@ -799,10 +803,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; e += 2) {
-          const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = vt * VT + nt * 8 + t4 * 2;
+          const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = vt * VTT + nt * 8 + t4 * 2;
           if (r < len)
             *reinterpret_cast<float2*>(o + ((size_t)(c0 + r) * Hv + h) * D + cc) = make_float2(oc[nt][e], oc[nt][e + 1]);
         }
@@ -817,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e2 = 0; e2 < 2; ++e2) {
             const float dec = expf(gl[(warp * MT + mt) * 16 + g4 + (e2 << 3)]);
 #pragma unroll
-            for (int nt = 0; nt < 8; ++nt) {
+            for (int nt = 0; nt < NTV; ++nt) {
               sf[mt][nt][2 * e2] *= dec;
               sf[mt][nt][2 * e2 + 1] *= dec;
             }
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 8; ++nt)
+          for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
             for (int e = 0; e < 4; ++e) sf[mt][nt][e] *= dec;
       }
@@ -838,7 +842,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t a[4];
           lda_t(St.kd, LDK, (warp * MT + mt) * 16, ks, a);
 #pragma unroll
-          for (int nt = 0; nt < 8; nt += 2) {
+          for (int nt = 0; nt < NTV; nt += 2) {
             uint32_t b0, b1, b2, b3;
             ldb_kn(sm.vp, LDV, nt * 8, ks, b0, b1, b2, b3);
             mma_bf16(sf[mt][nt], a, b0, b1);
@@ -852,11 +856,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < NTV; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int kr = (warp * MT + mt) * 16 + g4 + ((e >> 1) << 3);
-        const int vc = vt * VT + nt * 8 + t4 * 2 + (e & 1);
+        const int vc = vt * VTT + nt * 8 + t4 * 2 + (e & 1);
         Sg[(size_t)vc * D + kr] = sf[mt][nt][e];
       }
 }
@@ -867,19 +871,28 @@ static sn_status launch_two_phase(const float* qn, const float* kn, const void* 
                                   const int32_t* seq_chunk0, int num_chunks, void* ws, float* glast, float* o,
                                   float* state, const int32_t* slot_idx, int num_seqs, int Hk, int Hv,
                                   int init_state, cudaStream_t st) {
-  const int smem_a = (int)sizeof(IntraSmem<D>), smem_b = (int)sizeof(StateSmem<D>);
+  const int smem_a = (int)sizeof(IntraSmem<D>);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gdn_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
-    cudaFuncSetAttribute(gdn_chunk_state_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StateSmem<D, 64>));
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StateSmem<D, 32>));
     attr = true;
   }
   gdn_chunk_intra_kernel<T, D><<<dim3(num_chunks, Hv), kThreads, smem_a, st>>>(
       qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, Hk, Hv);
   sn_status e = check_launch("sn_gdn_chunk_prefill(intra)");
   if (e != SN_OK) return e;
-  gdn_chunk_state_kernel<D><<<dim3(D / VT, Hv, num_seqs), kThreads, smem_b, st>>>(
-      (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, Hv, init_state);
+  // the state pass is sequential over chunks: few (sequence, head) pairs -> narrower value
+  // tiles so more CTAs run the chain side by side
+  if (num_seqs * Hv * (D / 64) < 148)
+    gdn_chunk_state_kernel<D, false, 32><<<dim3(D / 32, Hv, num_seqs), kThreads, sizeof(StateSmem<D, 32>), st>>>(
+        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, Hv, init_state);
+  else
+    gdn_chunk_state_kernel<D, false, 64><<<dim3(D / 64, Hv, num_seqs), kThreads, sizeof(StateSmem<D, 64>), st>>>(
+        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, Hv, init_state);
   return check_launch("sn_gdn_chunk_prefill(state)");
 }
 
@@ -1132,19 +1145,26 @@ static sn_status launch_kda_two_phase(const float* qn, const float* kn, const vo
                                       const int32_t* seq_chunk0, int num_chunks, void* ws, float* glast, float* o,
                                       float* state, const int32_t* slot_idx, int num_seqs, int H, int init_state,
                                       cudaStream_t st) {
-  const int smem_a = (int)sizeof(KdaIntraSmem<D>), smem_b = (int)sizeof(StateSmem<D>);
+  const int smem_a = (int)sizeof(KdaIntraSmem<D>);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kda_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
-    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StateSmem<D, 64>));
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StateSmem<D, 32>));
     attr = true;
   }
   kda_chunk_intra_kernel<T, D><<<dim3(num_chunks, H), kThreads, smem_a, st>>>(
       qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, H);
   sn_status e = check_launch("sn_kda_chunk_prefill(intra)");
   if (e != SN_OK) return e;
-  gdn_chunk_state_kernel<D, true><<<dim3(D / VT, H, num_seqs), kThreads, smem_b, st>>>(
-      (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
+  if (num_seqs * H * (D / 64) < 148)
+    gdn_chunk_state_kernel<D, true, 32><<<dim3(D / 32, H, num_seqs), kThreads, sizeof(StateSmem<D, 32>), st>>>(
+        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
+  else
+    gdn_chunk_state_kernel<D, true, 64><<<dim3(D / 64, H, num_seqs), kThreads, sizeof(StateSmem<D, 64>), st>>>(
+        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
   return check_launch("sn_kda_chunk_prefill(state)");
 }
 

@@ -30,9 +30,11 @@ def _inputs(lens, Hk, Hv, D, seed):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("D,Hk,Hv", [(128, 2, 8), (64, 1, 4)])
-@pytest.mark.parametrize("lens", [[1], [63], [64], [65], [200, 17, 128], [1000]])
+@pytest.mark.parametrize("lens", [[1], [63], [64], [65], [200, 17, 128], [1000], [30] * 10])
 @pytest.mark.parametrize("init", [False, True])
 def test_chunked_matches_scan(D, Hk, Hv, lens, init):
+    """[30] * 10 at D=128: 10 sequences x 8 heads x 2 value tiles >= 148 CTAs -> the wide
+    (64-column) state-pass tiles; the other cases run the narrow (32-column) ones."""
     from paper_2604_19877_b200 import ops
     qn, kn, qkv, glog, beta, cu = _inputs(lens, Hk, Hv, D, seed=len(lens) * 7 + sum(lens))
     B = len(lens)
@@ -108,7 +110,7 @@ def _kda_gates(T, H, D, g):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("D,H", [(128, 4), (64, 4)])
-@pytest.mark.parametrize("lens", [[1], [63], [64], [65], [200, 17, 128], [1000]])
+@pytest.mark.parametrize("lens", [[1], [63], [64], [65], [200, 17, 128], [1000], [20] * 20])
 @pytest.mark.parametrize("init", [False, True])
 def test_kda_chunked_matches_scan(D, H, lens, init):
     from paper_2604_19877_b200 import ops
