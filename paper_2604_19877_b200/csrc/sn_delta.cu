@@ -356,6 +356,27 @@ __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __
   const int p0 = blockIdx.y * CH;
   if (p0 >= L) return;
   const int p1 = min(p0 + CH, L);
+  if (W == 4) {  // the pinned width: taps and history in registers, loads batched by 8
+    float w4[4];
+    load4<T>(w + (size_t)c * 4, w4);
+    const T* xc = x + (size_t)t0 * x_stride + c;
+    float h1 = p0 >= 1 ? io<T>::ld(xc + (size_t)(p0 - 1) * x_stride) : 0.f;
+    float h2 = p0 >= 2 ? io<T>::ld(xc + (size_t)(p0 - 2) * x_stride) : 0.f;
+    float h3 = p0 >= 3 ? io<T>::ld(xc + (size_t)(p0 - 3) * x_stride) : 0.f;
+    for (int p = p0; p < p1; p += 8) {
+      float xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = p + u < p1 ? io<T>::ld(xc + (size_t)(p + u) * x_stride) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (p + u < p1) {
+          const float acc = w4[3] * xv[u] + w4[2] * h1 + w4[1] * h2 + w4[0] * h3;
+          io<T>::st(y + (size_t)(t0 + p + u) * channels + c, silu_f(acc));
+        }
+        h3 = h2; h2 = h1; h1 = xv[u];
+      }
+    }
+  } else {
   float wt[8];
   for (int d = 0; d < W; ++d) wt[d] = io<T>::ld(w + (size_t)c * W + d);
   float hist[8];  // hist[d] = x at position p-1-d
@@ -371,6 +392,7 @@ __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __
     for (int d = W - 2; d > 0; --d) hist[d] = hist[d - 1];
     if (W > 1) hist[0] = xv;
   }
+  }
   if (p1 == L) {  // the chunk holding the last position leaves the ring for decode
     const int slot = slot_idx ? slot_idx[s] : s;
     T* rrow = ring + ((size_t)slot * channels + c) * W;
@@ -382,7 +404,8 @@ __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __
   }
 }
 
-// Per (row, value head): l2-normalised q/k, exp(gate), beta.
+// Per (row, key head): l2-normalised q/k (computed once per key head), then exp(gate),
+// log gate and beta of the G = Hv/Hk value heads that read it.
 template <typename T, int D, bool KDA>
 __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv, const T* __restrict__ proj,
                                                        int proj_stride, int b_off, int a_off,
@@ -391,31 +414,42 @@ __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv
                                                        float* __restrict__ kn, float* __restrict__ gexp,
                                                        float* __restrict__ glog, float* __restrict__ beta, int Hk,
                                                        int Hv, float scale, float eps_l2) {
-  __shared__ float red[D / 32];
-  const int r = blockIdx.x, h = blockIdx.y, i = threadIdx.x;  // rows on x: > 65535 tokens
-  const int G = Hv / Hk, kh = h / G;
+  __shared__ float red[2 * (D / 32)];
+  const int r = blockIdx.x, kh = blockIdx.y, i = threadIdx.x;  // rows on x: > 65535 tokens
+  const int G = Hv / Hk;
   const int qkv_stride = 2 * Hk * D + Hv * D;
   const T* row = qkv + (size_t)r * qkv_stride;
-  const float q = io<T>::ld(row + kh * D + i), k = io<T>::ld(row + Hk * D + kh * D + i);
-  const float qq = block_sum(q * q, red);
-  const float kk = block_sum(k * k, red);
-  if (h % G == 0) {
-    qn[((size_t)r * Hk + kh) * D + i] = q * rsqrtf(qq + eps_l2) * scale;
-    kn[((size_t)r * Hk + kh) * D + i] = k * rsqrtf(kk + eps_l2);
-  }
   const T* prow = proj + (size_t)r * proj_stride;
-  const float negA = -expf(A_log[h]);
+  const float q = io<T>::ld(row + kh * D + i), k = io<T>::ld(row + Hk * D + kh * D + i);
+  // gate inputs of this key head's value heads, loaded before the reductions
+  float fv = 0.f, araw = 0.f, braw = 0.f;
+  if (KDA) fv = io<T>::ld(f + (size_t)r * Hv * D + kh * D + i);  // KDA: G == 1
+  else if (i < G) araw = io<T>::ld(prow + a_off + kh * G + i);
+  if (i < G) braw = io<T>::ld(prow + b_off + kh * G + i);
+  float qq = q * q, kk = k * k;
+  qq = warp_sum(qq);
+  kk = warp_sum(kk);
+  const int lane = i & 31, warp = i >> 5;
+  if (lane == 0) { red[warp] = qq; red[D / 32 + warp] = kk; }
+  __syncthreads();
+  qq = 0.f;
+  kk = 0.f;
+#pragma unroll
+  for (int w = 0; w < D / 32; ++w) { qq += red[w]; kk += red[D / 32 + w]; }
+  qn[((size_t)r * Hk + kh) * D + i] = q * rsqrtf(qq + eps_l2) * scale;
+  kn[((size_t)r * Hk + kh) * D + i] = k * rsqrtf(kk + eps_l2);
   if (KDA) {
-    const float fv = io<T>::ld(f + (size_t)r * Hv * D + h * D + i);
-    const float gl = negA * softplus_f(fv + dt_bias[h * D + i]);
+    const int h = kh;
+    const float gl = -expf(A_log[h]) * softplus_f(fv + dt_bias[h * D + i]);
     gexp[((size_t)r * Hv + h) * D + i] = expf(gl);
     if (glog) glog[((size_t)r * Hv + h) * D + i] = gl;  // per-channel log gate (chunked KDA prefill)
-  } else if (i == 0) {
-    const float g = negA * softplus_f(io<T>::ld(prow + a_off + h) + dt_bias[h]);
+  } else if (i < G) {
+    const int h = kh * G + i;
+    const float g = -expf(A_log[h]) * softplus_f(araw + dt_bias[h]);
     gexp[(size_t)r * Hv + h] = expf(g);
     if (glog) glog[(size_t)r * Hv + h] = g;
   }
-  if (i == 0) beta[(size_t)r * Hv + h] = sigmoid_f(io<T>::ld(prow + b_off + h));
+  if (i < G) beta[(size_t)r * Hv + kh * G + i] = sigmoid_f(braw);
 }
 
 // Recurrent scan: CTA = 4 warps x 8 value columns of one (sequence, head); state in registers.
@@ -615,9 +649,11 @@ sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int pr
   SN_REQUIRE(kind == 0 || kind == 1, "sn_delta_prep: kind %d", kind);
   SN_REQUIRE(rows > 0 && Hk > 0 && Hv % Hk == 0, "sn_delta_prep: bad shape");
   SN_REQUIRE(kind == 0 || f != nullptr, "sn_delta_prep: KDA needs f");
+  SN_REQUIRE(kind == 0 || Hk == Hv, "sn_delta_prep: KDA has one key head per value head");
+  SN_REQUIRE(Hv / Hk <= D, "sn_delta_prep: too many value heads per key head");
   SN_REQUIRE(D == 64 || D == 128, "sn_delta_prep: D=%d unsupported", D);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    dim3 grid(rows, Hv);
+    dim3 grid(rows, Hk);
     cudaStream_t st = (cudaStream_t)stream;
     auto fn = D == 128 ? (kind ? launch_prep<T, 128, true> : launch_prep<T, 128, false>)
                        : (kind ? launch_prep<T, 64, true> : launch_prep<T, 64, false>);
