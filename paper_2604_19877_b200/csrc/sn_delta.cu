@@ -512,18 +512,41 @@ __global__ void __launch_bounds__(128) delta_scan_kernel(const float* __restrict
     for (int e = 0; e < EPL; ++e) S[(size_t)(c0 + n) * D + lane * EPL + e] = st[n][e];
 }
 
+// One warp per (row, head): D/32 values per lane (vectorised), a shuffle reduction, no
+// block barrier; 8 warps per CTA cover 8 (row, head) pairs.
 template <typename T, int D>
-__global__ void __launch_bounds__(D) gated_rmsnorm_kernel(const float* __restrict__ o, const T* __restrict__ gate,
-                                                          int gate_stride, const T* __restrict__ w,
-                                                          T* __restrict__ out, int H, float eps, int act) {
-  __shared__ float red[D / 32];
-  const int r = blockIdx.x, h = blockIdx.y, j = threadIdx.x;
-  const float v = o[((size_t)r * H + h) * D + j];
-  const float ss = block_sum(v * v, red);
+__global__ void __launch_bounds__(256) gated_rmsnorm_kernel(const float* __restrict__ o, const T* __restrict__ gate,
+                                                            int gate_stride, const T* __restrict__ w,
+                                                            T* __restrict__ out, int rows, int H, float eps, int act) {
+  constexpr int EPL = D / 32;
+  const int lane = threadIdx.x & 31;
+  const size_t pair = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (pair >= (size_t)rows * H) return;
+  const size_t r = pair / H;
+  const int h = (int)(pair % H);
+  const int j0 = lane * EPL;
+  float v[EPL], gz[EPL], wv[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; e += 2) {
+    const float2 t = *reinterpret_cast<const float2*>(o + pair * D + j0 + e);
+    v[e] = t.x;
+    v[e + 1] = t.y;
+  }
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    gz[e] = io<T>::ld(gate + r * gate_stride + h * D + j0 + e);
+    wv[e] = io<T>::ld(w + j0 + e);
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) ss += v[e] * v[e];
+  ss = warp_sum(ss);
   const float rstd = rsqrtf(ss / (float)D + eps);
-  const float gz = io<T>::ld(gate + (size_t)r * gate_stride + h * D + j);
-  const float a = act ? sigmoid_f(gz) : silu_f(gz);
-  io<T>::st(out + ((size_t)r * H + h) * D + j, v * rstd * io<T>::ld(w + j) * a);
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const float a = act ? sigmoid_f(gz[e]) : silu_f(gz[e]);
+    io<T>::st(out + pair * D + j0 + e, v[e] * rstd * wv[e] * a);
+  }
 }
 
 template <typename T, int D, bool KDA>
@@ -685,10 +708,10 @@ sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride, co
                            int rows, int H, int D, float eps, int act, int dtype, void* stream) {
   SN_REQUIRE(rows > 0 && H > 0, "sn_gated_rmsnorm: bad shape");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    dim3 grid(rows, H);
+    const unsigned grid = (unsigned)(((size_t)rows * H + 7) / 8);
     cudaStream_t st = (cudaStream_t)stream;
-    if (D == 128) gated_rmsnorm_kernel<T, 128><<<grid, 128, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, H, eps, act);
-    else if (D == 64) gated_rmsnorm_kernel<T, 64><<<grid, 64, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, H, eps, act);
+    if (D == 128) gated_rmsnorm_kernel<T, 128><<<grid, 256, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, rows, H, eps, act);
+    else if (D == 64) gated_rmsnorm_kernel<T, 64><<<grid, 256, 0, st>>>(o, (const T*)gate, gate_stride, (const T*)norm_w, (T*)out, rows, H, eps, act);
     else { set_error("sn_gated_rmsnorm: D=%d unsupported", D); return SN_EUNSUPPORTED; }
     return check_launch("sn_gated_rmsnorm");
   });
