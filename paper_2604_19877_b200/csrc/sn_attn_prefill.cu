@@ -225,9 +225,16 @@ static sn_status launch(const void* q, const void* k, const void* v, const int32
 
 }  // namespace fa
 
+sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
+                                 int num_seqs, int rows, int Hq, int Hkv, int window, float scale,
+                                 cudaStream_t st);  // sn_attn_prefill_umma.cu
+
 sn_status attn_prefill_tc_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale,
                                cudaStream_t st) {
+  // D = 128: tcgen05/TMEM kernel; SN_ATTN_PREFILL=mma keeps the mma.sync kernel (A/B, D = 64)
+  static const bool mma = getenv("SN_ATTN_PREFILL") && getenv("SN_ATTN_PREFILL")[0] == 'm';
+  if (D == 128 && !mma) return attn_prefill_umma_bf16(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, st);
   if (D == 128) return fa::launch<128>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, st);
   if (D == 64) return fa::launch<64>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, st);
   set_error("sn_attn_prefill: D=%d unsupported", D);

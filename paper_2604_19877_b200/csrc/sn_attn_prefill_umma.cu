@@ -1,0 +1,296 @@
+// Prefill attention on the 5th-generation tensor cores (tcgen05 / TMEM / TMA), D = 128, bf16.
+// Same contract as the mma.sync kernel in sn_attn_prefill.cu (packed ragged sequences,
+// causal or window mask per (row, key) with each row's own sequence start, GQA).
+//
+// CTA = 128 query rows x one q head; 6 warps:
+//   warp 5 (one lane): TMA producer — Q once, then K and V blocks of 128 keys into a
+//           two-stage ring (128B-swizzled 2-D boxes straight from the [rows][H*D] tensors);
+//   warp 4 (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
+//           K-major) into TMEM columns [0,128), then O += P V (A = P from shared memory,
+//           B = V read MN-major: the [key][d] tile is used as is) into columns [128,256);
+//   warps 0-3: softmax — thread t owns query row t = TMEM lane t: reads its S row with
+//           tcgen05.ld, masks / scales / takes the row max and exp2 in registers (no
+//           shuffles), rescales its O row in TMEM when the max moved (tcgen05.ld/st), writes
+//           its P row (bf16, 128B swizzle) for the PV MMA; finally O / l to global.
+// Per block the MMA warp waits for P, so S(j+1) and PV(j) run back to back on the tensor
+// core while the softmax of block j+1 waits for S(j+1) (no ping-pong of two Q tiles yet).
+#include "sn_tc.cuh"
+
+namespace sn {
+namespace fa5 {
+
+using namespace sn::tc;
+
+constexpr int BM = 128, BN = 128, HD = 128;
+constexpr int kThreads = 192;
+constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
+constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
+
+struct Smem {
+  uint8_t q[TILE];
+  uint8_t k[2][TILE];
+  uint8_t v[2][TILE];
+  uint8_t p[TILE];
+};
+
+// MN-major operand (V as the B operand of P V: N = head dim contiguous, K = keys):
+// LBO = stride between 64-element N chunks (the second TMA box), SBO = stride between
+// groups of 8 K rows (8 x 128 B).
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(ATOM >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ int seq_start(const int32_t* __restrict__ cu, int num_seqs, int r) {
+  int lo = 0, hi = num_seqs;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (cu[mid] <= r) lo = mid; else hi = mid;
+  }
+  return cu[lo];
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                             const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
+                             __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
+                             float scale) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t q_full, kv_full[2], kv_empty[2], s_full, p_full, o_done;
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  Smem& sm = *reinterpret_cast<Smem*>(base);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = (rows + BM - 1) / BM;
+  const int r0 = (tiles - 1 - (int)blockIdx.x) * BM;  // heavy (late) tiles first
+  const int h = blockIdx.y, hk = h / (Hq / Hkv);
+  const int s0 = seq_start(cu, num_seqs, r0);
+  const int r_last = min(r0 + BM - 1, rows - 1);
+  const int s_last = seq_start(cu, num_seqs, r_last);
+  const int j_lo = window > 0 ? max(s0, r0 - window + 1) : s0;
+  const int j_hi = r_last;
+  const int nblk = (j_hi - j_lo) / BN + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&q_full, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    mbar_init(&s_full, 1);
+    mbar_init(&p_full, 128);
+    mbar_init(&o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;  // S: columns [0,128), O: [128,256)
+
+  if (warp == 5) {
+    if (lane == 0) {  // ---------------- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+      const uint64_t keep = policy_evict_last();  // K/V blocks are re-read by the other q heads of the group
+      mbar_expect_tx(&q_full, TILE);
+      tma_load_2d(sm.q, &qmap, h * HD, r0, &q_full, policy_evict_first());
+      tma_load_2d(sm.q + ATOM, &qmap, h * HD + 64, r0, &q_full, policy_evict_first());
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        const int jb = j_lo + j * BN;
+        mbar_expect_tx(&kv_full[st], 2 * TILE);
+        tma_load_2d(sm.k[st], &kmap, hk * HD, jb, &kv_full[st], keep);
+        tma_load_2d(sm.k[st] + ATOM, &kmap, hk * HD + 64, jb, &kv_full[st], keep);
+        tma_load_2d(sm.v[st], &vmap, hk * HD, jb, &kv_full[st], keep);
+        tma_load_2d(sm.v[st] + ATOM, &vmap, hk * HD + 64, jb, &kv_full[st], keep);
+      }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t id_s = idesc_bf16(BM, BN);
+      const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
+      const uint32_t sq = smem_u32(sm.q), sp = smem_u32(sm.p);
+      mbar_wait(&q_full, 0);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(sm.k[st]), sv = smem_u32(sm.v[st]);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma(tmem, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32), desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32),
+               id_s, k > 0 ? 1u : 0u);
+        umma_commit(&s_full);
+        mbar_wait(&p_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)
+          umma(tmem + 128, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
+               (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&o_done);
+        umma_commit(&kv_empty[st]);
+      }
+    }
+  } else {
+    // ---------------- softmax: thread t <-> query row r0 + t <-> TMEM lane t
+    const int t = threadIdx.x;
+    const int r = r0 + t;
+    const int sr = seq_start(cu, num_seqs, min(r, rows - 1));
+    const int lo = window > 0 ? max(sr, r - window + 1) : sr;
+    const float qs = scale * 1.4426950408889634f;
+    const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr, o_addr = tmem + 128 + lane_addr;
+    uint8_t* prow = sm.p + t * 128;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int jb = j_lo + j * BN;
+      mbar_wait(&s_full, j & 1);
+      tc_fence_after();
+      float s[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+      tmem_wait_ld();
+      const bool full = jb >= s_last && jb + BN - 1 <= r0 && (window == 0 || jb > r_last - window);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < BN; ++i) {
+        float x = s[i] * qs;
+        if (!full) {
+          const int jj = jb + i;
+          if (jj > r || jj < lo) x = -INFINITY;
+        }
+        s[i] = x;
+        mx = fmaxf(mx, x);
+      }
+      const float mn = fmaxf(m, mx);
+      const float base_m = mn == -INFINITY ? 0.f : mn;
+      const float alpha = exp2f(m - base_m);
+      if (j > 0) {
+        mbar_wait(&o_done, (j - 1) & 1);  // PV(j-1) done: O is stable and the P tile is free
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            float o[32];
+            tmem_ld32(o_addr + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= alpha;
+            tmem_st32(o_addr + c * 32, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float p[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            p[e] = exp2f(s[a * 64 + c * 8 + e] - base_m);
+            rs += p[e];
+          }
+          uint4 pk;
+          pk.x = pack_bf16(p[0], p[1]);
+          pk.y = pack_bf16(p[2], p[3]);
+          pk.z = pack_bf16(p[4], p[5]);
+          pk.w = pack_bf16(p[6], p[7]);
+          *reinterpret_cast<uint4*>(prow + a * ATOM + ((c ^ (t & 7)) << 4)) = pk;
+        }
+      l = l * alpha + rs;
+      m = mn;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+      tc_fence_before();
+      mbar_arrive(&p_full);
+    }
+    mbar_wait(&o_done, (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      float o[32];
+      tmem_ld32(o_addr + c * 32, o);
+      tmem_wait_ld();
+      if (r < rows) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 pk;
+          pk.x = pack_bf16(o[e] * inv, o[e + 1] * inv);
+          pk.y = pack_bf16(o[e + 2] * inv, o[e + 3] * inv);
+          pk.z = pack_bf16(o[e + 4] * inv, o[e + 5] * inv);
+          pk.w = pack_bf16(o[e + 6] * inv, o[e + 7] * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + e) = pk;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+}  // namespace fa5
+
+sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
+                                 int num_seqs, int rows, int Hq, int Hkv, int window, float scale, cudaStream_t st) {
+  using namespace fa5;
+  CUtensorMap qm, km, vm;
+  if (!map_2d(&qm, q, rows, (uint64_t)Hq * HD, (uint64_t)Hq * HD, BM) ||
+      !map_2d(&km, k, rows, (uint64_t)Hkv * HD, (uint64_t)Hkv * HD, BN) ||
+      !map_2d(&vm, v, rows, (uint64_t)Hkv * HD, (uint64_t)Hkv * HD, BN)) {
+    set_error("sn_attn_prefill: cuTensorMapEncodeTiled failed");
+    return SN_ECUDA;
+  }
+  const int smem = (int)sizeof(Smem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_prefill_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  dim3 grid((rows + BM - 1) / BM, Hq);
+  attn_prefill_umma_kernel<<<grid, kThreads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq,
+                                                         Hkv, window, scale);
+  return check_launch("sn_attn_prefill(umma)");
+}
+
+}  // namespace sn
