@@ -6,14 +6,14 @@
 //   warp 5 (one lane): TMA producer — Q once, then K and V blocks of 128 keys into a
 //           two-stage ring (128B-swizzled 2-D boxes straight from the [rows][H*D] tensors);
 //   warp 4 (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
-//           K-major) into TMEM columns [0,128), then O += P V (A = P from shared memory,
-//           B = V read MN-major: the [key][d] tile is used as is) into columns [128,256);
+//           K-major) into one of two TMEM score buffers, then O += P V (A = P from shared
+//           memory, B = V read MN-major: the [key][d] tile is used as is) into TMEM;
 //   warps 0-3: softmax — thread t owns query row t = TMEM lane t: reads its S row with
 //           tcgen05.ld, masks / scales / takes the row max and exp2 in registers (no
 //           shuffles), rescales its O row in TMEM when the max moved (tcgen05.ld/st), writes
 //           its P row (bf16, 128B swizzle) for the PV MMA; finally O / l to global.
-// Per block the MMA warp waits for P, so S(j+1) and PV(j) run back to back on the tensor
-// core while the softmax of block j+1 waits for S(j+1) (no ping-pong of two Q tiles yet).
+// The scores of block j+1 are computed while the softmax of block j runs (two TMEM score
+// buffers); PV(j) follows as soon as P(j) is in shared memory.
 #include "sn_tc.cuh"
 
 namespace sn {
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
                              float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ uint64_t q_full, kv_full[2], kv_empty[2], s_full, p_full, o_done;
+  __shared__ uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full, o_done;
   __shared__ uint32_t tmem_base_s;
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   Smem& sm = *reinterpret_cast<Smem*>(base);
@@ -107,20 +107,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    mbar_init(&s_full, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     mbar_init(&p_full, 128);
     mbar_init(&o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_base_s;  // S: columns [0,128), O: [128,256)
+  const uint32_t tmem = tmem_base_s;  // S double buffer: columns [0,128) and [128,256); O: [256,384)
 
   if (warp == 5) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -148,21 +148,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
       const uint32_t sq = smem_u32(sm.q), sp = smem_u32(sm.p);
       mbar_wait(&q_full, 0);
-      for (int j = 0; j < nblk; ++j) {
+      // S(j+1) is issued before PV(j) waits for P(j): the tensor core computes the next scores
+      // while the softmax warps work on the current block (S double-buffered in TMEM).
+      auto issue_s = [&](int j) {
         const int st = j & 1;
         mbar_wait(&kv_full[st], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t sk = smem_u32(sm.k[st]), sv = smem_u32(sm.v[st]);
+        const uint32_t sk = smem_u32(sm.k[st]);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma(tmem, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32), desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32),
-               id_s, k > 0 ? 1u : 0u);
-        umma_commit(&s_full);
+          umma(tmem + st * 128, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
+               desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32), id_s, k > 0 ? 1u : 0u);
+        umma_commit(&s_full[st]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        if (j + 1 < nblk) issue_s(j + 1);  // its S buffer was read by softmax(j-1) (P(j-1) waited below)
         mbar_wait(&p_full, j & 1);
         tc_fence_after();
+        const uint32_t sv = smem_u32(sm.v[st]);
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
-          umma(tmem + 128, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
+          umma(tmem + 256, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
                (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(&o_done);
         umma_commit(&kv_empty[st]);
@@ -176,16 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lo = window > 0 ? max(sr, r - window + 1) : sr;
     const float qs = scale * 1.4426950408889634f;
     const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr, o_addr = tmem + 128 + lane_addr;
+    const uint32_t s_addr = tmem + lane_addr, o_addr = tmem + 256 + lane_addr;
     uint8_t* prow = sm.p + t * 128;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int jb = j_lo + j * BN;
-      mbar_wait(&s_full, j & 1);
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       float s[BN];
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + (j & 1) * 128 + c * 32, s + c * 32);
       tmem_wait_ld();
       const bool full = jb >= s_last && jb + BN - 1 <= r0 && (window == 0 || jb > r_last - window);
       float mx = -INFINITY;
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 }  // namespace fa5
