@@ -2,16 +2,17 @@
 // Same contract as the mma.sync kernel in sn_attn_prefill.cu (packed ragged sequences,
 // causal or window mask per (row, key) with each row's own sequence start, GQA).
 //
-// CTA = 128 query rows x one q head; 6 warps:
-//   warp 5 (one lane): TMA producer — Q once, then K and V blocks of 128 keys into a
+// CTA = 128 query rows x one q head; 10 warps:
+//   warp 9 (one lane): TMA producer — Q once, then K and V blocks of 128 keys into a
 //           two-stage ring (128B-swizzled 2-D boxes straight from the [rows][H*D] tensors);
-//   warp 4 (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
+//   warp 8 (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
 //           K-major) into one of two TMEM score buffers, then O += P V (A = P from shared
 //           memory, B = V read MN-major: the [key][d] tile is used as is) into TMEM;
-//   warps 0-3: softmax — thread t owns query row t = TMEM lane t: reads its S row with
-//           tcgen05.ld, masks / scales / takes the row max and exp2 in registers (no
-//           shuffles), rescales its O row in TMEM when the max moved (tcgen05.ld/st), writes
-//           its P row (bf16, 128B swizzle) for the PV MMA; finally O / l to global.
+//   warps 0-7: softmax — warps w and w+4 share query rows 32(w%4).. (TMEM lanes), one half
+//           of the 128 key columns each: tcgen05.ld of the S half-row, mask / scale / max /
+//           exp2 in registers, the row max combined through shared memory (64-thread named
+//           barrier), O half-row rescaled in TMEM when the max moved (tcgen05.ld/st), the
+//           P half-row written (bf16, 128B swizzle) for the PV MMA; finally O / l to global.
 // The scores of block j+1 are computed while the softmax of block j runs (two TMEM score
 // buffers); PV(j) follows as soon as P(j) is in shared memory.
 #include "sn_tc.cuh"
@@ -22,7 +23,7 @@ namespace fa5 {
 using namespace sn::tc;
 
 constexpr int BM = 128, BN = 128, HD = 128;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 8 softmax warps, MMA warp, TMA warp
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
 constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
 
@@ -71,6 +72,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ float ex2(float x) {  // 2^x, -inf -> 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -91,6 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full, o_done;
   __shared__ uint32_t tmem_base_s;
+  __shared__ float red_max[2][2][BM];  // [iteration parity][column half][row]
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   Smem& sm = *reinterpret_cast<Smem*>(base);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&q_full, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    mbar_init(&p_full, 128);
+    mbar_init(&p_full, 256);
     mbar_init(&o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;  // S double buffer: columns [0,128) and [128,256); O: [256,384)
 
-  if (warp == 5) {
+  if (warp == 9) {
     if (lane == 0) {  // ---------------- TMA producer
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sm.v[st] + ATOM, &vmap, hk * HD + 64, jb, &kv_full[st], keep);
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 8) {
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t id_s = idesc_bf16(BM, BN);
       const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
@@ -177,45 +184,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- softmax: thread t <-> query row r0 + t <-> TMEM lane t
-    const int t = threadIdx.x;
+    // ---------------- softmax: warps w and w+4 share TMEM lanes 32(w%4).. (query rows), each
+    // taking one half of the 128 key columns (and of the head dim for O); the row max is
+    // combined through shared memory with a 64-thread named barrier per warp pair.
+    const int sub = warp & 3, half = warp >> 2;
+    const int t = sub * 32 + lane;
     const int r = r0 + t;
     const int sr = seq_start(cu, num_seqs, min(r, rows - 1));
     const int lo = window > 0 ? max(sr, r - window + 1) : sr;
     const float qs = scale * 1.4426950408889634f;
-    const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr, o_addr = tmem + 256 + lane_addr;
-    uint8_t* prow = sm.p + t * 128;
+    const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + half * 64, o_addr = tmem + 256 + lane_addr + half * 64;
+    uint8_t* prow = sm.p + half * ATOM + t * 128;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int jb = j_lo + j * BN;
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      float s[BN];
-#pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_addr + (j & 1) * 128 + c * 32, s + c * 32);
+      float s[64];
+      tmem_ld32(s_addr + (j & 1) * 128, s);
+      tmem_ld32(s_addr + (j & 1) * 128 + 32, s + 32);
       tmem_wait_ld();
       const bool full = jb >= s_last && jb + BN - 1 <= r0 && (window == 0 || jb > r_last - window);
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < BN; ++i) {
+      for (int i = 0; i < 64; ++i) {
         float x = s[i] * qs;
         if (!full) {
-          const int jj = jb + i;
+          const int jj = jb + half * 64 + i;
           if (jj > r || jj < lo) x = -INFINITY;
         }
         s[i] = x;
         mx = fmaxf(mx, x);
       }
+      red_max[j & 1][half][t] = mx;
+      named_bar(1 + sub, 64);
+      mx = fmaxf(mx, red_max[j & 1][half ^ 1][t]);
       const float mn = fmaxf(m, mx);
       const float base_m = mn == -INFINITY ? 0.f : mn;
-      const float alpha = exp2f(m - base_m);
+      const float alpha = ex2(m - base_m);
       if (j > 0) {
         mbar_wait(&o_done, (j - 1) & 1);  // PV(j-1) done: O is stable and the P tile is free
         tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < HD / 32; ++c) {
+          for (int c = 0; c < 2; ++c) {
             float o[32];
             tmem_ld32(o_addr + c * 32, o);
             tmem_wait_ld();
@@ -228,34 +241,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float rs = 0.f;
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int c = 0; c < 8; ++c) {
+        float p[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = exp2f(s[a * 64 + c * 8 + e] - base_m);
-            rs += p[e];
-          }
-          uint4 pk;
-          pk.x = pack_bf16(p[0], p[1]);
-          pk.y = pack_bf16(p[2], p[3]);
-          pk.z = pack_bf16(p[4], p[5]);
-          pk.w = pack_bf16(p[6], p[7]);
-          *reinterpret_cast<uint4*>(prow + a * ATOM + ((c ^ (t & 7)) << 4)) = pk;
+        for (int e = 0; e < 8; ++e) {
+          p[e] = ex2(s[c * 8 + e] - base_m);
+          rs += p[e];
         }
+        uint4 pk;
+        pk.x = pack_bf16(p[0], p[1]);
+        pk.y = pack_bf16(p[2], p[3]);
+        pk.z = pack_bf16(p[4], p[5]);
+        pk.w = pack_bf16(p[6], p[7]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ (t & 7)) << 4)) = pk;
+      }
       l = l * alpha + rs;
       m = mn;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       tc_fence_before();
       mbar_arrive(&p_full);
     }
+    red_max[0][half][t] = l;  // row sum: the two halves' partial sums
+    named_bar(1 + sub, 64);
+    l += red_max[0][half ^ 1][t];
     mbar_wait(&o_done, (nblk - 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD;
+    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD + half * 64;
 #pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
       float o[32];
       tmem_ld32(o_addr + c * 32, o);
       tmem_wait_ld();
