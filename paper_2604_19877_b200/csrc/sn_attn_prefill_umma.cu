@@ -27,12 +27,21 @@ constexpr int kThreads = 320;  // 8 softmax warps, MMA warp, TMA warp
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
 constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
 
-struct Smem {
+struct Smem {         // 224 KB, 1024-byte aligned
   uint8_t q[TILE];
   uint8_t k[2][TILE];
   uint8_t v[2][TILE];
-  uint8_t p[TILE];
+  uint8_t p[2][TILE];  // double-buffered: softmax(j+1) writes while PV(j) reads
 };
+struct Sync {          // in front of the tiles, inside the dynamic allocation
+  uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full, o_done[2];
+  uint32_t tmem_base;
+  float red[2][2][BM];  // [iteration parity][column half][row]
+};
+constexpr int kSyncBytes = 3072;
+constexpr int kSmemBytes = 227 * 1024;
+static_assert(sizeof(Sync) <= kSyncBytes, "sync block");
+static_assert(sizeof(Smem) + kSyncBytes <= kSmemBytes, "tiles");
 
 // MN-major operand (V as the B operand of P V: N = head dim contiguous, K = keys):
 // LBO = stride between 64-element N chunks (the second TMA box), SBO = stride between
@@ -95,11 +104,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
                              float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full, o_done;
-  __shared__ uint32_t tmem_base_s;
-  __shared__ float red_max[2][2][BM];  // [iteration parity][column half][row]
-  uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  Sync& sy = *reinterpret_cast<Sync*>(smem_raw);
+  uint8_t* base = smem_raw + kSyncBytes;
+  base += (1024 - (smem_u32(base) & 1023)) & 1023;
+  if (base + sizeof(Smem) > smem_raw + kSmemBytes) __trap();  // dynamic smem base not 1 KB aligned
   Smem& sm = *reinterpret_cast<Smem*>(base);
+  uint64_t &q_full = sy.q_full, *kv_full = sy.kv_full, *kv_empty = sy.kv_empty, *s_full = sy.s_full;
+  uint64_t &p_full = sy.p_full, *o_done = sy.o_done;
+  uint32_t& tmem_base_s = sy.tmem_base;
+  auto& red_max = sy.red;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = (rows + BM - 1) / BM;
   const int r0 = (tiles - 1 - (int)blockIdx.x) * BM;  // heavy (late) tiles first
@@ -116,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     mbar_init(&p_full, 256);
-    mbar_init(&o_done, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&o_done[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -153,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t id_s = idesc_bf16(BM, BN);
       const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
-      const uint32_t sq = smem_u32(sm.q), sp = smem_u32(sm.p);
+      const uint32_t sq = smem_u32(sm.q);
       mbar_wait(&q_full, 0);
       // S(j+1) is issued before PV(j) waits for P(j): the tensor core computes the next scores
       // while the softmax warps work on the current block (S double-buffered in TMEM).
@@ -174,12 +187,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j + 1 < nblk) issue_s(j + 1);  // its S buffer was read by softmax(j-1) (P(j-1) waited below)
         mbar_wait(&p_full, j & 1);
         tc_fence_after();
-        const uint32_t sv = smem_u32(sm.v[st]);
+        const uint32_t sv = smem_u32(sm.v[st]), sp = smem_u32(sm.p[st]);
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
           umma(tmem + 256, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
                (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&o_done);
+        umma_commit(&o_done[st]);
         umma_commit(&kv_empty[st]);
       }
     }
@@ -195,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float qs = scale * 1.4426950408889634f;
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
     const uint32_t s_addr = tmem + lane_addr + half * 64, o_addr = tmem + 256 + lane_addr + half * 64;
-    uint8_t* prow = sm.p + half * ATOM + t * 128;
+    uint8_t* prow0 = sm.p[0] + half * ATOM + t * 128;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int jb = j_lo + j * BN;
@@ -223,10 +236,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float mn = fmaxf(m, mx);
       const float base_m = mn == -INFINITY ? 0.f : mn;
       const float alpha = ex2(m - base_m);
-      if (j > 0) {
-        mbar_wait(&o_done, (j - 1) & 1);  // PV(j-1) done: O is stable and the P tile is free
+      // P(j) goes to buffer j&1, last read by PV(j-2) — complete, since S(j) was committed after
+      // it.  O is only touched when a row max moved: then PV(j-1) must have finished (o_done of
+      // its parity; PV(j-3) on the same barrier completed before S(j-1), so the parity wait is
+      // exact).
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        {
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {
             float o[32];
@@ -253,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk.y = pack_bf16(p[2], p[3]);
         pk.z = pack_bf16(p[4], p[5]);
         pk.w = pack_bf16(p[6], p[7]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ (t & 7)) << 4)) = pk;
+        *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + ((c ^ (t & 7)) << 4)) = pk;
       }
       l = l * alpha + rs;
       m = mn;
@@ -264,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     red_max[0][half][t] = l;  // row sum: the two halves' partial sums
     named_bar(1 + sub, 64);
     l += red_max[0][half ^ 1][t];
-    mbar_wait(&o_done, (nblk - 1) & 1);
+    mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD + half * 64;
@@ -303,7 +320,7 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     set_error("sn_attn_prefill: cuTensorMapEncodeTiled failed");
     return SN_ECUDA;
   }
-  const int smem = (int)sizeof(Smem) + 1024;
+  const int smem = kSmemBytes;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_prefill_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
