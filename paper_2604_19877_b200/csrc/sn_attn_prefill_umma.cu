@@ -2,9 +2,10 @@
 // Same contract as the mma.sync kernel in sn_attn_prefill.cu (packed ragged sequences,
 // causal or window mask per (row, key) with each row's own sequence start, GQA).
 //
-// CTA = 128 query rows x one q head; 10 warps:
-//   warp 9 (one lane): TMA producer — Q once, then K and V blocks of 128 keys into a
-//           two-stage ring (128B-swizzled 2-D boxes straight from the [rows][H*D] tensors);
+// CTA = 128 query rows x one q head; 11 warps:
+//   warps 9 / 10 (one lane each): TMA producers — Q once and K blocks of 128 keys / V blocks,
+//           each into its own two-stage ring (128B-swizzled 2-D boxes straight from the
+//           [rows][H*D] tensors), so the next K block only waits for its S product;
 //   warp 8 (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
 //           K-major) into one of two TMEM score buffers, then O += P V (A = P from shared
 //           memory, B = V read MN-major: the [key][d] tile is used as is) into TMEM;
@@ -23,7 +24,7 @@ namespace fa5 {
 using namespace sn::tc;
 
 constexpr int BM = 128, BN = 128, HD = 128;
-constexpr int kThreads = 320;  // 8 softmax warps, MMA warp, TMA warp
+constexpr int kThreads = 352;  // 8 softmax warps, MMA warp, K/Q TMA warp, V TMA warp
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
 constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
 
@@ -34,7 +35,7 @@ struct Smem {         // 224 KB, 1024-byte aligned
   uint8_t p[2][TILE];  // double-buffered: softmax(j+1) writes while PV(j) reads
 };
 struct Sync {          // in front of the tiles, inside the dynamic allocation
-  uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full, o_done[2];
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full, o_done[2];
   uint32_t tmem_base;
   float red[2][2][BM];  // [iteration parity][column half][row]
 };
@@ -102,14 +103,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
-                             float scale) {
+                             float scale, unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Sync& sy = *reinterpret_cast<Sync*>(smem_raw);
   uint8_t* base = smem_raw + kSyncBytes;
   base += (1024 - (smem_u32(base) & 1023)) & 1023;
   if (base + sizeof(Smem) > smem_raw + kSmemBytes) __trap();  // dynamic smem base not 1 KB aligned
   Smem& sm = *reinterpret_cast<Smem*>(base);
-  uint64_t &q_full = sy.q_full, *kv_full = sy.kv_full, *kv_empty = sy.kv_empty, *s_full = sy.s_full;
+  uint64_t &q_full = sy.q_full, *k_full = sy.k_full, *k_empty = sy.k_empty, *v_full = sy.v_full;
+  uint64_t *v_empty = sy.v_empty, *s_full = sy.s_full;
   uint64_t &p_full = sy.p_full, *o_done = sy.o_done;
   uint32_t& tmem_base_s = sy.tmem_base;
   auto& red_max = sy.red;
@@ -126,7 +128,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     mbar_init(&p_full, 256);
     for (int i = 0; i < 2; ++i) mbar_init(&o_done[i], 1);
@@ -142,24 +147,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;  // S double buffer: columns [0,128) and [128,256); O: [256,384)
 
-  if (warp == 9) {
-    if (lane == 0) {  // ---------------- TMA producer
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+  if (warp >= 9) {
+    // ---------------- TMA producers: warp 9 loads Q and the K ring, warp 10 the V ring.  K and
+    // V have their own stages: K(j+2) only waits for S(j), V(j+2) for PV(j).
+    if (lane == 0) {
+      const bool is_k = warp == 9;
+      const CUtensorMap* map = is_k ? &kmap : &vmap;
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
       const uint64_t keep = policy_evict_last();  // K/V blocks are re-read by the other q heads of the group
-      mbar_expect_tx(&q_full, TILE);
-      tma_load_2d(sm.q, &qmap, h * HD, r0, &q_full, policy_evict_first());
-      tma_load_2d(sm.q + ATOM, &qmap, h * HD + 64, r0, &q_full, policy_evict_first());
+      if (is_k) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+        mbar_expect_tx(&q_full, TILE);
+        tma_load_2d(sm.q, &qmap, h * HD, r0, &q_full, policy_evict_first());
+        tma_load_2d(sm.q + ATOM, &qmap, h * HD + 64, r0, &q_full, policy_evict_first());
+      }
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
       for (int j = 0; j < nblk; ++j) {
         const int st = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        if (j >= 2) mbar_wait(&empty[st], ((j >> 1) - 1) & 1);
         const int jb = j_lo + j * BN;
-        mbar_expect_tx(&kv_full[st], 2 * TILE);
-        tma_load_2d(sm.k[st], &kmap, hk * HD, jb, &kv_full[st], keep);
-        tma_load_2d(sm.k[st] + ATOM, &kmap, hk * HD + 64, jb, &kv_full[st], keep);
-        tma_load_2d(sm.v[st], &vmap, hk * HD, jb, &kv_full[st], keep);
-        tma_load_2d(sm.v[st] + ATOM, &vmap, hk * HD + 64, jb, &kv_full[st], keep);
+        uint8_t* dst = is_k ? sm.k[st] : sm.v[st];
+        mbar_expect_tx(&full[st], TILE);
+        tma_load_2d(dst, map, hk * HD, jb, &full[st], keep);
+        tma_load_2d(dst + ATOM, map, hk * HD + 64, jb, &full[st], keep);
       }
     }
   } else if (warp == 8) {
@@ -170,9 +181,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&q_full, 0);
       // S(j+1) is issued before PV(j) waits for P(j): the tensor core computes the next scores
       // while the softmax warps work on the current block (S double-buffered in TMEM).
+      const bool rec = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+      auto stamp = [&](int j, int what) {
+        if (rec && j < 64) dbg[j * 4 + what] = clock64();
+      };
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        stamp(j, 0);
         tc_fence_after();
         const uint32_t sk = smem_u32(sm.k[st]);
 #pragma unroll
@@ -180,12 +196,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma(tmem + st * 128, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
                desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32), id_s, k > 0 ? 1u : 0u);
         umma_commit(&s_full[st]);
+        umma_commit(&k_empty[st]);
       };
       issue_s(0);
       for (int j = 0; j < nblk; ++j) {
         const int st = j & 1;
         if (j + 1 < nblk) issue_s(j + 1);  // its S buffer was read by softmax(j-1) (P(j-1) waited below)
+        stamp(j, 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
         mbar_wait(&p_full, j & 1);
+        stamp(j, 2);
         tc_fence_after();
         const uint32_t sv = smem_u32(sm.v[st]), sp = smem_u32(sm.p[st]);
 #pragma unroll
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma(tmem + 256, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
                (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(&o_done[st]);
-        umma_commit(&kv_empty[st]);
+        umma_commit(&v_empty[st]);
       }
     }
   } else {
@@ -310,6 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace fa5
 
+static unsigned long long* g_fa5_dbg = nullptr;
+extern "C" void sn_experimental_fa5_timeline(unsigned long long* p) { g_fa5_dbg = p; }
+
 sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                  int num_seqs, int rows, int Hq, int Hkv, int window, float scale, cudaStream_t st) {
   using namespace fa5;
@@ -328,7 +351,7 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
   attn_prefill_umma_kernel<<<grid, kThreads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq,
-                                                         Hkv, window, scale);
+                                                         Hkv, window, scale, g_fa5_dbg);
   return check_launch("sn_attn_prefill(umma)");
 }
 
