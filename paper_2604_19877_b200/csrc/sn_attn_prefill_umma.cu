@@ -23,6 +23,9 @@ namespace fa5 {
 
 using namespace sn::tc;
 
+#ifndef SN_FA_POLY_MASK
+#define SN_FA_POLY_MASK 3  // elements e with (e & mask) == mask use exp2_fma: 3 -> 1/4, 1 -> 1/2
+#endif
 constexpr int BM = 128, BN = 128, HD = 128;
 constexpr int kThreads = 352;  // 8 softmax warps, MMA warp, K/Q TMA warp, V TMA warp
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
@@ -86,6 +89,18 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, -inf -> 0
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split x = n + f, f in [-0.5, 0.5],
+// cubic in f, n added to the exponent.  Relative error < 7e-4 (P is stored as bf16,
+// 3.9e-3).  Part of the exponentials go this way so MUFU.EX2 (16 / clock / SM) is not the
+// limiter of the softmax (FA4's split).
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;                 // 1.5 * 2^23: rounds x to an integer
+  const float f = x - (t - 12582912.f);
+  const int n = __float_as_int(t) - 0x4B400000;
+  float p = fmaf(fmaf(fmaf(0.05550411f, f, 0.24022651f), f, 0.69314718f), f, 1.f);
+  return __int_as_float(__float_as_int(p) + (n << 23));
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -240,19 +255,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       const bool full = jb >= s_last && jb + BN - 1 <= r0 && (window == 0 || jb > r_last - window);
       float mx = -INFINITY;
+      if (!full) {
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        float x = s[i] * qs;
-        if (!full) {
+        for (int i = 0; i < 64; ++i) {
           const int jj = jb + half * 64 + i;
-          if (jj > r || jj < lo) x = -INFINITY;
+          if (jj > r || jj < lo) s[i] = -INFINITY;
         }
-        s[i] = x;
-        mx = fmaxf(mx, x);
       }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) mx = fmaxf(mx, s[i]);
       red_max[j & 1][half][t] = mx;
       named_bar(1 + sub, 64);
-      mx = fmaxf(mx, red_max[j & 1][half ^ 1][t]);
+      mx = fmaxf(mx, red_max[j & 1][half ^ 1][t]) * qs;  // scores stay unscaled; the max is scaled
       const float mn = fmaxf(m, mx);
       const float base_m = mn == -INFINITY ? 0.f : mn;
       const float alpha = ex2(m - base_m);
@@ -282,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float p[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          p[e] = ex2(s[c * 8 + e] - base_m);
+          const float x = fmaf(s[c * 8 + e], qs, -base_m);
+          p[e] = (e & SN_FA_POLY_MASK) == SN_FA_POLY_MASK ? exp2_fma(x) : ex2(x);  // part on the FMA pipe
           rs += p[e];
         }
         uint4 pk;

@@ -1,3 +1,5 @@
+"""Per-block timeline of the tcgen05 attention prefill (MMA-issuer clock64 stamps of CTA 0:
+S issued, next S issued, P ready) via sn_experimental_fa5_timeline."""
 import ctypes, math, sys, torch
 sys.path.insert(0, '.')
 from paper_2604_19877_b200 import ops, _lib
