@@ -23,9 +23,6 @@ namespace fa5 {
 
 using namespace sn::tc;
 
-#ifndef SN_FA_POLY_MASK
-#define SN_FA_POLY_MASK 3  // elements e with (e & mask) == mask use exp2_fma: 3 -> 1/4, 1 -> 1/2
-#endif
 constexpr int BM = 128, BN = 128, HD = 128;
 constexpr int kThreads = 352;  // 8 softmax warps, MMA warp, K/Q TMA warp, V TMA warp
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
@@ -92,15 +89,37 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, -inf -> 0
 }
 // 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split x = n + f, f in [-0.5, 0.5],
 // cubic in f, n added to the exponent.  Relative error < 7e-4 (P is stored as bf16,
-// 3.9e-3).  Part of the exponentials go this way so MUFU.EX2 (16 / clock / SM) is not the
+// 3.9e-3).  Part of the exponentials go this way (exp2_fma2, on pairs) so MUFU.EX2 (16 / clock / SM) is not the
 // limiter of the softmax (FA4's split).
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;                 // 1.5 * 2^23: rounds x to an integer
-  const float f = x - (t - 12582912.f);
-  const int n = __float_as_int(t) - 0x4B400000;
-  float p = fmaf(fmaf(fmaf(0.05550411f, f, 0.24022651f), f, 0.69314718f), f, 1.f);
-  return __int_as_float(__float_as_int(p) + (n << 23));
+// Paired fp32 arithmetic (FFMA2 / FADD2 on sm_100a): two lanes of work per instruction.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+// exp2_fma on a pair
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f), nmagic = make_float2(-12582912.f, -12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 r = fadd2(t, nmagic);
+  const float2 f = fadd2(x, make_float2(-r.x, -r.y));
+  float2 p = ffma2(make_float2(0.05550411f, 0.05550411f), f, make_float2(0.24022651f, 0.24022651f));
+  p = ffma2(p, f, make_float2(0.69314718f, 0.69314718f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  const int nx = __float_as_int(t.x) - 0x4B400000, ny = __float_as_int(t.y) - 0x4B400000;
+  return make_float2(__int_as_float(__float_as_int(p.x) + (nx << 23)), __int_as_float(__float_as_int(p.y) + (ny << 23)));
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -290,23 +309,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
-      float rs = 0.f;
+      float2 rs2 = make_float2(0.f, 0.f);
+      const float2 qs2 = make_float2(qs, qs), nb2 = make_float2(-base_m, -base_m);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        float p[8];
+        float2 p[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float x = fmaf(s[c * 8 + e], qs, -base_m);
-          p[e] = (e & SN_FA_POLY_MASK) == SN_FA_POLY_MASK ? exp2_fma(x) : ex2(x);  // part on the FMA pipe
-          rs += p[e];
+        for (int e = 0; e < 4; ++e) {
+          const float2 x = ffma2(make_float2(s[c * 8 + 2 * e], s[c * 8 + 2 * e + 1]), qs2, nb2);
+          // the last pair of every 8 on the FMA pipe (a quarter), the rest on MUFU.EX2
+          p[e] = e == 3 ? exp2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
+          rs2 = fadd2(rs2, p[e]);
         }
         uint4 pk;
-        pk.x = pack_bf16(p[0], p[1]);
-        pk.y = pack_bf16(p[2], p[3]);
-        pk.z = pack_bf16(p[4], p[5]);
-        pk.w = pack_bf16(p[6], p[7]);
+        pk.x = pack_bf16(p[0].x, p[0].y);
+        pk.y = pack_bf16(p[1].x, p[1].y);
+        pk.z = pack_bf16(p[2].x, p[2].y);
+        pk.w = pack_bf16(p[3].x, p[3].y);
         *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + ((c ^ (t & 7)) << 4)) = pk;
       }
+      const float rs = rs2.x + rs2.y;
       l = l * alpha + rs;
       m = mn;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
