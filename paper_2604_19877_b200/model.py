@@ -399,26 +399,42 @@ class Supernet:
     # ------------------------------------------------------------------ prefill
     @torch.no_grad()
     def prefill(self, tokens, return_all: bool = False):
-        """Parallel prefill of B prompts of equal length T from an empty state.
-        tokens [B, T] -> logits [B, T, V] (return_all) or [B, V] for the last position."""
+        """Parallel prefill from an empty state.  tokens: [B, T] (equal-length prompts) or a list
+        of B 1-D prompts of any lengths (ragged: packed rows, cu_seqlens, every kernel masks or
+        chunks per sequence).  Returns the last position's logits [B, V], or with return_all
+        [B, T, V] (equal lengths) / a list of [T_b, V] (ragged)."""
         cfg, w, dev, dt = self.cfg, self.w, self.device, self.dtype
-        tokens = torch.as_tensor(tokens).to(device=dev, dtype=torch.int32)
-        B, T = tokens.shape
+        ragged = isinstance(tokens, (list, tuple))
+        if ragged:
+            seqs = [torch.as_tensor(t).reshape(-1).to(device=dev, dtype=torch.int32) for t in tokens]
+            lens = [int(t.numel()) for t in seqs]
+            flat = torch.cat(seqs)
+        else:
+            t2 = torch.as_tensor(tokens).to(device=dev, dtype=torch.int32)
+            lens = [t2.shape[1]] * t2.shape[0]
+            flat = t2.reshape(-1)
+        B = len(lens)
         if B != self.B:
             raise ValueError(f"prefill batch {B} != engine batch {self.B}")
-        if T > self.max_len:
-            raise ValueError(f"prompt length {T} > max_len {self.max_len}")
-        rows = B * T
+        if min(lens) < 1 or max(lens) > self.max_len:
+            raise ValueError(f"prompt lengths must be in [1, max_len={self.max_len}], got {min(lens)}..{max(lens)}")
+        rows = sum(lens)
         i32 = dict(device=dev, dtype=torch.int32)
-        cu = torch.arange(0, rows + 1, T, **i32)
-        row_seq = torch.arange(B, **i32).repeat_interleave(T)
-        row_pos = torch.arange(T, **i32).repeat(B)
+        cu_host = [0]
+        for L in lens:
+            cu_host.append(cu_host[-1] + L)
+        self._cu_host = cu_host
+        cu = torch.tensor(cu_host, **i32)
+        lens_t = torch.tensor(lens, **i32)
+        row_seq = torch.repeat_interleave(torch.arange(B, **i32), lens_t)
+        row_pos = torch.arange(rows, **i32) - torch.repeat_interleave(cu[:-1], lens_t)
+        T = max(lens)
         self.reset()
-        self.seq_lens.fill_(T)
+        self.seq_lens.copy_(lens_t)
         e = lambda *s, d=dt: torch.empty(*s, device=dev, dtype=d)
         resid = e(rows, cfg.hidden, d=torch.float32)
         h, mix, ffn_o = e(rows, cfg.hidden), e(rows, cfg.hidden), e(rows, cfg.hidden)
-        ops.embed(tokens.reshape(-1), w["embed"], resid)
+        ops.embed(flat, w["embed"], resid)
         delta = None
         for l, kind in enumerate(self.kinds):
             lw = w["layers"][l]
@@ -441,8 +457,11 @@ class Supernet:
             delta = ffn_o
         ops.add_rmsnorm(delta, resid, w["final_norm"], h, cfg.norm_eps)
         if return_all:
-            return (h @ w["lm_head"].t()).view(B, T, cfg.vocab)
-        last = h.view(B, T, cfg.hidden)[:, -1]
+            logits = h @ w["lm_head"].t()
+            if ragged:
+                return [logits[a:b] for a, b in zip(cu_host[:-1], cu_host[1:])]
+            return logits.view(B, T, cfg.vocab)
+        last = h[cu[1:].long() - 1]
         return last @ w["lm_head"].t()
 
     def _tp_sum(self, t):
@@ -516,33 +535,37 @@ class Supernet:
         torch.mm(y_out, w["o"].t(), out=out)
 
     def _chunked_delta(self, kind, qn, kn, y, v_off, glog, beta, o, S, cu, Hk, Hv, D, ws_cap=2 << 30):
-        """Two-phase chunked prefill over groups of sequences whose chunk workspace fits ws_cap bytes
-        (B equal-length prompts: one chunk plan serves every group)."""
-        B, rows = S.shape[0], qn.shape[0]
-        T = rows // B
+        """Two-phase chunked prefill over groups of consecutive sequences whose chunk workspace
+        fits ws_cap bytes (ragged lengths: the chunk plan follows cu_seqlens)."""
+        B = S.shape[0]
+        cu_host = getattr(self, "_cu_host", None)
+        if cu_host is None or len(cu_host) != B + 1:
+            cu_host = [int(x) for x in cu.tolist()]
         lib = ops._lib.load()
         ws_fn = lib.sn_kda_chunk_workspace_bytes if kind == KDA else lib.sn_gdn_chunk_workspace_bytes
-        per_seq = ws_fn(-(-T // 64), Hv, D)
-        grp = max(1, min(B, ws_cap // max(per_seq, 1)))
-        key = (T, grp)
-        if getattr(self, "_chunk_key", None) != key:
-            self._chunk_key = key
-            self._chunk_plan = ops.chunk_plan(list(range(0, grp * T + 1, T)), device=qn.device)
-            self._chunk_ws = None
-        for b0 in range(0, B, grp):
-            b1 = min(B, b0 + grp)
-            r0, r1 = b0 * T, b1 * T
+        chunks_of = [-(-(b1 - b0) // 64) for b0, b1 in zip(cu_host[:-1], cu_host[1:])]
+        b0 = 0
+        while b0 < B:
+            b1, n = b0, 0
+            while b1 < B and (b1 == b0 or ws_fn(n + chunks_of[b1], Hv, D) <= ws_cap):
+                n += chunks_of[b1]
+                b1 += 1
+            r0, r1 = cu_host[b0], cu_host[b1]
+            key = (tuple(cu_host[b0:b1 + 1]),)
+            if getattr(self, "_chunk_key", None) != key:
+                self._chunk_key = key
+                self._chunk_plan = ops.chunk_plan([c - r0 for c in cu_host[b0:b1 + 1]], device=qn.device)
             chunks, c0 = self._chunk_plan
-            if b1 - b0 != grp:
-                chunks, c0 = ops.chunk_plan(list(range(0, (b1 - b0) * T + 1, T)), device=qn.device)
+            ws = getattr(self, "_chunk_ws", None)
             if kind == KDA:
                 self._chunk_ws = ops.kda_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
                                                         beta[r0:r1], chunks, c0, o[r0:r1], S[b0:b1], None, Hv, D,
-                                                        init_state=False, workspace=self._chunk_ws)
+                                                        init_state=False, workspace=ws)
             else:
                 self._chunk_ws = ops.gdn_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
                                                         beta[r0:r1], chunks, c0, o[r0:r1], S[b0:b1], None, Hk, Hv,
-                                                        D, init_state=False, workspace=self._chunk_ws)
+                                                        D, init_state=False, workspace=ws)
+            b0 = b1
 
     def _gdn_prefill(self, l, h, out, cu):
         self._delta_prefill(GDN, l, h, out, cu)

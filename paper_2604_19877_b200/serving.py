@@ -13,8 +13,8 @@ R/PAPER.md:1872-1896).  Here:
   shared by every engine.
 * `PlacementRouter` holds one engine (state pools + decode CUDA graph) per
   (placement, batch) and routes requests by placement: same-placement requests are batched
-  together (same prompt length per batch), each batch is prefilled and decoded greedily
-  through its placement's graph.
+  together (ragged prompt lengths in one packed prefill), then decoded greedily through
+  their placement's graph.
 """
 from __future__ import annotations
 
@@ -122,18 +122,20 @@ class PlacementRouter:
 
     def generate(self, requests, max_new_tokens: int):
         """requests: list of (placement, prompt tokens [T]).  Greedy decoding; returns a list of
-        int32 CPU tensors [max_new_tokens] in request order.  Requests are grouped by
-        (placement, prompt length) and each group runs as one batch through its graph."""
+        int32 CPU tensors [max_new_tokens] in request order.  Requests are grouped by placement
+        (same-placement batching, R/PAPER.md:860-865); each group is one ragged prefill (prompts
+        of any lengths) and then decodes through its placement's graph."""
         groups: OrderedDict = OrderedDict()
         for i, (placement, prompt) in enumerate(requests):
             prompt = torch.as_tensor(prompt, dtype=torch.int32).reshape(-1)
-            groups.setdefault((placement_code(placement), prompt.numel()), []).append((i, prompt))
+            groups.setdefault(placement_code(placement), []).append((i, prompt))
         out = [None] * len(requests)
-        for (code, T), items in groups.items():
+        for code, items in groups.items():
+            T = max(p.numel() for _, p in items)
             if T + max_new_tokens > self.max_len:
                 raise ValueError(f"prompt {T} + {max_new_tokens} new tokens > max_len {self.max_len}")
             model, graph = self.engine(code, len(items))
-            logits = model.prefill(torch.stack([p for _, p in items]))
+            logits = model.prefill([p for _, p in items])
             first = torch.argmax(logits.float(), dim=-1).to(torch.int32)
             model.step_tokens.copy_(first)
             toks = [first]
