@@ -236,6 +236,47 @@ def measure_preset(cfg, preset, B, ctx, steps, warmup, ws, rank, local, probe_st
     return res
 
 
+# ------------------------------------------------------------------ prefill (side measurement)
+def measure_prefill(cfg, preset, tokens, reps=2):
+    """One prompt of `tokens` tokens through the chunked / tensor-core prefill (B=1): tokens/s
+    with CUDA events, plus the attention-prefill kernel alone (TFLOP/s of the masked
+    attention, causal, same length, Apriel heads)."""
+    from paper_2604_19877_b200 import ops
+    from paper_2604_19877_b200.model import Supernet
+    model = Supernet(cfg, PRESETS[preset].layer_string, batch=1, max_len=tokens, dtype=torch.bfloat16, seed=0)
+    toks = torch.randint(0, cfg.vocab, (1, tokens), generator=torch.Generator().manual_seed(1))
+    model.prefill(toks)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for _ in range(reps):
+        e0.record()
+        model.prefill(toks)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del model
+    torch.cuda.empty_cache()
+    Hq, Hkv, D = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+    q = torch.randn(tokens, Hq, D, device="cuda").to(torch.bfloat16)
+    k = torch.randn(tokens, Hkv, D, device="cuda").to(torch.bfloat16)
+    v = torch.randn(tokens, Hkv, D, device="cuda").to(torch.bfloat16)
+    cu = torch.tensor([0, tokens], dtype=torch.int32, device="cuda")
+    o = torch.empty(tokens, Hq * D, device="cuda", dtype=torch.bfloat16)
+    ops.attn_prefill(q, k, v, cu, o, Hq, Hkv, D, 0, 1 / math.sqrt(D))
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(3):
+        ops.attn_prefill(q, k, v, cu, o, Hq, Hkv, D, 0, 1 / math.sqrt(D))
+    e1.record()
+    torch.cuda.synchronize()
+    attn_ms = e0.elapsed_time(e1) / 3
+    flops = 4.0 * (tokens * (tokens + 1) / 2) * Hq * D
+    return {"preset": preset, "tokens": tokens, "batch": 1, "ms": best, "tok_s": tokens / best * 1e3,
+            "attention_kernel": {"mask": "causal", "ms": attn_ms, "tflops": flops / attn_ms / 1e9,
+                                 "kernel": "tcgen05/TMEM flash attention (sn_attn_prefill_umma.cu)"}}
+
+
 # ------------------------------------------------------------------ CPU reference (oracle) arm
 class CPUComposedStep:
     """One decode step of a preset on the CPU fp32 oracle, composed from one measured layer per
@@ -368,6 +409,7 @@ def main():
     ap.add_argument("--context", type=int, default=32768)
     ap.add_argument("--cpu-batch", type=int, default=8)
     ap.add_argument("--no-fa-compare", action="store_true")
+    ap.add_argument("--prefill-tokens", type=int, default=16384, help="side measurement; 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -434,6 +476,8 @@ def main():
                          "speedup_of_preset": main_res["tok_s"] / fa_res["tok_s"],
                          "note": "all-FA batch capped by HBM capacity at this context",
                          "kernels": fa_res["kernels"]}
+    if ws == 1 and args.prefill_tokens > 0:
+        out["prefill"] = measure_prefill(cfg, args.preset, args.prefill_tokens)
     if ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args.preset, args.cpu_batch, args.context)
     print(json.dumps(out), flush=True)
