@@ -237,6 +237,22 @@ sn_status sn_gated_rmsnorm(const float* o, const void* gate, int gate_stride,
                            const void* norm_w, void* out, int rows, int H, int D,
                            float eps, int act, int dtype, void* stream);
 
+/* ---------------------------------------------------------------- head-parallel decode
+ * Row-parallel projection all-reduce fused into the residual add + RMSNorm over peer
+ * memory (NVLink P2P; csrc/sn_tp.cu).  Each rank's symmetric buffer (CUDA IPC, mapped in
+ * every peer) holds an arrival counter and fp32 split-K slabs; the rank writes its partial
+ * product there (sn_gemm_decode PARTIAL), bumps its counter (sn_tp_arrive), and
+ * sn_tp_allreduce_add_rmsnorm waits for every peer's counter to reach its own, then sums all
+ * ranks' slabs in rank order (bit-identical on every rank), adds the residual and normalises.
+ * peer_slabs / peer_counters: device arrays of `world` addresses (this rank's included).
+ * Replaces the NCCL all-reduce after the out-projection (north_star, config 5).          */
+sn_status sn_tp_arrive(unsigned int* counter, void* stream);
+sn_status sn_tp_allreduce_add_rmsnorm(const unsigned long long* peer_slabs,
+                                      const unsigned long long* peer_counters, int world,
+                                      int rank, int nsplit, float* residual,
+                                      const void* weight, void* out, int rows, int dim,
+                                      float eps, int dtype, void* stream);
+
 /* ---------------------------------------------------------------- decode GEMM
  * Weight-streaming projection GEMM for decode batches (M <= 128):
  * C[m][n] = sum_k X[m][k] W[n][k], X [M][ldx] bf16, W [N][ldw] bf16 (nn.Linear

@@ -135,3 +135,43 @@ def allreduce_sum_(t, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
+
+
+# ---------------------------------------------------------------- peer-memory all-reduce
+class SymmetricSlabs:
+    """One fp32 buffer per rank, mapped into every peer of the group through CUDA IPC
+    (torch's CUDA-tensor sharing: cudaIpcGetMemHandle / cudaIpcOpenMemHandle, P2P over
+    NVLink), for the fused all-reduce + residual + RMSNorm of the head-parallel decode
+    (csrc/sn_tp.cu).  Layout: [64-word header: word 0 = arrival counter]
+    [parity 0: nsplit_max x rows x dim][parity 1: same].  Collective: every rank of `group`
+    must construct it (the handles travel through group.all_gather_object)."""
+
+    HEADER = 64
+
+    def __init__(self, rows: int, dim: int, group=None, nsplit_max: int = 8, device="cuda"):
+        import torch.distributed as tdist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.world = tdist.get_world_size(group)
+        self.rank = tdist.get_rank(group)
+        self.rows, self.dim, self.nsplit_max = rows, dim, nsplit_max
+        self.region = nsplit_max * rows * dim
+        self.buf = torch.zeros(self.HEADER + 2 * self.region, device=device, dtype=torch.float32)
+        torch.cuda.synchronize()
+        shared = [None] * self.world
+        tdist.all_gather_object(shared, reduce_tensor(self.buf), group=group)
+        self.peers = []
+        for r, (rebuild, args) in enumerate(shared):
+            self.peers.append(self.buf if r == self.rank else rebuild(*args))
+        base = [p.data_ptr() for p in self.peers]
+        self.counters = torch.tensor(base, dtype=torch.int64, device=device)
+        self.slab_ptrs = [torch.tensor([b + 4 * (self.HEADER + q * self.region) for b in base], dtype=torch.int64,
+                                       device=device) for q in (0, 1)]
+        tdist.barrier(group)
+
+    def local_slabs(self, parity: int, nsplit: int = None) -> torch.Tensor:
+        """This rank's [nsplit_max, rows, dim] slab view of one parity region."""
+        off = self.HEADER + parity * self.region
+        return self.buf[off: off + self.region].view(self.nsplit_max, self.rows, self.dim)
+
+    def counter_ptr(self) -> int:
+        return self.buf.data_ptr()

@@ -20,6 +20,7 @@ projections / FFN / LM head; there is no CPU path.
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -80,6 +81,12 @@ class Supernet:
         self.scale_attn = attn_scale(cfg)
         self._alloc_state(fa_block_table)
         self._alloc_decode_buffers()
+        # head-parallel decode: the row-parallel all-reduces run through peer memory, fused into
+        # the next residual add + RMSNorm (csrc/sn_tp.cu); SN_TP_NCCL=1 keeps torch.distributed
+        self.sym = None
+        if self.tp > 1 and not os.environ.get("SN_TP_NCCL"):
+            from .dist import SymmetricSlabs
+            self.sym = SymmetricSlabs(batch, cfg.hidden, group=tp_group, device=self.device)
         self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
         self.force_simt = False
         # bf16 decode projections run on the tcgen05 weight-streaming GEMM (libsn100, batch-as-M
@@ -89,7 +96,7 @@ class Supernet:
         # down-projection; cuBLAS for the mixer in/out projections, where ours is ~par alone but
         # slower inside the step.  SN_DECODE_GEMMS=all switches every role to ours.
         tc_ok = dtype == torch.bfloat16 and batch <= 128
-        import os
+
         sel = os.environ.get("SN_DECODE_GEMMS", "lm_head,ffn_down,ffn_gate_up").split(",")
         self.sn_gemm = {r: tc_ok and (r in sel or "all" in sel)
                         for r in ("lm_head", "ffn_down", "ffn_gate_up", "in_proj", "attn_qkv", "out_proj")}
@@ -308,6 +315,16 @@ class Supernet:
     def _gemm_residual(self, x, w, slab, out_bf16, role):
         """Projection whose result is added to the residual stream.  Returns the pending
         update (delta, partials, nsplit) that the next add_rmsnorm applies."""
+        if self.sym is not None:  # row-parallel partial straight into this rank's symmetric slabs
+            parity = 0 if role == "out_proj" else 1
+            slabs = self.sym.local_slabs(parity)
+            if self.dtype == torch.bfloat16:
+                ns = ops.gemm_decode(x, w, slabs, "partial")
+            else:
+                torch.mm(x, w.t(), out=slabs[0])
+                ns = 1
+            ops.tp_arrive(self.sym.counter_ptr())
+            return ("tp", parity, ns)
         if self.tp > 1:  # row-parallel: fp32 partial of this rank, summed over the TP group
             from .dist import allreduce_sum_
             buf = slab[0]
@@ -329,6 +346,11 @@ class Supernet:
 
     def _norm(self, pending, weight):
         delta, part, ns = pending
+        if isinstance(delta, str):  # ("tp", parity, nsplit): peer-memory all-reduce fused with the norm
+            sym = self.sym
+            ops.tp_allreduce_add_rmsnorm(sym.slab_ptrs[part], sym.counters, sym.world, sym.rank, ns, self.residual,
+                                         weight, self.h, self.cfg.norm_eps)
+            return
         self._probe_begin("add_rmsnorm", fine=True)
         ops.add_rmsnorm(delta, self.residual, weight, self.h, self.cfg.norm_eps, partials=part, nsplit=ns)
         self._probe_end("add_rmsnorm", fine=True)

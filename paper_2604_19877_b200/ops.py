@@ -239,3 +239,15 @@ def kda_chunk_prefill2(qn, kn, qkv_conv, v_off, glog, beta, chunks, seq_chunk0, 
 def swiglu_il(gu_il, out, ffn, h):
     """out [rows, ffn] = silu(gate) * up from the interleaved gate/up GEMM output [rows, nb*2h]."""
     call("sn_swiglu_il", _p(gu_il), gu_il.stride(0), _p(out), gu_il.shape[0], ffn, h, dtype_code(out.dtype), _s())
+
+
+def tp_arrive(counter_ptr: int):
+    """Bump this rank's arrival counter (after the partial product in stream order)."""
+    call("sn_tp_arrive", counter_ptr, _s())
+
+
+def tp_allreduce_add_rmsnorm(peer_slabs, peer_counters, world, rank, nsplit, residual, weight, out, eps):
+    """residual += sum over ranks and slabs of the peers' partials (P2P), then out = RMSNorm(residual) * weight."""
+    rows, dim = residual.shape
+    call("sn_tp_allreduce_add_rmsnorm", _p(peer_slabs), _p(peer_counters), world, rank, nsplit, _p(residual),
+         _p(weight), _p(out), rows, dim, eps, dtype_code(out.dtype), _s())

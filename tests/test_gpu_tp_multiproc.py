@@ -2,7 +2,8 @@
 sharded Supernet (dist.shard_weights, local head counts) and runs the real kernels; the
 row-parallel partials meet in torch.distributed all-reduces (gloo here — only one GPU is
 available; the same calls run over NCCL on a multi-GPU node).  Rank 0's prefill logits and
-eager decode logits must match the unsharded single-process model."""
+decode logits must match the unsharded single-process model.  The decode all-reduces run
+through CUDA-IPC peer memory (sn_tp.cu), which two processes on one GPU exercise for real."""
 import os
 import socket
 import tempfile
@@ -21,14 +22,25 @@ def _tokens():
     return torch.randint(0, CFG.vocab, (B, T + STEPS), generator=torch.Generator().manual_seed(2))
 
 
-def _run(model, toks):
+def _run(model, toks, graph=False):
     outs = [model.prefill(toks[:, :T], return_all=True).float().cpu()]
-    for t in range(T, T + STEPS):
-        outs.append(model.decode(toks[:, t]).float().cpu()[:, None])
+    if graph:
+        from paper_2604_19877_b200.graphs import DecodeGraph
+        g = DecodeGraph(model)
+        for t in range(T, T + STEPS):
+            model.step_tokens.copy_(toks[:, t].to(torch.int32))
+            g.replay()
+            outs.append(model.logits.clone().float().cpu()[:, None])
+        torch.cuda.synchronize()
+    else:
+        for t in range(T, T + STEPS):
+            outs.append(model.decode(toks[:, t]).float().cpu()[:, None])
     return torch.cat(outs, 1)
 
 
-def _worker(rank, world, port, path):
+def _worker(rank, world, port, path, graph=False, nccl_path=False):
+    if nccl_path:
+        os.environ["SN_TP_NCCL"] = "1"
     import torch.distributed as dist
     from paper_2604_19877_b200.model import Supernet
     from paper_2604_19877_b200.placement import layer_kinds
@@ -38,7 +50,7 @@ def _worker(rank, world, port, path):
     w = init_weights(CFG, layer_kinds(PLACEMENT), seed=0)
     model = Supernet(CFG, PLACEMENT, batch=B, max_len=T + STEPS, dtype=torch.bfloat16, weights=w,
                      tp_group=dist.group.WORLD)
-    out = _run(model, _tokens())
+    out = _run(model, _tokens(), graph=graph)
     if rank == 0:
         torch.save(out, path)
     dist.barrier()
@@ -46,7 +58,10 @@ def _worker(rank, world, port, path):
 
 
 @pytest.mark.gpu
-def test_tp2_two_processes_match_unsharded():
+@pytest.mark.parametrize("graph,nccl_path", [(False, False), (True, False), (False, True)])
+def test_tp2_two_processes_match_unsharded(graph, nccl_path):
+    """Decode all-reduces through peer memory fused with the norm (default; eager and in a
+    CUDA graph), or through torch.distributed (SN_TP_NCCL=1)."""
     from paper_2604_19877_b200.model import Supernet
     from paper_2604_19877_b200.placement import layer_kinds
     from paper_2604_19877_b200.weights import init_weights
@@ -55,7 +70,7 @@ def test_tp2_two_processes_match_unsharded():
         port = s.getsockname()[1]
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "tp.pt")
-        mp.spawn(_worker, args=(2, port, path), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, port, path, graph, nccl_path), nprocs=2, join=True)
         tp_out = torch.load(path)
     ref_model = Supernet(CFG, PLACEMENT, batch=B, max_len=T + STEPS, dtype=torch.bfloat16,
                          weights=init_weights(CFG, layer_kinds(PLACEMENT), seed=0))
