@@ -420,11 +420,14 @@ class Supernet:
 
     # ------------------------------------------------------------------ prefill
     @torch.no_grad()
-    def prefill(self, tokens, return_all: bool = False):
+    def prefill(self, tokens, return_all: bool = False, slots=None):
         """Parallel prefill from an empty state.  tokens: [B, T] (equal-length prompts) or a list
-        of B 1-D prompts of any lengths (ragged: packed rows, cu_seqlens, every kernel masks or
-        chunks per sequence).  Returns the last position's logits [B, V], or with return_all
-        [B, T, V] (equal lengths) / a list of [T_b, V] (ragged)."""
+        of 1-D prompts of any lengths (ragged: packed rows, cu_seqlens, every kernel masks or
+        chunks per sequence).  slots: engine batch slots the prompts go to (continuous
+        batching: only those slots are reset and prefilled — their KV pages, rings, conv tails
+        and recurrent states are addressed through slot indices — while the other slots keep
+        decoding); default all B slots.  Returns the last position's logits [n, V], or with
+        return_all [n, T, V] (equal lengths) / a list of [T_b, V] (ragged)."""
         cfg, w, dev, dt = self.cfg, self.w, self.device, self.dtype
         ragged = isinstance(tokens, (list, tuple))
         if ragged:
@@ -436,8 +439,14 @@ class Supernet:
             lens = [t2.shape[1]] * t2.shape[0]
             flat = t2.reshape(-1)
         B = len(lens)
-        if B != self.B:
-            raise ValueError(f"prefill batch {B} != engine batch {self.B}")
+        if slots is None:
+            if B != self.B:
+                raise ValueError(f"prefill batch {B} != engine batch {self.B}")
+            slot_list = list(range(B))
+        else:
+            slot_list = [int(x) for x in slots]
+            if len(slot_list) != B or len(set(slot_list)) != B or not all(0 <= x < self.B for x in slot_list):
+                raise ValueError(f"slots {slot_list} must be {B} distinct indices in [0, {self.B})")
         if min(lens) < 1 or max(lens) > self.max_len:
             raise ValueError(f"prompt lengths must be in [1, max_len={self.max_len}], got {min(lens)}..{max(lens)}")
         rows = sum(lens)
@@ -448,11 +457,21 @@ class Supernet:
         self._cu_host = cu_host
         cu = torch.tensor(cu_host, **i32)
         lens_t = torch.tensor(lens, **i32)
-        row_seq = torch.repeat_interleave(torch.arange(B, **i32), lens_t)
+        slot_t = torch.tensor(slot_list, **i32)
+        self._slot_idx = None if slots is None else slot_t  # identity mapping: kernels take NULL
+        row_seq = torch.repeat_interleave(slot_t, lens_t)
         row_pos = torch.arange(rows, **i32) - torch.repeat_interleave(cu[:-1], lens_t)
         T = max(lens)
-        self.reset()
-        self.seq_lens.copy_(lens_t)
+        if slots is None:
+            self.reset()
+            self.seq_lens.copy_(lens_t)
+        else:
+            idx = slot_t.long()
+            for st in self.state:
+                for key in ("S", "conv"):
+                    if key in st:
+                        st[key].index_fill_(0, idx, 0)
+            self.seq_lens.index_copy_(0, idx, lens_t)
         e = lambda *s, d=dt: torch.empty(*s, device=dev, dtype=d)
         resid = e(rows, cfg.hidden, d=torch.float32)
         h, mix, ffn_o = e(rows, cfg.hidden), e(rows, cfg.hidden), e(rows, cfg.hidden)
@@ -534,7 +553,7 @@ class Supernet:
             gate = (proj[:, g1_off:g1_off + R] @ w["g2"].t() + w["g2_b"]).contiguous()
             gate_stride = gate.stride(0)
         y = torch.empty(rows, C, device=dev, dtype=h.dtype)
-        ops.conv_prefill(proj, proj.stride(0), y, w["conv_w"], st["conv"], cu, None, C, cfg.conv_width)
+        ops.conv_prefill(proj, proj.stride(0), y, w["conv_w"], st["conv"], cu, self._slot_idx, C, cfg.conv_width)
         f32 = dict(device=dev, dtype=torch.float32)
         qn, kn = torch.empty(rows, Hk, D, **f32), torch.empty(rows, Hk, D, **f32)
         gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
@@ -550,7 +569,7 @@ class Supernet:
         if chunked:
             self._chunked_delta(kind, qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], cu, Hk, Hv, D)
         else:
-            ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], None, cu, Hk, Hv, D,
+            ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], self._slot_idx, cu, Hk, Hv, D,
                            init_state=False)
         y_out = torch.empty(rows, Hv * D, device=dev, dtype=h.dtype)
         ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
@@ -559,7 +578,8 @@ class Supernet:
     def _chunked_delta(self, kind, qn, kn, y, v_off, glog, beta, o, S, cu, Hk, Hv, D, ws_cap=2 << 30):
         """Two-phase chunked prefill over groups of consecutive sequences whose chunk workspace
         fits ws_cap bytes (ragged lengths: the chunk plan follows cu_seqlens)."""
-        B = S.shape[0]
+        slot_idx = getattr(self, "_slot_idx", None)
+        B = S.shape[0] if slot_idx is None else slot_idx.numel()
         cu_host = getattr(self, "_cu_host", None)
         if cu_host is None or len(cu_host) != B + 1:
             cu_host = [int(x) for x in cu.tolist()]
@@ -579,13 +599,15 @@ class Supernet:
                 self._chunk_plan = ops.chunk_plan([c - r0 for c in cu_host[b0:b1 + 1]], device=qn.device)
             chunks, c0 = self._chunk_plan
             ws = getattr(self, "_chunk_ws", None)
+            # states by slot (continuous batching) or, for a full batch, the slice in prompt order
+            S_g, sl = (S[b0:b1], None) if slot_idx is None else (S, slot_idx[b0:b1])
             if kind == KDA:
                 self._chunk_ws = ops.kda_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
-                                                        beta[r0:r1], chunks, c0, o[r0:r1], S[b0:b1], None, Hv, D,
+                                                        beta[r0:r1], chunks, c0, o[r0:r1], S_g, sl, Hv, D,
                                                         init_state=False, workspace=ws)
             else:
                 self._chunk_ws = ops.gdn_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
-                                                        beta[r0:r1], chunks, c0, o[r0:r1], S[b0:b1], None, Hk, Hv,
+                                                        beta[r0:r1], chunks, c0, o[r0:r1], S_g, sl, Hk, Hv,
                                                         D, init_state=False, workspace=ws)
             b0 = b1
 

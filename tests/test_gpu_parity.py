@@ -121,3 +121,49 @@ def test_ragged_prefill_matches_per_sequence_oracle(placement):
         ref = OracleSupernet(TINY, kinds, w, batch=1, max_len=L + steps).run(s[None])[0]
         got = torch.cat([pre[b].float().cpu(), torch.stack([d[b] for d in dec])])
         assert rel_err(got, ref) <= TOL[torch.bfloat16], (b, rel_err(got, ref))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("placement", ["ASKG", "GKSA"])
+def test_continuous_batching_slot_prefill(placement):
+    """Prefill into a subset of engine slots while the others keep decoding: slot-indexed KV
+    pages / SWA rings / conv tails / recurrent states; every slot matches the oracle run of
+    its own token stream."""
+    from paper_2604_19877_b200.model import Supernet
+    kinds = layer_kinds(placement)
+    w = cast_weights(init_weights(TINY, kinds, seed=0), "cpu", torch.bfloat16)
+    g = torch.Generator().manual_seed(11)
+    lens = {0: 40, 2: 70, 1: 55}
+    n1, n2 = 3, 3  # decode steps before / after slot 1 joins
+    toks = {s: torch.randint(0, TINY.vocab, (L + n1 + n2,), generator=g) for s, L in lens.items()}
+    model = Supernet(TINY, placement, batch=3, max_len=80, dtype=torch.bfloat16, weights=w)
+    got = {s: [] for s in lens}
+    first = model.prefill([toks[0][:lens[0]], toks[2][:lens[2]]], slots=[0, 2])
+    got[0].append(first[0].float().cpu())
+    got[2].append(first[1].float().cpu())
+    step = {0: lens[0], 2: lens[2], 1: None}
+
+    def decode_all():
+        feed = torch.zeros(3, dtype=torch.int32)
+        for s in (0, 1, 2):
+            if step[s] is not None:
+                feed[s] = int(toks[s][step[s]])
+        lg = model.decode(feed).float().cpu()
+        for s in (0, 1, 2):
+            if step[s] is not None:
+                got[s].append(lg[s])
+                step[s] += 1
+
+    for _ in range(n1):
+        decode_all()
+    joined = model.prefill([toks[1][:lens[1]]], slots=[1])
+    got[1].append(joined[0].float().cpu())
+    step[1] = lens[1]
+    for _ in range(n2):
+        decode_all()
+    torch.cuda.synchronize()
+    for s, L in lens.items():
+        n = len(got[s]) - 1  # decode steps taken by this slot
+        ref = OracleSupernet(TINY, kinds, w, batch=1, max_len=L + n).run(toks[s][None, :L + n])[0]
+        want = ref[L - 1:L + n]
+        assert rel_err(torch.stack(got[s]), want) <= TOL[torch.bfloat16], (s, rel_err(torch.stack(got[s]), want))
