@@ -120,11 +120,16 @@ sn_status sn_attn_decode(const void* q, const void* k_cache, const void* v_cache
                          int window, int split_pages, int max_splits, float scale,
                          int dtype, void* stream);
 
-/* Causal (window==0) or sliding-window prefill attention over contiguous
- * per-sequence q [rows][Hq][D], k/v [rows][Hkv][D] (cu_seqlens, int32).     */
+/* Causal (window==0) or sliding-window prefill attention over packed sequences:
+ * q [rows][Hq][D] (cu_seqlens).  Plain prefill (cu_k, q_off NULL): k/v are the
+ * same rows [rows][Hkv][D].  Continuation: k/v [rows_k][Hkv][D] hold each
+ * sequence's keys packed by cu_k, and query row r of sequence s attends as key
+ * index cu_k[s] + (r - cu_seqlens[s]) + q_off[s] (q_off = position of the first
+ * new token minus the position of the first packed key).                     */
 sn_status sn_attn_prefill(const void* q, const void* k, const void* v,
-                          const int32_t* cu_seqlens, void* out, int num_seqs,
-                          int rows, int Hq, int Hkv, int D, int window,
+                          const int32_t* cu_seqlens, const int32_t* cu_k,
+                          const int32_t* q_off, void* out, int num_seqs, int rows,
+                          int rows_k, int Hq, int Hkv, int D, int window,
                           float scale, int dtype, void* stream);
 
 /* ---------------------------------------------------------------- GDN / KDA
@@ -160,15 +165,18 @@ sn_status sn_kda_decode(const void* proj, int proj_stride, int proj_nsplit, void
                         int H, int D, int rank, int conv_width, float scale,
                         float eps_l2, float eps_norm, int dtype, void* stream);
 
-/* Prefill building blocks (sequences packed by cu_seqlens, starting from an
- * empty state/conv ring).                                                  */
+/* Prefill building blocks (sequences packed by cu_seqlens).                */
 /* y[t, c] = silu(sum_w conv_w[c,w] * x[t-(W-1)+w, c]) for c < channels (x
  * row stride x_stride); leaves the conv ring of slot_idx[s] in the decode
- * layout.                                                                   */
+ * layout.  Continuation (appending to a live sequence): pos0[s] is the
+ * absolute position of the first new token and ring_hist a copy of the rings
+ * [num_seqs][channels][W] taken before the launch (inputs before pos0 come
+ * from it); both NULL = start from an empty ring at position 0.            */
 sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv_w,
-                          void* conv_ring, const int32_t* cu_seqlens,
-                          const int32_t* slot_idx, int num_seqs, int rows,
-                          int channels, int width, int dtype, void* stream);
+                          void* conv_ring, const void* ring_hist,
+                          const int32_t* cu_seqlens, const int32_t* slot_idx,
+                          const int32_t* pos0, int num_seqs, int rows, int channels,
+                          int width, int dtype, void* stream);
 
 /* Per-token gate prep: qn/kn = l2norm(q/k) (qn also * scale), fp32 [rows][Hk][D];
  * gexp = exp(g) fp32 ([rows][Hv] for GDN, [rows][Hv][D] for KDA);

@@ -29,10 +29,10 @@ SIGNATURES = {
     "sn_rope_kv_append": [P, I, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, P],
     "sn_attn_decode_workspace_bytes": [I, I, I, I, I],
     "sn_attn_decode": [P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, Fl, I, P],
-    "sn_attn_prefill": [P, P, P, P, P, I, I, I, I, I, I, Fl, I, P],
+    "sn_attn_prefill": [P, P, P, P, P, P, P, I, I, I, I, I, I, I, Fl, I, P],
     "sn_gdn_decode": [P, I, I, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
     "sn_kda_decode": [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
-    "sn_conv_prefill": [P, I, P, P, P, P, P, I, I, I, I, I, P],
+    "sn_conv_prefill": [P, I, P, P, P, P, P, P, P, I, I, I, I, I, P],
     "sn_delta_prep": [I, P, P, I, I, I, P, P, P, P, P, P, P, P, I, I, I, I, Fl, Fl, I, P],
     "sn_gdn_chunk_prefill": [P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gdn_chunk_workspace_bytes": [I, I, I],

@@ -173,22 +173,22 @@ template <typename T, int D>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                            const T* __restrict__ v, const int32_t* __restrict__ cu,
                                                            T* __restrict__ out, int num_seqs, int rows, int Hq,
-                                                           int Hkv, int window, float scale) {
+                                                           int Hkv, int window, float scale,
+                                                           const int32_t* __restrict__ cu_k,
+                                                           const int32_t* __restrict__ q_off) {
   constexpr int EPL = D / 32;
   __shared__ float s_q[4][D];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x * 4 + warp;
   const int h = blockIdx.y;
   if (r >= rows) return;
-  int s = 0;
-  while (s + 1 < num_seqs && cu[s + 1] <= r) ++s;
-  const int t0 = cu[s];
-  const int i = r - t0;
+  const KeyBounds kb = key_bounds(cu, cu_k, q_off, num_seqs, r, window);  // keys [lo, hi], packed key indices
+  const int i = kb.hi;
   const int G = Hq / Hkv, hk = h / G;
   const float qscale = scale * 1.4426950408889634f;
   for (int d = lane; d < D; d += 32) s_q[warp][d] = io<T>::ld(q + ((size_t)r * Hq + h) * D + d) * qscale;
   __syncwarp();
-  const int j_lo = window > 0 ? max(0, i - window + 1) : 0;
+  const int j_lo = kb.lo;
   float m = -INFINITY, l = 0.f, o[EPL];
 #pragma unroll
   for (int e = 0; e < EPL; ++e) o[e] = 0.f;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const T* __restrict__
     const int j = jb + lane;
     float sc = -INFINITY;
     if (j <= i) {
-      const T* kr = k + ((size_t)(t0 + j) * Hkv + hk) * D;
+      const T* kr = k + ((size_t)j * Hkv + hk) * D;
       float acc = 0.f;
       for (int d = 0; d < D; d += 8) {
         float f[8];
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const T* __restrict__
     const int nk = min(32, i - jb + 1);
     for (int x = 0; x < nk; ++x) {
       const float px = __shfl_sync(0xffffffffu, p, x);
-      const T* vr = v + ((size_t)(t0 + jb + x) * Hkv + hk) * D;
+      const T* vr = v + ((size_t)(jb + x) * Hkv + hk) * D;
 #pragma unroll
       for (int e = 0; e < EPL; ++e) o[e] += px * io<T>::ld(vr + lane + 32 * e);
     }
@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const T* __restrict__
 sn_status attn_decode_tc_bf16(const AttnDecodeArgs& a, int D, cudaStream_t st);  // sn_attn_tc.cu
 sn_status attn_prefill_tc_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale,
+                               const int32_t* cu_k, const int32_t* q_off, int rows_k,
                                cudaStream_t st);  // sn_attn_prefill.cu
 
 }  // namespace sn
@@ -288,18 +289,22 @@ sn_status sn_attn_decode(const void* q, const void* k_cache, const void* v_cache
   });
 }
 
-sn_status sn_attn_prefill(const void* q, const void* k, const void* v, const int32_t* cu_seqlens, void* out,
-                          int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale, int dtype,
+sn_status sn_attn_prefill(const void* q, const void* k, const void* v, const int32_t* cu_seqlens,
+                          const int32_t* cu_k, const int32_t* q_off, void* out, int num_seqs, int rows,
+                          int rows_k, int Hq, int Hkv, int D, int window, float scale, int dtype,
                           void* stream) {
   SN_REQUIRE(num_seqs > 0 && rows > 0 && Hkv > 0 && Hq % Hkv == 0, "sn_attn_prefill: bad shape");
-  if (dtype == SN_BF16)  // tensor-core flash attention (sn_attn_prefill.cu); fp32 I/O below
-    return attn_prefill_tc_bf16(q, k, v, cu_seqlens, out, num_seqs, rows, Hq, Hkv, D, window, scale,
-                                (cudaStream_t)stream);
+  SN_REQUIRE((cu_k == nullptr) == (q_off == nullptr), "sn_attn_prefill: cu_k and q_off go together");
+  if (cu_k == nullptr) rows_k = rows;
+  SN_REQUIRE(rows_k > 0, "sn_attn_prefill: no keys");
+  if (dtype == SN_BF16)  // tensor-core flash attention (sn_attn_prefill*.cu); fp32 I/O below
+    return attn_prefill_tc_bf16(q, k, v, cu_seqlens, out, num_seqs, rows, Hq, Hkv, D, window, scale, cu_k, q_off,
+                                rows_k, (cudaStream_t)stream);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(ceil_div(rows, 4), Hq);
     cudaStream_t st = (cudaStream_t)stream;
-    if (D == 128) attn_prefill_kernel<T, 128><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, cu_seqlens, (T*)out, num_seqs, rows, Hq, Hkv, window, scale);
-    else if (D == 64) attn_prefill_kernel<T, 64><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, cu_seqlens, (T*)out, num_seqs, rows, Hq, Hkv, window, scale);
+    if (D == 128) attn_prefill_kernel<T, 128><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, cu_seqlens, (T*)out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off);
+    else if (D == 64) attn_prefill_kernel<T, 64><<<grid, 128, 0, st>>>((const T*)q, (const T*)k, (const T*)v, cu_seqlens, (T*)out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off);
     else { set_error("sn_attn_prefill: D=%d unsupported", D); return SN_EUNSUPPORTED; }
     return check_launch("sn_attn_prefill");
   });

@@ -37,21 +37,13 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ int seq_start(const int32_t* __restrict__ cu, int num_seqs, int r) {
-  int lo = 0, hi = num_seqs;  // largest s with cu[s] <= r
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (cu[mid] <= r) lo = mid; else hi = mid;
-  }
-  return cu[lo];
-}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads)
     attn_prefill_tc_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                            const __nv_bfloat16* __restrict__ v, const int32_t* __restrict__ cu,
                            __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
-                           float scale) {
+                           float scale, const int32_t* __restrict__ cu_k, const int32_t* __restrict__ q_off) {
   using SM = Smem<D>;
   constexpr int LD = SM::LD, NT = D / 8, KS = D / 16;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -63,17 +55,16 @@ __global__ void __launch_bounds__(kThreads)
   const int h = blockIdx.y, hk = h / (Hq / Hkv);
   const float qs = scale * 1.4426950408889634f;  // exp2 domain
 
-  // this thread's two rows and their sequence starts / lower key bounds
+  // this thread's two rows and their key bounds
   const int ra = r0 + warp * 16 + g4, rb = ra + 8;
-  const int sa = seq_start(cu, num_seqs, min(ra, rows - 1)), sb = seq_start(cu, num_seqs, min(rb, rows - 1));
-  const int lo_a = window > 0 ? max(sa, ra - window + 1) : sa;
-  const int lo_b = window > 0 ? max(sb, rb - window + 1) : sb;
+  const KeyBounds kba = key_bounds(cu, cu_k, q_off, num_seqs, min(ra, rows - 1), window);
+  const KeyBounds kbb = key_bounds(cu, cu_k, q_off, num_seqs, min(rb, rows - 1), window);
+  const int lo_a = kba.lo, lo_b = kbb.lo, hi_a = kba.hi, hi_b = kbb.hi;
   // key range of the whole tile
-  const int s0 = seq_start(cu, num_seqs, r0);
   const int r_last = min(r0 + BM - 1, rows - 1);
-  const int j_lo = window > 0 ? max(s0, r0 - window + 1) : s0;
-  const int j_hi = r_last;
-  const int s_last = seq_start(cu, num_seqs, r_last);
+  const KeyBounds kb0 = key_bounds(cu, cu_k, q_off, num_seqs, r0, window);
+  const KeyBounds kbl = key_bounds(cu, cu_k, q_off, num_seqs, r_last, window);
+  const int j_lo = kb0.lo, j_hi = kbl.hi;
 
   auto load_kv = [&](int jb, int buf) {
 #pragma unroll
@@ -136,7 +127,7 @@ __global__ void __launch_bounds__(kThreads)
         mma_bf16(s[nt + 1], qa[ks], b2, b3);
       }
     // mask: only blocks touching a row's bounds need it
-    const bool full = jb >= s_last && jb + BN - 1 <= r0 && (window == 0 || jb > r_last - window);
+    const bool full = jb >= kbl.lo && jb + BN - 1 <= kb0.hi;
     float mx_a = -INFINITY, mx_b = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
@@ -146,8 +137,8 @@ __global__ void __launch_bounds__(kThreads)
         const bool rowb = e >= 2;
         float x = s[nt][e] * qs;
         if (!full) {
-          const int r = rowb ? rb : ra, lo = rowb ? lo_b : lo_a;
-          if (j > r || j < lo) x = -INFINITY;
+          const int hi = rowb ? hi_b : hi_a, lo = rowb ? lo_b : lo_a;
+          if (j > hi || j < lo) x = -INFINITY;
         }
         s[nt][e] = x;
         if (rowb) mx_b = fmaxf(mx_b, x); else mx_a = fmaxf(mx_a, x);
@@ -209,7 +200,8 @@ __global__ void __launch_bounds__(kThreads)
 
 template <int D>
 static sn_status launch(const void* q, const void* k, const void* v, const int32_t* cu, void* out, int num_seqs,
-                        int rows, int Hq, int Hkv, int window, float scale, cudaStream_t st) {
+                        int rows, int Hq, int Hkv, int window, float scale, const int32_t* cu_k,
+                        const int32_t* q_off, cudaStream_t st) {
   const int smem = (int)sizeof(Smem<D>);
   static bool attr = false;
   if (!attr) {
@@ -219,7 +211,7 @@ static sn_status launch(const void* q, const void* k, const void* v, const int32
   dim3 grid((rows + BM - 1) / BM, Hq);
   attn_prefill_tc_kernel<D><<<grid, kThreads, smem, st>>>(
       (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, cu, (__nv_bfloat16*)out, num_seqs,
-      rows, Hq, Hkv, window, scale);
+      rows, Hq, Hkv, window, scale, cu_k, q_off);
   return check_launch("sn_attn_prefill(tc)");
 }
 
@@ -227,16 +219,18 @@ static sn_status launch(const void* q, const void* k, const void* v, const int32
 
 sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                  int num_seqs, int rows, int Hq, int Hkv, int window, float scale,
+                                 const int32_t* cu_k, const int32_t* q_off, int rows_k,
                                  cudaStream_t st);  // sn_attn_prefill_umma.cu
 
 sn_status attn_prefill_tc_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale,
-                               cudaStream_t st) {
+                               const int32_t* cu_k, const int32_t* q_off, int rows_k, cudaStream_t st) {
   // D = 128: tcgen05/TMEM kernel; SN_ATTN_PREFILL=mma keeps the mma.sync kernel (A/B, D = 64)
   static const bool mma = getenv("SN_ATTN_PREFILL") && getenv("SN_ATTN_PREFILL")[0] == 'm';
-  if (D == 128 && !mma) return attn_prefill_umma_bf16(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, st);
-  if (D == 128) return fa::launch<128>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, st);
-  if (D == 64) return fa::launch<64>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, st);
+  if (D == 128 && !mma)
+    return attn_prefill_umma_bf16(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off, rows_k, st);
+  if (D == 128) return fa::launch<128>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off, st);
+  if (D == 64) return fa::launch<64>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off, st);
   set_error("sn_attn_prefill: D=%d unsupported", D);
   return SN_EUNSUPPORTED;
 }

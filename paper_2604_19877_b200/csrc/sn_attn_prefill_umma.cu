@@ -124,20 +124,13 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ int seq_start(const int32_t* __restrict__ cu, int num_seqs, int r) {
-  int lo = 0, hi = num_seqs;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (cu[mid] <= r) lo = mid; else hi = mid;
-  }
-  return cu[lo];
-}
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
-                             float scale, unsigned long long* __restrict__ dbg) {
+                             float scale, const int32_t* __restrict__ cu_k, const int32_t* __restrict__ q_off,
+                             unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Sync& sy = *reinterpret_cast<Sync*>(smem_raw);
   uint8_t* base = smem_raw + kSyncBytes;
@@ -153,11 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tiles = (rows + BM - 1) / BM;
   const int r0 = (tiles - 1 - (int)blockIdx.x) * BM;  // heavy (late) tiles first
   const int h = blockIdx.y, hk = h / (Hq / Hkv);
-  const int s0 = seq_start(cu, num_seqs, r0);
   const int r_last = min(r0 + BM - 1, rows - 1);
-  const int s_last = seq_start(cu, num_seqs, r_last);
-  const int j_lo = window > 0 ? max(s0, r0 - window + 1) : s0;
-  const int j_hi = r_last;
+  const KeyBounds kb0 = key_bounds(cu, cu_k, q_off, num_seqs, r0, window);
+  const KeyBounds kbl = key_bounds(cu, cu_k, q_off, num_seqs, r_last, window);
+  const int j_lo = kb0.lo, j_hi = kbl.hi;
   const int nblk = (j_hi - j_lo) / BN + 1;
 
   if (threadIdx.x == 0) {
@@ -257,8 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sub = warp & 3, half = warp >> 2;
     const int t = sub * 32 + lane;
     const int r = r0 + t;
-    const int sr = seq_start(cu, num_seqs, min(r, rows - 1));
-    const int lo = window > 0 ? max(sr, r - window + 1) : sr;
+    const KeyBounds kbr = key_bounds(cu, cu_k, q_off, num_seqs, min(r, rows - 1), window);
+    const int lo = kbr.lo, hi = kbr.hi;
     const float qs = scale * 1.4426950408889634f;
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
     const uint32_t s_addr = tmem + lane_addr + half * 64, o_addr = tmem + 256 + lane_addr + half * 64;
@@ -272,13 +264,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32(s_addr + (j & 1) * 128, s);
       tmem_ld32(s_addr + (j & 1) * 128 + 32, s + 32);
       tmem_wait_ld();
-      const bool full = jb >= s_last && jb + BN - 1 <= r0 && (window == 0 || jb > r_last - window);
+      const bool full = jb >= kbl.lo && jb + BN - 1 <= kb0.hi;
       float mx = -INFINITY;
       if (!full) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
           const int jj = jb + half * 64 + i;
-          if (jj > r || jj < lo) s[i] = -INFINITY;
+          if (jj > hi || jj < lo) s[i] = -INFINITY;
         }
       }
 #pragma unroll
@@ -371,12 +363,13 @@ static unsigned long long* g_fa5_dbg = nullptr;
 extern "C" void sn_experimental_fa5_timeline(unsigned long long* p) { g_fa5_dbg = p; }
 
 sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
-                                 int num_seqs, int rows, int Hq, int Hkv, int window, float scale, cudaStream_t st) {
+                                 int num_seqs, int rows, int Hq, int Hkv, int window, float scale,
+                                 const int32_t* cu_k, const int32_t* q_off, int rows_k, cudaStream_t st) {
   using namespace fa5;
   CUtensorMap qm, km, vm;
   if (!map_2d(&qm, q, rows, (uint64_t)Hq * HD, (uint64_t)Hq * HD, BM) ||
-      !map_2d(&km, k, rows, (uint64_t)Hkv * HD, (uint64_t)Hkv * HD, BN) ||
-      !map_2d(&vm, v, rows, (uint64_t)Hkv * HD, (uint64_t)Hkv * HD, BN)) {
+      !map_2d(&km, k, rows_k, (uint64_t)Hkv * HD, (uint64_t)Hkv * HD, BN) ||
+      !map_2d(&vm, v, rows_k, (uint64_t)Hkv * HD, (uint64_t)Hkv * HD, BN)) {
     set_error("sn_attn_prefill: cuTensorMapEncodeTiled failed");
     return SN_ECUDA;
   }
@@ -388,7 +381,7 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
   attn_prefill_umma_kernel<<<grid, kThreads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq,
-                                                         Hkv, window, scale, g_fa5_dbg);
+                                                         Hkv, window, scale, cu_k, q_off, g_fa5_dbg);
   return check_launch("sn_attn_prefill(umma)");
 }
 

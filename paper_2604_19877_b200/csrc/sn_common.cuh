@@ -146,6 +146,32 @@ inline bool pdl_enabled() {
   return on == 1;
 }
 
+// Key bounds [lo, hi] of packed query row r in prefill attention (mask j in (i - w, i],
+// SURVEY.md App. A item 3).  Plain prefill: queries and keys share the packed index space
+// (cu_k == nullptr).  Continuation: keys are packed per sequence by cu_k and row r of
+// sequence s sits at key index cu_k[s] + (r - cu_q[s]) + q_off[s].  Both bounds are
+// non-decreasing in r, so a tile's key range is [lo(first row), hi(last row)].
+struct KeyBounds {
+  int lo, hi;
+};
+__device__ __forceinline__ KeyBounds key_bounds(const int32_t* __restrict__ cu_q, const int32_t* __restrict__ cu_k,
+                                                const int32_t* __restrict__ q_off, int num_seqs, int r, int window) {
+  int a = 0, b = num_seqs;  // largest s with cu_q[s] <= r
+  while (b - a > 1) {
+    const int mid = (a + b) >> 1;
+    if (cu_q[mid] <= r) a = mid; else b = mid;
+  }
+  int ks, hi;
+  if (cu_k) {
+    ks = cu_k[a];
+    hi = ks + (r - cu_q[a]) + q_off[a];
+  } else {
+    ks = cu_q[a];
+    hi = r;
+  }
+  return {window > 0 ? max(ks, hi - window + 1) : ks, hi};
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args... args) {

@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
 // Causal conv + SiLU over time.  Thread per (channel, time chunk of 64).
 template <typename T>
 __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __restrict__ y,
-                                    const T* __restrict__ w, T* __restrict__ ring,
+                                    const T* __restrict__ w, T* __restrict__ ring, const T* __restrict__ ring_hist,
                                     const int32_t* __restrict__ cu, const int32_t* __restrict__ slot_idx,
-                                    int channels, int W) {
+                                    const int32_t* __restrict__ pos0s, int channels, int W) {
   constexpr int CH = 64;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = blockIdx.z;
@@ -356,13 +356,21 @@ __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __
   const int p0 = blockIdx.y * CH;
   if (p0 >= L) return;
   const int p1 = min(p0 + CH, L);
+  // continuation: the prompt starts at absolute position pos0; inputs before it come from a
+  // copy of the ring taken before this launch (the last chunk rewrites the ring)
+  const int pos0 = pos0s ? pos0s[s] : 0;
+  auto before = [&](int p) -> float {  // input at chunk-relative position p < 0
+    const int P = pos0 + p;
+    if (P < 0 || ring_hist == nullptr) return 0.f;
+    return io<T>::ld(ring_hist + ((size_t)s * channels + c) * W + (P % W));
+  };
   if (W == 4) {  // the pinned width: taps and history in registers, loads batched by 8
     float w4[4];
     load4<T>(w + (size_t)c * 4, w4);
     const T* xc = x + (size_t)t0 * x_stride + c;
-    float h1 = p0 >= 1 ? io<T>::ld(xc + (size_t)(p0 - 1) * x_stride) : 0.f;
-    float h2 = p0 >= 2 ? io<T>::ld(xc + (size_t)(p0 - 2) * x_stride) : 0.f;
-    float h3 = p0 >= 3 ? io<T>::ld(xc + (size_t)(p0 - 3) * x_stride) : 0.f;
+    float h1 = p0 >= 1 ? io<T>::ld(xc + (size_t)(p0 - 1) * x_stride) : before(p0 - 1);
+    float h2 = p0 >= 2 ? io<T>::ld(xc + (size_t)(p0 - 2) * x_stride) : before(p0 - 2);
+    float h3 = p0 >= 3 ? io<T>::ld(xc + (size_t)(p0 - 3) * x_stride) : before(p0 - 3);
     for (int p = p0; p < p1; p += 8) {
       float xv[8];
 #pragma unroll
@@ -382,7 +390,7 @@ __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __
   float hist[8];  // hist[d] = x at position p-1-d
   for (int d = 0; d < W - 1; ++d) {
     const int p = p0 - 1 - d;
-    hist[d] = p >= 0 ? io<T>::ld(x + (size_t)(t0 + p) * x_stride + c) : 0.f;
+    hist[d] = p >= 0 ? io<T>::ld(x + (size_t)(t0 + p) * x_stride + c) : before(p);
   }
   for (int p = p0; p < p1; ++p) {
     const float xv = io<T>::ld(x + (size_t)(t0 + p) * x_stride + c);
@@ -398,8 +406,9 @@ __global__ void conv_prefill_kernel(const T* __restrict__ x, int x_stride, T* __
     T* rrow = ring + ((size_t)slot * channels + c) * W;
     for (int d = 1; d < W; ++d) {
       const int p = L - d;
-      const float v = p >= 0 ? io<T>::ld(x + (size_t)(t0 + p) * x_stride + c) : 0.f;
-      io<T>::st(rrow + (((p % W) + W) % W), v);
+      const float v = p >= 0 ? io<T>::ld(x + (size_t)(t0 + p) * x_stride + c) : before(p);
+      const int P = pos0 + p;
+      io<T>::st(rrow + (((P % W) + W) % W), v);
     }
   }
 }
@@ -652,15 +661,17 @@ sn_status sn_kda_decode(const void* proj, int proj_stride, int proj_nsplit, void
 }
 
 sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv_w, void* conv_ring,
-                          const int32_t* cu_seqlens, const int32_t* slot_idx, int num_seqs, int rows,
-                          int channels, int width, int dtype, void* stream) {
+                          const void* ring_hist, const int32_t* cu_seqlens, const int32_t* slot_idx,
+                          const int32_t* pos0, int num_seqs, int rows, int channels, int width, int dtype,
+                          void* stream) {
+  SN_REQUIRE((pos0 == nullptr) == (ring_hist == nullptr), "sn_conv_prefill: pos0 and ring_hist go together");
   SN_REQUIRE(num_seqs > 0 && rows > 0 && channels > 0, "sn_conv_prefill: bad shape");
   SN_REQUIRE(width >= 1 && width <= 8, "sn_conv_prefill: width %d not in [1,8]", width);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(ceil_div(channels, 128), ceil_div(rows, 64), num_seqs);
     conv_prefill_kernel<T><<<grid, 128, 0, (cudaStream_t)stream>>>((const T*)x, x_stride, (T*)y, (const T*)conv_w,
-                                                                  (T*)conv_ring, cu_seqlens, slot_idx, channels,
-                                                                  width);
+                                                                  (T*)conv_ring, (const T*)ring_hist, cu_seqlens,
+                                                                  slot_idx, pos0, channels, width);
     return check_launch("sn_conv_prefill");
   });
 }

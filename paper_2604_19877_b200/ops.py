@@ -85,9 +85,11 @@ def attn_decode(q, k_cache, v_cache, block_table, seq_lens, out, workspace, coun
          _s())
 
 
-def attn_prefill(q, k, v, cu_seqlens, out, Hq, Hkv, D, window, scale):
-    call("sn_attn_prefill", _p(q), _p(k), _p(v), _p(cu_seqlens), _p(out), cu_seqlens.numel() - 1, q.shape[0], Hq, Hkv,
-         D, window, scale, dtype_code(q.dtype), _s())
+def attn_prefill(q, k, v, cu_seqlens, out, Hq, Hkv, D, window, scale, cu_k=None, q_off=None):
+    """Packed prefill attention; with cu_k / q_off the keys are a separate per-sequence packing
+    (continuation: cached prefix + new tokens), see include/sn_abi.h."""
+    call("sn_attn_prefill", _p(q), _p(k), _p(v), _p(cu_seqlens), _p(cu_k), _p(q_off), _p(out),
+         cu_seqlens.numel() - 1, q.shape[0], k.shape[0], Hq, Hkv, D, window, scale, dtype_code(q.dtype), _s())
 
 
 def gdn_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, norm_w, out, Hk, Hv, D, width,
@@ -109,9 +111,10 @@ def kda_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bi
          scale, eps_l2, eps_norm, dtype_code(out.dtype), _s())
 
 
-def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channels, width):
-    call("sn_conv_prefill", _p(x), x_stride, _p(y), _p(conv_w), _p(conv_ring), _p(cu_seqlens), _p(slot_idx),
-         cu_seqlens.numel() - 1, y.shape[0], channels, width, dtype_code(y.dtype), _s())
+def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channels, width, ring_hist=None,
+                 pos0=None):
+    call("sn_conv_prefill", _p(x), x_stride, _p(y), _p(conv_w), _p(conv_ring), _p(ring_hist), _p(cu_seqlens),
+         _p(slot_idx), _p(pos0), cu_seqlens.numel() - 1, y.shape[0], channels, width, dtype_code(y.dtype), _s())
 
 
 def delta_prep(kind, qkv_conv, proj, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, D, scale, eps_l2,

@@ -48,3 +48,40 @@ def test_attn_prefill_tc(D, window, lens):
     ref = reference(q, k, v, lens, window, scale).reshape(T, Hq * D)
     err = ((out.float().cpu() - ref).abs().max() / ref.abs().max()).item()
     assert err < TOL, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("D", [128, 64])
+@pytest.mark.parametrize("window", [0, 100])
+def test_attn_prefill_continuation(dtype, D, window):
+    """New tokens appended to live sequences: keys are each sequence's cached prefix (from the
+    first position the window can still see) plus the new tokens, packed by cu_k; the result
+    must equal rows P.. of a one-shot prefill of the whole sequence."""
+    from paper_2604_19877_b200 import ops
+    Hq, Hkv = 8, 2
+    prefix, new = [0, 150, 37], [70, 20, 130]
+    g = torch.Generator().manual_seed(D + window)
+    scale = 1.0 / math.sqrt(D)
+    qs, ks, vs, ref_rows, cu_q, cu_k, q_off = [], [], [], [], [0], [0], []
+    for P, N in zip(prefix, new):
+        q = torch.randn(P + N, Hq, D, generator=g).to(dtype)
+        k = torch.randn(P + N, Hkv, D, generator=g).to(dtype)
+        v = torch.randn(P + N, Hkv, D, generator=g).to(dtype)
+        ref_rows.append(reference(q, k, v, [P + N], window, scale)[P:])
+        k0 = max(0, P - window) if window else 0
+        qs.append(q[P:])
+        ks.append(k[k0:])
+        vs.append(v[k0:])
+        cu_q.append(cu_q[-1] + N)
+        cu_k.append(cu_k[-1] + P + N - k0)
+        q_off.append(P - k0)
+    q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
+    out = torch.empty(q.shape[0], Hq * D, dtype=dtype, device="cuda")
+    i32 = dict(dtype=torch.int32, device="cuda")
+    ops.attn_prefill(q.cuda(), k.cuda(), v.cuda(), torch.tensor(cu_q, **i32), out, Hq, Hkv, D, window, scale,
+                     cu_k=torch.tensor(cu_k, **i32), q_off=torch.tensor(q_off, **i32))
+    torch.cuda.synchronize()
+    ref = torch.cat(ref_rows).reshape(q.shape[0], Hq * D)
+    err = ((out.float().cpu() - ref).abs().max() / ref.abs().max()).item()
+    assert err < (TOL if dtype == torch.bfloat16 else 1e-4), err
