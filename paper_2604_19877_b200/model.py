@@ -420,14 +420,17 @@ class Supernet:
 
     # ------------------------------------------------------------------ prefill
     @torch.no_grad()
-    def prefill(self, tokens, return_all: bool = False, slots=None):
+    def prefill(self, tokens, return_all: bool = False, slots=None, append: bool = False):
         """Parallel prefill from an empty state.  tokens: [B, T] (equal-length prompts) or a list
         of 1-D prompts of any lengths (ragged: packed rows, cu_seqlens, every kernel masks or
         chunks per sequence).  slots: engine batch slots the prompts go to (continuous
         batching: only those slots are reset and prefilled — their KV pages, rings, conv tails
         and recurrent states are addressed through slot indices — while the other slots keep
-        decoding); default all B slots.  Returns the last position's logits [n, V], or with
-        return_all [n, T, V] (equal lengths) / a list of [T_b, V] (ragged)."""
+        decoding); default all B slots.  append: continue those sequences instead of starting
+        them (chunked prefill of long prompts, multi-turn): positions start at their current
+        lengths, attention also reads the cached prefix, the conv rings and recurrent states
+        carry over.  Returns the last position's logits [n, V], or with return_all [n, T, V]
+        (equal lengths) / a list of [T_b, V] (ragged)."""
         cfg, w, dev, dt = self.cfg, self.w, self.device, self.dtype
         ragged = isinstance(tokens, (list, tuple))
         if ragged:
@@ -447,8 +450,9 @@ class Supernet:
             slot_list = [int(x) for x in slots]
             if len(slot_list) != B or len(set(slot_list)) != B or not all(0 <= x < self.B for x in slot_list):
                 raise ValueError(f"slots {slot_list} must be {B} distinct indices in [0, {self.B})")
-        if min(lens) < 1 or max(lens) > self.max_len:
-            raise ValueError(f"prompt lengths must be in [1, max_len={self.max_len}], got {min(lens)}..{max(lens)}")
+        pos0 = [int(x) for x in self.seq_lens[slot_list].tolist()] if append else [0] * B
+        if min(lens) < 1 or max(p + L for p, L in zip(pos0, lens)) > self.max_len:
+            raise ValueError(f"prompt lengths must be >= 1 and fit max_len={self.max_len}")
         rows = sum(lens)
         i32 = dict(device=dev, dtype=torch.int32)
         cu_host = [0]
@@ -459,10 +463,15 @@ class Supernet:
         lens_t = torch.tensor(lens, **i32)
         slot_t = torch.tensor(slot_list, **i32)
         self._slot_idx = None if slots is None else slot_t  # identity mapping: kernels take NULL
+        pos0_t = torch.tensor(pos0, **i32)
+        self._append = (pos0, pos0_t) if append else None
         row_seq = torch.repeat_interleave(slot_t, lens_t)
-        row_pos = torch.arange(rows, **i32) - torch.repeat_interleave(cu[:-1], lens_t)
+        row_pos = (torch.arange(rows, **i32) - torch.repeat_interleave(cu[:-1], lens_t)
+                   + torch.repeat_interleave(pos0_t, lens_t))
         T = max(lens)
-        if slots is None:
+        if append:
+            self.seq_lens.index_copy_(0, slot_t.long(), pos0_t + lens_t)
+        elif slots is None:
             self.reset()
             self.seq_lens.copy_(lens_t)
         else:
@@ -526,11 +535,44 @@ class Supernet:
         q = torch.empty(rows, Hq, D, device=h.device, dtype=h.dtype)
         k = torch.empty(rows, Hkv, D, device=h.device, dtype=h.dtype)
         v = torch.empty_like(k)
+        cont = getattr(self, "_append", None)
+        if cont is not None:  # the cached prefix the new tokens can see, read before the append
+            prefix = self._gather_prefix(st, bt, window, cont[0])
         ops.rope_kv_append(qkv, row_seq, row_pos, self.seq_lens, self.inv_freq, q, k, v, st["k"], st["v"], bt, Hq,
                            Hkv, D, P, window)
         o = torch.empty(rows, Hq * D, device=h.device, dtype=h.dtype)
-        ops.attn_prefill(q, k, v, cu, o, Hq, Hkv, D, window, self.scale_attn)
+        if cont is None:
+            ops.attn_prefill(q, k, v, cu, o, Hq, Hkv, D, window, self.scale_attn)
+        else:  # keys per sequence: [cached prefix ; new tokens]
+            (pk, pv, k0), cu_host = prefix, self._cu_host
+            ks, vs, cu_k, q_off = [], [], [0], []
+            for b, (a, c) in enumerate(zip(cu_host[:-1], cu_host[1:])):
+                n_pre = cont[0][b] - k0[b]
+                ks += [pk[b], k[a:c]]
+                vs += [pv[b], v[a:c]]
+                cu_k.append(cu_k[-1] + n_pre + (c - a))
+                q_off.append(n_pre)
+            i32 = dict(device=h.device, dtype=torch.int32)
+            ops.attn_prefill(q, torch.cat(ks), torch.cat(vs), cu, o, Hq, Hkv, D, window, self.scale_attn,
+                             cu_k=torch.tensor(cu_k, **i32), q_off=torch.tensor(q_off, **i32))
         torch.mm(o, w["o"].t(), out=out)
+
+    def _gather_prefix(self, st, bt, window, pos0):
+        """K / V of the cached positions [k0, pos0) of each prefilled slot (k0 = 0 for FA, the
+        window start for SWA), from the page pool / ring, as contiguous [n, Hkv, D] tensors."""
+        P = self.cfg.page_size
+        slots = self._slot_idx.tolist() if self._slot_idx is not None else list(range(len(pos0)))
+        pk, pv, k0s = [], [], []
+        for slot, p0 in zip(slots, pos0):
+            k0 = max(0, p0 - window + 1) if window else 0
+            pos = torch.arange(k0, p0, device=self.device)
+            ring = pos % window if window else pos
+            pages = bt[slot][(ring // P).long()].long()
+            offs = (ring % P).long()
+            pk.append(st["k"][pages, :, offs])
+            pv.append(st["v"][pages, :, offs])
+            k0s.append(k0)
+        return pk, pv, k0s
 
     def _delta_prefill(self, kind, l, h, out, cu):
         cfg, st, w = self.cfg, self.state[l], self.w["layers"][l]["mixer"]
@@ -553,7 +595,13 @@ class Supernet:
             gate = (proj[:, g1_off:g1_off + R] @ w["g2"].t() + w["g2_b"]).contiguous()
             gate_stride = gate.stride(0)
         y = torch.empty(rows, C, device=dev, dtype=h.dtype)
-        ops.conv_prefill(proj, proj.stride(0), y, w["conv_w"], st["conv"], cu, self._slot_idx, C, cfg.conv_width)
+        cont = getattr(self, "_append", None)
+        hist = None
+        if cont is not None:  # inputs before the first new token come from a snapshot of the rings
+            sl = self._slot_idx.long() if self._slot_idx is not None else torch.arange(len(cont[0]), device=dev)
+            hist = st["conv"][sl].contiguous()
+        ops.conv_prefill(proj, proj.stride(0), y, w["conv_w"], st["conv"], cu, self._slot_idx, C, cfg.conv_width,
+                         ring_hist=hist, pos0=None if cont is None else cont[1])
         f32 = dict(device=dev, dtype=torch.float32)
         qn, kn = torch.empty(rows, Hk, D, **f32), torch.empty(rows, Hk, D, **f32)
         gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
@@ -570,7 +618,7 @@ class Supernet:
             self._chunked_delta(kind, qn, kn, y, 2 * Hk * D, glog, beta, o, st["S"], cu, Hk, Hv, D)
         else:
             ops.delta_scan(k_code, qn, kn, y, 2 * Hk * D, gexp, beta, o, st["S"], self._slot_idx, cu, Hk, Hv, D,
-                           init_state=False)
+                           init_state=cont is not None)
         y_out = torch.empty(rows, Hv * D, device=dev, dtype=h.dtype)
         ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
         torch.mm(y_out, w["o"].t(), out=out)
@@ -601,14 +649,15 @@ class Supernet:
             ws = getattr(self, "_chunk_ws", None)
             # states by slot (continuous batching) or, for a full batch, the slice in prompt order
             S_g, sl = (S[b0:b1], None) if slot_idx is None else (S, slot_idx[b0:b1])
+            init = getattr(self, "_append", None) is not None  # continuation: start from the live state
             if kind == KDA:
                 self._chunk_ws = ops.kda_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
                                                         beta[r0:r1], chunks, c0, o[r0:r1], S_g, sl, Hv, D,
-                                                        init_state=False, workspace=ws)
+                                                        init_state=init, workspace=ws)
             else:
                 self._chunk_ws = ops.gdn_chunk_prefill2(qn[r0:r1], kn[r0:r1], y[r0:r1], v_off, glog[r0:r1],
                                                         beta[r0:r1], chunks, c0, o[r0:r1], S_g, sl, Hk, Hv,
-                                                        D, init_state=False, workspace=ws)
+                                                        D, init_state=init, workspace=ws)
             b0 = b1
 
     def _gdn_prefill(self, l, h, out, cu):

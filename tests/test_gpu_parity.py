@@ -167,3 +167,36 @@ def test_continuous_batching_slot_prefill(placement):
         ref = OracleSupernet(TINY, kinds, w, batch=1, max_len=L + n).run(toks[s][None, :L + n])[0]
         want = ref[L - 1:L + n]
         assert rel_err(torch.stack(got[s]), want) <= TOL[torch.bfloat16], (s, rel_err(torch.stack(got[s]), want))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("placement", ["ASKG", "GKSA"])
+def test_chunked_prompt_append_matches_oracle(placement):
+    """A prompt prefilled in pieces (append=True: positions continue, attention reads the
+    cached prefix — FA pages and the SWA ring, window 128 smaller than the prompt — conv rings
+    and recurrent states carry over) and then decoded matches the oracle on the whole stream."""
+    from paper_2604_19877_b200.model import Supernet
+    kinds = layer_kinds(placement)
+    w = cast_weights(init_weights(TINY, kinds, seed=0), "cpu", torch.bfloat16)
+    g = torch.Generator().manual_seed(21)
+    total, steps = [230, 150], 3
+    pieces = [[64, 100, 66], [1, 129, 20]]
+    seqs = [torch.randint(0, TINY.vocab, (T + steps,), generator=g) for T in total]
+    model = Supernet(TINY, placement, batch=2, max_len=max(total) + steps, dtype=torch.bfloat16, weights=w)
+    got = [[], []]
+    for i in range(3):
+        a = [sum(p[:i]) for p in pieces]
+        chunk = [s[a[b]:a[b] + pieces[b][i]] for b, s in enumerate(seqs)]
+        lg = model.prefill(chunk, return_all=True, append=i > 0)
+        for b in range(2):
+            got[b].append(lg[b].float().cpu())
+    for t in range(steps):
+        lg = model.decode(torch.tensor([int(s[T + t]) for s, T in zip(seqs, total)], dtype=torch.int32))
+        for b in range(2):
+            got[b].append(lg[b].float().cpu()[None])
+    torch.cuda.synchronize()
+    for b, (s, T) in enumerate(zip(seqs, total)):
+        ref = OracleSupernet(TINY, kinds, w, batch=1, max_len=T + steps).run(s[None])[0]
+        out = torch.cat(got[b])
+        assert out.shape[0] == T + steps
+        assert rel_err(out, ref) <= TOL[torch.bfloat16], (b, rel_err(out, ref))
