@@ -85,3 +85,30 @@ def test_speculative_traces_match_oracle_logprobs():
     # draft == target: every ratio is 1, so every drafted token is accepted
     same = acceptance_traces(store, "AAAA", "AAAA", prompts, completion_len=8)
     assert all(r["log_q"] == r["log_p"] for r in same)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("target,draft", [("AAAA", "GGGG"), ("AKGA", "GGGG")])
+def test_speculative_decoding_is_lossless(target, draft):
+    """Self-speculative decoding (draft proposals verified by one append prefill of the target)
+    emits exactly the target's own greedy decode (fp32 parity mode, so decode and prefill
+    arithmetic agree to 1e-4 and argmax ties cannot flip)."""
+    from paper_2604_19877_b200.model import Supernet
+    from paper_2604_19877_b200.serving import SupernetStore
+    from paper_2604_19877_b200.speculative import speculative_generate
+    store = SupernetStore(TINY, seed=0, dtype=torch.float32, init_device="cpu")
+    prompt = torch.randint(0, TINY.vocab, (50,), generator=torch.Generator().manual_seed(8))
+    n = 24
+    spec, accepted = speculative_generate(store, draft, target, prompt, n, gamma=4)
+    ref_model = Supernet(TINY, target, batch=1, max_len=50 + n + 8, dtype=torch.float32,
+                         weights=store.weights(target))
+    t = int(torch.argmax(ref_model.prefill(prompt[None]).float(), dim=-1)[0])
+    ref = []
+    for _ in range(n):
+        ref.append(t)
+        t = int(torch.argmax(ref_model.decode(torch.tensor([t], dtype=torch.int32)).float(), dim=-1)[0])
+    assert spec.tolist() == ref
+    assert len(accepted) >= 1 and all(0 <= a <= 4 for a in accepted)
+    # the same draft as target accepts everything
+    same, acc_same = speculative_generate(store, target, target, prompt, 12, gamma=4)
+    assert all(a == 4 for a in acc_same[:-1])
