@@ -865,6 +865,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 }
 
+// The state pass is sequential over chunks: with few (sequence, head) pairs the value tiles get
+// narrower (64 -> 32 columns) so that more CTAs run their chains side by side.  (16 columns
+// measured slower: every CTA still streams the full W / Qg / Kd tiles of each chunk.)
+template <int D, bool PERCH>
+static void launch_state_pass(const __nv_bfloat16* ws, const float* glast, const int32_t* chunks,
+                              const int32_t* seq_chunk0, float* o, float* state, const int32_t* slot_idx,
+                              int num_seqs, int H, int init_state, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, PERCH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StateSmem<D, 64>));
+    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, PERCH, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StateSmem<D, 32>));
+    attr = true;
+  }
+  int vt = 64;
+  if (num_seqs * H * (D / 64) < 148) vt = 32;
+  if (vt == 64)
+    gdn_chunk_state_kernel<D, PERCH, 64><<<dim3(D / 64, H, num_seqs), kThreads, sizeof(StateSmem<D, 64>), st>>>(
+        ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
+  else
+    gdn_chunk_state_kernel<D, PERCH, 32><<<dim3(D / 32, H, num_seqs), kThreads, sizeof(StateSmem<D, 32>), st>>>(
+        ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
+}
+
 template <typename T, int D>
 static sn_status launch_two_phase(const float* qn, const float* kn, const void* qkv, int v_off, int qkv_stride,
                                   const float* glog, const float* beta, const int32_t* chunks,
@@ -875,24 +900,14 @@ static sn_status launch_two_phase(const float* qn, const float* kn, const void* 
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gdn_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
-    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StateSmem<D, 64>));
-    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StateSmem<D, 32>));
     attr = true;
   }
   gdn_chunk_intra_kernel<T, D><<<dim3(num_chunks, Hv), kThreads, smem_a, st>>>(
       qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, Hk, Hv);
   sn_status e = check_launch("sn_gdn_chunk_prefill(intra)");
   if (e != SN_OK) return e;
-  // the state pass is sequential over chunks: few (sequence, head) pairs -> narrower value
-  // tiles so more CTAs run the chain side by side
-  if (num_seqs * Hv * (D / 64) < 148)
-    gdn_chunk_state_kernel<D, false, 32><<<dim3(D / 32, Hv, num_seqs), kThreads, sizeof(StateSmem<D, 32>), st>>>(
-        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, Hv, init_state);
-  else
-    gdn_chunk_state_kernel<D, false, 64><<<dim3(D / 64, Hv, num_seqs), kThreads, sizeof(StateSmem<D, 64>), st>>>(
-        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, Hv, init_state);
+  launch_state_pass<D, false>((const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, num_seqs, Hv,
+                              init_state, st);
   return check_launch("sn_gdn_chunk_prefill(state)");
 }
 
@@ -1149,22 +1164,14 @@ static sn_status launch_kda_two_phase(const float* qn, const float* kn, const vo
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kda_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
-    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StateSmem<D, 64>));
-    cudaFuncSetAttribute(gdn_chunk_state_kernel<D, true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StateSmem<D, 32>));
     attr = true;
   }
   kda_chunk_intra_kernel<T, D><<<dim3(num_chunks, H), kThreads, smem_a, st>>>(
       qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, H);
   sn_status e = check_launch("sn_kda_chunk_prefill(intra)");
   if (e != SN_OK) return e;
-  if (num_seqs * H * (D / 64) < 148)
-    gdn_chunk_state_kernel<D, true, 32><<<dim3(D / 32, H, num_seqs), kThreads, sizeof(StateSmem<D, 32>), st>>>(
-        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
-  else
-    gdn_chunk_state_kernel<D, true, 64><<<dim3(D / 64, H, num_seqs), kThreads, sizeof(StateSmem<D, 64>), st>>>(
-        (const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
+  launch_state_pass<D, true>((const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, num_seqs, H,
+                             init_state, st);
   return check_launch("sn_kda_chunk_prefill(state)");
 }
 
