@@ -43,7 +43,17 @@ def gemm_noop_roles(roles):
     return f
 
 
+def gemm_skip_if(pred):
+    def f(x, w, out, mode="store"):
+        if pred(x, w, mode):
+            return ops.gemm_decode_splits(x.shape[0], out.shape[-1], x.shape[1], "partial") if mode == "partial" else None
+        return _gemm(x, w, out, mode)
+    return f
+
+
 ABL = {
+    "ffn_down": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, m: m == "partial" and x.shape[1] == APRIEL.ffn))],
+    "ffn_gate_up": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, m: m == "swiglu_il"))],
     "norm": [(ops, "add_rmsnorm", noop)],
     "rope": [(ops, "rope_kv_append", noop)],
     "gdn": [(ops, "gdn_decode", noop)],
