@@ -79,6 +79,15 @@ def test_baseline_configs_1_2(placement, dtype):
 
 
 @pytest.mark.gpu
+def test_large_batch_graph_decode():
+    """B=96 (> 64: the decode GEMMs switch to the 128-row batch tile, the attention / delta
+    kernels get more CTAs than SMs) through prefill and graphed decode."""
+    model, oracle, got, ref = run_pair("ASKG", torch.bfloat16, B=96, T_prefill=48, n_decode=6, graph=True)
+    assert rel_err(got, ref) <= TOL[torch.bfloat16]
+    check_states(model, oracle, TOL[torch.bfloat16])
+
+
+@pytest.mark.gpu
 def test_simt_attention_path_matches_oracle():
     """The CUDA-core decode attention (bf16 cross-check path) is also within tolerance."""
     model, oracle, got, ref = run_pair("ASAS", torch.bfloat16, B=2, T_prefill=150, n_decode=20, force_simt=True)
