@@ -16,17 +16,14 @@ namespace sn {
 // (rotate, write q_out), the next Hkv are key heads (rotate, append to the cache),
 // the last Hkv are value heads (copy to the cache).  Thread i owns rotary pair i.
 template <typename T>
-__global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __restrict__ row_seq,
-                                      const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
-                                      const float* __restrict__ inv_freq, T* __restrict__ q_out,
-                                      T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
-                                      T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
-                                      int Hkv, int D, int page_size, int max_blocks, int window) {
-  sn::pdl_launch_dependents();
-  sn::pdl_wait();
-  const int r = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
+__device__ __forceinline__ void rope_kv_one(const GemmIn<T>& qkv, const int32_t* __restrict__ row_seq,
+                                            const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
+                                            const float* __restrict__ inv_freq, T* __restrict__ q_out,
+                                            T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
+                                            T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
+                                            int Hkv, int D, int page_size, int max_blocks, int window, int r,
+                                            int head, int i) {
   const int half = D / 2;
-  if (i >= half) return;
   const int seq = row_seq ? row_seq[r] : r;
   const int pos = row_pos[r];
   const size_t src = (size_t)r * (Hq + 2 * Hkv) * D + (size_t)head * D;
@@ -71,6 +68,36 @@ __global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __rest
     io<T>::st(dst + i, y1);
     io<T>::st(dst + i + half, y2);
   }
+}
+
+// Decode: a CTA per (row, head), a thread per rotation pair.
+template <typename T>
+__global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __restrict__ row_seq,
+                                      const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
+                                      const float* __restrict__ inv_freq, T* __restrict__ q_out,
+                                      T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
+                                      T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
+                                      int Hkv, int D, int page_size, int max_blocks, int window) {
+  sn::pdl_launch_dependents();
+  sn::pdl_wait();
+  if ((int)threadIdx.x >= D / 2) return;
+  rope_kv_one<T>(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table, Hq,
+                 Hkv, D, page_size, max_blocks, window, blockIdx.x, blockIdx.y, threadIdx.x);
+}
+
+// Prefill (many rows): a 256-thread CTA per row loops over every (head, pair) of the row.
+template <typename T>
+__global__ void __launch_bounds__(256) rope_kv_append_rows_kernel(
+    const GemmIn<T> qkv, const int32_t* __restrict__ row_seq, const int32_t* __restrict__ row_pos,
+    const int32_t* __restrict__ seq_lens, const float* __restrict__ inv_freq, T* __restrict__ q_out,
+    T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache, T* __restrict__ v_cache,
+    const int32_t* __restrict__ block_table, int Hq, int Hkv, int D, int page_size, int max_blocks, int window) {
+  sn::pdl_launch_dependents();
+  sn::pdl_wait();
+  const int half = D / 2, n = (Hq + 2 * Hkv) * half;
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x)
+    rope_kv_one<T>(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,
+                   Hq, Hkv, D, page_size, max_blocks, window, blockIdx.x, idx / half, idx % half);
 }
 
 // ------------------------------------------------------------------ CUDA-core decode
@@ -250,11 +277,15 @@ sn_status sn_rope_kv_append(const void* qkv, int qkv_nsplit, const int32_t* row_
   SN_REQUIRE(qkv && row_pos && inv_freq && q_out && k_cache && v_cache && block_table,
              "sn_rope_kv_append: NULL pointer argument");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    dim3 grid(rows, Hq + 2 * Hkv);
     const GemmIn<T> in{qkv, qkv_nsplit, (size_t)rows * (Hq + 2 * Hkv) * D};
-    launch_pdl(rope_kv_append_kernel<T>, grid, dim3(((D / 2 + 31) / 32) * 32), 0, (cudaStream_t)stream,
-        in, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache,
-        (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
+    if (rows > 1024)
+      launch_pdl(rope_kv_append_rows_kernel<T>, dim3(rows), dim3(256), 0, (cudaStream_t)stream, in, row_seq,
+                 row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache, (T*)v_cache,
+                 block_table, Hq, Hkv, D, page_size, max_blocks, window);
+    else
+      launch_pdl(rope_kv_append_kernel<T>, dim3(rows, Hq + 2 * Hkv), dim3(((D / 2 + 31) / 32) * 32), 0,
+                 (cudaStream_t)stream, in, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out,
+                 (T*)k_cache, (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
     return check_launch("sn_rope_kv_append");
   });
 }
