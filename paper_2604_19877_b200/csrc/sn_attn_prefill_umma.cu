@@ -2,18 +2,20 @@
 // Same contract as the mma.sync kernel in sn_attn_prefill.cu (packed ragged sequences,
 // causal or window mask per (row, key) with each row's own sequence start, GQA).
 //
-// CTA = 128 query rows x one q head; 11 warps:
-//   warps 9 / 10 (one lane each): TMA producers — Q once and K blocks of 128 keys / V blocks,
+// CTA = 128 query rows x one q head; 4*NS softmax warps + 3 (NS = 2: 11 warps):
+//   warps 4NS+1 / 4NS+2 (one lane each): TMA producers — Q once and K blocks of 128 keys / V blocks,
 //           each into its own two-stage ring (128B-swizzled 2-D boxes straight from the
 //           [rows][H*D] tensors), so the next K block only waits for its S product;
-//   warp 8 (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
+//   warp 4NS (one lane): MMA issuer — S = Q K^T (UMMA M=128, N=128, K=128; both operands
 //           K-major) into one of two TMEM score buffers, then O += P V (A = P from shared
 //           memory, B = V read MN-major: the [key][d] tile is used as is) into TMEM;
-//   warps 0-7: softmax — warps w and w+4 share query rows 32(w%4).. (TMEM lanes), one half
-//           of the 128 key columns each: tcgen05.ld of the S half-row, mask / scale / max /
-//           exp2 in registers, the row max combined through shared memory (64-thread named
-//           barrier), O half-row rescaled in TMEM when the max moved (tcgen05.ld/st), the
-//           P half-row written (bf16, 128B swizzle) for the PV MMA; finally O / l to global.
+//   warps 0..4NS-1: softmax — warps w, w+4, .. share query rows 32(w%4).. (TMEM lanes), each
+//           taking 128/NS of the key columns: tcgen05.ld of its S slice, mask / scale / max /
+//           exp2 in registers, the row max combined through a shared-memory atomic max
+//           (one 32NS-thread named barrier per lane quadrant), its O slice rescaled in TMEM
+//           when the max moved (tcgen05.ld/st), its P slice written (bf16, 128B swizzle) for
+//           the PV MMA; finally O / l to global.  More, narrower softmax warps hide the
+//           latency of each warp's dependent max / exp chain (the softmax is the limiter).
 // The scores of block j+1 are computed while the softmax of block j runs (two TMEM score
 // buffers); PV(j) follows as soon as P(j) is in shared memory.
 #include "sn_tc.cuh"
@@ -24,7 +26,9 @@ namespace fa5 {
 using namespace sn::tc;
 
 constexpr int BM = 128, BN = 128, HD = 128;
-constexpr int kThreads = 352;  // 8 softmax warps, MMA warp, K/Q TMA warp, V TMA warp
+template <int NS>
+constexpr int threads_for() { return NS * 128 + 96; }  // softmax warps, MMA warp, K/Q TMA warp, V TMA warp
+constexpr float kLazy = 8.f;  // log2 headroom of the stale running max
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
 constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
 
@@ -37,7 +41,8 @@ struct Smem {         // 224 KB, 1024-byte aligned
 struct Sync {          // in front of the tiles, inside the dynamic allocation
   uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full, o_done[2];
   uint32_t tmem_base;
-  float red[2][2][BM];  // [iteration parity][column half][row]
+  float red[3][BM];  // row max of iteration j in red[j % 3] (float atomic max over the slices)
+  float lsum[BM];    // final row sums
 };
 constexpr int kSyncBytes = 3072;
 constexpr int kSmemBytes = 227 * 1024;
@@ -87,7 +92,7 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, -inf -> 0
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split x = n + f, f in [-0.5, 0.5],
+// 2^x on the FMA/ALU pipes (x <= 8): round-to-nearest split x = n + f, f in [-0.5, 0.5],
 // cubic in f, n added to the exponent.  Relative error < 7e-4 (P is stored as bf16,
 // 3.9e-3).  Part of the exponentials go this way (exp2_fma2, on pairs) so MUFU.EX2 (16 / clock / SM) is not the
 // limiter of the softmax (FA4's split).
@@ -121,11 +126,16 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
   const int nx = __float_as_int(t.x) - 0x4B400000, ny = __float_as_int(t.y) - 0x4B400000;
   return make_float2(__int_as_float(__float_as_int(p.x) + (nx << 23)), __int_as_float(__float_as_int(p.y) + (ny << 23)));
 }
+__device__ __forceinline__ void smem_max_f32(float* addr, float v) {  // order-preserving int encoding
+  if (v >= 0.f) atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+  else atomicMin(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NS>
+__global__ void __launch_bounds__(threads_for<NS>(), 1)
     attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
@@ -141,7 +151,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *v_empty = sy.v_empty, *s_full = sy.s_full;
   uint64_t &p_full = sy.p_full, *o_done = sy.o_done;
   uint32_t& tmem_base_s = sy.tmem_base;
-  auto& red_max = sy.red;
+  constexpr int SW = 4 * NS;       // softmax warps
+  constexpr int COLS = BN / NS;    // key columns (and head-dim columns of O) per softmax warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = (rows + BM - 1) / BM;
   const int r0 = (tiles - 1 - (int)blockIdx.x) * BM;  // heavy (late) tiles first
@@ -159,8 +170,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    mbar_init(&p_full, 256);
+    mbar_init(&p_full, SW * 32);
     for (int i = 0; i < 2; ++i) mbar_init(&o_done[i], 1);
+  }
+  if (threadIdx.x < BM) {
+    for (int i = 0; i < 3; ++i) sy.red[i][threadIdx.x] = -INFINITY;
+    sy.lsum[threadIdx.x] = 0.f;
+  }
+  if (threadIdx.x == 0) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -173,11 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;  // S double buffer: columns [0,128) and [128,256); O: [256,384)
 
-  if (warp >= 9) {
+  if (warp > SW) {
     // ---------------- TMA producers: warp 9 loads Q and the K ring, warp 10 the V ring.  K and
     // V have their own stages: K(j+2) only waits for S(j), V(j+2) for PV(j).
     if (lane == 0) {
-      const bool is_k = warp == 9;
+      const bool is_k = warp == SW + 1;
       const CUtensorMap* map = is_k ? &kmap : &vmap;
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
       const uint64_t keep = policy_evict_last();  // K/V blocks are re-read by the other q heads of the group
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(dst + ATOM, map, hk * HD + 64, jb, &full[st], keep);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == SW) {
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t id_s = idesc_bf16(BM, BN);
       const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
@@ -243,42 +260,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- softmax: warps w and w+4 share TMEM lanes 32(w%4).. (query rows), each
-    // taking one half of the 128 key columns (and of the head dim for O); the row max is
-    // combined through shared memory with a 64-thread named barrier per warp pair.
-    const int sub = warp & 3, half = warp >> 2;
+    // ---------------- softmax: warps w, w+4, .. share TMEM lanes 32(w%4).. (query rows), each
+    // taking COLS of the 128 key columns (and of the head dim for O).
+    const int sub = warp & 3, part = warp >> 2;
     const int t = sub * 32 + lane;
     const int r = r0 + t;
     const KeyBounds kbr = key_bounds(cu, cu_k, q_off, num_seqs, min(r, rows - 1), window);
     const int lo = kbr.lo, hi = kbr.hi;
     const float qs = scale * 1.4426950408889634f;
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + half * 64, o_addr = tmem + 256 + lane_addr + half * 64;
-    uint8_t* prow0 = sm.p[0] + half * ATOM + t * 128;
+    const uint32_t s_addr = tmem + lane_addr + part * COLS, o_addr = tmem + 256 + lane_addr + part * COLS;
+    // P slice: keys part*COLS.. live in atom (part*COLS)/64, 16-byte chunks from ((part*COLS)%64)/8
+    uint8_t* prow0 = sm.p[0] + ((part * COLS) >> 6) * ATOM + t * 128;
+    const int chunk0 = ((part * COLS) & 63) >> 3;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int jb = j_lo + j * BN;
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      float s[64];
-      tmem_ld32(s_addr + (j & 1) * 128, s);
-      tmem_ld32(s_addr + (j & 1) * 128 + 32, s + 32);
+      float s[COLS];
+#pragma unroll
+      for (int c = 0; c < COLS; c += 32) tmem_ld32(s_addr + (j & 1) * 128 + c, s + c);
       tmem_wait_ld();
       const bool full = jb >= kbl.lo && jb + BN - 1 <= kb0.hi;
       float mx = -INFINITY;
       if (!full) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const int jj = jb + half * 64 + i;
+        for (int i = 0; i < COLS; ++i) {
+          const int jj = jb + part * COLS + i;
           if (jj > hi || jj < lo) s[i] = -INFINITY;
         }
       }
 #pragma unroll
-      for (int i = 0; i < 64; ++i) mx = fmaxf(mx, s[i]);
-      red_max[j & 1][half][t] = mx;
-      named_bar(1 + sub, 64);
-      mx = fmaxf(mx, red_max[j & 1][half ^ 1][t]) * qs;  // scores stay unscaled; the max is scaled
-      const float mn = fmaxf(m, mx);
+      for (int i = 0; i < COLS; ++i) mx = fmaxf(mx, s[i]);
+      // Row max over the slices: red[j % 3] was reset (to -inf) by slice 0 in iteration j-2,
+      // after every slice had read it in iteration j-3 (the barrier of j-2 orders both).
+      float* red = sy.red[j % 3];
+      smem_max_f32(red + t, mx);
+      named_bar(1 + sub, NS * 32);
+      mx = red[t] * qs;  // scores stay unscaled; the max is scaled
+      if (part == 0) sy.red[(j + 2) % 3][t] = -INFINITY;
+      // Lazy rescaling (FA4): the running max only moves when the block max exceeds it by more
+      // than 2^8, so P = 2^(s - m) <= 256 (exact after the final 1/l) and O is rarely rescaled —
+      // each rescale must wait for PV(j-1), which serialises the softmax behind the tensor core.
+      const float mn = mx > m + kLazy ? mx : m;
       const float base_m = mn == -INFINITY ? 0.f : mn;
       const float alpha = ex2(m - base_m);
       // P(j) goes to buffer j&1, last read by PV(j-2) — complete, since S(j) was committed after
@@ -288,23 +313,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
         mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        {
 #pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
-            float o[32];
-            tmem_ld32(o_addr + c * 32, o);
-            tmem_wait_ld();
+        for (int c = 0; c < COLS; c += 32) {
+          float o[32];
+          tmem_ld32(o_addr + c, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            tmem_st32(o_addr + c * 32, o);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          for (int e = 0; e < 32; ++e) o[e] *= alpha;
+          tmem_st32(o_addr + c, o);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       float2 rs2 = make_float2(0.f, 0.f);
       const float2 qs2 = make_float2(qs, qs), nb2 = make_float2(-base_m, -base_m);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < COLS / 8; ++c) {
         float2 p[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -318,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk.y = pack_bf16(p[1].x, p[1].y);
         pk.z = pack_bf16(p[2].x, p[2].y);
         pk.w = pack_bf16(p[3].x, p[3].y);
-        *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + ((c ^ (t & 7)) << 4)) = pk;
+        *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + (((chunk0 + c) ^ (t & 7)) << 4)) = pk;
       }
       const float rs = rs2.x + rs2.y;
       l = l * alpha + rs;
@@ -327,17 +350,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&p_full);
     }
-    red_max[0][half][t] = l;  // row sum: the two halves' partial sums
-    named_bar(1 + sub, 64);
-    l += red_max[0][half ^ 1][t];
+    atomicAdd(&sy.lsum[t], l);  // row sum: the slices' partial sums
+    named_bar(1 + sub, NS * 32);
+    l = sy.lsum[t];
     mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD + half * 64;
+    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD + part * COLS;
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < COLS; c += 32) {
       float o[32];
-      tmem_ld32(o_addr + c * 32, o);
+      tmem_ld32(o_addr + c, o);
       tmem_wait_ld();
       if (r < rows) {
 #pragma unroll
@@ -347,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk.y = pack_bf16(o[e + 2] * inv, o[e + 3] * inv);
           pk.z = pack_bf16(o[e + 4] * inv, o[e + 5] * inv);
           pk.w = pack_bf16(o[e + 6] * inv, o[e + 7] * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + e) = pk;
+          *reinterpret_cast<uint4*>(orow + c + e) = pk;
         }
       }
     }
@@ -374,14 +397,25 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     return SN_ECUDA;
   }
   const int smem = kSmemBytes;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_prefill_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+  static int ns = 0;
+  if (!ns) {
+    // softmax slices per row: 2 (8 softmax warps) by default; 4 (16 warps) measured no faster
+    // (1025 vs 1044 TFLOP/s causal at 16K) — the per-block chain is the MMA issue order, not
+    // softmax latency.  SN_FA5_SLICES=4 is the A/B switch.
+    const char* e = getenv("SN_FA5_SLICES");
+    ns = e && atoi(e) == 4 ? 4 : 2;
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
-  attn_prefill_umma_kernel<<<grid, kThreads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq,
-                                                         Hkv, window, scale, cu_k, q_off, g_fa5_dbg);
+  if (ns == 2)
+    attn_prefill_umma_kernel<2><<<grid, threads_for<2>(), smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs,
+                                                                       rows, Hq, Hkv, window, scale, cu_k, q_off,
+                                                                       g_fa5_dbg);
+  else
+    attn_prefill_umma_kernel<4><<<grid, threads_for<4>(), smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs,
+                                                                       rows, Hq, Hkv, window, scale, cu_k, q_off,
+                                                                       g_fa5_dbg);
   return check_launch("sn_attn_prefill(umma)");
 }
 

@@ -85,3 +85,25 @@ def test_attn_prefill_continuation(dtype, D, window):
     ref = torch.cat(ref_rows).reshape(q.shape[0], Hq * D)
     err = ((out.float().cpu() - ref).abs().max() / ref.abs().max()).item()
     assert err < (TOL if dtype == torch.bfloat16 else 1e-4), err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window", [0, 300])
+def test_attn_prefill_rising_scores(window):
+    """Key norms growing along the sequence: the running row max keeps moving by more than
+    the lazy-rescale headroom (2^8), so O is rescaled many times (and sometimes not)."""
+    from paper_2604_19877_b200 import ops
+    Hq, Hkv, D, T = 8, 2, 128, 1100
+    g = torch.Generator().manual_seed(7 + window)
+    ramp = torch.linspace(0.1, 8.0, T)[:, None, None]
+    q = torch.randn(T, Hq, D, generator=g).to(torch.bfloat16)
+    k = (torch.randn(T, Hkv, D, generator=g) * ramp).to(torch.bfloat16)
+    v = torch.randn(T, Hkv, D, generator=g).to(torch.bfloat16)
+    cu = torch.tensor([0, T], dtype=torch.int32)
+    scale = 1.0 / math.sqrt(D)
+    out = torch.empty(T, Hq * D, dtype=torch.bfloat16, device="cuda")
+    ops.attn_prefill(q.cuda(), k.cuda(), v.cuda(), cu.cuda(), out, Hq, Hkv, D, window, scale)
+    torch.cuda.synchronize()
+    ref = reference(q, k, v, [T], window, scale).reshape(T, Hq * D)
+    err = ((out.float().cpu() - ref).abs().max() / ref.abs().max()).item()
+    assert err < TOL, err
