@@ -39,7 +39,7 @@ struct Smem {         // 224 KB, 1024-byte aligned
   uint8_t p[2][TILE];  // double-buffered: softmax(j+1) writes while PV(j) reads
 };
 struct Sync {          // in front of the tiles, inside the dynamic allocation
-  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full, o_done[2];
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_done[2];
   uint32_t tmem_base;
   float red[3][BM];  // row max of iteration j in red[j % 3] (float atomic max over the slices)
   float lsum[BM];    // final row sums
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
                              float scale, const int32_t* __restrict__ cu_k, const int32_t* __restrict__ q_off,
-                             unsigned long long* __restrict__ dbg) {
+                             unsigned long long* __restrict__ dbg, int skip_softmax) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Sync& sy = *reinterpret_cast<Sync*>(smem_raw);
   uint8_t* base = smem_raw + kSyncBytes;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
   Smem& sm = *reinterpret_cast<Smem*>(base);
   uint64_t &q_full = sy.q_full, *k_full = sy.k_full, *k_empty = sy.k_empty, *v_full = sy.v_full;
   uint64_t *v_empty = sy.v_empty, *s_full = sy.s_full;
-  uint64_t &p_full = sy.p_full, *o_done = sy.o_done;
+  uint64_t *p_full = sy.p_full, *o_done = sy.o_done;
   uint32_t& tmem_base_s = sy.tmem_base;
   constexpr int SW = 4 * NS;       // softmax warps
   constexpr int COLS = BN / NS;    // key columns (and head-dim columns of O) per softmax warp
@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    mbar_init(&p_full, SW * 32);
+    // P(j) completes p_full[j & 1]: the softmax can run at most one block ahead of the MMA
+    // issuer's wait (S(j+2) is issued after P(j) was consumed), so the phase parity is exact
+    for (int i = 0; i < 2; ++i) mbar_init(&p_full[i], SW * 32);
     for (int i = 0; i < 2; ++i) mbar_init(&o_done[i], 1);
   }
   if (threadIdx.x < BM) {
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         if (j + 1 < nblk) issue_s(j + 1);  // its S buffer was read by softmax(j-1) (P(j-1) waited below)
         stamp(j, 1);
         mbar_wait(&v_full[st], (j >> 1) & 1);
-        mbar_wait(&p_full, j & 1);
+        mbar_wait(&p_full[st], (j >> 1) & 1);
         stamp(j, 2);
         tc_fence_after();
         const uint32_t sv = smem_u32(sm.v[st]), sp = smem_u32(sm.p[st]);
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
                (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(&o_done[st]);
         umma_commit(&v_empty[st]);
+        stamp(j, 3);
       }
     }
   } else {
@@ -278,6 +281,11 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       const int jb = j_lo + j * BN;
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
+      if (skip_softmax) {  // experiment: the MMA / TMA pipeline alone (results wrong)
+        tc_fence_before();
+        mbar_arrive(&p_full[j & 1]);
+        continue;
+      }
       float s[COLS];
 #pragma unroll
       for (int c = 0; c < COLS; c += 32) tmem_ld32(s_addr + (j & 1) * 128 + c, s + c);
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       m = mn;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       tc_fence_before();
-      mbar_arrive(&p_full);
+      mbar_arrive(&p_full[j & 1]);
     }
     atomicAdd(&sy.lsum[t], l);  // row sum: the slices' partial sums
     named_bar(1 + sub, NS * 32);
@@ -397,13 +405,15 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     return SN_ECUDA;
   }
   const int smem = kSmemBytes;
-  static int ns = 0;
+  static int ns = 0, skip = 0;
   if (!ns) {
     // softmax slices per row: 2 (8 softmax warps) by default; 4 (16 warps) measured no faster
     // (1025 vs 1044 TFLOP/s causal at 16K) — the per-block chain is the MMA issue order, not
     // softmax latency.  SN_FA5_SLICES=4 is the A/B switch.
     const char* e = getenv("SN_FA5_SLICES");
     ns = e && atoi(e) == 4 ? 4 : 2;
+    const char* d = getenv("SN_FA5_SKIP_SOFTMAX");
+    skip = d && atoi(d) == 1;
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
@@ -411,11 +421,11 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
   if (ns == 2)
     attn_prefill_umma_kernel<2><<<grid, threads_for<2>(), smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs,
                                                                        rows, Hq, Hkv, window, scale, cu_k, q_off,
-                                                                       g_fa5_dbg);
+                                                                       g_fa5_dbg, skip);
   else
     attn_prefill_umma_kernel<4><<<grid, threads_for<4>(), smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs,
                                                                        rows, Hq, Hkv, window, scale, cu_k, q_off,
-                                                                       g_fa5_dbg);
+                                                                       g_fa5_dbg, skip);
   return check_launch("sn_attn_prefill(umma)");
 }
 

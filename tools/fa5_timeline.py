@@ -18,4 +18,4 @@ f(dbg.data_ptr()); ops.attn_prefill(q, k, v, cu, out, Hq, Hkv, D, 0, 1 / math.sq
 d = dbg.view(64, 4).cpu().double(); t0 = d[0, 0]
 nb = min(64, (T + 127) // 128)
 for j in range(0, nb - 1, max(1, nb // 16)):
-    print(j, ["%7.0f" % (x - t0) for x in d[j, :3].tolist()], "S issue->p_full wait start %5.0f, p_full wait %5.0f, block %5.0f" % (d[j,1]-d[j,0], d[j,2]-d[j,1], (d[j+1,0]-d[j,0]) if j < 63 else 0))
+    print(j, ["%7.0f" % (x - t0) for x in d[j, :4].tolist()], "K(j) ready->S(j+1) issued %5.0f, P wait %5.0f, PV issue %5.0f, block %5.0f" % (d[j,1]-d[j,0], d[j,2]-d[j,1], d[j,3]-d[j,2], (d[j+1,0]-d[j,0]) if j < 63 else 0))
