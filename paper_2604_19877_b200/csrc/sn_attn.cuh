@@ -50,16 +50,24 @@ __device__ __forceinline__ void finish_split(const AttnDecodeArgs& a, int b, int
   const float* ws_ml = a.workspace + (size_t)a.B * a.Hkv * a.max_splits * G * D;
   const size_t base = ((size_t)b * a.Hkv + hk) * a.max_splits;
   T* out = reinterpret_cast<T*>(a.out);
+  // Unrolled so that 8 splits' partials are in flight at once (one merging CTA per (sequence,
+  // kv head) walks every split; a dependent load per split made many-split merges slow).
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int g = idx / D, d = idx - g * D;
+    const float* ml = ws_ml + (base * G + g) * 2;
+    const float* po = ws_o + base * G * D + (size_t)g * D + d;
     float M = -INFINITY;
-    for (int s = 0; s < num_splits; ++s) M = fmaxf(M, __ldcg(ws_ml + ((base + s) * G + g) * 2));
+#pragma unroll 8
+    for (int s = 0; s < num_splits; ++s) M = fmaxf(M, __ldcg(ml + (size_t)s * G * 2));
     float L = 0.f, O = 0.f;
+#pragma unroll 8
     for (int s = 0; s < num_splits; ++s) {
-      const float ms = __ldcg(ws_ml + ((base + s) * G + g) * 2);
+      const float ms = __ldcg(ml + (size_t)s * G * 2);
+      const float ls = __ldcg(ml + (size_t)s * G * 2 + 1);
+      const float os = __ldcg(po + (size_t)s * G * D);
       const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-      L += __ldcg(ws_ml + ((base + s) * G + g) * 2 + 1) * f;
-      O += __ldcg(ws_o + ((base + s) * G + g) * D + d) * f;
+      L += ls * f;
+      O += os * f;
     }
     io<T>::st(out + ((size_t)b * a.Hq + hk * G + g) * D + d, L > 0.f ? O / L : 0.f);
   }

@@ -35,11 +35,20 @@ def _ceil(a, b):
     return (a + b - 1) // b
 
 
-def choose_split(max_pages: int, rows: int, sms: int = 148, cap: int = 32) -> tuple[int, int]:
+def choose_split(max_pages: int, rows: int, sms: int = 148, cap: int = 64, floor: int = 4,
+                 per_sm: int | None = None) -> tuple[int, int]:
     """Split-KV decomposition for decode attention: aim for ~4 CTAs per SM over
-    (sequence x kv head x split); returns (split_pages, max_splits)."""
-    want = max(1, _ceil(4 * sms, max(rows, 1)))
-    split_pages = max(1, min(cap, _ceil(max_pages, want)))
+    (sequence x kv head x split); returns (split_pages, max_splits).  A split gets at least
+    `floor` pages (every warp of the CTA streams >= 2 tiles) unless the sequence is shorter:
+    with one-page splits at B=1 the CTAs were mostly setup and the last CTA's merge over 64
+    partials dominated (SWA decode 59 us/layer at B=1, tools/ablate.py).  The bf16 kernel holds
+    one CTA per SM (196 KB of TMA stages), so with fewer (sequence x kv head) rows than SMs the
+    splits fill exactly one wave (all-FA B=1: 8.78 -> 7.51 ms/step at 32K, 11.6 -> 10.3 at 128K);
+    with more, ~4 CTAs per SM balance the tail."""
+    if per_sm is None:
+        per_sm = 1 if rows < sms else 4
+    want = max(1, _ceil(per_sm * sms, max(rows, 1)))
+    split_pages = max(1, min(cap, max(min(floor, max_pages), _ceil(max_pages, want))))
     return split_pages, _ceil(max_pages, split_pages)
 
 
@@ -206,7 +215,11 @@ class Supernet:
             self.attn_split = {}
             for kind, max_keys in ((FA, self.max_len), (SWA, cfg.window)):
                 if kind in kinds:
-                    sp, ms = choose_split(_ceil(max_keys, cfg.page_size), B * Hkv)
+                    sp, ms = choose_split(_ceil(max_keys, cfg.page_size), B * Hkv,
+                                          cap=int(os.environ.get("SN_SPLIT_CAP", 64)),
+                                          floor=int(os.environ.get("SN_SPLIT_FLOOR", 4)),
+                                          per_sm=int(os.environ["SN_SPLIT_PER_SM"]) if "SN_SPLIT_PER_SM" in os.environ
+                                          else None)
                     self.attn_split[kind] = (sp, ms)
             ms_max = max(ms for _, ms in self.attn_split.values())
             nbytes = ops.attn_decode_workspace_bytes(B, Hq, Hkv, D, ms_max)
