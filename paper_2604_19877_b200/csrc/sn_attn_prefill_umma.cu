@@ -32,14 +32,29 @@ constexpr float kLazy = 8.f;  // log2 headroom of the stale running max
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
 constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
 
-struct Smem {         // 224 KB, 1024-byte aligned
+// PT = false: P (bf16) goes through shared memory (double-buffered), K / V rings of 2 stages.
+// PT = true: P is written over its own scores in TMEM (packed bf16, tcgen05.st) and the PV
+// product reads A from TMEM; the freed 64 KB give the K and V rings a third stage, so the next
+// K tile is requested a block earlier (the issuer waited ~220 cycles per block for it).
+template <bool PT>
+struct Smem;
+template <>
+struct Smem<false> {  // 224 KB, 1024-byte aligned
+  static constexpr int KVS = 2;
   uint8_t q[TILE];
-  uint8_t k[2][TILE];
-  uint8_t v[2][TILE];
+  uint8_t k[KVS][TILE];
+  uint8_t v[KVS][TILE];
   uint8_t p[2][TILE];  // double-buffered: softmax(j+1) writes while PV(j) reads
 };
+template <>
+struct Smem<true> {   // 224 KB
+  static constexpr int KVS = 3;
+  uint8_t q[TILE];
+  uint8_t k[KVS][TILE];
+  uint8_t v[KVS][TILE];
+};
 struct Sync {          // in front of the tiles, inside the dynamic allocation
-  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_done[2];
+  uint64_t q_full, k_full[3], k_empty[3], v_full[3], v_empty[3], s_full[2], p_full[2], o_done[2];
   uint32_t tmem_base;
   float red[3][BM];  // row max of iteration j in red[j % 3] (float atomic max over the slices)
   float lsum[BM];    // final row sums
@@ -47,7 +62,8 @@ struct Sync {          // in front of the tiles, inside the dynamic allocation
 constexpr int kSyncBytes = 3072;
 constexpr int kSmemBytes = 227 * 1024;
 static_assert(sizeof(Sync) <= kSyncBytes, "sync block");
-static_assert(sizeof(Smem) + kSyncBytes <= kSmemBytes, "tiles");
+static_assert(sizeof(Smem<false>) + kSyncBytes <= kSmemBytes, "tiles");
+static_assert(sizeof(Smem<true>) + kSyncBytes <= kSmemBytes, "tiles");
 
 // MN-major operand (V as the B operand of P V: N = head dim contiguous, K = keys):
 // LBO = stride between 64-element N chunks (the second TMA box), SBO = stride between
@@ -130,11 +146,19 @@ __device__ __forceinline__ void smem_max_f32(float* addr, float v) {  // order-p
   if (v >= 0.f) atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
   else atomicMin(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
 }
+// D (TMEM) += A (TMEM, M lanes x K/2 packed bf16 columns) * B (shared memory descriptor)
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 
-template <int NS>
+template <int NS, bool PT>
 __global__ void __launch_bounds__(threads_for<NS>(), 1)
     attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
@@ -145,8 +169,10 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
   Sync& sy = *reinterpret_cast<Sync*>(smem_raw);
   uint8_t* base = smem_raw + kSyncBytes;
   base += (1024 - (smem_u32(base) & 1023)) & 1023;
-  if (base + sizeof(Smem) > smem_raw + kSmemBytes) __trap();  // dynamic smem base not 1 KB aligned
-  Smem& sm = *reinterpret_cast<Smem*>(base);
+  using SM = Smem<PT>;
+  constexpr int KVS = SM::KVS;
+  if (base + sizeof(SM) > smem_raw + kSmemBytes) __trap();  // dynamic smem base not 1 KB aligned
+  SM& sm = *reinterpret_cast<SM*>(base);
   uint64_t &q_full = sy.q_full, *k_full = sy.k_full, *k_empty = sy.k_empty, *v_full = sy.v_full;
   uint64_t *v_empty = sy.v_empty, *s_full = sy.s_full;
   uint64_t *p_full = sy.p_full, *o_done = sy.o_done;
@@ -165,7 +191,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KVS; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
     }
@@ -209,8 +235,8 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       uint64_t* full = is_k ? k_full : v_full;
       uint64_t* empty = is_k ? k_empty : v_empty;
       for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&empty[st], ((j >> 1) - 1) & 1);
+        const int st = j % KVS;
+        if (j >= KVS) mbar_wait(&empty[st], ((j / KVS) - 1) & 1);
         const int jb = j_lo + j * BN;
         uint8_t* dst = is_k ? sm.k[st] : sm.v[st];
         mbar_expect_tx(&full[st], TILE);
@@ -231,34 +257,43 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         if (rec && j < 64) dbg[j * 4 + what] = clock64();
       };
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+        const int st = j & 1, ks = j % KVS;
+        mbar_wait(&k_full[ks], (j / KVS) & 1);
         stamp(j, 0);
         tc_fence_after();
-        const uint32_t sk = smem_u32(sm.k[st]);
+        const uint32_t sk = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma(tmem + st * 128, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
                desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32), id_s, k > 0 ? 1u : 0u);
         umma_commit(&s_full[st]);
-        umma_commit(&k_empty[st]);
+        umma_commit(&k_empty[ks]);
       };
       issue_s(0);
       for (int j = 0; j < nblk; ++j) {
         const int st = j & 1;
         if (j + 1 < nblk) issue_s(j + 1);  // its S buffer was read by softmax(j-1) (P(j-1) waited below)
         stamp(j, 1);
-        mbar_wait(&v_full[st], (j >> 1) & 1);
+        const int vs = j % KVS;
+        mbar_wait(&v_full[vs], (j / KVS) & 1);
         mbar_wait(&p_full[st], (j >> 1) & 1);
         stamp(j, 2);
         tc_fence_after();
-        const uint32_t sv = smem_u32(sm.v[st]), sp = smem_u32(sm.p[st]);
+        const uint32_t sv = smem_u32(sm.v[vs]);
+        if constexpr (PT) {  // P(j): packed bf16 over the first 64 columns of its score buffer
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k)
-          umma(tmem + 256, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
-               (j > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < BN / 16; ++k)
+            umma_ts(tmem + 256, tmem + st * 128 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
+                    (j > 0 || k > 0) ? 1u : 0u);
+        } else {
+          const uint32_t sp = smem_u32(sm.p[st]);
+#pragma unroll
+          for (int k = 0; k < BN / 16; ++k)
+            umma(tmem + 256, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
+                 (j > 0 || k > 0) ? 1u : 0u);
+        }
         umma_commit(&o_done[st]);
-        umma_commit(&v_empty[st]);
+        umma_commit(&v_empty[vs]);
         stamp(j, 3);
       }
     }
@@ -274,7 +309,9 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
     const uint32_t s_addr = tmem + lane_addr + part * COLS, o_addr = tmem + 256 + lane_addr + part * COLS;
     // P slice: keys part*COLS.. live in atom (part*COLS)/64, 16-byte chunks from ((part*COLS)%64)/8
-    uint8_t* prow0 = sm.p[0] + ((part * COLS) >> 6) * ATOM + t * 128;
+    uint8_t* prow0 = nullptr;
+    if constexpr (!PT) prow0 = &sm.p[0][0] + ((part * COLS) >> 6) * ATOM + t * 128;
+    static_assert(!PT || COLS == 64, "P in TMEM: one x32 store of 32 packed columns per slice");
     const int chunk0 = ((part * COLS) & 63) >> 3;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
@@ -305,7 +342,9 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       // after every slice had read it in iteration j-3 (the barrier of j-2 orders both).
       float* red = sy.red[j % 3];
       smem_max_f32(red + t, mx);
+      if (PT) tc_fence_before();  // every slice's S loads complete before any P overwrites the buffer
       named_bar(1 + sub, NS * 32);
+      if (PT) tc_fence_after();
       mx = red[t] * qs;  // scores stay unscaled; the max is scaled
       if (part == 0) sy.red[(j + 2) % 3][t] = -INFINITY;
       // Lazy rescaling (FA4): the running max only moves when the block max exceeds it by more
@@ -334,6 +373,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       }
       float2 rs2 = make_float2(0.f, 0.f);
       const float2 qs2 = make_float2(qs, qs), nb2 = make_float2(-base_m, -base_m);
+      uint32_t p32[PT ? COLS / 2 : 1];
 #pragma unroll
       for (int c = 0; c < COLS / 8; ++c) {
         float2 p[4];
@@ -344,17 +384,27 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
           p[e] = e == 3 ? exp2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
           rs2 = fadd2(rs2, p[e]);
         }
-        uint4 pk;
-        pk.x = pack_bf16(p[0].x, p[0].y);
-        pk.y = pack_bf16(p[1].x, p[1].y);
-        pk.z = pack_bf16(p[2].x, p[2].y);
-        pk.w = pack_bf16(p[3].x, p[3].y);
-        *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + (((chunk0 + c) ^ (t & 7)) << 4)) = pk;
+        if constexpr (PT) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) p32[c * 4 + e] = pack_bf16(p[e].x, p[e].y);
+        } else {
+          uint4 pk;
+          pk.x = pack_bf16(p[0].x, p[0].y);
+          pk.y = pack_bf16(p[1].x, p[1].y);
+          pk.z = pack_bf16(p[2].x, p[2].y);
+          pk.w = pack_bf16(p[3].x, p[3].y);
+          *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + (((chunk0 + c) ^ (t & 7)) << 4)) = pk;
+        }
       }
       const float rs = rs2.x + rs2.y;
       l = l * alpha + rs;
       m = mn;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+      if constexpr (PT) {  // P over the scores: keys 64*part.. -> columns 32*part.. of the buffer
+        tmem_st32(tmem + lane_addr + (j & 1) * 128 + part * (COLS / 2), reinterpret_cast<const float*>(p32));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      } else {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+      }
       tc_fence_before();
       mbar_arrive(&p_full[j & 1]);
     }
@@ -405,27 +455,33 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     return SN_ECUDA;
   }
   const int smem = kSmemBytes;
-  static int ns = 0, skip = 0;
+  static int ns = 0, skip = 0, pt = 1;
   if (!ns) {
     // softmax slices per row: 2 (8 softmax warps) by default; 4 (16 warps) measured no faster
     // (1025 vs 1044 TFLOP/s causal at 16K) — the per-block chain is the MMA issue order, not
-    // softmax latency.  SN_FA5_SLICES=4 is the A/B switch.
+    // softmax latency.  SN_FA5_SLICES=4 (with SN_FA5_PTMEM=0) is the A/B switch.
     const char* e = getenv("SN_FA5_SLICES");
-    ns = e && atoi(e) == 4 ? 4 : 2;
     const char* d = getenv("SN_FA5_SKIP_SOFTMAX");
+    const char* t = getenv("SN_FA5_PTMEM");  // P in TMEM + 3-stage K/V rings (default) or in smem
+    ns = e && atoi(e) == 4 ? 4 : 2;
     skip = d && atoi(d) == 1;
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    pt = !(t && atoi(t) == 0);
+    if (ns == 4) pt = 0;
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
-  if (ns == 2)
-    attn_prefill_umma_kernel<2><<<grid, threads_for<2>(), smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs,
-                                                                       rows, Hq, Hkv, window, scale, cu_k, q_off,
-                                                                       g_fa5_dbg, skip);
+  auto go = [&](auto kern, int threads) {
+    kern<<<grid, threads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq, Hkv, window, scale,
+                                      cu_k, q_off, g_fa5_dbg, skip);
+  };
+  if (ns == 4)
+    go(attn_prefill_umma_kernel<4, false>, threads_for<4>());
+  else if (pt)
+    go(attn_prefill_umma_kernel<2, true>, threads_for<2>());
   else
-    attn_prefill_umma_kernel<4><<<grid, threads_for<4>(), smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs,
-                                                                       rows, Hq, Hkv, window, scale, cu_k, q_off,
-                                                                       g_fa5_dbg, skip);
+    go(attn_prefill_umma_kernel<2, false>, threads_for<2>());
   return check_launch("sn_attn_prefill(umma)");
 }
 
