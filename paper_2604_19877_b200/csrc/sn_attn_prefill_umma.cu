@@ -54,7 +54,7 @@ struct Smem<true> {   // 224 KB
   uint8_t v[KVS][TILE];
 };
 struct Sync {          // in front of the tiles, inside the dynamic allocation
-  uint64_t q_full, k_full[3], k_empty[3], v_full[3], v_empty[3], s_full[2], p_full[2], o_done[2];
+  uint64_t q_full, k_full[3], k_empty[3], v_full[3], v_empty[3], s_full[3], p_full[3], o_done[2];
   uint32_t tmem_base;
   float red[3][BM];  // row max of iteration j in red[j % 3] (float atomic max over the slices)
   float lsum[BM];    // final row sums
@@ -171,6 +171,10 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
   base += (1024 - (smem_u32(base) & 1023)) & 1023;
   using SM = Smem<PT>;
   constexpr int KVS = SM::KVS;
+  // TMEM score buffers: 2 (P in smem) or 3 (P in TMEM: S(j+2) is issued before PV(j), so the
+  // tensor pipe always has a score product queued while the issuer waits for P(j)); O after them
+  constexpr int SB = PT ? 3 : 2;
+  constexpr uint32_t O_COL = SB * 128;
   if (base + sizeof(SM) > smem_raw + kSmemBytes) __trap();  // dynamic smem base not 1 KB aligned
   SM& sm = *reinterpret_cast<SM*>(base);
   uint64_t &q_full = sy.q_full, *k_full = sy.k_full, *k_empty = sy.k_empty, *v_full = sy.v_full;
@@ -195,10 +199,10 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    // P(j) completes p_full[j & 1]: the softmax can run at most one block ahead of the MMA
+    for (int i = 0; i < SB; ++i) mbar_init(&s_full[i], 1);
+    // P(j) completes p_full[j % SB]: the softmax can run at most one block ahead of the MMA
     // issuer's wait (S(j+2) is issued after P(j) was consumed), so the phase parity is exact
-    for (int i = 0; i < 2; ++i) mbar_init(&p_full[i], SW * 32);
+    for (int i = 0; i < SB; ++i) mbar_init(&p_full[i], SW * 32);
     for (int i = 0; i < 2; ++i) mbar_init(&o_done[i], 1);
   }
   if (threadIdx.x < BM) {
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_base_s;  // S double buffer: columns [0,128) and [128,256); O: [256,384)
+  const uint32_t tmem = tmem_base_s;  // S buffers: columns [128 b, 128 b + 128); O: [O_COL, O_COL + 128)
 
   if (warp > SW) {
     // ---------------- TMA producers: warp 9 loads Q and the K ring, warp 10 the V ring.  K and
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         if (rec && j < 64) dbg[j * 4 + what] = clock64();
       };
       auto issue_s = [&](int j) {
-        const int st = j & 1, ks = j % KVS;
+        const int st = j % SB, ks = j % KVS;
         mbar_wait(&k_full[ks], (j / KVS) & 1);
         stamp(j, 0);
         tc_fence_after();
@@ -270,29 +274,31 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         umma_commit(&k_empty[ks]);
       };
       issue_s(0);
+      if (SB == 3 && nblk > 1) issue_s(1);
       for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        if (j + 1 < nblk) issue_s(j + 1);  // its S buffer was read by softmax(j-1) (P(j-1) waited below)
+        const int st = j % SB;
+        // its S buffer was last read as S / P of block j+1-SB, whose PV was issued before (in order)
+        if (j + SB - 1 < nblk) issue_s(j + SB - 1);
         stamp(j, 1);
         const int vs = j % KVS;
         mbar_wait(&v_full[vs], (j / KVS) & 1);
-        mbar_wait(&p_full[st], (j >> 1) & 1);
+        mbar_wait(&p_full[st], (j / SB) & 1);
         stamp(j, 2);
         tc_fence_after();
         const uint32_t sv = smem_u32(sm.v[vs]);
         if constexpr (PT) {  // P(j): packed bf16 over the first 64 columns of its score buffer
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            umma_ts(tmem + 256, tmem + st * 128 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
+            umma_ts(tmem + O_COL, tmem + st * 128 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
                     (j > 0 || k > 0) ? 1u : 0u);
         } else {
           const uint32_t sp = smem_u32(sm.p[st]);
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            umma(tmem + 256, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
+            umma(tmem + O_COL, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
                  (j > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&o_done[st]);
+        umma_commit(&o_done[j & 1]);
         umma_commit(&v_empty[vs]);
         stamp(j, 3);
       }
@@ -307,7 +313,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
     const int lo = kbr.lo, hi = kbr.hi;
     const float qs = scale * 1.4426950408889634f;
     const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + part * COLS, o_addr = tmem + 256 + lane_addr + part * COLS;
+    const uint32_t s_addr = tmem + lane_addr + part * COLS, o_addr = tmem + O_COL + lane_addr + part * COLS;
     // P slice: keys part*COLS.. live in atom (part*COLS)/64, 16-byte chunks from ((part*COLS)%64)/8
     uint8_t* prow0 = nullptr;
     if constexpr (!PT) prow0 = &sm.p[0][0] + ((part * COLS) >> 6) * ATOM + t * 128;
@@ -316,16 +322,17 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int jb = j_lo + j * BN;
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const int sb = j % SB;
+      mbar_wait(&s_full[sb], (j / SB) & 1);
       tc_fence_after();
       if (skip_softmax) {  // experiment: the MMA / TMA pipeline alone (results wrong)
         tc_fence_before();
-        mbar_arrive(&p_full[j & 1]);
+        mbar_arrive(&p_full[sb]);
         continue;
       }
       float s[COLS];
 #pragma unroll
-      for (int c = 0; c < COLS; c += 32) tmem_ld32(s_addr + (j & 1) * 128 + c, s + c);
+      for (int c = 0; c < COLS; c += 32) tmem_ld32(s_addr + sb * 128 + c, s + c);
       tmem_wait_ld();
       const bool full = jb >= kbl.lo && jb + BN - 1 <= kb0.hi;
       float mx = -INFINITY;
@@ -400,13 +407,13 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       l = l * alpha + rs;
       m = mn;
       if constexpr (PT) {  // P over the scores: keys 64*part.. -> columns 32*part.. of the buffer
-        tmem_st32(tmem + lane_addr + (j & 1) * 128 + part * (COLS / 2), reinterpret_cast<const float*>(p32));
+        tmem_st32(tmem + lane_addr + sb * 128 + part * (COLS / 2), reinterpret_cast<const float*>(p32));
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       } else {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       }
       tc_fence_before();
-      mbar_arrive(&p_full[j & 1]);
+      mbar_arrive(&p_full[sb]);
     }
     atomicAdd(&sy.lsum[t], l);  // row sum: the slices' partial sums
     named_bar(1 + sub, NS * 32);
