@@ -99,6 +99,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -146,13 +154,30 @@ __device__ __forceinline__ void smem_max_f32(float* addr, float v) {  // order-p
   if (v >= 0.f) atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
   else atomicMin(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
 }
-// D (TMEM) += A (TMEM, M lanes x K/2 packed bf16 columns) * B (shared memory descriptor)
-__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                        uint32_t accumulate) {
+// The MMA warp runs converged (all 32 lanes), so its descriptors stay in uniform registers;
+// one elected lane issues.  (Issuing from a lane-0 branch cost ~15 instructions per UMMA with
+// register -> uniform-register moves: the single issuing thread was the limiter.)
+// D (TMEM) += A (smem descriptor) * B (smem descriptor)
+__device__ __forceinline__ void umma_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// D (TMEM) += A (TMEM, M lanes x K/2 packed bf16 columns) * B (shared memory descriptor)
+__device__ __forceinline__ void umma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -249,7 +274,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       }
     }
   } else if (warp == SW) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (whole warp, one elected lane issues)
       const uint32_t id_s = idesc_bf16(BM, BN);
       const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
       const uint32_t sq = smem_u32(sm.q);
@@ -258,7 +283,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       // while the softmax warps work on the current block (S double-buffered in TMEM).
       const bool rec = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
       auto stamp = [&](int j, int what) {
-        if (rec && j < 64) dbg[j * 4 + what] = clock64();
+        if (rec && lane == 0 && j < 64) dbg[j * 4 + what] = clock64();
       };
       auto issue_s = [&](int j) {
         const int st = j % SB, ks = j % KVS;
@@ -268,10 +293,10 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         const uint32_t sk = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma(tmem + st * 128, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
+          umma_w(tmem + st * 128, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
                desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32), id_s, k > 0 ? 1u : 0u);
-        umma_commit(&s_full[st]);
-        umma_commit(&k_empty[ks]);
+        commit_w(&s_full[st]);
+        commit_w(&k_empty[ks]);
       };
       issue_s(0);
       if (SB == 3 && nblk > 1) issue_s(1);
@@ -289,17 +314,17 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         if constexpr (PT) {  // P(j): packed bf16 over the first 64 columns of its score buffer
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            umma_ts(tmem + O_COL, tmem + st * 128 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
+            umma_ts_w(tmem + O_COL, tmem + st * 128 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
                     (j > 0 || k > 0) ? 1u : 0u);
         } else {
           const uint32_t sp = smem_u32(sm.p[st]);
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            umma(tmem + O_COL, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
+            umma_w(tmem + O_COL, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
                  (j > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&o_done[j & 1]);
-        umma_commit(&v_empty[vs]);
+        commit_w(&o_done[j & 1]);
+        commit_w(&v_empty[vs]);
         stamp(j, 3);
       }
     }
@@ -317,7 +342,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
     // P slice: keys part*COLS.. live in atom (part*COLS)/64, 16-byte chunks from ((part*COLS)%64)/8
     uint8_t* prow0 = nullptr;
     if constexpr (!PT) prow0 = &sm.p[0][0] + ((part * COLS) >> 6) * ATOM + t * 128;
-    static_assert(!PT || COLS == 64, "P in TMEM: one x32 store of 32 packed columns per slice");
+    static_assert(!PT || COLS == 64 || COLS == 32, "P in TMEM: one x32 / x16 store of packed columns per slice");
     const int chunk0 = ((part * COLS) & 63) >> 3;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
@@ -407,7 +432,9 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       l = l * alpha + rs;
       m = mn;
       if constexpr (PT) {  // P over the scores: keys 64*part.. -> columns 32*part.. of the buffer
-        tmem_st32(tmem + lane_addr + sb * 128 + part * (COLS / 2), reinterpret_cast<const float*>(p32));
+        const uint32_t pa = tmem + lane_addr + sb * 128 + part * (COLS / 2);
+        if constexpr (COLS == 64) tmem_st32(pa, reinterpret_cast<const float*>(p32));
+        else tmem_st16u(pa, p32);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       } else {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
@@ -473,17 +500,19 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     ns = e && atoi(e) == 4 ? 4 : 2;
     skip = d && atoi(d) == 1;
     pt = !(t && atoi(t) == 0);
-    if (ns == 4) pt = 0;
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
   auto go = [&](auto kern, int threads) {
     kern<<<grid, threads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq, Hkv, window, scale,
                                       cu_k, q_off, g_fa5_dbg, skip);
   };
-  if (ns == 4)
+  if (ns == 4 && pt)
+    go(attn_prefill_umma_kernel<4, true>, threads_for<4>());
+  else if (ns == 4)
     go(attn_prefill_umma_kernel<4, false>, threads_for<4>());
   else if (pt)
     go(attn_prefill_umma_kernel<2, true>, threads_for<2>());
