@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (g.stats) g.stats[blockIdx.x * 8 + 1] = clock64();
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (whole warp converged, one elected lane issues)
       const uint32_t idesc = idesc_bf16(UM, BR);
       int s = 0;
       uint32_t ph = 0;
@@ -168,15 +168,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int a = 0; a < KS; ++a) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma(acc, desc_sw128(sx + a * X_BYTES + k * 32), desc_sw128(sw + a * w_atom + k * 32), idesc,
+              umma_w(acc, desc_sw128(sx + a * X_BYTES + k * 32), desc_sw128(sw + a * w_atom + k * 32), idesc,
                    (ku | a | k) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[s]);
+          commit_w(&empty_bar[s]);
           if (++s == NS) { s = 0; ph ^= 1; }
         }
-        umma_commit(&tfull_bar[buf]);
+        commit_w(&tfull_bar[buf]);
       }
-      if (g.stats) g.stats[blockIdx.x * 8 + 6] = clock64();
+      if (g.stats && lane == 0) g.stats[blockIdx.x * 8 + 6] = clock64();
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: warp w drains TMEM lanes [32*(w%4), +32); lane <-> batch row
