@@ -48,6 +48,7 @@ struct DeltaDecodeArgs {
   int Hk, Hv, rank, W, conv_channels;
   int q_off, k_off, v_off, z_off, b_off, a_off, f1_off, g1_off;
   float scale, eps_l2, eps_norm;
+  int l2_prefetch;  // bytes of this CTA's state requested into L2 at entry (0 = off)
 };
 
 template <int EPL> struct vecf;
@@ -140,6 +141,10 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
   // stream is software-pipelined (batch j+1 in flight while batch j is updated).
   const int slot = a.slot_idx ? a.slot_idx[b] : b;
   float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
+  // Experiment (SN_DELTA_L2PF=1, off by default): the whole (b, h) state requested into L2 at
+  // entry so that HBM is busy during the first wave's prologue — measured slower.
+  if (a.l2_prefetch && tid == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(S), "r"(a.l2_prefetch) : "memory");
   float s_nx[NB][EPL];
 #pragma unroll
   for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
@@ -559,7 +564,11 @@ __global__ void __launch_bounds__(256) gated_rmsnorm_kernel(const float* __restr
 }
 
 template <typename T, int D, bool KDA>
-static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStream_t st) {
+static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a_in, int B, cudaStream_t st) {
+  // experiment switch, off: the L2 prefetch slowed GDN decode 51.9 -> 62.4 us (r01_decode_ablation.md)
+  static const int pf = getenv("SN_DELTA_L2PF") ? atoi(getenv("SN_DELTA_L2PF")) : 0;
+  DeltaDecodeArgs a = a_in;
+  a.l2_prefetch = pf ? D * D * (int)sizeof(float) : 0;
   const int smem = 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.Hv, B);
