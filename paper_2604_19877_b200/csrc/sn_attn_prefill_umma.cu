@@ -154,11 +154,16 @@ __device__ __forceinline__ void smem_max_f32(float* addr, float v) {  // order-p
   if (v >= 0.f) atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
   else atomicMin(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
 }
+__device__ __forceinline__ float max3(float a, float b, float c) {  // FMNMX3 (sm_100)
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 
-template <int NS, bool PT>
+template <int NS, bool PT, int POLY = 1>
 __global__ void __launch_bounds__(threads_for<NS>(), 1)
     attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       // while the softmax warps work on the current block (S double-buffered in TMEM).
       const bool rec = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
       auto stamp = [&](int j, int what) {
-        if (rec && lane == 0 && j < 64) dbg[j * 4 + what] = clock64();
+        if (rec && lane == 0 && j < 64) dbg[j * 8 + what] = clock64();
       };
       auto issue_s = [&](int j) {
         const int st = j % SB, ks = j % KVS;
@@ -320,10 +325,15 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
     static_assert(!PT || COLS == 64 || COLS == 32, "P in TMEM: one x32 / x16 store of packed columns per slice");
     const int chunk0 = ((part * COLS) & 63) >> 3;
     float m = -INFINITY, l = 0.f;
+    const bool srec = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0;
+    auto sstamp = [&](int j, int what) {
+      if (srec && j < 64) dbg[j * 8 + what] = clock64();
+    };
     for (int j = 0; j < nblk; ++j) {
       const int jb = j_lo + j * BN;
       const int sb = j % SB;
       mbar_wait(&s_full[sb], (j / SB) & 1);
+      sstamp(j, 4);
       tc_fence_after();
       if (skip_softmax) {  // experiment: the MMA / TMA pipeline alone (results wrong)
         tc_fence_before();
@@ -334,6 +344,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
 #pragma unroll
       for (int c = 0; c < COLS; c += 32) tmem_ld32(s_addr + sb * 128 + c, s + c);
       tmem_wait_ld();
+      sstamp(j, 5);
       const bool full = jb >= kbl.lo && jb + BN - 1 <= kb0.hi;
       float mx = -INFINITY;
       if (!full) {
@@ -343,8 +354,17 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
           if (jj > hi || jj < lo) s[i] = -INFINITY;
         }
       }
+      {  // four independent three-input max chains
+        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < COLS; ++i) mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < COLS; i += 8) {
+          m0 = max3(m0, s[i], s[i + 1]);
+          m1 = max3(m1, s[i + 2], s[i + 3]);
+          m2 = max3(m2, s[i + 4], s[i + 5]);
+          m3 = max3(m3, s[i + 6], s[i + 7]);
+        }
+        mx = max3(max3(m0, m1, m2), m3, mx);
+      }
       // Row max over the slices: red[j % 3] was reset (to -inf) by slice 0 in iteration j-2,
       // after every slice had read it in iteration j-3 (the barrier of j-2 orders both).
       float* red = sy.red[j % 3];
@@ -352,6 +372,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
       if (PT) tc_fence_before();  // every slice's S loads complete before any P overwrites the buffer
       named_bar(1 + sub, NS * 32);
       if (PT) tc_fence_after();
+      sstamp(j, 6);
       mx = red[t] * qs;  // scores stay unscaled; the max is scaled
       if (part == 0) sy.red[(j + 2) % 3][t] = -INFINITY;
       // Lazy rescaling (FA4): the running max only moves when the block max exceeds it by more
@@ -387,8 +408,8 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 x = ffma2(make_float2(s[c * 8 + 2 * e], s[c * 8 + 2 * e + 1]), qs2, nb2);
-          // the last pair of every 8 on the FMA pipe (a quarter), the rest on MUFU.EX2
-          p[e] = e == 3 ? exp2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
+          // POLY of every 4 pairs on the FMA pipe (cubic exp2), the rest on MUFU.EX2
+          p[e] = (e >= 4 - POLY) ? exp2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
           rs2 = fadd2(rs2, p[e]);
         }
         if constexpr (PT) {
@@ -415,6 +436,7 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       }
       tc_fence_before();
+      sstamp(j, 7);
       mbar_arrive(&p_full[sb]);
     }
     atomicAdd(&sy.lsum[t], l);  // row sum: the slices' partial sums
@@ -464,7 +486,7 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     return SN_ECUDA;
   }
   const int smem = kSmemBytes;
-  static int ns = 0, skip = 0, pt = 1;
+  static int ns = 0, skip = 0, pt = 1, poly = 1;
   if (!ns) {
     // softmax slices per row: 2 (8 softmax warps) by default; 4 (16 warps) measured no faster
     // (1025 vs 1044 TFLOP/s causal at 16K) — the per-block chain is the MMA issue order, not
@@ -475,10 +497,13 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     ns = e && atoi(e) == 4 ? 4 : 2;
     skip = d && atoi(d) == 1;
     pt = !(t && atoi(t) == 0);
+    const char* y = getenv("SN_FA5_POLY");  // pairs of 4 whose exp2 runs on the FMA pipe (1 or 2)
+    poly = y && atoi(y) == 2 ? 2 : 1;
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
   auto go = [&](auto kern, int threads) {
@@ -489,6 +514,8 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     go(attn_prefill_umma_kernel<4, true>, threads_for<4>());
   else if (ns == 4)
     go(attn_prefill_umma_kernel<4, false>, threads_for<4>());
+  else if (pt && poly == 2)
+    go(attn_prefill_umma_kernel<2, true, 2>, threads_for<2>());
   else if (pt)
     go(attn_prefill_umma_kernel<2, true>, threads_for<2>());
   else
