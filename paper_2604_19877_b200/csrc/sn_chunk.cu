@@ -486,10 +486,11 @@ static sn_status launch(const float* qn, const float* kn, const void* qkv, int v
 // Workspace per (chunk, head), bf16: W, Qg, Kd, U [64][D] and P [64][64]; glast fp32.
 
 template <int D>
-struct IntraSmem {  // ~90 KB at D = 128: two CTAs per SM
+struct IntraSmem {  // ~74 KB at D = 128: three CTAs per SM
   static constexpr int LDK = D + 8, LDC = C + 8;
   union {
     __nv_bfloat16 q[C * LDK];   // Q until e^G o Q is written out
+    float x[C][C + 1];          // then the fp32 inverse
     __nv_bfloat16 vb[C * LDK];  // then b o V
   } qv;
   __nv_bfloat16 k[C * LDK];
@@ -498,7 +499,6 @@ struct IntraSmem {  // ~90 KB at D = 128: two CTAs per SM
     float l[C][C + 1];            // L until inverted
     __nv_bfloat16 t[C * LDC];     // then T (bf16 operand)
   } lt;
-  float x[C][C + 1];
   float scr[4 * 16 * 17];
   float g[C], beta[C];
 };
@@ -603,14 +603,17 @@ __global__ void __launch_bounds__(kThreads)
     if (tid == 0) glast[(size_t)n * Hv + h] = gl;
   }
   __syncthreads();
-  // T = (I - L)^{-1}: 16x16 diagonal blocks, then the block rows below them
-  // Q is dead (e^G o Q went out): its tile takes b o V
-  load_vb_tile<T, D>(qkv, qkv_stride, v_off, h, c0, len, sm.beta, sm.qv.vb, LDK);
-  invert_unit_lower(sm.lt.l, sm.x, sm.scr);
+  // T = (I - L)^{-1}: 16x16 diagonal blocks, then the block rows below them.  Q is dead
+  // (e^G o Q went out): its tile holds the fp32 inverse, then b o V (the shared memory fits
+  // three CTAs per SM instead of two; the V loads no longer overlap the inverse, the other
+  // CTAs on the SM cover that latency)
+  invert_unit_lower(sm.lt.l, sm.qv.x, sm.scr);
   for (int idx = tid; idx < C * C; idx += kThreads) {
     const int i = idx / C, j = idx % C;
-    sm.lt.t[i * LDC + j] = __float2bfloat16_rn(sm.x[i][j]);
+    sm.lt.t[i * LDC + j] = __float2bfloat16_rn(sm.qv.x[i][j]);
   }
+  __syncthreads();
+  load_vb_tile<T, D>(qkv, qkv_stride, v_off, h, c0, len, sm.beta, sm.qv.vb, LDK);
   __syncthreads();
   // W = T Kb, U = T Vb  (both [64][D]) -> workspace
   {
