@@ -102,11 +102,14 @@ class Supernet:
         # UMMA, persistent balanced grid; fp32 split-K slabs are summed by the consuming kernel,
         # the gate/up projection fuses SiLU-mul) or on cuBLAS.  Default from in-step B200 A/B
         # runs (tools/step_time.py): ours for the LM head, the fused FFN gate/up and the FFN
-        # down-projection; cuBLAS for the mixer in/out projections, where ours is ~par alone but
-        # slower inside the step.  SN_DECODE_GEMMS=all switches every role to ours.
+        # down-projection, and from B=16 also the mixer out-projection (split-K slabs into the
+        # residual add: B=64 9.844 -> 9.809 ms/step, B=16 7.17 -> 7.09; at B=1-4 cuBLAS is
+        # faster); cuBLAS for the mixer in-projections (ours +0.23 ms/step at B=64, the
+        # consuming mixer kernels start later).  SN_DECODE_GEMMS=all switches every role to ours.
         tc_ok = dtype == torch.bfloat16 and batch <= 128
 
-        sel = os.environ.get("SN_DECODE_GEMMS", "lm_head,ffn_down,ffn_gate_up").split(",")
+        default_roles = "lm_head,ffn_down,ffn_gate_up" + (",out_proj" if batch >= 16 else "")
+        sel = os.environ.get("SN_DECODE_GEMMS", default_roles).split(",")
         self.sn_gemm = {r: tc_ok and (r in sel or "all" in sel)
                         for r in ("lm_head", "ffn_down", "ffn_gate_up", "in_proj", "attn_qkv", "out_proj")}
         if tc_ok:  # fp32 split-K slabs of the input-side projections, summed by their consumers
