@@ -469,6 +469,274 @@ __global__ void __launch_bounds__(threads_for<NS>(), 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------------------------------------
+// Two query tiles per CTA (FA4's ping-pong): CTA = 256 query rows (tiles A, B of 128) x one q
+// head; every K / V tile feeds both tiles' products, and while one tile's softmax runs the
+// tensor pipe works on the other tile's products, so neither the softmax chain nor the issue
+// order leaves the tensor pipe idle.  TMEM: S_A [0,128), O_A [128,256), S_B [256,384),
+// O_B [384,512); P written over its scores.  Issue order per key block j:
+//   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+// Warps 0-7 softmax of tile A, 8-15 tile B (two per TMEM lane quadrant, half a row each),
+// 16 MMA (converged, elected issue), 17 Q + K ring, 18 V ring.
+constexpr int kThreads2 = 16 * 32 + 96;
+struct Smem2 {
+  uint8_t q[2][TILE];
+  uint8_t k[2][TILE];
+  uint8_t v[2][TILE];
+};
+struct Sync2 {
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_done[2];
+  uint32_t tmem_base;
+  float red[2][3][BM];
+  float lsum[2][BM];
+};
+constexpr int kSync2Bytes = 5120;
+static_assert(sizeof(Sync2) <= kSync2Bytes, "sync2 block");
+static_assert(sizeof(Smem2) + kSync2Bytes + 1024 <= kSmemBytes, "tiles2");
+
+__global__ void __launch_bounds__(kThreads2, 1)
+    attn_prefill_umma2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                              const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
+                              __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
+                              float scale, const int32_t* __restrict__ cu_k, const int32_t* __restrict__ q_off) {
+  constexpr int COLS = 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Sync2& sy = *reinterpret_cast<Sync2*>(smem_raw);
+  uint8_t* base = smem_raw + kSync2Bytes;
+  base += (1024 - (smem_u32(base) & 1023)) & 1023;
+  Smem2& sm = *reinterpret_cast<Smem2*>(base);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ctas = (rows + 2 * BM - 1) / (2 * BM);
+  const int r0 = (ctas - 1 - (int)blockIdx.x) * 2 * BM;  // heavy (late) tiles first
+  const int h = blockIdx.y, hk = h / (Hq / Hkv);
+  // the CTA walks the union of both tiles' key blocks
+  const int j_lo = min(key_bounds(cu, cu_k, q_off, num_seqs, min(r0, rows - 1), window).lo,
+                       key_bounds(cu, cu_k, q_off, num_seqs, min(r0 + BM, rows - 1), window).lo);
+  const int j_hi = max(key_bounds(cu, cu_k, q_off, num_seqs, min(r0 + BM - 1, rows - 1), window).hi,
+                       key_bounds(cu, cu_k, q_off, num_seqs, min(r0 + 2 * BM - 1, rows - 1), window).hi);
+  const int nblk = (j_hi - j_lo) / BN + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sy.q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sy.k_full[i], 1); mbar_init(&sy.k_empty[i], 1);
+      mbar_init(&sy.v_full[i], 1); mbar_init(&sy.v_empty[i], 1);
+      mbar_init(&sy.s_full[i], 1); mbar_init(&sy.p_full[i], 8 * 32); mbar_init(&sy.o_done[i], 1);
+    }
+  }
+  if (threadIdx.x < 2 * BM) {
+    const int q = threadIdx.x / BM, t = threadIdx.x % BM;
+    for (int i = 0; i < 3; ++i) sy.red[q][i][t] = -INFINITY;
+    sy.lsum[q][t] = 0.f;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sy.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sy.tmem_base;
+
+  if (warp >= 17) {
+    if (lane == 0) {  // ---------------- TMA producers
+      const bool is_k = warp == 17;
+      const CUtensorMap* map = is_k ? &kmap : &vmap;
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+      const uint64_t keep = policy_evict_last();
+      if (is_k) {
+        mbar_expect_tx(&sy.q_full, 2 * TILE);
+        for (int q = 0; q < 2; ++q) {
+          tma_load_2d(sm.q[q], &qmap, h * HD, r0 + q * BM, &sy.q_full, policy_evict_first());
+          tma_load_2d(sm.q[q] + ATOM, &qmap, h * HD + 64, r0 + q * BM, &sy.q_full, policy_evict_first());
+        }
+      }
+      uint64_t* full = is_k ? sy.k_full : sy.v_full;
+      uint64_t* empty = is_k ? sy.k_empty : sy.v_empty;
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&empty[st], ((j >> 1) - 1) & 1);
+        const int jb = j_lo + j * BN;
+        uint8_t* dst = is_k ? sm.k[st] : sm.v[st];
+        mbar_expect_tx(&full[st], TILE);
+        tma_load_2d(dst, map, hk * HD, jb, &full[st], keep);
+        tma_load_2d(dst + ATOM, map, hk * HD + 64, jb, &full[st], keep);
+      }
+    }
+  } else if (warp == 16) {
+    // ---------------- MMA issuer (whole warp converged, one elected lane issues)
+    const uint32_t id_s = idesc_bf16(BM, BN);
+    const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
+    mbar_wait(&sy.q_full, 0);
+    auto issue_s = [&](int q, int j) {  // S_q(j) = Q_q K(j)^T into tile q's score columns
+      const uint32_t sq = smem_u32(sm.q[q]), sk = smem_u32(sm.k[j & 1]);
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        umma_w(tmem + q * 256, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
+               desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32), id_s, k > 0 ? 1u : 0u);
+      commit_w(&sy.s_full[q]);
+    };
+    auto issue_pv = [&](int q, int j) {  // O_q += P_q(j) V(j)
+      const uint32_t sv = smem_u32(sm.v[j & 1]);
+#pragma unroll
+      for (int k = 0; k < BN / 16; ++k)
+        umma_ts_w(tmem + q * 256 + 128, tmem + q * 256 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
+                  (j > 0 || k > 0) ? 1u : 0u);
+      commit_w(&sy.o_done[q]);
+    };
+    mbar_wait(&sy.k_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    commit_w(&sy.k_empty[0]);
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&sy.v_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&sy.p_full[0], j & 1);
+      tc_fence_after();
+      issue_pv(0, j);
+      const bool more = j + 1 < nblk;
+      if (more) {
+        mbar_wait(&sy.k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        tc_fence_after();
+        issue_s(0, j + 1);  // over P_A(j): PV_A(j) was issued first (in order)
+      }
+      mbar_wait(&sy.p_full[1], j & 1);
+      tc_fence_after();
+      issue_pv(1, j);
+      commit_w(&sy.v_empty[j & 1]);
+      if (more) {
+        issue_s(1, j + 1);
+        commit_w(&sy.k_empty[(j + 1) & 1]);
+      }
+    }
+  } else {
+    // ---------------- softmax: tile q = warp / 8; warps w, w+4 of a tile share TMEM lanes
+    // 32(w%4).. (query rows), one half of the 128 key columns (and of O's head dim) each
+    const int q = warp >> 3, sub = warp & 3, part = (warp >> 2) & 1;
+    const int t = sub * 32 + lane;
+    const int r = r0 + q * BM + t;
+    const KeyBounds kbr = key_bounds(cu, cu_k, q_off, num_seqs, min(r, rows - 1), window);
+    const int lo = kbr.lo, hi = kbr.hi;
+    // this tile's first / last rows: blocks inside both bounds need no mask
+    const int full_lo = key_bounds(cu, cu_k, q_off, num_seqs, min(r0 + q * BM + BM - 1, rows - 1), window).lo;
+    const int full_hi = key_bounds(cu, cu_k, q_off, num_seqs, min(r0 + q * BM, rows - 1), window).hi;
+    const float qs = scale * 1.4426950408889634f;
+    const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + q * 256 + part * COLS;
+    const uint32_t o_addr = tmem + lane_addr + q * 256 + 128 + part * COLS;
+    const uint32_t p_addr = tmem + lane_addr + q * 256 + part * (COLS / 2);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int jb = j_lo + j * BN;
+      mbar_wait(&sy.s_full[q], j & 1);
+      tc_fence_after();
+      float s[COLS];
+      tmem_ld32(s_addr, s);
+      tmem_ld32(s_addr + 32, s + 32);
+      tmem_wait_ld();
+      const bool full = jb >= full_lo && jb + BN - 1 <= full_hi;
+      float mx = -INFINITY;
+      if (!full) {
+#pragma unroll
+        for (int i = 0; i < COLS; ++i) {
+          const int jj = jb + part * COLS + i;
+          if (jj > hi || jj < lo) s[i] = -INFINITY;
+        }
+      }
+      {
+        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < COLS; i += 8) {
+          m0 = max3(m0, s[i], s[i + 1]);
+          m1 = max3(m1, s[i + 2], s[i + 3]);
+          m2 = max3(m2, s[i + 4], s[i + 5]);
+          m3 = max3(m3, s[i + 6], s[i + 7]);
+        }
+        mx = max3(max3(m0, m1, m2), m3, mx);
+      }
+      float* red = sy.red[q][j % 3];
+      smem_max_f32(red + t, mx);
+      tc_fence_before();
+      named_bar(1 + q * 4 + sub, 64);
+      tc_fence_after();
+      mx = red[t] * qs;
+      if (part == 0) sy.red[q][(j + 2) % 3][t] = -INFINITY;
+      const float mn = mx > m + kLazy ? mx : m;
+      const float base_m = mn == -INFINITY ? 0.f : mn;
+      const float alpha = ex2(m - base_m);
+      float2 rs2 = make_float2(0.f, 0.f);
+      const float2 qs2 = make_float2(qs, qs), nb2 = make_float2(-base_m, -base_m);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {  // P in two 16-column stores (fewer live registers)
+        uint32_t p16[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = hf * 32 + c * 8 + 2 * e;
+            const float2 x = ffma2(make_float2(s[i], s[i + 1]), qs2, nb2);
+            const float2 pv = e == 3 ? exp2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
+            rs2 = fadd2(rs2, pv);
+            p16[c * 4 + e] = pack_bf16(pv.x, pv.y);
+          }
+        }
+        tmem_st16u(p_addr + hf * 16, p16);
+      }
+      l = l * alpha + (rs2.x + rs2.y);
+      m = mn;
+      // O rescale after the scores are dead (register pressure); PV_q(j) is issued only after
+      // p_full, so rescaling here is still before P(j) V(j) is added.  PV_q(j-1) must be done.
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        mbar_wait(&sy.o_done[q], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < COLS; c += 32) {
+          float o[32];
+          tmem_ld32(o_addr + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] *= alpha;
+          tmem_st32(o_addr + c, o);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&sy.p_full[q]);
+    }
+    atomicAdd(&sy.lsum[q][t], l);
+    named_bar(1 + q * 4 + sub, 64);
+    l = sy.lsum[q][t];
+    mbar_wait(&sy.o_done[q], (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD + part * COLS;
+#pragma unroll 1
+    for (int c = 0; c < COLS; c += 32) {
+      float o[32];
+      tmem_ld32(o_addr + c, o);
+      tmem_wait_ld();
+      if (r < rows) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 pk;
+          pk.x = pack_bf16(o[e] * inv, o[e + 1] * inv);
+          pk.y = pack_bf16(o[e + 2] * inv, o[e + 3] * inv);
+          pk.z = pack_bf16(o[e + 4] * inv, o[e + 5] * inv);
+          pk.w = pack_bf16(o[e + 6] * inv, o[e + 7] * inv);
+          *reinterpret_cast<uint4*>(orow + c + e) = pk;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 }  // namespace fa5
 
 static unsigned long long* g_fa5_dbg = nullptr;
@@ -486,7 +754,7 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     return SN_ECUDA;
   }
   const int smem = kSmemBytes;
-  static int ns = 0, skip = 0, pt = 1, poly = 1;
+  static int ns = 0, skip = 0, pt = 1, poly = 1, two = 1;
   if (!ns) {
     // softmax slices per row: 2 (8 softmax warps) by default; 4 (16 warps) measured no faster
     // (1025 vs 1044 TFLOP/s causal at 16K) — the per-block chain is the MMA issue order, not
@@ -499,11 +767,19 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     pt = !(t && atoi(t) == 0);
     const char* y = getenv("SN_FA5_POLY");  // pairs of 4 whose exp2 runs on the FMA pipe (1 or 2)
     poly = y && atoi(y) == 2 ? 2 : 1;
+    const char* w2 = getenv("SN_FA5_TWO");  // two query tiles per CTA (default) or one
+    two = !(w2 && atoi(w2) == 0);
+    cudaFuncSetAttribute(attn_prefill_umma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  if (two && !skip && ns == 2 && pt && poly == 1) {
+    attn_prefill_umma2_kernel<<<dim3((rows + 2 * BM - 1) / (2 * BM), Hq), kThreads2, smem, st>>>(
+        qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off);
+    return check_launch("sn_attn_prefill(umma2)");
   }
   dim3 grid((rows + BM - 1) / BM, Hq);
   auto go = [&](auto kern, int threads) {
