@@ -112,10 +112,13 @@ __device__ __forceinline__ float row_dot(const T* __restrict__ row, const float*
 
 constexpr int kDecodeThreads = 256;
 
-template <typename T, int D, bool KDA>
-__global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kernel(const DeltaDecodeArgs a) {
+// THREADS = 256 (4 CTAs per SM) normally; 512 when (heads x batch) leaves most SMs idle (small
+// batches): twice the state columns of one CTA in flight.
+template <typename T, int D, bool KDA, int THREADS = kDecodeThreads>
+__global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 : 4) : 1)
+    delta_decode_kernel(const DeltaDecodeArgs a) {
   sn::pdl_launch_dependents();
-  constexpr int NW = kDecodeThreads / 32;
+  constexpr int NW = THREADS / 32;
   constexpr int EPL = D / 32;     // key entries per lane
   constexpr int CPW = D / NW;     // value columns per warp
   constexpr int NB = 4;           // columns in flight per warp
@@ -155,12 +158,12 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
   const int W = a.W;
   T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * W;
   const T* cw = reinterpret_cast<const T*>(a.conv_w);
-  constexpr int NCH = (3 * D + kDecodeThreads - 1) / kDecodeThreads;
+  constexpr int NCH = (3 * D + THREADS - 1) / THREADS;
   float xin[NCH], wt[NCH][4], rg[NCH][4];
   int chn[NCH];
 #pragma unroll
   for (int u = 0; u < NCH; ++u) {
-    const int c = tid + u * kDecodeThreads;
+    const int c = tid + u * THREADS;
     chn[u] = -1;
     if (c < 3 * D) {
       const int part = c / D, i = c - part * D;
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
 #pragma unroll
   for (int u = 0; u < NCH; ++u) {
     if (chn[u] < 0) continue;
-    const int c = tid + u * kDecodeThreads;
+    const int c = tid + u * THREADS;
     const int part = c / D, i = c - part * D;
     const int ch = chn[u];
     float acc;
@@ -234,12 +237,12 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
 
   // ---- 3. L2 norms (one two-value block reduction), gates, beta
   float qq = 0.f, kk = 0.f;
-  for (int i = tid; i < D; i += kDecodeThreads) { qq += s_q[i] * s_q[i]; kk += s_k[i] * s_k[i]; }
+  for (int i = tid; i < D; i += THREADS) { qq += s_q[i] * s_q[i]; kk += s_k[i] * s_k[i]; }
   block_sum2(qq, kk, s_red);
   const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
   if (!KDA) {
     const float eg = expf(negA * softplus_f(graw));
-    for (int i = tid; i < D; i += kDecodeThreads) s_eg[i] = eg;
+    for (int i = tid; i < D; i += THREADS) s_eg[i] = eg;
   } else if (!have_fg) {
     // second low-rank factors: rows h*D .. h*D+D-1 of f2 (-> gate g) and g2 (-> output gate),
     // half a warp per row (16 lanes x 16 B = one 256-B row when R = 128), coalesced
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
     const T* g2 = reinterpret_cast<const T*>(a.g2_w);
     const T* g2b = reinterpret_cast<const T*>(a.g2_b);
     const int half = lane >> 4, hl = lane & 15;
-    for (int rr = warp * 2 + half; rr < 2 * D; rr += 2 * (kDecodeThreads / 32)) {
+    for (int rr = warp * 2 + half; rr < 2 * D; rr += 2 * (THREADS / 32)) {
       const bool is_f = rr < D;
       const int i = is_f ? rr : rr - D;
       const T* row = (is_f ? f2 : g2) + (size_t)(h * D + i) * a.rank;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
   if (tid == 0) s_beta = sigmoid_f(braw);
   __syncthreads();
   float qk = 0.f;
-  for (int i = tid; i < D; i += kDecodeThreads) {
+  for (int i = tid; i < D; i += THREADS) {
     const float qi = s_q[i] * rq, ki = s_k[i] * rk;
     s_q[i] = qi;
     s_k[i] = ki;
@@ -332,12 +335,12 @@ __global__ void __launch_bounds__(kDecodeThreads, KDA ? 3 : 4) delta_decode_kern
 
   // ---- 4. gated RMSNorm over the head
   float oo = 0.f;
-  for (int j = tid; j < D; j += kDecodeThreads) oo += s_o[j] * s_o[j];
+  for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
   oo = block_sum(oo, s_red);
   const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
   const T* nw = reinterpret_cast<const T*>(a.norm_w);
   T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
-  for (int j = tid; j < D; j += kDecodeThreads) {
+  for (int j = tid; j < D; j += THREADS) {
     const float gz = s_gate[j];
     const float act = KDA ? sigmoid_f(gz) : silu_f(gz);
     io<T>::st(out + j, s_o[j] * rstd * io<T>::ld(nw + j) * act);
@@ -627,8 +630,10 @@ static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a_in, int B, cudaS
   a.l2_prefetch = pf ? D * D * (int)sizeof(float) : 0;
   const int smem = 0;
   cudaLaunchConfig_t cfg = {};
+  static const int wide_env = getenv("SN_DELTA_WIDE") ? atoi(getenv("SN_DELTA_WIDE")) : 1;
+  const bool wide = wide_env && a.Hv * B < 148;
   cfg.gridDim = dim3(a.Hv, B);
-  cfg.blockDim = dim3(kDecodeThreads);
+  cfg.blockDim = dim3(wide ? 2 * kDecodeThreads : kDecodeThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -636,7 +641,8 @@ static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a_in, int B, cudaS
   attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA>, a);
+  cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA, 2 * kDecodeThreads>, a)
+                       : cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA>, a);
   if (e != cudaSuccess) {
     set_error("%s launch: %s", KDA ? "sn_kda_decode" : "sn_gdn_decode", cudaGetErrorString(e));
     return SN_ECUDA;
