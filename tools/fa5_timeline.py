@@ -3,7 +3,8 @@ S issued, next S issued, P ready) via sn_experimental_fa5_timeline.
 
   python tools/fa5_timeline.py [T Hq Hkv]   (default 16384 32 8)
 """
-import ctypes, math, sys, torch
+import ctypes, math, os, sys, torch
+os.environ.setdefault("SN_FA5_TWO", "0")  # the stamps are in the one-tile kernel
 sys.path.insert(0, '.')
 from paper_2604_19877_b200 import ops, _lib
 lib = _lib.load()
