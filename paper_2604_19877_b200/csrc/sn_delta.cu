@@ -97,6 +97,22 @@ __device__ __forceinline__ void block_sum2(float& x, float& y, float* scratch) {
   y = ty;
 }
 
+// Three block-wide sums in one pass (scratch: 3 * blockDim.x/32 floats).
+__device__ __forceinline__ void block_sum3(float& x, float& y, float& z, float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  x = warp_sum(x);
+  y = warp_sum(y);
+  z = warp_sum(z);
+  __syncthreads();
+  if (lane == 0) { scratch[warp] = x; scratch[nw + warp] = y; scratch[2 * nw + warp] = z; }
+  __syncthreads();
+  float tx = 0.f, ty = 0.f, tz = 0.f;
+  for (int i = 0; i < nw; ++i) { tx += scratch[i]; ty += scratch[nw + i]; tz += scratch[2 * nw + i]; }
+  x = tx;
+  y = ty;
+  z = tz;
+}
+
 // Dot of a T row (len R, 16B aligned) with an fp32 smem vector.
 template <typename T>
 __device__ __forceinline__ float row_dot(const T* __restrict__ row, const float* vec, int R) {
@@ -132,7 +148,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   __shared__ __align__(16) float s_o[D];
   __shared__ __align__(16) float s_f1[KDA ? 256 : 1];
   __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
-  __shared__ float s_red[2 * NW];
+  __shared__ float s_red[3 * NW];
   __shared__ float s_beta;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -235,10 +251,15 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   if (!KDA && tid < D) s_gate[tid] = zval;
   __syncthreads();
 
-  // ---- 3. L2 norms (one two-value block reduction), gates, beta
-  float qq = 0.f, kk = 0.f;
-  for (int i = tid; i < D; i += THREADS) { qq += s_q[i] * s_q[i]; kk += s_k[i] * s_k[i]; }
-  block_sum2(qq, kk, s_red);
+  // ---- 3. L2 norms and the q.k product of the raw vectors (one three-value block reduction;
+  //      the normalisation is applied in registers below), gates, beta
+  float qq = 0.f, kk = 0.f, qkr = 0.f;
+  for (int i = tid; i < D; i += THREADS) {
+    qq += s_q[i] * s_q[i];
+    kk += s_k[i] * s_k[i];
+    qkr += s_q[i] * s_k[i];
+  }
+  block_sum3(qq, kk, qkr, s_red);
   const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
   if (!KDA) {
     const float eg = expf(negA * softplus_f(graw));
@@ -272,14 +293,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   }
   if (tid == 0) s_beta = sigmoid_f(braw);
   __syncthreads();
-  float qk = 0.f;
-  for (int i = tid; i < D; i += THREADS) {
-    const float qi = s_q[i] * rq, ki = s_k[i] * rk;
-    s_q[i] = qi;
-    s_k[i] = ki;
-    qk += qi * ki;
-  }
-  qk = block_sum(qk, s_red);  // (contains the __syncthreads that publishes s_q/s_k)
+  const float qk = qkr * rq * rk;
   const float beta = s_beta;
 
   // ---- 3. stream the state: warp owns columns [warp*CPW, +CPW), lane owns keys [lane*EPL, +EPL)
@@ -287,10 +301,10 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
 #pragma unroll
   for (int e = 0; e < EPL; ++e) {
     const int i = lane * EPL + e;
-    kr[e] = s_k[i];
+    kr[e] = s_k[i] * rk;
     eg[e] = s_eg[i];
-    kg[e] = s_k[i] * eg[e];
-    qg[e] = s_q[i] * eg[e];
+    kg[e] = kr[e] * eg[e];
+    qg[e] = s_q[i] * rq * eg[e];
   }
 #pragma unroll 1
   for (int c0 = warp * CPW; c0 < (warp + 1) * CPW; c0 += NB) {
