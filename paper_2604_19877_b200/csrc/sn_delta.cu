@@ -149,7 +149,6 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   __shared__ __align__(16) float s_f1[KDA ? 256 : 1];
   __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
   __shared__ float s_red[3 * NW];
-  __shared__ float s_beta;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = blockIdx.x, b = blockIdx.y;
@@ -261,10 +260,10 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   }
   block_sum3(qq, kk, qkr, s_red);
   const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
-  if (!KDA) {
-    const float eg = expf(negA * softplus_f(graw));
-    for (int i = tid; i < D; i += THREADS) s_eg[i] = eg;
-  } else if (!have_fg) {
+  // GDN: one decay per head, kept in registers; KDA: per-channel decays in s_eg (written
+  // before the first barrier when the gate factors were precomputed)
+  const float eg_head = KDA ? 0.f : expf(negA * softplus_f(graw));
+  if (KDA && !have_fg) {
     // second low-rank factors: rows h*D .. h*D+D-1 of f2 (-> gate g) and g2 (-> output gate),
     // half a warp per row (16 lanes x 16 B = one 256-B row when R = 128), coalesced
     const T* f2 = reinterpret_cast<const T*>(a.f2_w);
@@ -291,10 +290,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
       }
     }
   }
-  if (tid == 0) s_beta = sigmoid_f(braw);
-  __syncthreads();
+  const float beta = sigmoid_f(braw);  // every thread loaded b
+  if (KDA && !have_fg) __syncthreads();  // s_eg / s_gate from the low-rank factors
   const float qk = qkr * rq * rk;
-  const float beta = s_beta;
 
   // ---- 3. stream the state: warp owns columns [warp*CPW, +CPW), lane owns keys [lane*EPL, +EPL)
   float kr[EPL], eg[EPL], kg[EPL], qg[EPL];
@@ -302,7 +300,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   for (int e = 0; e < EPL; ++e) {
     const int i = lane * EPL + e;
     kr[e] = s_k[i] * rk;
-    eg[e] = s_eg[i];
+    eg[e] = KDA ? s_eg[i] : eg_head;
     kg[e] = kr[e] * eg[e];
     qg[e] = s_q[i] * rq * eg[e];
   }
