@@ -97,13 +97,13 @@ __device__ __forceinline__ void block_sum2(float& x, float& y, float* scratch) {
   y = ty;
 }
 
-// Three block-wide sums in one pass (scratch: 3 * blockDim.x/32 floats).
+// Three block-wide sums in one pass (scratch: 3 * blockDim.x/32 floats).  The caller
+// guarantees no thread still reads `scratch` from an earlier use (no leading barrier).
 __device__ __forceinline__ void block_sum3(float& x, float& y, float& z, float* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   x = warp_sum(x);
   y = warp_sum(y);
   z = warp_sum(z);
-  __syncthreads();
   if (lane == 0) { scratch[warp] = x; scratch[nw + warp] = y; scratch[2 * nw + warp] = z; }
   __syncthreads();
   float tx = 0.f, ty = 0.f, tz = 0.f;
@@ -345,10 +345,16 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   }
   __syncthreads();
 
-  // ---- 4. gated RMSNorm over the head
+  // ---- 4. gated RMSNorm over the head (the barrier above also retires every read of s_red
+  //      from the prologue reduction, so the sum needs only one more)
   float oo = 0.f;
   for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
-  oo = block_sum(oo, s_red);
+  oo = warp_sum(oo);
+  if (lane == 0) s_red[warp] = oo;
+  __syncthreads();
+  oo = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) oo += s_red[w];
   const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
   const T* nw = reinterpret_cast<const T*>(a.norm_w);
   T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
