@@ -165,8 +165,8 @@ def measure_preset(cfg, preset, B, ctx, steps, warmup, ws, rank, local, probe_st
     extra = warmup + 2 * steps + probe_steps + 16
     model = Supernet(cfg, PRESETS[preset].layer_string, batch=B, max_len=ctx + extra, dtype=torch.bfloat16,
                      seed=0)
+    graph = DecodeGraph(model, feedback=True)  # warm-up + capture on the empty engine (then reset)
     fill_synthetic(model, ctx)
-    graph = DecodeGraph(model, feedback=True, preserve_state=False)
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         graph.replay()

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SN_ABI_VERSION 1
+#define SN_ABI_VERSION 2
 
 typedef enum { SN_OK = 0, SN_EINVAL = 1, SN_ECUDA = 2, SN_EUNSUPPORTED = 3 } sn_status;
 typedef enum { SN_F32 = 0, SN_BF16 = 1 } sn_dtype;
@@ -62,18 +62,12 @@ sn_status sn_embed(const int32_t* tokens, const void* table, float* residual,
                    int32_t* seq_lens, int32_t* positions, int rows, int dim,
                    int dtype, void* stream);
 
-/* residual += delta (if non-NULL) + sum_{s<nsplit} partials[s] (fp32 slabs
- * [nsplit][rows][dim] from SN_GEMM_PARTIAL, added in slab order);
+/* residual += delta (if non-NULL) + sum_{s<nsplit} partials[s] (the fp32 K-split slabs
+ * [nsplit][rows][dim] of SN_GEMM_PARTIAL, added in slab order: deterministic);
  * out = rmsnorm(residual) * weight.                                          */
 sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit,
                          float* residual, const void* weight, void* out, int rows,
                          int dim, float eps, int dtype, void* stream);
-
-/* out[r,i] = silu(gate_up[r,i]) * gate_up[r,ffn+i].  gate_up is a [rows][2*ffn]
- * dtype matrix (gu_nsplit == 0) or the fp32 split-K slabs of SN_GEMM_PARTIAL
- * ([gu_nsplit][rows][2*ffn], summed in slab order).                          */
-sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, int ffn,
-                      int dtype, void* stream);
 
 /* out[r, i] = silu(g) * u for the interleaved gate/up layout of GEMM mode
  * SN_GEMM_SWIGLU_IL (row of ceil(ffn/h) blocks of [h gate | h up] columns, row
@@ -91,17 +85,18 @@ sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens
  * with (FlashInfer in vLLM, R/PAPER.md:1793).                               */
 
 /* Rotary embedding (rotate-half) on q and k of a fused qkv row
- * [q Hq*D | k Hkv*D | v Hkv*D], then append k,v at the row's position into
+ * [q Hq*D | k Hkv*D | v Hkv*D] (pair_il != 0: the q / k columns of each head in the
+ * rotary-pair interleaved order of sn_gemm_decode_attn_in), then append k,v at the row's
+ * position into
  * the page pool (window==0: slot = pos; window>0: ring slot = pos % window,
  * rows older than seq_lens[seq]-window are not written).  q_out [rows][Hq][D];
- * k_out/v_out [rows][Hkv][D] optional (prefill attention input).  qkv may be
- * fp32 split-K slabs (qkv_nsplit > 0, see SN_GEMM_PARTIAL).                  */
-sn_status sn_rope_kv_append(const void* qkv, int qkv_nsplit, const int32_t* row_seq,
+ * k_out/v_out [rows][Hkv][D] optional (prefill attention input).                */
+sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq,
                             const int32_t* row_pos, const int32_t* seq_lens,
                             const float* inv_freq, void* q_out, void* k_out,
                             void* v_out, void* k_cache, void* v_cache,
                             const int32_t* block_table, int rows, int Hq, int Hkv,
-                            int D, int page_size, int max_blocks, int window,
+                            int D, int page_size, int max_blocks, int window, int pair_il,
                             int dtype, void* stream);
 
 /* Split-KV flash-decode over the page pool: one CTA per (split, kv head,
@@ -133,18 +128,19 @@ sn_status sn_attn_prefill(const void* q, const void* k, const void* v,
                           float scale, int dtype, void* stream);
 
 /* ---------------------------------------------------------------- GDN / KDA
- * R/PAPER.md:1565-1625.  Decode = one fused kernel per layer: causal-conv
- * update (+SiLU), L2-norm q,k, gates, delta-rule state update in place,
- * o = S^T q, gated RMSNorm.  State in HBM is touched exactly once (read +
- * write), in coalesced 512 B column rows.
+ * R/PAPER.md:1565-1625.  Decode = the in-projection (sn_gemm_decode STORE) and one fused
+ * kernel per layer: causal-conv update (+SiLU), L2-norm q,k, gates, delta-rule state update
+ * in place, o = S^T q, gated RMSNorm.  State in HBM is touched exactly once (read + write),
+ * in coalesced 512 B column rows.  Replaces FLA's fused_recurrent_gated_delta_rule /
+ * fused_recurrent_kda decode path (3P-FLA/ops/gated_delta_rule/fused_recurrent.py:291-337)
+ * behind the paper's GDN / KDA mixers.  conv_width must be 4.
  *
  * GDN proj row layout (one fused in-proj GEMM output, R/PAPER.md:1584-1587):
  *   [ q Hk*D | k Hk*D | v Hv*D | z Hv*D | b Hv | a Hv ]   conv channels = q|k|v
  *   g = -exp(A_log[h]) * softplus(a + dt_bias[h]),  beta = sigmoid(b),
  *   out = RMSNorm(o) * norm_w * silu(z)
- * proj is a [B][proj_stride] dtype matrix (proj_nsplit == 0) or the fp32 split-K
- * slabs [proj_nsplit][B][proj_stride] of SN_GEMM_PARTIAL (summed on load).     */
-sn_status sn_gdn_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring,
+ * proj is a [B][proj_stride] dtype matrix.                                        */
+sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring,
                         const void* conv_w, float* state, const int32_t* slot_idx,
                         const int32_t* positions, const float* A_log,
                         const float* dt_bias, const void* norm_w, void* out, int B,
@@ -152,17 +148,15 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, int proj_nsplit, void
                         float eps_l2, float eps_norm, int dtype, void* stream);
 
 /* KDA proj row layout: [ q H*D | k H*D | v H*D | f1 R | g1 R | b H ]
- *   g[h,i] = -exp(A_log[h]) * softplus((f1 @ f2_w^T)[h*D+i] + dt_bias[h*D+i])
- *   gate   = g1 @ g2_w^T + g2_b ;  out = RMSNorm(o) * norm_w * sigmoid(gate)
- *   (f2_w, g2_w: [H*D][R] row-major; the second low-rank factors are fused
- *    into the decode kernel) — or, if fg != NULL, fg = [2][B][H*D] holds the
- *   precomputed (f1 @ f2_w^T, g1 @ g2_w^T) (f2_w/g2_w unused; g2_b still added). */
-sn_status sn_kda_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring,
+ *   g[h,i] = -exp(A_log[h]) * softplus(f[h*D+i] + dt_bias[h*D+i]),  f = f1 @ f2_w^T
+ *   out = RMSNorm(o) * norm_w * sigmoid(g1 @ g2_w^T + g2_b)
+ * fg = [2][B][H*D] dtype: (f1 @ f2_w^T, g1 @ g2_w^T), the second low-rank factors, from two
+ * decode GEMMs on the f1 / g1 columns of proj (R/PAPER.md:1614-1622).                   */
+sn_status sn_kda_decode(const void* proj, int proj_stride, const void* fg, void* conv_ring,
                         const void* conv_w, float* state, const int32_t* slot_idx,
                         const int32_t* positions, const float* A_log,
-                        const float* dt_bias, const void* f2_w, const void* g2_w,
-                        const void* g2_b, const void* fg, const void* norm_w, void* out, int B,
-                        int H, int D, int rank, int conv_width, float scale,
+                        const float* dt_bias, const void* g2_b, const void* norm_w, void* out,
+                        int B, int H, int D, int rank, int conv_width, float scale,
                         float eps_l2, float eps_norm, int dtype, void* stream);
 
 /* Prefill building blocks (sequences packed by cu_seqlens).                */
@@ -198,17 +192,6 @@ sn_status sn_delta_scan(int kind, const float* qn, const float* kn,
                         float* state, const int32_t* slot_idx,
                         const int32_t* cu_seqlens, int num_seqs, int Hk, int Hv,
                         int D, int init_state, int dtype, void* stream);
-
-/* Chunked (WY, C = 64) GDN prefill on tensor cores, bf16 only: same inputs/outputs
- * as sn_delta_scan (kind 0) plus glog from sn_delta_prep; one CTA per
- * (sequence, value head, 64-wide value tile), chunks in order, state in registers.
- * R/PAPER.md:1599 (WY representation), 845-848 (prefill path).                  */
-sn_status sn_gdn_chunk_prefill(const float* qn, const float* kn, const void* qkv_conv,
-                               int v_off, int qkv_stride, const float* glog,
-                               const float* beta, float* o, float* state,
-                               const int32_t* slot_idx, const int32_t* cu_seqlens,
-                               int num_seqs, int Hk, int Hv, int D, int init_state,
-                               int dtype, void* stream);
 
 /* Two-phase chunked GDN prefill (long prompts): phase 1 computes every chunk's
  * local WY tiles in parallel (one CTA per (chunk, value head)), phase 2 runs the
@@ -262,36 +245,48 @@ sn_status sn_tp_allreduce_add_rmsnorm(const unsigned long long* peer_slabs,
                                       float eps, int dtype, void* stream);
 
 /* ---------------------------------------------------------------- decode GEMM
- * Weight-streaming projection GEMM for decode batches (M <= 128):
- * C[m][n] = sum_k X[m][k] W[n][k], X [M][ldx] bf16, W [N][ldw] bf16 (nn.Linear
- * layout), on tcgen05/TMEM/TMA: the batch tile is the UMMA M operand (64 or 128
- * rows) and blocks of up to 256 weight rows the N operand, streamed once from HBM
- * by a persistent grid (block height / split-K chosen to balance the SMs); launched
- * with programmatic dependent launch so W starts streaming while the previous kernel
- * finishes.  Replaces the projection / FFN / LM-head GEMMs of the decode step (the
+ * Weight-streaming projection GEMM for decode batches: C[m][n] = sum_k X[m][k] W[n][k],
+ * X [M][ldx], W [N][ldw] (nn.Linear layout), every projection of the decode step (the
  * trunk of R/PAPER.md:175-182 and each mixer's projections, R/PAPER.md:1540-1625).
- *   SN_GEMM_STORE : out bf16 [M][ldo] = C
- *   SN_GEMM_SWIGLU: W is [2N][K] = [gate; up]; out bf16 [M][ldo] = silu(C_g)*C_u
- *   SN_GEMM_SWIGLU_IL: same result, W pre-interleaved in blocks of h gate rows followed
- *                   by the same h up rows (h = sn_gemm_swiglu_block(M, N, K); the last
- *                   block zero-padded to 2h rows): one contiguous weight stream
- *   SN_GEMM_RESID : out fp32 [M][ldo] += C   (residual stream)
- *   SN_GEMM_PARTIAL: split-K; out fp32 [S][M][ldo] gets one K-split partial per slab,
- *                   S = sn_gemm_decode_splits(M, N, K, mode) (also returned in *splits_out);
- *                   the consumer sums the slabs (sn_add_rmsnorm does, in slab order).   */
+ * bf16 (M <= 128): tcgen05/TMEM/TMA, the batch tile as the UMMA M operand and weight
+ * blocks as N, (block, K split) items dealt to a persistent grid, block height / split
+ * count chosen per shape to balance the SMs (sn_gemm_decode_plan), programmatic dependent
+ * launch.  fp32 (numerics mode, any M): CUDA-core tiles with the same epilogues.
+ *   SN_GEMM_STORE    : out T [M][ldo] = C
+ *   SN_GEMM_RESID    : out fp32 [M][ldo] += C  (residual stream)
+ *   SN_GEMM_PARTIAL  : out fp32 [S][M][ldo]: K split s writes slab s; S (1..8) is returned
+ *                      in *splits_out; the consumer sums the slabs in order (sn_add_rmsnorm)
+ *   SN_GEMM_SWIGLU_IL: W in blocks of h gate rows followed by the same h up rows
+ *                      (h = sn_gemm_swiglu_block(N), last block zero-padded to 2h rows);
+ *                      out T [M][ldo] = silu(C_gate) * C_up, N = FFN width
+ *   SN_GEMM_ATTN_IN  : attention in-projection with RoPE + KV append fused
+ *                      (sn_gemm_decode_attn_in)                                         */
 typedef enum {
   SN_GEMM_STORE = 0,
-  SN_GEMM_SWIGLU = 1,
   SN_GEMM_RESID = 2,
   SN_GEMM_PARTIAL = 3,
-  SN_GEMM_SWIGLU_IL = 4
+  SN_GEMM_SWIGLU_IL = 4,
+  SN_GEMM_ATTN_IN = 6
 } sn_gemm_mode;
-int sn_gemm_decode_splits(int M, int N, int K, int mode);
-int sn_gemm_swiglu_block(int M, int N, int K);
-/* profiling aid: per-CTA pipeline counters of later launches (8 x #SMs u64), NULL = off */
-void sn_gemm_debug_stats(unsigned long long* dev_stats);
+int sn_gemm_swiglu_block(int N);
+/* plan introspection: out[6] = {block rows, K splits, atoms per stage, blocks, grid, stages} */
+int sn_gemm_decode_plan(int M, int N, int K, int mode, int* out);
+/* tuning hook for benchmarks: force block rows (multiple of 16), atoms per stage, K splits
+ * (PARTIAL) and a smaller grid for later launches in this process; zeros = the built-in plan */
+void sn_gemm_decode_tune(int br, int ks, int splits, int grid);
 sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, int N, int ldw,
-                         void* out, int ldo, int mode, int* splits_out, void* stream);
+                         void* out, int ldo, int mode, int* splits_out, int dtype, void* stream);
+/* Attention in-projection.  W = [q Hq*D | k Hkv*D | v Hkv*D] rows with the q and k rows of
+ * every head rotary-pair interleaved (sn_rope_pair_interleave order: row 2i = dim i, row 2i+1
+ * = dim i + D/2; v rows as is).  q_out [M][Hq][D] gets RoPE(q) at positions[m]; RoPE(k) and
+ * v are appended to the page pool at slot (window ? pos % window : pos) through block_table
+ * [M][max_blocks] (the decode half of sn_rope_kv_append).  A slot past the block table is
+ * not written and sets *err_flag = 1 (err_flag may be NULL).                           */
+sn_status sn_gemm_decode_attn_in(const void* x, int M, int K, int ldx, const void* w, int ldw,
+                                 const int32_t* positions, const float* inv_freq, void* q_out,
+                                 void* k_cache, void* v_cache, const int32_t* block_table,
+                                 int Hq, int Hkv, int D, int page_size, int max_blocks,
+                                 int window, int32_t* err_flag, int dtype, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,8 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# SN_LIB: A/B experiments against another build of the same ABI (tools/); default in-tree
-LIB_PATH = os.environ.get("SN_LIB") or os.path.join(_HERE, "libsn100.so")
+LIB_PATH = os.path.join(_HERE, "libsn100.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int
@@ -23,18 +22,16 @@ SIGNATURES = {
     "sn_abi_version": [],
     "sn_embed": [P, P, P, P, P, I, I, I, P],
     "sn_add_rmsnorm": [P, P, I, P, P, P, I, I, Fl, I, P],
-    "sn_silu_mul": [P, I, P, I, I, I, P],
     "sn_argmax": [P, I, I, P, I, P],
     "sn_swiglu_il": [P, I, P, I, I, I, I, P],
-    "sn_rope_kv_append": [P, I, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, P],
+    "sn_rope_kv_append": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, P],
     "sn_attn_decode_workspace_bytes": [I, I, I, I, I],
     "sn_attn_decode": [P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, Fl, I, P],
     "sn_attn_prefill": [P, P, P, P, P, P, P, I, I, I, I, I, I, I, Fl, I, P],
-    "sn_gdn_decode": [P, I, I, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
-    "sn_kda_decode": [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
+    "sn_gdn_decode": [P, I, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
+    "sn_kda_decode": [P, I, P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
     "sn_conv_prefill": [P, I, P, P, P, P, P, P, P, I, I, I, I, I, P],
     "sn_delta_prep": [I, P, P, I, I, I, P, P, P, P, P, P, P, P, I, I, I, I, Fl, Fl, I, P],
-    "sn_gdn_chunk_prefill": [P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gdn_chunk_workspace_bytes": [I, I, I],
     "sn_gdn_chunk_prefill2": [P, P, P, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, I, P],
     "sn_kda_chunk_workspace_bytes": [I, I, I],
@@ -43,17 +40,20 @@ SIGNATURES = {
     "sn_kda_chunk_prefill2": [P, P, P, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, P],
     "sn_delta_scan": [I, P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gated_rmsnorm": [P, P, I, P, P, I, I, I, Fl, I, I, P],
-    "sn_gemm_decode_splits": [I, I, I, I],
-    "sn_gemm_swiglu_block": [I, I, I],
-    "sn_gemm_debug_stats": [P],
-    "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, P],
+    "sn_gemm_swiglu_block": [I],
+    "sn_gemm_decode_plan": [I, I, I, I, P],
+    "sn_gemm_decode_tune": [I, I, I, I],
+    "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, I, P],
+    "sn_gemm_decode_attn_in": [P, I, I, I, P, I, P, P, P, P, P, P, I, I, I, I, I, I, P, I, P],
 }
-RESTYPES = {"sn_gdn_chunk_workspace_bytes": ctypes.c_size_t, "sn_kda_chunk_workspace_bytes": ctypes.c_size_t, "sn_gemm_debug_stats": None, "sn_attn_decode_workspace_bytes": ctypes.c_size_t, "sn_abi_version": ctypes.c_int}
+RESTYPES = {"sn_gdn_chunk_workspace_bytes": ctypes.c_size_t, "sn_kda_chunk_workspace_bytes": ctypes.c_size_t,
+            "sn_attn_decode_workspace_bytes": ctypes.c_size_t,
+            "sn_abi_version": ctypes.c_int, "sn_gemm_swiglu_block": ctypes.c_int, "sn_gemm_decode_plan": ctypes.c_int,
+            "sn_gemm_decode_tune": None}
 
 SN_F32, SN_BF16 = 0, 1
-SN_ATTN_FORCE_SIMT = 0x100
-SN_GEMM_STORE, SN_GEMM_SWIGLU, SN_GEMM_RESID, SN_GEMM_PARTIAL, SN_GEMM_SWIGLU_IL = 0, 1, 2, 3, 4
-ABI_VERSION = 1
+SN_GEMM_STORE, SN_GEMM_RESID, SN_GEMM_PARTIAL, SN_GEMM_SWIGLU_IL, SN_GEMM_ATTN_IN = 0, 2, 3, 4, 6
+ABI_VERSION = 2
 
 _lib = None
 

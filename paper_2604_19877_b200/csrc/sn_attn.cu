@@ -16,23 +16,25 @@ namespace sn {
 // (rotate, write q_out), the next Hkv are key heads (rotate, append to the cache),
 // the last Hkv are value heads (copy to the cache).  Thread i owns rotary pair i.
 template <typename T>
-__device__ __forceinline__ void rope_kv_one(const GemmIn<T>& qkv, const int32_t* __restrict__ row_seq,
+__device__ __forceinline__ void rope_kv_one(const T* __restrict__ qkv, const int32_t* __restrict__ row_seq,
                                             const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
                                             const float* __restrict__ inv_freq, T* __restrict__ q_out,
                                             T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
                                             T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
                                             int Hkv, int D, int page_size, int max_blocks, int window, int r,
-                                            int head, int i) {
+                                            int head, int i, int pair_il) {
   const int half = D / 2;
   const int seq = row_seq ? row_seq[r] : r;
   const int pos = row_pos[r];
   const size_t src = (size_t)r * (Hq + 2 * Hkv) * D + (size_t)head * D;
   // cache slot (FA: the position; SWA: ring slot), SWA rows older than the window are not stored
   const int slot = window > 0 ? pos % window : pos;
-  const bool write = !(window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window);
+  // a slot past the block table (position beyond the allocated length) is never written
+  const bool write = !(window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window) && pos >= 0 &&
+                     slot / page_size < max_blocks;
   if (head >= Hq + Hkv) {  // value head: plain copy
     const int hk = head - Hq - Hkv;
-    const float v1 = qkv(src + i), v2 = qkv(src + i + half);
+    const float v1 = io<T>::ld(qkv + src + i), v2 = io<T>::ld(qkv + src + i + half);
     if (v_out) {
       T* dst = v_out + ((size_t)r * Hkv + hk) * D;
       io<T>::st(dst + i, v1);
@@ -48,7 +50,10 @@ __device__ __forceinline__ void rope_kv_one(const GemmIn<T>& qkv, const int32_t*
   }
   float sn, cs;
   sincosf((float)pos * inv_freq[i], &sn, &cs);
-  const float x1 = qkv(src + i), x2 = qkv(src + i + half);
+  // q / k rows rotary-pair interleaved (the decode in-projection's weight order): dims i and
+  // i + D/2 sit at columns 2i and 2i + 1 of the head
+  const int c1 = pair_il ? 2 * i : i, c2 = pair_il ? 2 * i + 1 : i + half;
+  const float x1 = io<T>::ld(qkv + src + c1), x2 = io<T>::ld(qkv + src + c2);
   const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
   if (head < Hq) {
     T* dst = q_out + ((size_t)r * Hq + head) * D;
@@ -72,32 +77,33 @@ __device__ __forceinline__ void rope_kv_one(const GemmIn<T>& qkv, const int32_t*
 
 // Decode: a CTA per (row, head), a thread per rotation pair.
 template <typename T>
-__global__ void rope_kv_append_kernel(const GemmIn<T> qkv, const int32_t* __restrict__ row_seq,
+__global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* __restrict__ row_seq,
                                       const int32_t* __restrict__ row_pos, const int32_t* __restrict__ seq_lens,
                                       const float* __restrict__ inv_freq, T* __restrict__ q_out,
                                       T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache,
                                       T* __restrict__ v_cache, const int32_t* __restrict__ block_table, int Hq,
-                                      int Hkv, int D, int page_size, int max_blocks, int window) {
+                                      int Hkv, int D, int page_size, int max_blocks, int window, int pair_il) {
   sn::pdl_launch_dependents();
   sn::pdl_wait();
   if ((int)threadIdx.x >= D / 2) return;
   rope_kv_one<T>(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table, Hq,
-                 Hkv, D, page_size, max_blocks, window, blockIdx.x, blockIdx.y, threadIdx.x);
+                 Hkv, D, page_size, max_blocks, window, blockIdx.x, blockIdx.y, threadIdx.x, pair_il);
 }
 
 // Prefill (many rows): a 256-thread CTA per row loops over every (head, pair) of the row.
 template <typename T>
 __global__ void __launch_bounds__(256) rope_kv_append_rows_kernel(
-    const GemmIn<T> qkv, const int32_t* __restrict__ row_seq, const int32_t* __restrict__ row_pos,
+    const T* __restrict__ qkv, const int32_t* __restrict__ row_seq, const int32_t* __restrict__ row_pos,
     const int32_t* __restrict__ seq_lens, const float* __restrict__ inv_freq, T* __restrict__ q_out,
     T* __restrict__ k_out, T* __restrict__ v_out, T* __restrict__ k_cache, T* __restrict__ v_cache,
-    const int32_t* __restrict__ block_table, int Hq, int Hkv, int D, int page_size, int max_blocks, int window) {
+    const int32_t* __restrict__ block_table, int Hq, int Hkv, int D, int page_size, int max_blocks, int window,
+    int pair_il) {
   sn::pdl_launch_dependents();
   sn::pdl_wait();
   const int half = D / 2, n = (Hq + 2 * Hkv) * half;
   for (int idx = threadIdx.x; idx < n; idx += blockDim.x)
     rope_kv_one<T>(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,
-                   Hq, Hkv, D, page_size, max_blocks, window, blockIdx.x, idx / half, idx % half);
+                   Hq, Hkv, D, page_size, max_blocks, window, blockIdx.x, idx / half, idx % half, pair_il);
 }
 
 // ------------------------------------------------------------------ CUDA-core decode
@@ -114,8 +120,7 @@ __global__ void __launch_bounds__(128) attn_decode_simt_kernel(AttnDecodeArgs a)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
   const int G = a.Hq / a.Hkv;
-  const int len = a.seq_lens[b];
-  const int n_keys = a.window > 0 ? min(len, a.window) : len;
+  const int n_keys = attn_num_keys(a, b);
   const int split_keys = a.split_pages * a.page_size;
   const int num_splits = max(1, (n_keys + split_keys - 1) / split_keys);
   if (split >= num_splits) return;
@@ -265,27 +270,26 @@ using namespace sn;
 
 extern "C" {
 
-sn_status sn_rope_kv_append(const void* qkv, int qkv_nsplit, const int32_t* row_seq, const int32_t* row_pos,
+sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq, const int32_t* row_pos,
                             const int32_t* seq_lens, const float* inv_freq, void* q_out, void* k_out,
                             void* v_out, void* k_cache, void* v_cache, const int32_t* block_table, int rows,
-                            int Hq, int Hkv, int D, int page_size, int max_blocks, int window, int dtype,
-                            void* stream) {
+                            int Hq, int Hkv, int D, int page_size, int max_blocks, int window, int pair_il,
+                            int dtype, void* stream) {
   SN_REQUIRE(rows > 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0 && D % 2 == 0, "sn_rope_kv_append: bad shape");
   SN_REQUIRE(page_size > 0 && (window == 0 || window % page_size == 0),
              "sn_rope_kv_append: window %d must be a multiple of page_size %d", window, page_size);
-  SN_REQUIRE(qkv_nsplit >= 0 && qkv_nsplit <= kMaxSplit, "sn_rope_kv_append: qkv_nsplit %d", qkv_nsplit);
   SN_REQUIRE(qkv && row_pos && inv_freq && q_out && k_cache && v_cache && block_table,
              "sn_rope_kv_append: NULL pointer argument");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    const GemmIn<T> in{qkv, qkv_nsplit, (size_t)rows * (Hq + 2 * Hkv) * D};
+    const T* in = (const T*)qkv;
     if (rows > 1024)
       launch_pdl(rope_kv_append_rows_kernel<T>, dim3(rows), dim3(256), 0, (cudaStream_t)stream, in, row_seq,
                  row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out, (T*)k_cache, (T*)v_cache,
-                 block_table, Hq, Hkv, D, page_size, max_blocks, window);
+                 block_table, Hq, Hkv, D, page_size, max_blocks, window, pair_il);
     else
       launch_pdl(rope_kv_append_kernel<T>, dim3(rows, Hq + 2 * Hkv), dim3(((D / 2 + 31) / 32) * 32), 0,
                  (cudaStream_t)stream, in, row_seq, row_pos, seq_lens, inv_freq, (T*)q_out, (T*)k_out, (T*)v_out,
-                 (T*)k_cache, (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window);
+                 (T*)k_cache, (T*)v_cache, block_table, Hq, Hkv, D, page_size, max_blocks, window, pair_il);
     return check_launch("sn_rope_kv_append");
   });
 }
@@ -307,10 +311,10 @@ sn_status sn_attn_decode(const void* q, const void* k_cache, const void* v_cache
   AttnDecodeArgs a{q, k_cache, v_cache, block_table, seq_lens, out, workspace, counters, B, Hq, Hkv,
                    page_size, max_blocks, window, split_pages, max_splits, scale};
   cudaStream_t st = (cudaStream_t)stream;
-  const bool force_simt = (dtype & SN_ATTN_FORCE_SIMT) != 0;
-  dtype &= ~SN_ATTN_FORCE_SIMT;
-  if (dtype == SN_BF16 && !force_simt && (D == 128 || D == 64) && page_size == 64)
+  if (dtype == SN_BF16) {  // tensor-core split-KV decode (sn_attn_tc.cu); fp32 I/O below
+    SN_REQUIRE((D == 128 || D == 64) && page_size == 64, "sn_attn_decode: bf16 needs D in {64, 128}, page 64");
     return attn_decode_tc_bf16(a, D, st);
+  }
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     dim3 grid(max_splits, Hkv, B);
     if (D == 128) launch_pdl(attn_decode_simt_kernel<T, 128, 8>, grid, dim3(128), 0, st, a);

@@ -2,10 +2,6 @@
 #pragma once
 #include "sn_common.cuh"
 
-// OR-ed into the dtype argument of sn_attn_decode to force the CUDA-core
-// kernel for bf16 (cross-check path used by the parity tests).
-#define SN_ATTN_FORCE_SIMT 0x100
-
 namespace sn {
 
 struct AttnDecodeArgs {
@@ -23,10 +19,11 @@ struct AttnDecodeArgs {
 
 // Number of keys a sequence attends to at decode: all of them (FA) or the
 // ring's live slots (SWA: min(len, window), ring slot order is irrelevant
-// because keys are stored post-RoPE).
+// because keys are stored post-RoPE).  Never more than the block table maps (a length
+// past the allocation is a caller error the append reported; nothing is read past it).
 __device__ __forceinline__ int attn_num_keys(const AttnDecodeArgs& a, int b) {
-  const int len = a.seq_lens[b];
-  return a.window > 0 ? min(len, a.window) : len;
+  const int len = min(a.seq_lens[b], a.max_blocks * a.page_size);
+  return a.window > 0 ? min(len, a.window) : max(len, 0);
 }
 
 // Called by every CTA after it wrote its split partial (o unnormalised, m, l in

@@ -154,330 +154,6 @@ __device__ __forceinline__ void load_f32_tiles(const float* const* src, int head
   }
 }
 
-template <int D>
-struct Smem {
-  static constexpr int LDK = D + 8, LDV = VT + 8, LDC = C + 8;
-  __nv_bfloat16 q[C * LDK];    // Q, then e^G o Q
-  __nv_bfloat16 k[C * LDK];    // K, then e^{G_C - G} o K
-  __nv_bfloat16 kb[C * LDK];   // b o e^G o K
-  __nv_bfloat16 w[C * LDK];    // W
-  __nv_bfloat16 s[D * LDV];    // S (bf16 operand copy), [k][v]
-  __nv_bfloat16 vb[C * LDV];   // b o V
-  __nv_bfloat16 vp[C * LDV];   // V'
-  __nv_bfloat16 t[C * LDC];    // T = (I - L)^{-1}
-  __nv_bfloat16 p[C * LDC];    // P
-  float l[C][C + 1];           // L (fp32)
-  float x[C][C + 1];           // T = (I - L)^{-1}
-  float scr[4 * 16 * 17];      // invert_unit_lower scratch
-  float g[C], beta[C];
-};
-
-template <typename T, int D>
-__global__ void __launch_bounds__(kThreads, 1)
-    gdn_chunk_prefill_kernel(const float* __restrict__ qn, const float* __restrict__ kn, const T* __restrict__ qkv,
-                             int v_off, int qkv_stride, const float* __restrict__ glog, const float* __restrict__ beta,
-                             float* __restrict__ o, float* __restrict__ state, const int32_t* __restrict__ slot_idx,
-                             const int32_t* __restrict__ cu, int Hk, int Hv, int init_state) {
-  pdl_launch_dependents();
-  using SM = Smem<D>;
-  constexpr int LDK = SM::LDK, LDV = SM::LDV, LDC = SM::LDC;
-  constexpr int MT = D / 64;  // m16 tiles of the state per warp (D / 16 tiles over 4 warps)
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  SM& sm = *reinterpret_cast<SM*>(smem_raw);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g4 = lane >> 2, t4 = lane & 3;
-  const int vt = blockIdx.x, h = blockIdx.y, seq = blockIdx.z;
-  const int G = Hv / Hk, kh = h / G;
-  const int slot = slot_idx ? slot_idx[seq] : seq;
-  const int t_begin = cu[seq], t_end = cu[seq + 1];
-  float* Sg = state + ((size_t)slot * Hv + h) * D * D;  // device layout [v][k]
-
-  // state fragments: warp owns k-rows [warp*16*MT, +16*MT) of S[k][v], 8 n-tiles of v
-  float sf[MT][8][4];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int kr = (warp * MT + mt) * 16 + g4 + ((e >> 1) << 3);
-        const int vc = vt * VT + nt * 8 + t4 * 2 + (e & 1);
-        sf[mt][nt][e] = init_state ? Sg[(size_t)vc * D + kr] : 0.f;
-      }
-
-  for (int c0 = t_begin; c0 < t_end; c0 += C) {
-    const int len = min(C, t_end - c0);
-    // ---- load Q, K (fp32 -> bf16), V tile, g, beta (rows >= len zero)
-    for (int idx = tid; idx < C * D / 4; idx += kThreads) {
-      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
-      float4 qv = make_float4(0.f, 0.f, 0.f, 0.f), kv = qv;
-      if (r < len) {
-        qv = *reinterpret_cast<const float4*>(qn + ((size_t)(c0 + r) * Hk + kh) * D + c4);
-        kv = *reinterpret_cast<const float4*>(kn + ((size_t)(c0 + r) * Hk + kh) * D + c4);
-      }
-      *reinterpret_cast<uint2*>(&sm.q[r * LDK + c4]) = make_uint2(pack_bf16(qv.x, qv.y), pack_bf16(qv.z, qv.w));
-      *reinterpret_cast<uint2*>(&sm.k[r * LDK + c4]) = make_uint2(pack_bf16(kv.x, kv.y), pack_bf16(kv.z, kv.w));
-    }
-    if (tid < C) {
-      sm.g[tid] = tid < len ? glog[(size_t)(c0 + tid) * Hv + h] : 0.f;
-      sm.beta[tid] = tid < len ? beta[(size_t)(c0 + tid) * Hv + h] : 0.f;
-    }
-    __syncthreads();
-    // in-chunk cumulative log decay (warp 0, sequential scan over 64 values in 2 x 32)
-    if (warp == 0) {
-      float a0 = sm.g[lane], a1 = sm.g[32 + lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const float n0 = __shfl_up_sync(0xffffffffu, a0, o), n1 = __shfl_up_sync(0xffffffffu, a1, o);
-        if (lane >= o) { a0 += n0; a1 += n1; }
-      }
-      a1 += __shfl_sync(0xffffffffu, a0, 31);
-      sm.g[lane] = a0;
-      sm.g[32 + lane] = a1;
-    }
-    // V tile scaled by beta (bf16), rows >= len zero
-    for (int idx = tid; idx < C * VT; idx += kThreads) {
-      const int r = idx / VT, cc = idx % VT;
-      const float v = r < len ? io<T>::ld(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + vt * VT + cc) : 0.f;
-      sm.vb[r * LDV + cc] = __float2bfloat16_rn(v * sm.beta[r]);
-    }
-    __syncthreads();
-
-    // ---- K K^T -> L and Q K^T -> P   (warp w: rows 16w..16w+15, all 64 columns)
-    {
-      float kk[8][4], qk[8][4];
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) kk[nt][e] = qk[nt][e] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < D; ks += 16) {
-        uint32_t ak[4], aq[4];
-        lda(sm.k, LDK, warp * 16, ks, ak);
-        lda(sm.q, LDK, warp * 16, ks, aq);
-#pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldb_nk(sm.k, LDK, nt * 8, ks, b0, b1, b2, b3);
-          mma_bf16(kk[nt], ak, b0, b1);
-          mma_bf16(kk[nt + 1], ak, b2, b3);
-          mma_bf16(qk[nt], aq, b0, b1);
-          mma_bf16(qk[nt + 1], aq, b2, b3);
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = warp * 16 + g4 + ((e >> 1) << 3), j = nt * 8 + t4 * 2 + (e & 1);
-          const float gam = i >= j ? expf(sm.g[i] - sm.g[j]) : 0.f;
-          sm.l[i][j] = i > j ? -sm.beta[i] * kk[nt][e] * gam : 0.f;
-          sm.p[i * LDC + j] = __float2bfloat16_rn(qk[nt][e] * gam);
-        }
-    }
-    __syncthreads();
-
-    // ---- operand scaling, then T = (I - L)^{-1} (invert_unit_lower)
-    // operand scaling: Kb = b e^G K, Kd = e^{G_C - G} K (in place of K), Qg = e^G Q (in place of Q)
-    {
-      const float gl = sm.g[C - 1];
-      for (int idx = tid; idx < C * D; idx += kThreads) {
-        const int r = idx / D, cc = idx % D;
-        const float eg = expf(sm.g[r]);
-        const float kv = __bfloat162float(sm.k[r * LDK + cc]);
-        sm.kb[r * LDK + cc] = __float2bfloat16_rn(kv * sm.beta[r] * eg);
-        sm.k[r * LDK + cc] = __float2bfloat16_rn(kv * expf(gl - sm.g[r]));
-        sm.q[r * LDK + cc] = __float2bfloat16_rn(__bfloat162float(sm.q[r * LDK + cc]) * eg);
-      }
-    }
-    __syncthreads();
-    invert_unit_lower(sm.l, sm.x, sm.scr);
-    for (int idx = tid; idx < C * C; idx += kThreads) {
-      const int i = idx / C, j = idx % C;
-      sm.t[i * LDC + j] = __float2bfloat16_rn(sm.x[i][j]);
-    }
-    // S -> bf16 operand [k][v]
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; e += 2) {
-          const int kr = (warp * MT + mt) * 16 + g4 + ((e >> 1) << 3);
-          const int vc = nt * 8 + t4 * 2;
-          *reinterpret_cast<uint32_t*>(&sm.s[kr * LDV + vc]) = pack_bf16(sf[mt][nt][e], sf[mt][nt][e + 1]);
-        }
-    __syncthreads();
-
-    // ---- W = T Kb (-> smem), U = T Vb (registers)
-    float u[8][4];
-    {
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) u[nt][e] = 0.f;
-      float wacc[D / 8][4];
-#pragma unroll
-      for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) wacc[nt][e] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < C; ks += 16) {
-        uint32_t a[4];
-        lda(sm.t, LDC, warp * 16, ks, a);
-#pragma unroll
-        for (int nt = 0; nt < D / 8; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldb_kn(sm.kb, LDK, nt * 8, ks, b0, b1, b2, b3);
-          mma_bf16(wacc[nt], a, b0, b1);
-          mma_bf16(wacc[nt + 1], a, b2, b3);
-        }
-#pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldb_kn(sm.vb, LDV, nt * 8, ks, b0, b1, b2, b3);
-          mma_bf16(u[nt], a, b0, b1);
-          mma_bf16(u[nt + 1], a, b2, b3);
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; e += 2) {
-          const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = nt * 8 + t4 * 2;
-          *reinterpret_cast<uint32_t*>(&sm.w[r * LDK + cc]) = pack_bf16(wacc[nt][e], wacc[nt][e + 1]);
-        }
-    }
-    __syncwarp();  // each warp reads back only its own 16 rows of W
-
-    // ---- V' = U - W S  (-> smem, bf16)
-    {
-#pragma unroll
-      for (int ks = 0; ks < D; ks += 16) {
-        uint32_t a[4];
-        lda(sm.w, LDK, warp * 16, ks, a);
-        // negate by accumulating W S into a separate tile and subtracting below
-#pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldb_kn(sm.s, LDV, nt * 8, ks, b0, b1, b2, b3);
-          float ws0[4] = {0.f, 0.f, 0.f, 0.f}, ws1[4] = {0.f, 0.f, 0.f, 0.f};
-          mma_bf16(ws0, a, b0, b1);
-          mma_bf16(ws1, a, b2, b3);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) { u[nt][e] -= ws0[e]; u[nt + 1][e] -= ws1[e]; }
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; e += 2) {
-          const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = nt * 8 + t4 * 2;
-          *reinterpret_cast<uint32_t*>(&sm.vp[r * LDV + cc]) = pack_bf16(u[nt][e], u[nt][e + 1]);
-        }
-    }
-    __syncthreads();
-
-    // ---- O = (e^G Q) S + P V'  -> global (fp32)
-    {
-      float oc[8][4];
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) oc[nt][e] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < D; ks += 16) {
-        uint32_t a[4];
-        lda(sm.q, LDK, warp * 16, ks, a);
-#pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldb_kn(sm.s, LDV, nt * 8, ks, b0, b1, b2, b3);
-          mma_bf16(oc[nt], a, b0, b1);
-          mma_bf16(oc[nt + 1], a, b2, b3);
-        }
-      }
-#pragma unroll
-      for (int ks = 0; ks < C; ks += 16) {
-        uint32_t a[4];
-        lda(sm.p, LDC, warp * 16, ks, a);
-#pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          ldb_kn(sm.vp, LDV, nt * 8, ks, b0, b1, b2, b3);
-          mma_bf16(oc[nt], a, b0, b1);
-          mma_bf16(oc[nt + 1], a, b2, b3);
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; e += 2) {
-          const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = vt * VT + nt * 8 + t4 * 2;
-          if (r < len)
-            *reinterpret_cast<float2*>(o + ((size_t)(c0 + r) * Hv + h) * D + cc) = make_float2(oc[nt][e], oc[nt][e + 1]);
-        }
-    }
-
-    // ---- S = e^{G_C} S + (e^{G_C - G} K)^T V'   (K was replaced by e^{G_C - G} K above)
-    {
-      const float dec = expf(sm.g[C - 1]);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sf[mt][nt][e] *= dec;
-#pragma unroll
-      for (int ks = 0; ks < C; ks += 16) {
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          uint32_t a[4];
-          lda_t(sm.k, LDK, (warp * MT + mt) * 16, ks, a);
-#pragma unroll
-          for (int nt = 0; nt < 8; nt += 2) {
-            uint32_t b0, b1, b2, b3;
-            ldb_kn(sm.vp, LDV, nt * 8, ks, b0, b1, b2, b3);
-            mma_bf16(sf[mt][nt], a, b0, b1);
-            mma_bf16(sf[mt][nt + 1], a, b2, b3);
-          }
-        }
-      }
-    }
-    __syncthreads();  // smem is rewritten by the next chunk
-  }
-
-  // final state -> [v][k]
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int kr = (warp * MT + mt) * 16 + g4 + ((e >> 1) << 3);
-        const int vc = vt * VT + nt * 8 + t4 * 2 + (e & 1);
-        Sg[(size_t)vc * D + kr] = sf[mt][nt][e];
-      }
-}
-
-template <typename T, int D>
-static sn_status launch(const float* qn, const float* kn, const void* qkv, int v_off, int qkv_stride,
-                        const float* glog, const float* beta, float* o, float* state, const int32_t* slot_idx,
-                        const int32_t* cu, int num_seqs, int Hk, int Hv, int init_state, cudaStream_t st) {
-  const int smem = (int)sizeof(Smem<D>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gdn_chunk_prefill_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  dim3 grid(D / VT, Hv, num_seqs);
-  gdn_chunk_prefill_kernel<T, D><<<grid, kThreads, smem, st>>>(qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta,
-                                                              o, state, slot_idx, cu, Hk, Hv, init_state);
-  return check_launch("sn_gdn_chunk_prefill");
-}
-
-
 // =====================================================================================
 // Two-phase version (the long-prefill path): the chunk-local work (inverse, W, U, P and
 // the decayed operands) of all chunks runs in parallel, one CTA per (chunk, value head);
@@ -1184,22 +860,6 @@ static sn_status launch_kda_two_phase(const float* qn, const float* kn, const vo
 using namespace sn;
 
 extern "C" {
-
-sn_status sn_gdn_chunk_prefill(const float* qn, const float* kn, const void* qkv_conv, int v_off, int qkv_stride,
-                               const float* glog, const float* beta, float* o, float* state, const int32_t* slot_idx,
-                               const int32_t* cu_seqlens, int num_seqs, int Hk, int Hv, int D, int init_state,
-                               int dtype, void* stream) {
-  SN_REQUIRE(qn && kn && qkv_conv && glog && beta && o && state && cu_seqlens, "sn_gdn_chunk_prefill: NULL pointer");
-  SN_REQUIRE(num_seqs > 0 && Hk > 0 && Hv % Hk == 0, "sn_gdn_chunk_prefill: bad shape");
-  SN_REQUIRE(D == 64 || D == 128, "sn_gdn_chunk_prefill: D=%d unsupported", D);
-  SN_REQUIRE(dtype == SN_BF16, "sn_gdn_chunk_prefill: bf16 tensor-core path only (fp32 uses sn_delta_scan)");
-  cudaStream_t st = (cudaStream_t)stream;
-  if (D == 128)
-    return chunk::launch<__nv_bfloat16, 128>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, o, state, slot_idx,
-                                              cu_seqlens, num_seqs, Hk, Hv, init_state, st);
-  return chunk::launch<__nv_bfloat16, 64>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, o, state, slot_idx,
-                                           cu_seqlens, num_seqs, Hk, Hv, init_state, st);
-}
 
 size_t sn_kda_chunk_workspace_bytes(int num_chunks, int H, int D) {
   return (size_t)num_chunks * H * (4 * (size_t)chunk::C * D + (size_t)chunk::C * chunk::C) * 2 +

@@ -101,28 +101,6 @@ __device__ __forceinline__ float block_sum(float v, float* scratch) {
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// A GEMM output consumed by a kernel: either a plain T matrix (nsplit == 0) or the
-// fp32 split-K slabs [nsplit][rows][ld] of SN_GEMM_PARTIAL, summed in slab order.
-// `slab` is the element stride between slabs (rows * ld).
-constexpr int kMaxSplit = 8;
-template <typename T>
-struct GemmIn {
-  const void* base;
-  int nsplit;
-  size_t slab;
-  __device__ __forceinline__ float operator()(size_t idx) const {
-    if (nsplit == 0) return io<T>::ld(reinterpret_cast<const T*>(base) + idx);
-    const float* p = reinterpret_cast<const float*>(base) + idx;
-    float v[kMaxSplit];
-#pragma unroll
-    for (int s = 0; s < kMaxSplit; ++s) v[s] = s < nsplit ? __ldcg(p + s * slab) : 0.f;
-    float acc = 0.f;
-#pragma unroll
-    for (int s = 0; s < kMaxSplit; ++s) acc += v[s];
-    return acc;
-  }
-};
-
 // Programmatic dependent launch: lets the next kernel in the stream (if it was
 // launched with the PDL attribute — the decode GEMMs are) start its prologue and
 // its weight prefetch while this kernel is still running.  No-op otherwise.

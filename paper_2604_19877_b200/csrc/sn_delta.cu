@@ -24,14 +24,15 @@
 //      same registers, using  q.S_new = (q*e^g).S + (q.k) u,
 //   4. applies the gated RMSNorm over the head and writes bf16/fp32 output.
 // The state is read once and written once: 2*D*D*4 bytes per (sequence, head).
+#include <type_traits>
+
 #include "sn_common.cuh"
 
 namespace sn {
 
 struct DeltaDecodeArgs {
-  const void* proj;
+  const void* proj;   // in-projection row [B][proj_stride] (sn_gemm_decode STORE output)
   int proj_stride;
-  int proj_nsplit;  // 0: T rows; >0: fp32 split-K slabs [nsplit][B][proj_stride]
   void* conv_ring;
   const void* conv_w;
   float* state;
@@ -39,16 +40,13 @@ struct DeltaDecodeArgs {
   const int32_t* positions;
   const float* A_log;
   const float* dt_bias;
-  const void* f2_w;
-  const void* g2_w;
+  const void* fg;     // KDA: [2][B][H*D] = (f1 @ f2^T, g1 @ g2^T), the second low-rank factors
   const void* g2_b;
-  const void* fg;     // KDA: optional precomputed [2][B][H*D] = (f1 @ f2^T, g1 @ g2^T); then f2/g2 unused
   const void* norm_w;
   void* out;
-  int Hk, Hv, rank, W, conv_channels;
+  int Hk, Hv, rank, conv_channels;
   int q_off, k_off, v_off, z_off, b_off, a_off, f1_off, g1_off;
   float scale, eps_l2, eps_norm;
-  int l2_prefetch;  // bytes of this CTA's state requested into L2 at entry (0 = off)
 };
 
 template <int EPL> struct vecf;
@@ -82,19 +80,14 @@ template <> __device__ __forceinline__ void load4<float>(const float* p, float* 
   const float4 v = *reinterpret_cast<const float4*>(p);
   f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
 }
-
-// Two block-wide sums in one pass (scratch: 2 * blockDim.x/32 floats).
-__device__ __forceinline__ void block_sum2(float& x, float& y, float* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  x = warp_sum(x);
-  y = warp_sum(y);
-  __syncthreads();
-  if (lane == 0) { scratch[warp] = x; scratch[nw + warp] = y; }
-  __syncthreads();
-  float tx = 0.f, ty = 0.f;
-  for (int i = 0; i < nw; ++i) { tx += scratch[i]; ty += scratch[nw + i]; }
-  x = tx;
-  y = ty;
+// n (= 2 or 4) consecutive elements
+template <typename T, int N> __device__ __forceinline__ void loadn(const T* p, float* f) {
+  if (N == 4) {
+    load4<T>(p, f);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) f[i] = io<T>::ld(p + i);
+  }
 }
 
 // Three block-wide sums in one pass (scratch: 3 * blockDim.x/32 floats).  The caller
@@ -113,31 +106,252 @@ __device__ __forceinline__ void block_sum3(float& x, float& y, float& z, float* 
   z = tz;
 }
 
-// Dot of a T row (len R, 16B aligned) with an fp32 smem vector.
-template <typename T>
-__device__ __forceinline__ float row_dot(const T* __restrict__ row, const float* vec, int R) {
-  float acc = 0.f;
-  for (int r = 0; r < R; r += 8) {
-    float w[8];
-    load8<T>(row + r, w);
+constexpr int kDecodeThreads = 256;
+
+// Width-4 causal conv of one channel at position pos: the ring holds the inputs of
+// positions pos-1..pos-3 at slots (pos-d) & 3; x is the new input.
+__device__ __forceinline__ float conv4(const float* w, const float* ring, float x, int pos) {
+  float acc = w[3] * x;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc += w[k] * vec[r + k];
-  }
+  for (int d = 1; d < 4; ++d)
+    if (pos - d >= 0) acc += w[3 - d] * ring[(pos - d) & 3];
   return acc;
 }
 
-constexpr int kDecodeThreads = 256;
+// N consecutive elements of T kept packed in 32-bit registers (bf16: two per register), loaded
+// with 16-byte (or 8-byte) vector loads; element i comes back as float.
+template <typename T, int N>
+struct Packed {
+  static constexpr int R = N * (int)sizeof(T) / 4;
+  uint32_t r[R];
+  __device__ __forceinline__ void load(const T* p) {
+    if (R % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < R; i += 4) {
+        const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(p) + i);
+        r[i] = u.x; r[i + 1] = u.y; r[i + 2] = u.z; r[i + 3] = u.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; i += 2) {
+        const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint32_t*>(p) + i);
+        r[i] = u.x; r[i + 1] = u.y;
+      }
+    }
+  }
+  __device__ __forceinline__ float operator[](int i) const {  // i must be a compile-time constant
+    if (sizeof(T) == 4) return __uint_as_float(r[i]);
+    return __uint_as_float((i & 1) ? (r[i >> 1] & 0xffff0000u) : (r[i >> 1] << 16));
+  }
+};
 
-// THREADS = 256 (4 CTAs per SM) normally; 512 when (heads x batch) leaves most SMs idle (small
-// batches): twice the state columns of one CTA in flight.
-template <typename T, int D, bool KDA, int THREADS = kDecodeThreads>
-__global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 : 4) : 1)
-    delta_decode_kernel(const DeltaDecodeArgs a) {
+// conv4 over channel e of a packed [channels][4] tap block and ring block, p = pos & 3 known
+// at compile time (so every ring index is a register, not a local-memory array access).
+template <int P, typename TP>
+__device__ __forceinline__ float conv4p(const TP& w, const TP& ring, int e, float x, int pos) {
+  float acc = w[4 * e + 3] * x;
+  acc += pos >= 1 ? w[4 * e + 2] * ring[4 * e + ((P + 3) & 3)] : 0.f;
+  acc += pos >= 2 ? w[4 * e + 1] * ring[4 * e + ((P + 2) & 3)] : 0.f;
+  acc += pos >= 3 ? w[4 * e + 0] * ring[4 * e + ((P + 1) & 3)] : 0.f;
+  return acc;
+}
+
+// ---------------------------------------------------------------------------------------
+// GDN decode: one CTA per (value head h, sequence b), THREADS/32 warps; lane l of every warp
+// owns key entries [l*EPL, +EPL) of the head, warp w owns value columns [w*CPW, +CPW).
+//
+// Barrier-free prologue: every warp computes, in registers, exactly what it needs —
+// the conv + SiLU of its lanes' EPL q and k channels (all D key entries across the warp, so
+// |q|^2, |k|^2 and q.k are warp shuffles) and of its own CPW v channels (lane j < CPW holds
+// v of column w*CPW + j) — so no block barrier sits between griddepcontrol.wait and the
+// state stream.  The conv taps, the ring slots and the first state columns are requested
+// before griddepcontrol.wait (none depends on the in-projection); only the projection row
+// itself is loaded after it.  The state is then streamed once, software-pipelined (NB columns
+// in flight per warp): both dot products come from the same registers using
+// q.S_new = (q*e^g).S + (q.k) u, and each new column is stored immediately.  One barrier at
+// the end gathers o for the gated RMSNorm over the head.
+template <typename T, int D, int THREADS = kDecodeThreads>
+__global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
+    gdn_decode_kernel(const DeltaDecodeArgs a) {
   sn::pdl_launch_dependents();
   constexpr int NW = THREADS / 32;
   constexpr int EPL = D / 32;     // key entries per lane
   constexpr int CPW = D / NW;     // value columns per warp
   constexpr int NB = 4;           // columns in flight per warp
+  static_assert(CPW % NB == 0 && CPW <= 32, "columns per warp");
+  __shared__ __align__(16) float s_o[D];
+  __shared__ float s_red[NW];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int G = a.Hv / a.Hk, kh = h / G;
+  const int slot = a.slot_idx ? a.slot_idx[b] : b;
+  float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
+  float s_nx[NB][EPL];
+#pragma unroll
+  for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
+
+  // ring slots (this layer's previous step): before the wait; the conv taps are L2-resident
+  // weights loaded after it, in the same round trip as the projection row
+  T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * 4;
+  const T* cw = reinterpret_cast<const T*>(a.conv_w);
+  const int qch = a.q_off + kh * D + lane * EPL, kch = a.k_off + kh * D + lane * EPL;
+  const int vcol = warp * CPW + (lane < CPW ? lane : 0);
+  const int vch = a.v_off + h * D + vcol;
+  Packed<T, 4 * EPL> rgq, rgk;
+  Packed<T, 4> rgv;
+  rgq.load(ring + (size_t)qch * 4);
+  rgk.load(ring + (size_t)kch * 4);
+  rgv.load(ring + (size_t)vch * 4);
+  const float negA = -expf(a.A_log[h]);
+  const float dtb = a.dt_bias[h];
+  const T* nwp = reinterpret_cast<const T*>(a.norm_w);
+  const float nw = tid < D ? io<T>::ld(nwp + tid) : 0.f;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  // ---- the in-projection row: this lane's q, k, v inputs, the output gate z, a, b; taps
+  const int pos = a.positions[b];
+  const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
+  float xq[EPL], xk[EPL];
+  loadn<T, EPL>(prow + qch, xq);
+  loadn<T, EPL>(prow + kch, xk);
+  const float xv = io<T>::ld(prow + vch);
+  const float zval = tid < D ? io<T>::ld(prow + a.z_off + h * D + tid) : 0.f;
+  const float braw = io<T>::ld(prow + a.b_off + h);
+  const float graw = io<T>::ld(prow + a.a_off + h) + dtb;
+  Packed<T, 4 * EPL> wq, wk;
+  Packed<T, 4> wv;
+  wq.load(cw + (size_t)qch * 4);
+  wk.load(cw + (size_t)kch * 4);
+  wv.load(cw + (size_t)vch * 4);
+
+  // ---- conv + SiLU in registers; ring slot pos % 4 takes the new input (q/k channels are
+  //      shared by the G value heads of a key head: the first of them writes)
+  float qv[EPL], kv[EPL], vv = 0.f;
+  auto conv_all = [&](auto P) {
+    constexpr int p = decltype(P)::value;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      qv[e] = silu_f(conv4p<p>(wq, rgq, e, xq[e], pos));
+      kv[e] = silu_f(conv4p<p>(wk, rgk, e, xk[e], pos));
+    }
+    vv = silu_f(conv4p<p>(wv, rgv, 0, xv, pos));
+  };
+  switch (pos & 3) {
+    case 0: conv_all(std::integral_constant<int, 0>{}); break;
+    case 1: conv_all(std::integral_constant<int, 1>{}); break;
+    case 2: conv_all(std::integral_constant<int, 2>{}); break;
+    default: conv_all(std::integral_constant<int, 3>{}); break;
+  }
+  if ((h % G) == 0 && warp == 0) {
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      io<T>::st(ring + (size_t)(qch + e) * 4 + (pos & 3), xq[e]);
+      io<T>::st(ring + (size_t)(kch + e) * 4 + (pos & 3), xk[e]);
+    }
+  }
+  if (lane < CPW) io<T>::st(ring + (size_t)vch * 4 + (pos & 3), xv);
+
+  // ---- L2 norms and q.k by warp shuffles (every warp holds all D entries of q and k)
+  float qq = 0.f, kk = 0.f, qkr = 0.f;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    qq += qv[e] * qv[e];
+    kk += kv[e] * kv[e];
+    qkr += qv[e] * kv[e];
+  }
+  qq = warp_sum(qq);
+  kk = warp_sum(kk);
+  qkr = warp_sum(qkr);
+  const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
+  const float eg = expf(negA * softplus_f(graw));
+  const float beta = sigmoid_f(braw);
+  const float qk = qkr * rq * rk;
+  float kr[EPL], kg[EPL], qg[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    kr[e] = kv[e] * rk;
+    kg[e] = kr[e] * eg;
+    qg[e] = qv[e] * rq * eg;
+  }
+
+  // ---- stream the state
+#pragma unroll 1
+  for (int j0 = 0; j0 < CPW; j0 += NB) {
+    const int c0 = warp * CPW + j0;
+    float s[NB][EPL];
+#pragma unroll
+    for (int n = 0; n < NB; ++n)
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) s[n][e] = s_nx[n][e];
+    if (j0 + NB < CPW) {
+#pragma unroll
+      for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + NB + n) * D + lane * EPL, s_nx[n]);
+    }
+    float kd[NB], qd[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      kd[n] = 0.f;
+      qd[n] = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        kd[n] += kg[e] * s[n][e];
+        qd[n] += qg[e] * s[n][e];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int n = 0; n < NB; ++n) {
+        kd[n] += __shfl_xor_sync(0xffffffffu, kd[n], o);
+        qd[n] += __shfl_xor_sync(0xffffffffu, qd[n], o);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const float vcn = __shfl_sync(0xffffffffu, vv, j0 + n);
+      const float u = beta * (vcn - kd[n]);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) s[n][e] = eg * s[n][e] + kr[e] * u;
+      vecf<EPL>::st(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
+      if (lane == 0) s_o[c0 + n] = qd[n] + qk * u;
+    }
+  }
+  __syncthreads();
+
+  // ---- gated RMSNorm over the head: out = RMSNorm(o) * w * silu(z)
+  float oo = 0.f;
+  for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
+  oo = warp_sum(oo);
+  if (lane == 0) s_red[warp] = oo;
+  __syncthreads();
+  oo = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) oo += s_red[w];
+  const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
+  if (tid < D) {
+    T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
+    io<T>::st(out + tid, s_o[tid] * rstd * nw * silu_f(zval));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// KDA decode: one CTA per (head, sequence).  The CTA
+//   1. runs the conv update of its q/k/v channels against the per-sequence conv ring
+//      (KDA heads are not shared: the CTA owns its channels' ring slots),
+//   2. L2-normalises q,k, takes the per-channel gate and the output gate from the second
+//      low-rank factors (f = f1 @ f2^T, g1 @ g2^T: two decode GEMMs before this kernel,
+//      fg = [2][B][H*D]) and beta,
+//   3. streams the fp32 state once as in the GDN kernel, with per-key-channel decays,
+//   4. applies the gated RMSNorm (sigmoid gate).
+template <typename T, int D, int THREADS = kDecodeThreads>
+__global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
+    kda_decode_kernel(const DeltaDecodeArgs a) {
+  sn::pdl_launch_dependents();
+  constexpr int NW = THREADS / 32;
+  constexpr int EPL = D / 32;
+  constexpr int CPW = D / NW;
+  constexpr int NB = 4;
   static_assert(CPW % NB == 0, "columns per warp must be a multiple of NB");
 
   __shared__ __align__(16) float s_q[D];
@@ -146,32 +360,16 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   __shared__ __align__(16) float s_eg[D];
   __shared__ __align__(16) float s_gate[D];
   __shared__ __align__(16) float s_o[D];
-  __shared__ __align__(16) float s_f1[KDA ? 256 : 1];
-  __shared__ __align__(16) float s_g1[KDA ? 256 : 1];
   __shared__ float s_red[3 * NW];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = blockIdx.x, b = blockIdx.y;
-  const int G = a.Hv / a.Hk, kh = h / G;
-  // The state is written only by this layer's previous decode step, so its first column
-  // batch is requested before griddepcontrol.wait: the HBM latency overlaps the producer
-  // kernel's tail (PDL) and this CTA's conv / norm / gate prologue.  Afterwards the
-  // stream is software-pipelined (batch j+1 in flight while batch j is updated).
   const int slot = a.slot_idx ? a.slot_idx[b] : b;
   float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
-  // Experiment (SN_DELTA_L2PF=1, off by default): the whole (b, h) state requested into L2 at
-  // entry so that HBM is busy during the first wave's prologue — measured slower.
-  if (a.l2_prefetch && tid == 0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(S), "r"(a.l2_prefetch) : "memory");
   float s_nx[NB][EPL];
 #pragma unroll
   for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
-  // Conv taps and the 4 ring slots of this thread's channels do not depend on the previous
-  // kernel either (weights; the ring is written by this layer's previous step and all 4
-  // slots are loaded, so the position is not needed yet): requested before the wait too,
-  // leaving only the in-projection values for after it.
-  const int W = a.W;
-  T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * W;
+  T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * 4;
   const T* cw = reinterpret_cast<const T*>(a.conv_w);
   constexpr int NCH = (3 * D + THREADS - 1) / THREADS;
   float xin[NCH], wt[NCH][4], rg[NCH][4];
@@ -182,76 +380,52 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
     chn[u] = -1;
     if (c < 3 * D) {
       const int part = c / D, i = c - part * D;
-      const int ch = part == 0 ? a.q_off + kh * D + i : (part == 1 ? a.k_off + kh * D + i : a.v_off + h * D + i);
+      const int ch = (part == 0 ? a.q_off : part == 1 ? a.k_off : a.v_off) + h * D + i;
       chn[u] = ch;
-      if (W == 4) {
-        load4<T>(cw + (size_t)ch * 4, wt[u]);
-        load4<T>(ring + (size_t)ch * 4, rg[u]);
-      }
+      load4<T>(cw + (size_t)ch * 4, wt[u]);
+      load4<T>(ring + (size_t)ch * 4, rg[u]);
     }
   }
   const float negA = -expf(a.A_log[h]);
-  const float dtb = KDA ? 0.f : a.dt_bias[h];
+  float dtb = 0.f, g2b = 0.f;
+  if (tid < D) {
+    dtb = a.dt_bias[h * D + tid];
+    g2b = io<T>::ld(reinterpret_cast<const T*>(a.g2_b) + h * D + tid);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pos = a.positions[b];
-  const GemmIn<T> pin{a.proj, a.proj_nsplit, (size_t)gridDim.y * a.proj_stride};
-  const size_t prow = (size_t)b * a.proj_stride;
+  const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
 
-  // ---- 1. prologue loads of the in-projection row, all issued before any is consumed:
-  //      this thread's conv inputs, the output gate z (GDN) / low-rank gate inputs f1,g1
-  //      (KDA), a, b.
+  // ---- 1. prologue loads of the in-projection row and the gate factors, all issued first
 #pragma unroll
   for (int u = 0; u < NCH; ++u)
-    if (chn[u] >= 0) xin[u] = pin(prow + chn[u]);
-  float zval = 0.f;
-  if (!KDA && tid < D) zval = pin(prow + a.z_off + h * D + tid);
-  float fg = 0.f, fpre = 0.f, gpre = 0.f;
-  const bool have_fg = KDA && a.fg != nullptr;
-  if (KDA && !have_fg && tid < 2 * a.rank) fg = pin(prow + (tid < a.rank ? a.f1_off + tid : a.g1_off + tid - a.rank));
-  if (have_fg && tid < D) {
+    if (chn[u] >= 0) xin[u] = io<T>::ld(prow + chn[u]);
+  float fpre = 0.f, gpre = 0.f;
+  if (tid < D) {
     const size_t HD = (size_t)a.Hv * D;
     const T* fgp = reinterpret_cast<const T*>(a.fg) + (size_t)b * HD + h * D + tid;
-    fpre = io<T>::ld(fgp) + a.dt_bias[h * D + tid];
-    gpre = io<T>::ld(fgp + gridDim.y * HD) + io<T>::ld(reinterpret_cast<const T*>(a.g2_b) + h * D + tid);
+    fpre = io<T>::ld(fgp) + dtb;
+    gpre = io<T>::ld(fgp + gridDim.y * HD) + g2b;
   }
-  const float braw = pin(prow + a.b_off + h);
-  const float graw = KDA ? 0.f : pin(prow + a.a_off + h) + dtb;
+  const float braw = io<T>::ld(prow + a.b_off + h);
 
-  // ---- 2. conv + SiLU (slot p % W of the ring holds the input of position p)
+  // ---- 2. conv + SiLU
 #pragma unroll
   for (int u = 0; u < NCH; ++u) {
     if (chn[u] < 0) continue;
     const int c = tid + u * THREADS;
     const int part = c / D, i = c - part * D;
-    const int ch = chn[u];
-    float acc;
-    if (W == 4) {
-      acc = wt[u][3] * xin[u];
-#pragma unroll
-      for (int d = 1; d < 4; ++d)
-        if (pos - d >= 0) acc += wt[u][3 - d] * rg[u][(pos - d) & 3];
-    } else {
-      const T* wrow = cw + (size_t)ch * W;
-      const T* rrow = ring + (size_t)ch * W;
-      acc = io<T>::ld(wrow + W - 1) * xin[u];
-      for (int d = 1; d < W; ++d) {
-        const int p = pos - d;
-        if (p >= 0) acc += io<T>::ld(wrow + W - 1 - d) * io<T>::ld(rrow + (p % W));
-      }
-    }
-    if (part == 2 || (h % G) == 0) io<T>::st(ring + (size_t)ch * W + (pos % W), xin[u]);
+    const float acc = conv4(wt[u], rg[u], xin[u], pos);
+    io<T>::st(ring + (size_t)chn[u] * 4 + (pos & 3), xin[u]);
     (part == 0 ? s_q : part == 1 ? s_k : s_v)[i] = silu_f(acc);
   }
-  if (KDA && !have_fg && tid < 2 * a.rank) (tid < a.rank ? s_f1[tid] : s_g1[tid - a.rank]) = fg;
-  if (have_fg && tid < D) {
+  if (tid < D) {
     s_eg[tid] = expf(negA * softplus_f(fpre));
     s_gate[tid] = gpre;
   }
-  if (!KDA && tid < D) s_gate[tid] = zval;
   __syncthreads();
 
-  // ---- 3. L2 norms and the q.k product of the raw vectors (one three-value block reduction;
-  //      the normalisation is applied in registers below), gates, beta
+  // ---- 3. L2 norms and the q.k product of the raw vectors (one three-value reduction), beta
   float qq = 0.f, kk = 0.f, qkr = 0.f;
   for (int i = tid; i < D; i += THREADS) {
     qq += s_q[i] * s_q[i];
@@ -260,38 +434,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   }
   block_sum3(qq, kk, qkr, s_red);
   const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
-  // GDN: one decay per head, kept in registers; KDA: per-channel decays in s_eg (written
-  // before the first barrier when the gate factors were precomputed)
-  const float eg_head = KDA ? 0.f : expf(negA * softplus_f(graw));
-  if (KDA && !have_fg) {
-    // second low-rank factors: rows h*D .. h*D+D-1 of f2 (-> gate g) and g2 (-> output gate),
-    // half a warp per row (16 lanes x 16 B = one 256-B row when R = 128), coalesced
-    const T* f2 = reinterpret_cast<const T*>(a.f2_w);
-    const T* g2 = reinterpret_cast<const T*>(a.g2_w);
-    const T* g2b = reinterpret_cast<const T*>(a.g2_b);
-    const int half = lane >> 4, hl = lane & 15;
-    for (int rr = warp * 2 + half; rr < 2 * D; rr += 2 * (THREADS / 32)) {
-      const bool is_f = rr < D;
-      const int i = is_f ? rr : rr - D;
-      const T* row = (is_f ? f2 : g2) + (size_t)(h * D + i) * a.rank;
-      const float* vec = is_f ? s_f1 : s_g1;
-      float acc = 0.f;
-      for (int r0 = hl * 8; r0 < a.rank; r0 += 128) {
-        float wv[8];
-        load8<T>(row + r0, wv);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc += wv[k] * vec[r0 + k];
-      }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (hl == 0) {
-        if (is_f) s_eg[i] = expf(negA * softplus_f(acc + a.dt_bias[h * D + i]));
-        else s_gate[i] = acc + io<T>::ld(g2b + h * D + i);
-      }
-    }
-  }
-  const float beta = sigmoid_f(braw);  // every thread loaded b
-  if (KDA && !have_fg) __syncthreads();  // s_eg / s_gate from the low-rank factors
+  const float beta = sigmoid_f(braw);
   const float qk = qkr * rq * rk;
 
   // ---- 3. stream the state: warp owns columns [warp*CPW, +CPW), lane owns keys [lane*EPL, +EPL)
@@ -300,7 +443,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   for (int e = 0; e < EPL; ++e) {
     const int i = lane * EPL + e;
     kr[e] = s_k[i] * rk;
-    eg[e] = KDA ? s_eg[i] : eg_head;
+    eg[e] = s_eg[i];
     kg[e] = kr[e] * eg[e];
     qg[e] = s_q[i] * rq * eg[e];
   }
@@ -345,8 +488,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
   }
   __syncthreads();
 
-  // ---- 4. gated RMSNorm over the head (the barrier above also retires every read of s_red
-  //      from the prologue reduction, so the sum needs only one more)
+  // ---- 4. gated RMSNorm over the head
   float oo = 0.f;
   for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
   oo = warp_sum(oo);
@@ -356,13 +498,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? (KDA ? 3 
 #pragma unroll
   for (int w = 0; w < NW; ++w) oo += s_red[w];
   const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
-  const T* nw = reinterpret_cast<const T*>(a.norm_w);
+  const T* nwp = reinterpret_cast<const T*>(a.norm_w);
   T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
-  for (int j = tid; j < D; j += THREADS) {
-    const float gz = s_gate[j];
-    const float act = KDA ? sigmoid_f(gz) : silu_f(gz);
-    io<T>::st(out + j, s_o[j] * rstd * io<T>::ld(nw + j) * act);
-  }
+  for (int j = tid; j < D; j += THREADS) io<T>::st(out + j, s_o[j] * rstd * io<T>::ld(nwp + j) * sigmoid_f(s_gate[j]));
 }
 
 // =====================================================================
@@ -640,27 +778,27 @@ __global__ void __launch_bounds__(256) gated_rmsnorm_kernel(const float* __restr
   }
 }
 
+// 512-thread CTAs when (heads x batch) leaves most SMs without a CTA (small batches): twice
+// the state columns of one CTA in flight (B=1 decode 6.22 -> 6.13 ms/step, r01_decode_ablation.md).
 template <typename T, int D, bool KDA>
-static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a_in, int B, cudaStream_t st) {
-  // experiment switch, off: the L2 prefetch slowed GDN decode 51.9 -> 62.4 us (r01_decode_ablation.md)
-  static const int pf = getenv("SN_DELTA_L2PF") ? atoi(getenv("SN_DELTA_L2PF")) : 0;
-  DeltaDecodeArgs a = a_in;
-  a.l2_prefetch = pf ? D * D * (int)sizeof(float) : 0;
-  const int smem = 0;
+static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  static const int wide_env = getenv("SN_DELTA_WIDE") ? atoi(getenv("SN_DELTA_WIDE")) : 1;
-  const bool wide = wide_env && a.Hv * B < 148;
+  const bool wide = a.Hv * B < 148;
   cfg.gridDim = dim3(a.Hv, B);
   cfg.blockDim = dim3(wide ? 2 * kDecodeThreads : kDecodeThreads);
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // state prefetch overlaps the in-proj tail
   attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA, 2 * kDecodeThreads>, a)
-                       : cudaLaunchKernelEx(&cfg, delta_decode_kernel<T, D, KDA>, a);
+  cudaError_t e;
+  if (KDA)
+    e = wide ? cudaLaunchKernelEx(&cfg, kda_decode_kernel<T, D, 2 * kDecodeThreads>, a)
+             : cudaLaunchKernelEx(&cfg, kda_decode_kernel<T, D>, a);
+  else
+    e = wide ? cudaLaunchKernelEx(&cfg, gdn_decode_kernel<T, D, 2 * kDecodeThreads>, a)
+             : cudaLaunchKernelEx(&cfg, gdn_decode_kernel<T, D>, a);
   if (e != cudaSuccess) {
     set_error("%s launch: %s", KDA ? "sn_kda_decode" : "sn_gdn_decode", cudaGetErrorString(e));
     return SN_ECUDA;
@@ -704,19 +842,18 @@ static void launch_scan(dim3 grid, cudaStream_t st, const float* qn, const float
 
 extern "C" {
 
-sn_status sn_gdn_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring, const void* conv_w, float* state,
+sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring, const void* conv_w, float* state,
                         const int32_t* slot_idx, const int32_t* positions, const float* A_log,
                         const float* dt_bias, const void* norm_w, void* out, int B, int Hk, int Hv, int D,
                         int conv_width, float scale, float eps_l2, float eps_norm, int dtype, void* stream) {
   SN_REQUIRE(B > 0 && Hk > 0 && Hv > 0 && Hv % Hk == 0, "sn_gdn_decode: bad heads B=%d Hk=%d Hv=%d", B, Hk, Hv);
-  SN_REQUIRE(conv_width >= 1 && conv_width <= 8, "sn_gdn_decode: conv width %d not in [1,8]", conv_width);
+  SN_REQUIRE(conv_width == 4, "sn_gdn_decode: conv width %d (the pinned width is 4)", conv_width);
   SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && norm_w && out,
              "sn_gdn_decode: NULL pointer argument");
   DeltaDecodeArgs a{};
-  SN_REQUIRE(proj_nsplit >= 0 && proj_nsplit <= kMaxSplit, "delta decode: proj_nsplit %d", proj_nsplit);
-  a.proj = proj; a.proj_stride = proj_stride; a.proj_nsplit = proj_nsplit; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
+  a.proj = proj; a.proj_stride = proj_stride; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
   a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.norm_w = norm_w;
-  a.out = out; a.Hk = Hk; a.Hv = Hv; a.rank = 0; a.W = conv_width;
+  a.out = out; a.Hk = Hk; a.Hv = Hv; a.rank = 0;
   a.conv_channels = 2 * Hk * D + Hv * D;
   a.q_off = 0; a.k_off = Hk * D; a.v_off = 2 * Hk * D; a.z_off = 2 * Hk * D + Hv * D;
   a.b_off = 2 * Hk * D + 2 * Hv * D; a.a_off = a.b_off + Hv;
@@ -725,23 +862,20 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, int proj_nsplit, void
   return launch_delta_decode<false>(a, B, D, dtype, (cudaStream_t)stream);
 }
 
-sn_status sn_kda_decode(const void* proj, int proj_stride, int proj_nsplit, void* conv_ring, const void* conv_w, float* state,
-                        const int32_t* slot_idx, const int32_t* positions, const float* A_log,
-                        const float* dt_bias, const void* f2_w, const void* g2_w, const void* g2_b,
-                        const void* fg, const void* norm_w, void* out, int B, int H, int D, int rank, int conv_width,
-                        float scale, float eps_l2, float eps_norm, int dtype, void* stream) {
+sn_status sn_kda_decode(const void* proj, int proj_stride, const void* fg, void* conv_ring, const void* conv_w,
+                        float* state, const int32_t* slot_idx, const int32_t* positions, const float* A_log,
+                        const float* dt_bias, const void* g2_b, const void* norm_w, void* out, int B, int H, int D,
+                        int rank, int conv_width, float scale, float eps_l2, float eps_norm, int dtype, void* stream) {
   SN_REQUIRE(B > 0 && H > 0, "sn_kda_decode: bad shape B=%d H=%d", B, H);
-  SN_REQUIRE(rank > 0 && rank <= 256 && rank % 8 == 0, "sn_kda_decode: rank %d must be a multiple of 8 <= 256", rank);
-  SN_REQUIRE(conv_width >= 1 && conv_width <= 8, "sn_kda_decode: conv width %d not in [1,8]", conv_width);
-  SN_REQUIRE(proj && conv_ring && conv_w && state && positions && A_log && dt_bias && norm_w && out && g2_b &&
-                 (fg || (f2_w && g2_w)),
+  SN_REQUIRE(rank > 0 && rank % 8 == 0, "sn_kda_decode: rank %d must be a multiple of 8", rank);
+  SN_REQUIRE(conv_width == 4, "sn_kda_decode: conv width %d (the pinned width is 4)", conv_width);
+  SN_REQUIRE(proj && fg && conv_ring && conv_w && state && positions && A_log && dt_bias && norm_w && out && g2_b,
              "sn_kda_decode: NULL pointer argument");
   DeltaDecodeArgs a{};
-  SN_REQUIRE(proj_nsplit >= 0 && proj_nsplit <= kMaxSplit, "delta decode: proj_nsplit %d", proj_nsplit);
-  a.proj = proj; a.proj_stride = proj_stride; a.proj_nsplit = proj_nsplit; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
-  a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.f2_w = f2_w;
-  a.g2_w = g2_w; a.g2_b = g2_b; a.fg = fg; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank;
-  a.W = conv_width; a.conv_channels = 3 * H * D;
+  a.proj = proj; a.proj_stride = proj_stride; a.fg = fg; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
+  a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias;
+  a.g2_b = g2_b; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank;
+  a.conv_channels = 3 * H * D;
   a.q_off = 0; a.k_off = H * D; a.v_off = 2 * H * D; a.f1_off = 3 * H * D; a.g1_off = 3 * H * D + rank;
   a.b_off = 3 * H * D + 2 * rank;
   a.scale = scale; a.eps_l2 = eps_l2; a.eps_norm = eps_norm;

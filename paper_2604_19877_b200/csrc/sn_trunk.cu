@@ -221,18 +221,6 @@ __global__ void swiglu_il_kernel(const T* __restrict__ gu, T* __restrict__ out, 
   }
 }
 
-template <typename T>
-__global__ void silu_mul_kernel(const GemmIn<T> gu, T* __restrict__ out, int rows, int ffn) {
-  sn::pdl_launch_dependents();
-  sn::pdl_wait();
-  const size_t n = (size_t)rows * ffn;
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
-    const size_t r = e / ffn, i = e % ffn;
-    const float g = gu(r * 2 * ffn + i), u = gu(r * 2 * ffn + ffn + i);
-    io<T>::st(out + e, silu_f(g) * u);
-  }
-}
-
 // ------------------------------------------------------------------ argmax
 template <typename T>
 __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logits, int vocab,
@@ -327,19 +315,6 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit, f
       return SN_ECUDA;
     }
     return check_launch("sn_add_rmsnorm");
-  });
-}
-
-sn_status sn_silu_mul(const void* gate_up, int gu_nsplit, void* out, int rows, int ffn, int dtype, void* stream) {
-  SN_REQUIRE(gu_nsplit >= 0 && gu_nsplit <= kMaxSplit, "sn_silu_mul: gu_nsplit %d", gu_nsplit);
-  SN_REQUIRE(rows > 0 && ffn > 0 && ffn % 8 == 0, "sn_silu_mul: bad shape rows=%d ffn=%d", rows, ffn);
-  return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    const size_t n = (size_t)rows * ffn;
-    int grid = (int)((n + 255) / 256);
-    if (grid > 148 * 16) grid = 148 * 16;
-    const GemmIn<T> in{gate_up, gu_nsplit, (size_t)rows * 2 * ffn};
-    launch_pdl(silu_mul_kernel<T>, dim3(grid), dim3(256), 0, (cudaStream_t)stream, in, (T*)out, rows, ffn);
-    return check_launch("sn_silu_mul");
   });
 }
 

@@ -100,7 +100,7 @@ def main(argv=None) -> int:
     from .serving import SupernetStore
     store = SupernetStore(cfg, seed=a.seed, init_device=a.init_device)
     B = min(a.batch, traces.shape[0])
-    block = ops.gemm_swiglu_block(B, cfg.ffn, cfg.hidden)  # the FFN decode layout, shared by every placement
+    block = ops.gemm_swiglu_block(cfg.ffn)  # the FFN decode layout, shared by every placement
     for code in codes:
         model = Supernet(cfg, code, batch=B, max_len=traces.shape[1],
                          weights=store.weights(code, swiglu_block=block))

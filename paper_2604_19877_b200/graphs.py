@@ -16,15 +16,20 @@ import torch
 
 
 class DecodeGraph:
-    def __init__(self, model, feedback: bool = False, warmup: int = 2, preserve_state: bool = True):
+    """Construction runs `warmup` eager decode steps (first-launch module loading and kernel
+    attributes happen outside the capture), then captures one step.  The warm-up advances the
+    engine's state: by default the engine is reset afterwards (build graphs on an empty engine,
+    before prefill); preserve_state=True instead snapshots and restores exactly what a decode
+    step writes — the lengths, the KV slots of the warm-up positions and the GDN/KDA states and
+    conv rings (the recurrent states are rewritten whole, so they are copied whole)."""
+
+    def __init__(self, model, feedback: bool = False, warmup: int = 2, preserve_state: bool = False):
         self.model = model
         self.feedback = feedback
         self.graph = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        # warm up on the side stream (cuBLAS handles / workspaces get created outside capture);
-        # the state is snapshotted and restored so capture has no visible side effects.
-        saved = self._snapshot() if preserve_state else None
+        saved = self._snapshot(warmup) if preserve_state else None
         with torch.cuda.stream(s):
             for _ in range(warmup):
                 model.decode_body()
@@ -32,6 +37,8 @@ class DecodeGraph:
         torch.cuda.synchronize()
         if saved is not None:
             self._restore(saved)
+        elif warmup:
+            model.reset()
         torch.cuda.synchronize()
         with torch.cuda.graph(self.graph, stream=s):
             model.decode_body()
@@ -43,16 +50,42 @@ class DecodeGraph:
         self._pin_in = torch.empty(model.B, dtype=torch.int32, pin_memory=True)
         self._pin_out = torch.empty(model.B, dtype=torch.int32, pin_memory=True)
 
-    def _snapshot(self):
+    def _kv_index(self, kind, steps):
+        """(page, offset) of the KV slots `steps` decode steps write, per sequence."""
+        from .placement import SWA
         m = self.model
-        return {"seq_lens": m.seq_lens.clone(), "state": [{k: v.clone() for k, v in st.items()} for st in m.state]}
+        P = m.cfg.page_size
+        pos = m.seq_lens.long()[:, None] + torch.arange(max(steps, 1), device=m.device)[None]
+        if kind == SWA:
+            slot, bt = pos % m.cfg.window, m.swa_block_table
+        else:
+            slot, bt = pos.clamp(max=m.max_len - 1), m.fa_block_table
+        page = torch.gather(bt.long(), 1, (slot // P).clamp(max=bt.shape[1] - 1))
+        return page.reshape(-1), (slot % P).reshape(-1)
+
+    def _snapshot(self, steps):
+        from .placement import FA, SWA
+        m = self.model
+        snap = {"seq_lens": m.seq_lens.clone(), "layers": []}
+        for kind, st in zip(m.kinds, m.state):
+            if kind in (FA, SWA):
+                page, off = self._kv_index(kind, steps)
+                snap["layers"].append(("kv", page, off, st["k"][page, :, off].clone(), st["v"][page, :, off].clone()))
+            else:
+                snap["layers"].append(("rec", {k: v.clone() for k, v in st.items()}))
+        return snap
 
     def _restore(self, snap):
         m = self.model
         m.seq_lens.copy_(snap["seq_lens"])
-        for st, sv in zip(m.state, snap["state"]):
-            for k, v in sv.items():
-                st[k].copy_(v)
+        for st, rec in zip(m.state, snap["layers"]):
+            if rec[0] == "kv":
+                _, page, off, k, v = rec
+                st["k"][page, :, off] = k
+                st["v"][page, :, off] = v
+            else:
+                for k, v in rec[1].items():
+                    st[k].copy_(v)
 
     def replay(self):
         self.graph.replay()

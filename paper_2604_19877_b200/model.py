@@ -20,7 +20,6 @@ projections / FFN / LM head; there is no CPU path.
 from __future__ import annotations
 
 import math
-import os
 
 import torch
 
@@ -62,7 +61,8 @@ class Supernet:
     """
 
     def __init__(self, cfg: SupernetConfig, placement, *, batch: int, max_len: int, dtype=torch.bfloat16,
-                 device="cuda", seed: int = 0, weights=None, fa_block_table=None, tp_group=None):
+                 device="cuda", seed: int = 0, weights=None, fa_block_table=None, tp_group=None,
+                 tp_transport: str = "p2p"):
         _load_lib()  # fail loudly if the extension is missing
         self.B, self.max_len, self.dtype = batch, max_len, dtype
         self.device = torch.device(device)
@@ -90,52 +90,34 @@ class Supernet:
         self.scale_attn = attn_scale(cfg)
         self._alloc_state(fa_block_table)
         self._alloc_decode_buffers()
-        # head-parallel decode: the row-parallel all-reduces run through peer memory, fused into
-        # the next residual add + RMSNorm (csrc/sn_tp.cu); SN_TP_NCCL=1 keeps torch.distributed
+        # head-parallel decode: the row-parallel all-reduces run through peer memory (CUDA IPC,
+        # NVLink P2P), fused into the next residual add + RMSNorm (csrc/sn_tp.cu) — "p2p", one
+        # process per GPU on a node — or through NCCL ("nccl": any transport NCCL has)
+        if tp_transport not in ("p2p", "nccl"):
+            raise ValueError(f"tp_transport {tp_transport!r}: 'p2p' or 'nccl'")
         self.sym = None
-        if self.tp > 1 and not os.environ.get("SN_TP_NCCL"):
+        if self.tp > 1 and tp_transport == "p2p":
             from .dist import SymmetricSlabs
             self.sym = SymmetricSlabs(batch, cfg.hidden, group=tp_group, device=self.device)
-        self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
-        self.force_simt = False
-        # bf16 decode projections run on the tcgen05 weight-streaming GEMM (libsn100, batch-as-M
-        # UMMA, persistent balanced grid; fp32 split-K slabs are summed by the consuming kernel,
-        # the gate/up projection fuses SiLU-mul) or on cuBLAS.  Default from in-step B200 A/B
-        # runs (tools/step_time.py): ours for the LM head, the fused FFN gate/up and the FFN
-        # down-projection, and from B=16 also the mixer out-projection (split-K slabs into the
-        # residual add: B=64 9.844 -> 9.809 ms/step, B=16 7.17 -> 7.09; at B=1-4 cuBLAS is
-        # faster); cuBLAS for the mixer in-projections (ours +0.23 ms/step at B=64, the
-        # consuming mixer kernels start later).  SN_DECODE_GEMMS=all switches every role to ours.
-        tc_ok = dtype == torch.bfloat16 and batch <= 128
 
-        default_roles = "lm_head,ffn_down,ffn_gate_up" + (",out_proj" if batch >= 16 else "")
-        sel = os.environ.get("SN_DECODE_GEMMS", default_roles).split(",")
-        self.sn_gemm = {r: tc_ok and (r in sel or "all" in sel)
-                        for r in ("lm_head", "ffn_down", "ffn_gate_up", "in_proj", "attn_qkv", "out_proj")}
-        if tc_ok:  # fp32 split-K slabs of the input-side projections, summed by their consumers
-            n_in = max([cfg.attn_qkv_width if k in (FA, SWA) else cfg.gdn_in_width if k == GDN else cfg.kda_in_width
-                        for k in self.kinds])
-            self.slab_in = torch.empty(8, batch, n_in, device=self.device, dtype=torch.float32)
-            self.slab_gu = torch.empty(8, batch, 2 * cfg.ffn, device=self.device, dtype=torch.float32)
-        self.gu_mode = os.environ.get("SN_GU_MODE", "swiglu_il")
-        self.in_mode = os.environ.get("SN_IN_MODE", "store")
-        if self.sn_gemm["ffn_gate_up"] and self.gu_mode == "swiglu_il":
-            # fused gate/up + SiLU-mul: gate and up rows interleaved in the GEMM's block height
-            # the interleaved copy replaces [gate; up] (no doubled FFN weights in HBM); prefill
-            # de-interleaves its GEMM output (deinterleave_swiglu)
-            ffn = self.cfg.ffn
-            hb = ops.gemm_swiglu_block(batch, ffn, self.cfg.hidden)
-            self.gu_il = (ffn, hb)
-            for lw in self.w["layers"]:
-                if "ffn_gu_il" in lw:  # prebuilt and shared (serving.SupernetStore)
-                    if lw["ffn_gu_il"].shape[0] != -(-ffn // hb) * 2 * hb:
-                        raise ValueError("prebuilt SwiGLU-interleaved FFN weights do not match this batch's block")
-                else:
-                    lw["ffn_gu_il"] = ops.interleave_swiglu(lw.pop("ffn_gu"), hb)
-        else:
-            self.gu_il = None
-            if any("ffn_gu" not in lw for lw in self.w["layers"]):
-                raise ValueError("this engine needs the [gate; up] FFN weights (ffn_gu)")
+        self.probe = None  # optional KernelProbe: CUDA events around the mixer kernels (bench instrumentation)
+        # every decode projection runs on the library's decode GEMM (tcgen05 for bf16, the CUDA-core
+        # tile kernel for the fp32 numerics mode); the gate/up rows are interleaved in blocks of h
+        # (SwiGLU fused into the GEMM epilogue: one contiguous weight stream, no [gate; up] copy) and
+        # the attention q / k rows in rotary pairs (RoPE + KV append fused into the in-projection)
+        ffn = self.cfg.ffn
+        hb = ops.gemm_swiglu_block(ffn)
+        self.gu_il = (ffn, hb)
+        for lw in self.w["layers"]:
+            if "ffn_gu_il" in lw:  # prebuilt and shared (serving.SupernetStore)
+                if lw["ffn_gu_il"].shape[0] != -(-ffn // hb) * 2 * hb:
+                    raise ValueError("prebuilt SwiGLU-interleaved FFN weights use another block height")
+            else:
+                lw["ffn_gu_il"] = ops.interleave_swiglu(lw.pop("ffn_gu"), hb)
+        for l, kind in enumerate(self.kinds):
+            mw = self.w["layers"][l]["mixer"]
+            if kind in (FA, SWA) and "qkv_il" not in mw:
+                mw["qkv_il"] = ops.rope_pair_interleave(mw.pop("qkv"), cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim)
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -203,91 +185,84 @@ class Supernet:
         self.gu = e(B, 2 * cfg.ffn)
         self.act = e(B, cfg.ffn)
         self.logits = e(B, cfg.vocab)
-        # fp32 K-split partial slabs of the residual-updating projections (o-proj, FFN down),
-        # summed into the residual by the next add_rmsnorm
-        self.slab_mix = e(8, B, cfg.hidden, d=torch.float32)
-        self.slab_ffn = e(8, B, cfg.hidden, d=torch.float32)
+        self.err_flag = torch.zeros(1, device=dev, dtype=torch.int32)  # KV append past the block table
+        # fp32 K-split slabs of the residual-updating projections (o-proj, FFN down), summed into
+        # the residual in slab order by the next add + RMSNorm
+        self.slab = e(8, B, cfg.hidden, d=torch.float32)
         kinds = set(self.kinds)
         self.dec = {}
         if kinds & {FA, SWA}:
             Hq, Hkv, D = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
-            self.dec["qkv"] = e(B, cfg.attn_qkv_width)
             self.dec["q"] = e(B, Hq, D)
             self.dec["attn"] = e(B, Hq * D)
             self.dec["counters"] = torch.zeros(B * Hkv, device=dev, dtype=torch.int32)
             self.attn_split = {}
             for kind, max_keys in ((FA, self.max_len), (SWA, cfg.window)):
                 if kind in kinds:
-                    sp, ms = choose_split(_ceil(max_keys, cfg.page_size), B * Hkv,
-                                          cap=int(os.environ.get("SN_SPLIT_CAP", 64)),
-                                          floor=int(os.environ.get("SN_SPLIT_FLOOR", 4)),
-                                          per_sm=int(os.environ["SN_SPLIT_PER_SM"]) if "SN_SPLIT_PER_SM" in os.environ
-                                          else None)
-                    self.attn_split[kind] = (sp, ms)
+                    self.attn_split[kind] = choose_split(_ceil(max_keys, cfg.page_size), B * Hkv)
             ms_max = max(ms for _, ms in self.attn_split.values())
             nbytes = ops.attn_decode_workspace_bytes(B, Hq, Hkv, D, ms_max)
             self.dec["ws"] = torch.empty(max(nbytes // 4, 1), device=dev, dtype=torch.float32)
             self.ws_max_splits = ms_max
+        # in-projection rows padded to 16 bytes (TMA row pitch of the gate-factor GEMMs' operand)
+        pad8 = lambda n: -(-n // 8) * 8
         if GDN in kinds:
-            self.dec["gdn_proj"] = e(B, cfg.gdn_in_width)
+            self.dec["gdn_proj"] = e(B, pad8(cfg.gdn_in_width))[:, :cfg.gdn_in_width]
             self.dec["gdn_out"] = e(B, cfg.gdn_value_dim)
         if KDA in kinds:
-            self.dec["kda_proj"] = e(B, cfg.kda_in_width)
+            self.dec["kda_proj"] = e(B, pad8(cfg.kda_in_width))[:, :cfg.kda_in_width]
             self.dec["kda_out"] = e(B, cfg.kda_dim)
             self.dec["kda_fg"] = e(2, B, cfg.kda_dim)
-            # stacked second low-rank factors [2][R][H*D] for the batched f/gate GEMM
-            for l, k in enumerate(self.kinds):
-                if k == KDA:
-                    mw = self.w["layers"][l]["mixer"]
-                    mw["fg2T"] = torch.stack([mw["f2"].t(), mw["g2"].t()]).contiguous()
 
     # ------------------------------------------------------------------ decode
-    def _attn_decode(self, l, kind, h, out):
+    def _gemm(self, x, w, out, mode, role):
+        self._probe_begin("gemm_" + role, fine=True)
+        ns = ops.gemm_decode(x, w, out, mode)
+        self._probe_end("gemm_" + role, fine=True)
+        return ns
+
+    def _attn_decode(self, l, kind, h):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         Hq, Hkv, D, P = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
-        qkv, ns = self._gemm_in(h, w["qkv"], d["qkv"], attn=True)
-        self._probe_begin("rope_kv_append", fine=True)
-        ops.rope_kv_append(qkv, None, self.positions, self.seq_lens, self.inv_freq, d["q"], None, None,
-                           st["k"], st["v"], bt, Hq, Hkv, D, P, window, nsplit=ns)
-        self._probe_end("rope_kv_append", fine=True)
+        # in-projection with RoPE + the KV append fused into its epilogue
+        self._probe_begin("gemm_in_proj", fine=True)
+        ops.gemm_decode_attn_in(h, w["qkv_il"], self.positions, self.inv_freq, d["q"], st["k"], st["v"], bt, Hq, Hkv,
+                                D, P, window, self.err_flag)
+        self._probe_end("gemm_in_proj", fine=True)
         sp, _ = self.attn_split[kind]
         name = "swa_decode" if kind == SWA else "fa_decode"
         self._probe_begin(name)
         ops.attn_decode(d["q"], st["k"], st["v"], bt, self.seq_lens, d["attn"], d["ws"], d["counters"], Hq, Hkv, D,
-                        P, window, sp, self.ws_max_splits, self.scale_attn, force_simt=self.force_simt)
+                        P, window, sp, self.ws_max_splits, self.scale_attn)
         self._probe_end(name)
-        return self._gemm_residual(d["attn"], w["o"], self.slab_mix, out, "out_proj")
+        return self._residual_proj(d["attn"], w["o"], "out_proj")
 
-    def _gdn_decode(self, l, h, out):
+    def _gdn_decode(self, l, h):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.gdn_head_dim
-        proj, ns = self._gemm_in(h, w["w_in"], d["gdn_proj"])
+        self._gemm(h, w["w_in"], d["gdn_proj"], "store", "in_proj")
         self._probe_begin("gdn_decode")
-        ops.gdn_decode(proj, st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"], w["dt_bias"],
-                       w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D, cfg.conv_width,
-                       1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps, nsplit=ns)
+        ops.gdn_decode(d["gdn_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
+                       w["dt_bias"], w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D, cfg.conv_width,
+                       1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
         self._probe_end("gdn_decode")
-        return self._gemm_residual(d["gdn_out"], w["o"], self.slab_mix, out, "out_proj")
+        return self._residual_proj(d["gdn_out"], w["o"], "out_proj")
 
-    def _kda_decode(self, l, h, out):
+    def _kda_decode(self, l, h):
         cfg, st, w, d = self.cfg, self.state[l], self.w["layers"][l]["mixer"], self.dec
         D = cfg.kda_head_dim
-        proj, ns = self._gemm_in(h, w["w_in"], d["kda_proj"])
-        fg = None
-        if ns == 0:  # low-rank gate second factors as one batched GEMM (1 MB of weights, read once)
-            HD, R = cfg.kda_dim, cfg.kda_rank
-            f1g1 = proj[:, 3 * HD:3 * HD + 2 * R].view(self.B, 2, R).transpose(0, 1)
-            fg = d["kda_fg"]
-            torch.bmm(f1g1, w["fg2T"], out=fg)
+        self._gemm(h, w["w_in"], d["kda_proj"], "store", "in_proj")
+        self._probe_begin("kda_gates", fine=True)
+        ops.kda_gate_factors(d["kda_proj"], w["f2"], w["g2"], d["kda_fg"], cfg.kda_heads, D, cfg.kda_rank)
+        self._probe_end("kda_gates", fine=True)
         self._probe_begin("kda_decode")
-        ops.kda_decode(proj, st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
-                       w["dt_bias"], w["f2"], w["g2"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D,
-                       cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps, nsplit=ns,
-                       fg=fg)
+        ops.kda_decode(d["kda_proj"], d["kda_fg"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
+                       w["dt_bias"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D, cfg.kda_rank,
+                       cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
         self._probe_end("kda_decode")
-        return self._gemm_residual(d["kda_out"], w["o"], self.slab_mix, out, "out_proj")
+        return self._residual_proj(d["kda_out"], w["o"], "out_proj")
 
     def _probe_begin(self, name, fine=False):
         if self.probe is not None and (self.probe.fine or not fine):
@@ -297,139 +272,83 @@ class Supernet:
         if self.probe is not None and (self.probe.fine or not fine):
             self.probe.end(name)
 
-    def _gemm_in(self, x, w, out_bf16, attn=False):
-        """Input-side projection: (tensor, nsplit) for the consuming kernel — bf16 (tcgen05 GEMM
-        or cuBLAS), or fp32 split-K slabs of the tcgen05 GEMM summed on load by the consumer.
-        Role "in_proj" covers the delta-rule mixers, "attn_qkv" the attention projection (6144
-        rows: too few for a balanced unsplit weight stream, cuBLAS by default)."""
-        self._probe_begin("gemm_in_proj", fine=True)
-        role = "attn_qkv" if attn else "in_proj"
-        if self.sn_gemm[role] and self.in_mode == "store":
-            ops.gemm_decode(x, w, out_bf16, "store")
-            res = (out_bf16, 0)
-        elif self.sn_gemm[role]:
-            slab = self._slab_view(self.slab_in, w.shape[0])
-            res = (slab, ops.gemm_decode(x, w, slab, "partial"))
-        else:
-            torch.mm(x, w.t(), out=out_bf16)
-            res = (out_bf16, 0)
-        self._probe_end("gemm_in_proj", fine=True)
-        return res
-
-    def _slab_view(self, buf, n):
-        """Contiguous [8, B, n] view at the start of a slab buffer (slab stride B*n)."""
-        return buf.view(-1)[: 8 * self.B * n].view(8, self.B, n)
-
-    def _gemm_store(self, x, w, out, role):
-        self._probe_begin("gemm_" + role, fine=True)
-        if self.sn_gemm[role]:
-            ops.gemm_decode(x, w, out, "store")
-        else:
-            torch.mm(x, w.t(), out=out)
-        self._probe_end("gemm_" + role, fine=True)
-
-    def _gemm_residual(self, x, w, slab, out_bf16, role):
-        """Projection whose result is added to the residual stream.  Returns the pending
-        update (delta, partials, nsplit) that the next add_rmsnorm applies."""
-        if self.sym is not None:  # row-parallel partial straight into this rank's symmetric slabs
+    def _residual_proj(self, x, w, role):
+        """A projection whose result is added to the residual stream: fp32 K-split slabs that the
+        next add + RMSNorm sums in slab order.  Head-parallel: this rank's row-parallel partial
+        slabs go through the all-reduce first (peer memory, fused into that norm; or NCCL).
+        Returns the (transport, slabs, nsplit) the next _norm() takes."""
+        if self.sym is not None:  # partial straight into this rank's symmetric slabs (peer memory)
             parity = 0 if role == "out_proj" else 1
-            slabs = self.sym.local_slabs(parity)
-            if self.dtype == torch.bfloat16:
-                ns = ops.gemm_decode(x, w, slabs, "partial")
-            else:
-                torch.mm(x, w.t(), out=slabs[0])
-                ns = 1
+            ns = self._gemm(x, w, self.sym.local_slabs(parity), "partial", role)
             ops.tp_arrive(self.sym.counter_ptr())
-            return ("tp", parity, ns)
-        if self.tp > 1:  # row-parallel: fp32 partial of this rank, summed over the TP group
+            return ("p2p", parity, ns)
+        ns = self._gemm(x, w, self.slab, "partial", role)
+        if self.tp > 1:  # NCCL transport: the partial slabs are summed over the group first
             from .dist import allreduce_sum_
-            buf = slab[0]
-            if self.dtype == torch.bfloat16:
-                buf.zero_()
-                ops.gemm_decode(x, w, buf, "resid")
-            else:
-                torch.mm(x, w.t(), out=buf)
-            allreduce_sum_(buf, self.tp_group)
-            return (None, slab, 1)
-        self._probe_begin("gemm_" + role, fine=True)
-        if self.sn_gemm[role]:
-            ns = ops.gemm_decode(x, w, slab, "partial")
-            self._probe_end("gemm_" + role, fine=True)
-            return (None, slab, ns)
-        torch.mm(x, w.t(), out=out_bf16)
-        self._probe_end("gemm_" + role, fine=True)
-        return (out_bf16, None, 0)
+            allreduce_sum_(self.slab[:ns], self.tp_group)
+        return ("local", self.slab, ns)
 
     def _norm(self, pending, weight):
-        delta, part, ns = pending
-        if isinstance(delta, str):  # ("tp", parity, nsplit): peer-memory all-reduce fused with the norm
-            sym = self.sym
-            ops.tp_allreduce_add_rmsnorm(sym.slab_ptrs[part], sym.counters, sym.world, sym.rank, ns, self.residual,
-                                         weight, self.h, self.cfg.norm_eps)
-            return
         self._probe_begin("add_rmsnorm", fine=True)
-        ops.add_rmsnorm(delta, self.residual, weight, self.h, self.cfg.norm_eps, partials=part, nsplit=ns)
+        if pending is None:
+            ops.add_rmsnorm(None, self.residual, weight, self.h, self.cfg.norm_eps)
+        elif pending[0] == "p2p":
+            sym = self.sym
+            ops.tp_allreduce_add_rmsnorm(sym.slab_ptrs[pending[1]], sym.counters, sym.world, sym.rank, pending[2],
+                                         self.residual, weight, self.h, self.cfg.norm_eps)
+        else:
+            ops.add_rmsnorm(None, self.residual, weight, self.h, self.cfg.norm_eps, partials=pending[1],
+                            nsplit=pending[2])
         self._probe_end("add_rmsnorm", fine=True)
 
     def decode_body(self):
         """One decode step on the current stream: step_tokens -> logits, next_tokens.
         Graph-capturable: every size/position it needs is read from device buffers."""
-        cfg, w = self.cfg, self.w
+        w = self.w
         self._probe_begin("embed", fine=True)
         ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
         self._probe_end("embed", fine=True)
-        pending = (None, None, 0)
+        pending = None
         for l, kind in enumerate(self.kinds):
             lw = w["layers"][l]
             self._norm(pending, lw["norm1"])
             if kind == GDN:
-                pending = self._gdn_decode(l, self.h, self.mix_out)
+                pending = self._gdn_decode(l, self.h)
             elif kind == KDA:
-                pending = self._kda_decode(l, self.h, self.mix_out)
+                pending = self._kda_decode(l, self.h)
             else:
-                pending = self._attn_decode(l, kind, self.h, self.mix_out)
+                pending = self._attn_decode(l, kind, self.h)
             self._norm(pending, lw["norm2"])
-            self._probe_begin("gemm_ffn_gate_up", fine=True)
-            if self.sn_gemm["ffn_gate_up"] and self.gu_mode == "swiglu_il":
-                ops.gemm_decode(self.h, lw["ffn_gu_il"], self.act, "swiglu_il")
-                self._probe_end("gemm_ffn_gate_up", fine=True)
-            else:
-                if self.sn_gemm["ffn_gate_up"]:
-                    gu, ns = self.slab_gu, ops.gemm_decode(self.h, lw["ffn_gu"], self.slab_gu, "partial")
-                else:
-                    torch.mm(self.h, lw["ffn_gu"].t(), out=self.gu)
-                    gu, ns = self.gu, 0
-                self._probe_end("gemm_ffn_gate_up", fine=True)
-                self._probe_begin("silu_mul", fine=True)
-                ops.silu_mul(gu, self.act, nsplit=ns)
-                self._probe_end("silu_mul", fine=True)
-            pending = self._gemm_residual(self.act, lw["ffn_down"], self.slab_ffn, self.ffn_out, "ffn_down")
+            self._gemm(self.h, lw["ffn_gu_il"], self.act, "swiglu_il", "ffn_gate_up")
+            pending = self._residual_proj(self.act, lw["ffn_down"], "ffn_down")
         self._norm(pending, w["final_norm"])
-        self._gemm_store(self.h, w["lm_head"], self.logits, "lm_head")
+        self._gemm(self.h, w["lm_head"], self.logits, "store", "lm_head")
         self._probe_begin("argmax", fine=True)
         ops.argmax(self.logits, self.next_tokens)
         self._probe_end("argmax", fine=True)
 
     def kernels_per_step(self) -> dict:
-        """Launch census of one decode step: {"sn": libsn100 kernels, "cublas": library GEMMs}."""
-        g = self.sn_gemm
-        sn = 3                                 # embed, final norm, argmax
-        lib = 0
-        sn, lib = (sn + 1, lib) if g["lm_head"] else (sn, lib + 1)
+        """Launch census of one decode step (all libsn100 kernels; the decode step launches no
+        library GEMMs).  NCCL all-reduces of the head-parallel NCCL transport are counted apart."""
+        sn = 4                                     # embed, final norm, LM head, argmax
         for kind in self.kinds:
-            sn += 2                            # two add_rmsnorm
-            sn += 2 if kind in (FA, SWA) else 1    # rope+attention | fused delta-rule decode
-            for role in ("attn_qkv" if kind in (FA, SWA) else "in_proj", "out_proj", "ffn_down", "ffn_gate_up"):
-                sn, lib = (sn + 1, lib) if g[role] else (sn, lib + 1)
-            if kind == KDA and not g["in_proj"]:
-                lib += 1                       # low-rank gate second factors (batched GEMM)
-            if not (g["ffn_gate_up"] and self.gu_mode == "swiglu_il"):
-                sn += 1                        # silu_mul (fused into the gate/up GEMM otherwise)
-        return {"sn": sn, "cublas": lib}
+            sn += 2 + 4 + 1 + (2 if kind == KDA else 0)  # norms, in/out-proj, gate/up, down, mixer (+KDA gates)
+        nccl = 2 * len(self.kinds) if (self.tp > 1 and self.sym is None) else 0
+        return {"sn": sn + (2 * len(self.kinds) if self.sym is not None else 0), "cublas": 0, "nccl": nccl}
+
+    def check_capacity(self, steps: int = 1):
+        """Raise before a decode that would take a sequence past max_len (its KV append would
+        fall off the block table; the kernels skip such writes and set err_flag)."""
+        top = int(self.seq_lens.max().item()) if self.B else 0
+        if top + steps > self.max_len:
+            raise ValueError(f"decode of {steps} step(s) would exceed max_len={self.max_len} (longest sequence {top})")
+        if int(self.err_flag.item()):
+            raise RuntimeError("a KV append fell outside the block table (err_flag set)")
 
     @torch.no_grad()
     def decode(self, tokens):
         """Eager decode step.  tokens: [B] ints (any device) -> logits [B, V] (device buffer)."""
+        self.check_capacity()
         self.step_tokens.copy_(torch.as_tensor(tokens, dtype=torch.int32))
         self.decode_body()
         return self.logits
@@ -514,10 +433,7 @@ class Supernet:
             self._tp_sum(mix)
             ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
             act = e(rows, cfg.ffn)
-            if self.gu_il is not None:
-                ops.swiglu_il(h @ lw["ffn_gu_il"].t(), act, *self.gu_il)
-            else:
-                ops.silu_mul(h @ lw["ffn_gu"].t(), act)
+            ops.swiglu_il(h @ lw["ffn_gu_il"].t(), act, *self.gu_il)
             torch.mm(act, lw["ffn_down"].t(), out=ffn_o)
             self._tp_sum(ffn_o)
             delta = ffn_o
@@ -547,7 +463,7 @@ class Supernet:
         rows = h.shape[0]
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
-        qkv = h @ w["qkv"].t()
+        qkv = h @ w["qkv_il"].t()
         q = torch.empty(rows, Hq, D, device=h.device, dtype=h.dtype)
         k = torch.empty(rows, Hkv, D, device=h.device, dtype=h.dtype)
         v = torch.empty_like(k)
@@ -555,7 +471,7 @@ class Supernet:
         if cont is not None:  # the cached prefix the new tokens can see, read before the append
             prefix = self._gather_prefix(st, bt, window, cont[0])
         ops.rope_kv_append(qkv, row_seq, row_pos, self.seq_lens, self.inv_freq, q, k, v, st["k"], st["v"], bt, Hq,
-                           Hkv, D, P, window)
+                           Hkv, D, P, window, pair_il=True)
         o = torch.empty(rows, Hq * D, device=h.device, dtype=h.dtype)
         if cont is None:
             ops.attn_prefill(q, k, v, cu, o, Hq, Hkv, D, window, self.scale_attn)

@@ -11,8 +11,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (SN_ATTN_FORCE_SIMT, SN_BF16, SN_F32, SN_GEMM_PARTIAL, SN_GEMM_RESID, SN_GEMM_STORE, SN_GEMM_SWIGLU,
-                   SN_GEMM_SWIGLU_IL,
+from ._lib import (SN_BF16, SN_F32, SN_GEMM_ATTN_IN, SN_GEMM_PARTIAL, SN_GEMM_RESID, SN_GEMM_STORE, SN_GEMM_SWIGLU_IL,
                    call)
 
 _DT = {torch.bfloat16: SN_BF16, torch.float32: SN_F32}
@@ -44,18 +43,12 @@ def embed(tokens, table, residual, seq_lens=None, positions=None):
 
 
 def add_rmsnorm(delta, residual, weight, out, eps, partials=None, nsplit=0):
-    """residual += delta + sum(partials[:nsplit]); out = rmsnorm(residual) * weight."""
+    """residual += delta + sum(partials[:nsplit]) (slab order); out = rmsnorm(residual) * weight."""
     rows, dim = residual.shape
     if nsplit:
         assert partials is not None and partials.dtype == torch.float32 and partials.numel() >= nsplit * rows * dim
     call("sn_add_rmsnorm", _p(delta), _p(partials) if nsplit else None, int(nsplit), _p(residual), _p(weight),
          _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
-
-
-def silu_mul(gate_up, out, nsplit=0):
-    """gate_up: [rows, 2F] (dtype of out) or fp32 split-K slabs [>=nsplit, rows, 2F]."""
-    rows, ffn = out.shape
-    call("sn_silu_mul", _p(gate_up), int(nsplit), _p(out), rows, ffn, dtype_code(out.dtype), _s())
 
 
 def argmax(logits, out_tokens):
@@ -64,12 +57,13 @@ def argmax(logits, out_tokens):
 
 
 def rope_kv_append(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,
-                   Hq, Hkv, D, page_size, window, nsplit=0):
-    """qkv: [rows, (Hq+2Hkv)D] (dtype of the cache) or fp32 split-K slabs [>=nsplit, rows, ...]."""
+                   Hq, Hkv, D, page_size, window, pair_il=False):
+    """qkv: [rows, (Hq+2Hkv)D] (dtype of the cache); pair_il: q / k columns in the rotary-pair
+    interleaved order of the decode in-projection weights (rope_pair_interleave)."""
     rows = q_out.shape[0]
-    call("sn_rope_kv_append", _p(qkv), int(nsplit), _p(row_seq), _p(row_pos), _p(seq_lens), _p(inv_freq), _p(q_out), _p(k_out),
+    call("sn_rope_kv_append", _p(qkv), _p(row_seq), _p(row_pos), _p(seq_lens), _p(inv_freq), _p(q_out), _p(k_out),
          _p(v_out), _p(k_cache), _p(v_cache), _p(block_table), rows, Hq, Hkv, D, page_size, block_table.shape[1],
-         window, dtype_code(q_out.dtype), _s())
+         window, int(pair_il), dtype_code(q_out.dtype), _s())
 
 
 def attn_decode_workspace_bytes(B, Hq, Hkv, D, max_splits):
@@ -77,9 +71,9 @@ def attn_decode_workspace_bytes(B, Hq, Hkv, D, max_splits):
 
 
 def attn_decode(q, k_cache, v_cache, block_table, seq_lens, out, workspace, counters, Hq, Hkv, D, page_size, window,
-                split_pages, max_splits, scale, force_simt=False):
+                split_pages, max_splits, scale):
     B = seq_lens.shape[0]
-    code = dtype_code(q.dtype) | (SN_ATTN_FORCE_SIMT if force_simt else 0)
+    code = dtype_code(q.dtype)
     call("sn_attn_decode", _p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_lens), _p(out), _p(workspace),
          _p(counters), B, Hq, Hkv, D, page_size, block_table.shape[1], window, split_pages, max_splits, scale, code,
          _s())
@@ -93,22 +87,29 @@ def attn_prefill(q, k, v, cu_seqlens, out, Hq, Hkv, D, window, scale, cu_k=None,
 
 
 def gdn_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, norm_w, out, Hk, Hv, D, width,
-               scale, eps_l2, eps_norm, nsplit=0):
-    """proj: [B, N_in] (dtype of out) or fp32 split-K slabs [>=nsplit, B, N_in]."""
+               scale, eps_l2, eps_norm):
+    """proj: the in-projection rows [B, N_in] (dtype of out)."""
     B = positions.shape[0]
-    call("sn_gdn_decode", _p(proj), proj.stride(-2), int(nsplit), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
+    call("sn_gdn_decode", _p(proj), proj.stride(0), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
          _p(positions), _p(A_log), _p(dt_bias), _p(norm_w), _p(out), B, Hk, Hv, D, width, scale, eps_l2, eps_norm,
          dtype_code(out.dtype), _s())
 
 
-def kda_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, f2, g2, g2_b, norm_w, out, H, D,
-               rank, width, scale, eps_l2, eps_norm, nsplit=0, fg=None):
-    """proj: [B, N_in] (dtype of out) or fp32 split-K slabs [>=nsplit, B, N_in]."""
+def kda_decode(proj, fg, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, g2_b, norm_w, out, H, D,
+               rank, width, scale, eps_l2, eps_norm):
+    """proj: the in-projection rows [B, N_in]; fg [2, B, H*D] = (f1 @ f2^T, g1 @ g2^T) (dtype of out)."""
     B = positions.shape[0]
-    call("sn_kda_decode", _p(proj), proj.stride(-2), int(nsplit), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
-         _p(positions), _p(A_log), _p(dt_bias), _p(f2), _p(g2), _p(g2_b), _p(fg), _p(norm_w), _p(out), B, H, D, rank,
-         width,
+    call("sn_kda_decode", _p(proj), proj.stride(0), _p(fg), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
+         _p(positions), _p(A_log), _p(dt_bias), _p(g2_b), _p(norm_w), _p(out), B, H, D, rank, width,
          scale, eps_l2, eps_norm, dtype_code(out.dtype), _s())
+
+
+def kda_gate_factors(proj, f2, g2, fg, H, D, rank):
+    """fg[0] = f1 @ f2^T, fg[1] = g1 @ g2^T from the f1 / g1 columns of the KDA in-projection
+    (two decode GEMMs: 2 x H*D x rank weights, read once per step)."""
+    f1_off = 3 * H * D
+    gemm_decode(proj[:, f1_off:f1_off + rank], f2, fg[0], "store")
+    gemm_decode(proj[:, f1_off + rank:f1_off + 2 * rank], g2, fg[1], "store")
 
 
 def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channels, width, ring_hist=None,
@@ -124,12 +125,6 @@ def delta_prep(kind, qkv_conv, proj, b_off, a_off, f, A_log, dt_bias, qn, kn, ge
          dtype_code(qkv_conv.dtype), _s())
 
 
-def gdn_chunk_prefill(qn, kn, qkv_conv, v_off, glog, beta, o, state, slot_idx, cu_seqlens, Hk, Hv, D, init_state):
-    call("sn_gdn_chunk_prefill", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(glog), _p(beta), _p(o),
-         _p(state), _p(slot_idx), _p(cu_seqlens), cu_seqlens.numel() - 1, Hk, Hv, D, int(init_state),
-         dtype_code(qkv_conv.dtype), _s())
-
-
 def delta_scan(kind, qn, kn, qkv_conv, v_off, gexp, beta, o, state, slot_idx, cu_seqlens, Hk, Hv, D, init_state):
     call("sn_delta_scan", kind, _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(gexp), _p(beta), _p(o),
          _p(state), _p(slot_idx), _p(cu_seqlens), cu_seqlens.numel() - 1, Hk, Hv, D, int(init_state),
@@ -141,13 +136,24 @@ def gated_rmsnorm(o, gate, gate_stride, norm_w, out, H, D, eps, act):
          dtype_code(out.dtype), _s())
 
 
-GEMM_MODES = {"store": SN_GEMM_STORE, "swiglu": SN_GEMM_SWIGLU, "resid": SN_GEMM_RESID, "partial": SN_GEMM_PARTIAL,
-              "swiglu_il": SN_GEMM_SWIGLU_IL}
+GEMM_MODES = {"store": SN_GEMM_STORE, "resid": SN_GEMM_RESID, "partial": SN_GEMM_PARTIAL,
+              "swiglu_il": SN_GEMM_SWIGLU_IL, "attn_in": SN_GEMM_ATTN_IN}
 
 
-def gemm_swiglu_block(M, N, K):
+def gemm_swiglu_block(N):
     """Block half-height h of the interleaved SwiGLU weight layout (mode "swiglu_il")."""
-    return _lib.load().sn_gemm_swiglu_block(M, N, K)
+    return _lib.load().sn_gemm_swiglu_block(N)
+
+
+def rope_pair_interleave(w_qkv, Hq, Hkv, D):
+    """Reorder the q and k rows of every head of a fused [q | k | v] projection weight so that
+    rotary partners sit next to each other (row 2i = dim i, row 2i+1 = dim i + D/2); v rows
+    unchanged.  The decode in-projection (mode "attn_in") and the prefill RoPE (pair_il=True)
+    read this order."""
+    half = D // 2
+    perm = torch.arange(D).view(2, half).t().reshape(-1)  # [0, D/2, 1, D/2+1, ...]
+    idx = torch.cat([h * D + perm for h in range(Hq + Hkv)] + [torch.arange((Hq + Hkv) * D, (Hq + 2 * Hkv) * D)])
+    return w_qkv[idx.to(w_qkv.device)].contiguous()
 
 
 def interleave_swiglu(w_gu, h):
@@ -171,35 +177,42 @@ def deinterleave_swiglu(gu_il, N, h):
     return torch.cat([v[:, :, 0].reshape(rows, -1)[:, :N], v[:, :, 1].reshape(rows, -1)[:, :N]], 1)
 
 
-def gemm_decode_splits(M, N, K, mode="partial"):
-    return _lib.load().sn_gemm_decode_splits(M, N, K, GEMM_MODES[mode])
+def gemm_decode_plan(M, N, K, mode="store"):
+    """{br, splits, ks, blocks, grid, stages} the library picks for this shape (introspection)."""
+    out = (ctypes.c_int * 6)()
+    _lib.load().sn_gemm_decode_plan(M, N, K, GEMM_MODES.get(mode, mode), out)
+    return dict(zip(("br", "splits", "ks", "blocks", "grid", "stages"), list(out)))
 
 
-def gemm_decode(x, w, out, mode="store"):
-    """out (+)= x @ w.T on tensor cores (tcgen05).  x [M, K] bf16 (M <= 128), w [N(or 2N), K] bf16.
-    mode "store": out bf16 [M, N]; "swiglu": w = [gate; up], out bf16 [M, N] = silu(g) * u;
-    "resid": out fp32 [M, N] += x @ w.T; "partial": out fp32 [S, M, N] K-split partial slabs
-    (S = gemm_decode_splits(M, N, K)), returned."""
+def gemm_decode(x, w, out, mode):
+    """out (+)= x @ w.T with the decode GEMM (tcgen05 for bf16, CUDA cores for fp32); returns
+    the K split count S.  x [M, K], w [N, K] (mode "swiglu_il": the interleaved [nb*2h, K]
+    layout, out [M, N] = silu(g)*u); "store": out dtype [M, N]; "resid": out fp32 [M, N] +=
+    x @ w.T; "partial": out fp32 [>=S, M, N] K-split slabs (slab order sums them)."""
     M, K = x.shape
-    code = GEMM_MODES[mode]
-    N = out.shape[-1] if mode not in ("store",) else w.shape[0]
+    N = out.shape[-1]
     if mode == "swiglu_il":
-        h = gemm_swiglu_block(M, N, K)
-        assert h > 0 and w.shape[0] == -(-N // h) * 2 * h, "weight not in the interleaved layout for this shape"
-    if mode == "swiglu":
-        assert w.shape[0] == 2 * N
-    if mode in ("resid", "partial"):
-        assert out.dtype == torch.float32
+        h = gemm_swiglu_block(N)
+        assert w.shape[0] == -(-N // h) * 2 * h, "weight not in the interleaved layout for this shape"
     else:
-        assert out.dtype == torch.bfloat16
+        assert w.shape[0] == N
+    assert out.dtype == (torch.float32 if mode in ("resid", "partial") else x.dtype)
     if mode == "partial":
-        S = gemm_decode_splits(M, N, K)
-        assert out.dim() == 3 and out.shape[0] >= S and out.shape[1] == M and out.is_contiguous()
-    assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and x.stride(1) == 1 and w.stride(1) == 1
+        assert out.dim() == 3 and out.shape[1] == M and out.is_contiguous()
+    assert x.dtype == w.dtype and x.stride(1) == 1 and w.stride(1) == 1 and out.stride(-1) == 1
     s_out = ctypes.c_int(1)
-    call("sn_gemm_decode", _p(x), M, K, x.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(-2), code,
-         ctypes.byref(s_out), _s())
+    call("sn_gemm_decode", _p(x), M, K, x.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(-2),
+         GEMM_MODES[mode], ctypes.byref(s_out), dtype_code(x.dtype), _s())
     return s_out.value
+
+
+def gemm_decode_attn_in(x, w, positions, inv_freq, q_out, k_cache, v_cache, block_table, Hq, Hkv, D, page_size,
+                        window, err_flag):
+    """Attention in-projection with RoPE + KV append fused; w in rope_pair_interleave order."""
+    M, K = x.shape
+    call("sn_gemm_decode_attn_in", _p(x), M, K, x.stride(0), _p(w), w.stride(0), _p(positions), _p(inv_freq),
+         _p(q_out), _p(k_cache), _p(v_cache), _p(block_table), Hq, Hkv, D, page_size, block_table.shape[1], window,
+         _p(err_flag), dtype_code(x.dtype), _s())
 
 
 def chunk_plan(cu_seqlens_host, chunk=64, device="cuda"):

@@ -111,10 +111,10 @@ class PlacementRouter:
             self._engines.move_to_end(key)
             return self._engines[key]
         cfg = self.store.cfg
-        block = ops.gemm_swiglu_block(batch, cfg.ffn, cfg.hidden) if self.store.dtype == torch.bfloat16 else None
+        block = ops.gemm_swiglu_block(cfg.ffn)
         model = Supernet(cfg, key[0], batch=batch, max_len=self.max_len, dtype=self.store.dtype,
                          device=self.store.device, weights=self.store.weights(key[0], swiglu_block=block))
-        graph = DecodeGraph(model, feedback=True)
+        graph = DecodeGraph(model, feedback=True)  # built on the empty engine (construction resets it)
         self._engines[key] = (model, graph)
         while len(self._engines) > self.max_engines:
             self._engines.popitem(last=False)

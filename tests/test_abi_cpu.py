@@ -42,9 +42,41 @@ def test_ctypes_signatures_match_header():
 def test_error_path_without_gpu():
     """Argument validation happens before any CUDA call: a bad call fails cleanly on CPU."""
     lib = _lib.load()
-    st = lib.sn_gdn_decode(None, 0, 0, None, None, None, None, None, None, None, None, None, 1, 1, 1, 128, 4,
+    st = lib.sn_gdn_decode(None, 0, None, None, None, None, None, None, None, None, None, 1, 1, 1, 128, 4,
                            1.0, 1e-6, 1e-5, 1, None)
     assert st == 1 and b"NULL" in lib.sn_last_error()
     st = lib.sn_attn_decode(None, None, None, None, None, None, None, None, 1, 32, 7, 128, 64, 8, 0, 1, 1, 1.0, 1,
                             None)
     assert st == 1
+
+
+def test_decode_gemm_plans_without_gpu():
+    """The decode GEMM plan is host arithmetic (148 SMs assumed without a device): every Apriel
+    decode projection keeps >= 96 CTAs streaming; fused modes keep their block constraints."""
+    from paper_2604_19877_b200 import APRIEL, ops
+    cfg = APRIEL
+    for N, K, mode in ((cfg.gdn_in_width, cfg.hidden, "store"), (cfg.hidden, cfg.ffn, "partial"),
+                       (cfg.hidden, cfg.gdn_value_dim, "partial"), (cfg.ffn, cfg.hidden, "swiglu_il"),
+                       (cfg.attn_qkv_width, cfg.hidden, "attn_in"), (cfg.vocab, cfg.hidden, "store")):
+        p = ops.gemm_decode_plan(64, N, K, mode)
+        assert 96 <= p["grid"] <= 148 and p["stages"] >= 3, (N, K, p)
+        if mode == "swiglu_il":
+            assert p["br"] == 256 and p["splits"] == 1
+        if mode == "attn_in":
+            assert p["br"] % 32 == 0 and p["splits"] == 1
+        if mode == "store":
+            assert p["splits"] == 1
+    assert ops.gemm_swiglu_block(cfg.ffn) == 128
+
+
+def test_rope_pair_interleave_is_a_permutation():
+    import torch
+    from paper_2604_19877_b200 import TINY, ops
+    c = TINY
+    w = torch.arange(c.attn_qkv_width, dtype=torch.float32)[:, None].repeat(1, 3)
+    il = ops.rope_pair_interleave(w, c.n_q_heads, c.n_kv_heads, c.head_dim)
+    assert sorted(il[:, 0].tolist()) == w[:, 0].tolist()
+    D, half = c.head_dim, c.head_dim // 2
+    assert il[0, 0] == 0 and il[1, 0] == half and il[2, 0] == 1 and il[D, 0] == D
+    v0 = (c.n_q_heads + c.n_kv_heads) * D
+    assert torch.equal(il[v0:], w[v0:])

@@ -1,6 +1,8 @@
-"""Chunked WY GDN / KDA prefill (tensor cores) vs the token-sequential scan on the same prepared
-inputs: outputs and final states within the bf16 tolerance, ragged / multi-sequence batches,
-chunk-boundary lengths, and a non-zero initial state (chunked continuation)."""
+"""Chunked WY GDN / KDA prefill (tensor cores) and the token-sequential scan, each against the
+oracle recurrence (delta_rule_recurrent, pinned to FLA's naive_recurrent_*) for EVERY sequence
+of the batch: outputs and final states within the bf16 tolerance (scan: 1e-4), ragged /
+multi-sequence batches, chunk-boundary lengths, and a non-zero initial state (chunked
+continuation)."""
 import math
 
 import pytest
@@ -13,6 +15,20 @@ TOL = 2e-2
 
 def rel(a, b):
     return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+def _oracle_per_seq(lens, qn, kn, v_all, beta, glog, S0, G):
+    """delta_rule_recurrent of every sequence: (o [T, Hv, D], S [B, Hv, K, V])."""
+    outs, states, t0 = [], [], 0
+    for b, L in enumerate(lens):
+        sl = slice(t0, t0 + L)
+        o, S = delta_rule_recurrent(qn[sl].repeat_interleave(G, 1)[None], kn[sl].repeat_interleave(G, 1)[None],
+                                    v_all[sl][None], beta[sl][None], glog[sl][None],
+                                    initial_state=S0[b:b + 1].transpose(-1, -2), scale=1.0)
+        outs.append(o[0])
+        states.append(S[0])
+        t0 += L
+    return torch.cat(outs), torch.stack(states)
 
 
 def _inputs(lens, Hk, Hv, D, seed):
@@ -32,7 +48,7 @@ def _inputs(lens, Hk, Hv, D, seed):
 @pytest.mark.parametrize("D,Hk,Hv", [(128, 2, 8), (64, 1, 4)])
 @pytest.mark.parametrize("lens", [[1], [63], [64], [65], [200, 17, 128], [1000], [30] * 10])
 @pytest.mark.parametrize("init", [False, True])
-def test_chunked_matches_scan(D, Hk, Hv, lens, init):
+def test_chunked_and_scan_match_oracle(D, Hk, Hv, lens, init):
     """[30] * 10 at D=128: 10 sequences x 8 heads x 2 value tiles >= 148 CTAs -> the wide
     (64-column) state-pass tiles; the other cases run the narrow (32-column) ones."""
     from paper_2604_19877_b200 import ops
@@ -42,34 +58,26 @@ def test_chunked_matches_scan(D, Hk, Hv, lens, init):
     dev = {k: v.cuda() for k, v in dict(qn=qn, kn=kn, qkv=qkv, glog=glog, beta=beta, cu=cu).items()}
     gexp = dev["glog"].exp()
     outs = {}
-    for name in ("scan", "chunk", "chunk2"):
+    for name in ("scan", "chunk2"):
         S = S0.clone().cuda()
         o = torch.zeros(sum(lens), Hv, D, device="cuda")
         if name == "scan":
             ops.delta_scan(0, dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, gexp, dev["beta"], o, S, None, dev["cu"],
                            Hk, Hv, D, init_state=init)
-        elif name == "chunk2":
+        else:
             chunks, c0 = ops.chunk_plan(cu.tolist())
             ops.gdn_chunk_prefill2(dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, dev["glog"], dev["beta"], chunks, c0,
                                    o, S, None, Hk, Hv, D, init_state=init)
-        else:
-            ops.gdn_chunk_prefill(dev["qn"], dev["kn"], dev["qkv"], 2 * Hk * D, dev["glog"], dev["beta"], o, S, None,
-                                  dev["cu"], Hk, Hv, D, init_state=init)
         torch.cuda.synchronize()
-        outs[name] = (o.cpu(), S.cpu())
-    assert rel(outs["chunk"][0], outs["scan"][0]) < TOL
-    assert rel(outs["chunk"][1], outs["scan"][1]) < TOL
-    assert rel(outs["chunk2"][0], outs["scan"][0]) < TOL
-    assert rel(outs["chunk2"][1], outs["scan"][1]) < TOL
-    # and the scan itself against the oracle recurrence (first sequence)
-    L0 = lens[0]
-    G = Hv // Hk
-    v = qkv[:L0, 2 * Hk * D:].float().view(1, L0, Hv, D)
-    o_ref, S_ref = delta_rule_recurrent(qn[:L0].repeat_interleave(G, 1)[None], kn[:L0].repeat_interleave(G, 1)[None], v,
-                                        beta[:L0][None], glog[:L0][None], initial_state=S0[:1].transpose(-1, -2),
-                                        scale=1.0)
-    assert rel(outs["scan"][0][:L0], o_ref[0]) < 1e-4
-    assert rel(outs["scan"][1][0].transpose(-1, -2), S_ref[0]) < 1e-4
+        outs[name] = (o.cpu(), S.cpu().transpose(-1, -2))
+    v = qkv[:, 2 * Hk * D:].float().view(-1, Hv, D)
+    o_ref, S_ref = _oracle_per_seq(lens, qn, kn, v, beta, glog, S0, Hv // Hk)
+    assert rel(outs["scan"][0], o_ref) < 1e-4 and rel(outs["scan"][1], S_ref) < 1e-4
+    assert rel(outs["chunk2"][0], o_ref) < TOL and rel(outs["chunk2"][1], S_ref) < TOL
+    for b in range(B):  # per sequence, so a short sequence's error is not hidden by a long one's scale
+        t0, t1 = int(cu[b]), int(cu[b + 1])
+        assert rel(outs["chunk2"][0][t0:t1], o_ref[t0:t1]) < TOL, b
+        assert rel(outs["chunk2"][1][b], S_ref[b]) < TOL, b
 
 
 @pytest.mark.gpu
@@ -112,7 +120,7 @@ def _kda_gates(T, H, D, g):
 @pytest.mark.parametrize("D,H", [(128, 4), (64, 4)])
 @pytest.mark.parametrize("lens", [[1], [63], [64], [65], [200, 17, 128], [1000], [20] * 20])
 @pytest.mark.parametrize("init", [False, True])
-def test_kda_chunked_matches_scan(D, H, lens, init):
+def test_kda_chunked_and_scan_match_oracle(D, H, lens, init):
     from paper_2604_19877_b200 import ops
     g = torch.Generator().manual_seed(len(lens) * 11 + sum(lens))
     T = sum(lens)
@@ -137,17 +145,16 @@ def test_kda_chunked_matches_scan(D, H, lens, init):
             ops.kda_chunk_prefill2(dev["qn"], dev["kn"], dev["qkv"], 2 * H * D, dev["glog"], dev["beta"], chunks, c0,
                                    o, S, None, H, D, init_state=init)
         torch.cuda.synchronize()
-        outs[name] = (o.cpu(), S.cpu())
+        outs[name] = (o.cpu(), S.cpu().transpose(-1, -2))
     assert torch.isfinite(outs["chunk2"][0]).all() and torch.isfinite(outs["chunk2"][1]).all()
-    assert rel(outs["chunk2"][0], outs["scan"][0]) < TOL
-    assert rel(outs["chunk2"][1], outs["scan"][1]) < TOL
-    # the scan against the oracle recurrence (FLA naive_recurrent_kda convention), first sequence
-    L0 = lens[0]
-    v = qkv[:L0, 2 * H * D:].float().view(1, L0, H, D)
-    o_ref, S_ref = delta_rule_recurrent(qn[:L0][None], kn[:L0][None], v, beta[:L0][None], glog[:L0][None],
-                                        initial_state=S0[:1].transpose(-1, -2), scale=1.0)
-    assert rel(outs["scan"][0][:L0], o_ref[0]) < 1e-4
-    assert rel(outs["scan"][1][0].transpose(-1, -2), S_ref[0]) < 1e-4
+    # every sequence against the oracle recurrence (FLA naive_recurrent_kda convention)
+    v = qkv[:, 2 * H * D:].float().view(T, H, D)
+    o_ref, S_ref = _oracle_per_seq(lens, qn, kn, v, beta, glog, S0, 1)
+    assert rel(outs["scan"][0], o_ref) < 1e-4 and rel(outs["scan"][1], S_ref) < 1e-4
+    for b in range(B):
+        t0, t1 = int(cu[b]), int(cu[b + 1])
+        assert rel(outs["chunk2"][0][t0:t1], o_ref[t0:t1]) < TOL, b
+        assert rel(outs["chunk2"][1][b], S_ref[b]) < TOL, b
 
 
 @pytest.mark.gpu

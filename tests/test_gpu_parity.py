@@ -36,7 +36,7 @@ def run_pair(placement, dtype, B, T_prefill, n_decode, cfg=TINY, seed=0, graph=F
     outs = [pre]
     if graph:
         from paper_2604_19877_b200.graphs import DecodeGraph
-        dg = DecodeGraph(model)
+        dg = DecodeGraph(model, preserve_state=True)
         for t in range(T_prefill, T_prefill + n_decode):
             model.step_tokens.copy_(toks[:, t].to(torch.int32))
             dg.replay()
@@ -119,7 +119,7 @@ def test_ragged_prefill_matches_per_sequence_oracle(placement):
     seqs = [torch.randint(0, TINY.vocab, (L + steps,), generator=g) for L in lens]
     model = Supernet(TINY, placement, batch=len(lens), max_len=max(lens) + steps, dtype=torch.bfloat16, weights=w)
     pre = model.prefill([s[:L] for s, L in zip(seqs, lens)], return_all=True)
-    graph = DecodeGraph(model)
+    graph = DecodeGraph(model, preserve_state=True)
     dec = []
     for t in range(steps):
         model.step_tokens.copy_(torch.tensor([int(s[L + t]) for s, L in zip(seqs, lens)], dtype=torch.int32))

@@ -26,7 +26,7 @@ def _run(model, toks, graph=False):
     outs = [model.prefill(toks[:, :T], return_all=True).float().cpu()]
     if graph:
         from paper_2604_19877_b200.graphs import DecodeGraph
-        g = DecodeGraph(model)
+        g = DecodeGraph(model, preserve_state=True)
         for t in range(T, T + STEPS):
             model.step_tokens.copy_(toks[:, t].to(torch.int32))
             g.replay()
@@ -39,8 +39,6 @@ def _run(model, toks, graph=False):
 
 
 def _worker(rank, world, port, path, graph=False, nccl_path=False):
-    if nccl_path:
-        os.environ["SN_TP_NCCL"] = "1"
     import torch.distributed as dist
     from paper_2604_19877_b200.model import Supernet
     from paper_2604_19877_b200.placement import layer_kinds
@@ -49,7 +47,7 @@ def _worker(rank, world, port, path, graph=False, nccl_path=False):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     w = init_weights(CFG, layer_kinds(PLACEMENT), seed=0)
     model = Supernet(CFG, PLACEMENT, batch=B, max_len=T + STEPS, dtype=torch.bfloat16, weights=w,
-                     tp_group=dist.group.WORLD)
+                     tp_group=dist.group.WORLD, tp_transport="nccl" if nccl_path else "p2p")
     out = _run(model, _tokens(), graph=graph)
     if rank == 0:
         torch.save(out, path)
@@ -61,7 +59,7 @@ def _worker(rank, world, port, path, graph=False, nccl_path=False):
 @pytest.mark.parametrize("graph,nccl_path", [(False, False), (True, False), (False, True)])
 def test_tp2_two_processes_match_unsharded(graph, nccl_path):
     """Decode all-reduces through peer memory fused with the norm (default; eager and in a
-    CUDA graph), or through torch.distributed (SN_TP_NCCL=1)."""
+    CUDA graph), or through torch.distributed (tp_transport="nccl")."""
     from paper_2604_19877_b200.model import Supernet
     from paper_2604_19877_b200.placement import layer_kinds
     from paper_2604_19877_b200.weights import init_weights

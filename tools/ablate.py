@@ -15,7 +15,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from bench import fill_synthetic  # noqa: E402
 from paper_2604_19877_b200 import APRIEL, PRESETS, ops  # noqa: E402
-from paper_2604_19877_b200 import model as model_mod  # noqa: E402
 from paper_2604_19877_b200.graphs import DecodeGraph  # noqa: E402
 from paper_2604_19877_b200.model import Supernet  # noqa: E402
 
@@ -35,40 +34,36 @@ def noop(*args, **kw):
 _gemm = ops.gemm_decode
 
 
-def gemm_noop_roles(roles):
-    def f(x, w, out, mode="store"):
-        if mode == "partial":
-            return ops.gemm_decode_splits(x.shape[0], out.shape[-1], x.shape[1], "partial")
-        return None
-    return f
-
-
 def gemm_skip_if(pred):
-    def f(x, w, out, mode="store"):
-        if pred(x, w, mode):
-            return ops.gemm_decode_splits(x.shape[0], out.shape[-1], x.shape[1], "partial") if mode == "partial" else None
+    def f(x, w, out, mode):
+        if pred(x, w, out, mode):
+            return 1
         return _gemm(x, w, out, mode)
     return f
 
 
+c = APRIEL
 ABL = {
-    "ffn_down": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, m: m == "partial" and x.shape[1] == APRIEL.ffn))],
-    "ffn_gate_up": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, m: m == "swiglu_il"))],
+    "in_proj": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, o, m: m == "store" and x.shape[1] == c.hidden
+                                                  and o.shape[-1] in (c.gdn_in_width, c.kda_in_width))),
+                (ops, "gemm_decode_attn_in", noop)],
+    "out_proj": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, o, m: m == "partial" and x.shape[1] != c.ffn))],
+    "ffn_down": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, o, m: m == "partial" and x.shape[1] == c.ffn))],
+    "ffn_gate_up": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, o, m: m == "swiglu_il"))],
+    "lm_head": [(ops, "gemm_decode", gemm_skip_if(lambda x, w, o, m: o.shape[-1] == c.vocab))],
+    "kda_gates": [(ops, "kda_gate_factors", noop)],
     "norm": [(ops, "add_rmsnorm", noop)],
-    "rope": [(ops, "rope_kv_append", noop)],
     "gdn": [(ops, "gdn_decode", noop)],
     "kda": [(ops, "kda_decode", noop)],
     "attn": [(ops, "attn_decode", noop)],
-    "sn_gemm": [(ops, "gemm_decode", gemm_noop_roles(None))],
-    "cublas_mm": [(torch, "mm", lambda *a, **k: None), (torch, "bmm", lambda *a, **k: None)],
 }
 
 m = Supernet(APRIEL, PRESETS[a.preset].layer_string, batch=a.batch, max_len=a.context + 256, dtype=torch.bfloat16)
-fill_synthetic(m, a.context)
 
 
 def step_ms():
-    g = DecodeGraph(m, feedback=False, preserve_state=False)
+    g = DecodeGraph(m, feedback=False)
+    fill_synthetic(m, a.context)
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
