@@ -104,6 +104,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed plumbing
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with one rank
+    per GPU (NCCL, 127.0.0.1 rendezvous).  Fails loudly when the box has fewer than N GPUs
+    instead of measuring one GPU and calling it N."""
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} requested but this box has {have} visible GPU(s)", file=sys.stderr)
+        return 2
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the driver can see the communicator's rank count
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -357,7 +376,8 @@ def cpu_baseline(cfg, preset, B_cpu, ctx):
     runner.run()
     samples = [runner.run() for _ in range(3)]
     step, times = min(samples, key=lambda s: s[0])
-    return {"value": B_cpu / step, "unit": UNIT, "cores": threads, "kind": "port",
+    return {"value": B_cpu / step, "unit": UNIT, "cores": threads, "kind": "port", "composed": True,
+            "batch": B_cpu,
             "sample": (f"CPU fp32 oracle (oracle/supernet_oracle.py), batch {B_cpu} x {ctx} context: one decode "
                        f"step of one layer per mixer type + one FFN layer + LM head, composed over the "
                        f"{preset} allocation {PRESETS[preset].counts} (additive cost model, "
@@ -365,6 +385,13 @@ def cpu_baseline(cfg, preset, B_cpu, ctx):
 
 
 def run_reference(args):
+    """The reference arm: the CPU fp32 oracle (the reference ships no implementation of this
+    path) on the same preset, batch and context as our arm, on all host threads.
+    A step is COMPOSED (marked "composed": true): one decode step of one layer per mixer type,
+    one FFN layer and the LM head are executed and timed, then weighted by the preset's
+    allocation — the reference's own additive cost model (R/pkg/src/placeopt/cost.py:73-80) —
+    because an executed 48-layer fp32 step at B=64 does not fit the host's RAM or a
+    minutes-long run.  The seconds actually executed are reported beside the composed ones."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -375,24 +402,35 @@ def run_reference(args):
     runner = CPUComposedStep(cfg, PRESETS[args.preset].counts, B_cpu, args.context, threads)
     for _ in range(args.warmup):
         runner.run()
-    t = 0.0
-    detail = None
+    t, executed, per = 0.0, 0.0, {}
+    w0 = time.perf_counter()
     for _ in range(args.steps):
         s, detail = runner.run()
         t += s
+        for k, v in detail.items():
+            per[k] = per.get(k, 0.0) + v / args.steps
+    executed = time.perf_counter() - w0
     value = B_cpu * args.steps / t
+    counts = PRESETS[args.preset].counts
+    mult = {"lm_head": 1, "ffn_layer": cfg.num_layers}
+    mult.update({n: c for n, c in zip(("FA", "SWA", "KDA", "GDN"), counts) if c})
     sample = (f"CPU fp32 oracle, batch {B_cpu} x {args.context} context; each step = one decode step of one "
-              f"layer per mixer type + one FFN layer + LM head composed over the {args.preset} allocation "
-              f"{PRESETS[args.preset].counts} (R/pkg/src/placeopt/cost.py:73-80)")
+              f"layer per mixer type + one FFN layer + LM head, executed, then composed over the {args.preset} "
+              f"allocation {counts} (R/pkg/src/placeopt/cost.py:73-80)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (random-init weights, random KV/state)",
-            "config": {"workload": "apriel48-decode", "preset": args.preset, "batch": B_cpu,
-                       "context": args.context},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "per_layer_seconds": {k: round(v, 5) for k, v in (detail or {}).items()}}
+            "config": {"workload": "apriel48-decode", "preset": args.preset,
+                       "placement": PRESETS[args.preset].layer_string, "batch_per_gpu": B_cpu,
+                       "global_batch": B_cpu, "context": args.context},
+            "composed": True,
+            "composition": {"per_layer_seconds": {k: round(v, 5) for k, v in per.items()},
+                            "multiplicity": mult, "executed_seconds_timed_region": round(executed, 3),
+                            "composed_seconds_timed_region": round(t, 3)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "composed": True},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -407,15 +445,24 @@ def main():
     ap.add_argument("--preset", default="Reg|Lklhd-10")
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--context", type=int, default=32768)
-    ap.add_argument("--cpu-batch", type=int, default=8)
+    ap.add_argument("--cpu-batch", type=int, default=None,
+                    help="batch of the CPU oracle legs (default: --batch, i.e. the same config)")
     ap.add_argument("--no-fa-compare", action="store_true")
     ap.add_argument("--prefill-tokens", type=int, default=16384, help="side measurement; 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    env_ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and env_ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_ws} (launch one rank per GPU)", file=sys.stderr)
+        return 2
+    if args.cpu_batch is None:
+        args.cpu_batch = args.batch
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
 
     ws, rank, local = dist_setup()
     cfg = APRIEL

@@ -59,6 +59,25 @@ def rope(x, pos, inv_freq):
     return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
 
 
+def gdn_gate(a_raw, A_log, dt_bias):
+    """GDN log-decay per value head: g = -exp(A_log) * softplus(a + dt_bias)
+    (3P-FLA/ops/gated_delta_rule/gate.py:20-45, naive_gdn_gate).  a_raw [..., Hv]."""
+    return -A_log.exp() * F.softplus(a_raw + dt_bias)
+
+
+def kda_gate(f, A_log, dt_bias):
+    """KDA log-decay per key channel: g = -exp(A_log[h]) * softplus(f + dt_bias[h, k])
+    (3P-FLA/ops/kda/gate.py:26-54, naive_kda_gate).  f [..., H, K]; dt_bias [H*K]."""
+    H = f.shape[-2]
+    return -A_log.view(H, 1).exp() * F.softplus(f + dt_bias.view(H, -1))
+
+
+def gated_rmsnorm(o, w, gate, eps, act):
+    """Per-head RMSNorm(o) * w * act(gate), act 'silu' (GDN) or 'sigmoid' (KDA)
+    (3P-FLA/modules/fused_norm_gate.py:94-100, FusedRMSNormGated)."""
+    return rmsnorm(o, w, eps) * (F.silu(gate) if act == "silu" else torch.sigmoid(gate))
+
+
 def causal_conv_step(x, hist, w):
     """One step of the SiLU causal conv.  x [B, C]; hist [B, C, W-1] (oldest first); w [C, W].
     Returns (y [B, C], new hist)."""
@@ -74,26 +93,34 @@ class OracleSupernet:
     (any float dtype; converted to fp32 here).  kinds: per-layer mixer kind.
     """
 
-    def __init__(self, cfg, kinds, weights, batch: int, max_len: int):
+    def __init__(self, cfg, kinds, weights, batch: int, max_len: int, device="cpu"):
+        """device: where the fp32 arithmetic runs.  "cpu" is the oracle proper; a CUDA device
+        runs the SAME fp32 torch code (TF32 must be off — the Apriel-shaped parity tests assert
+        it) only so that checks at Apriel widths finish in seconds.  Either way this is the
+        checker, never the product."""
         self.cfg, self.kinds, self.B, self.max_len = cfg, tuple(kinds), batch, max_len
-        f32 = lambda t: t.detach().to("cpu", torch.float32)
+        self.device = torch.device(device)
+        if self.device.type == "cuda" and torch.backends.cuda.matmul.allow_tf32:
+            raise ValueError("oracle on CUDA needs torch.backends.cuda.matmul.allow_tf32 = False (fp32 checker)")
+        f32 = lambda t: t.detach().to(self.device, torch.float32)
         self.w = _map_tensors(weights, f32)
-        self.inv_freq = cfg.inv_freq().to(torch.float32)
+        self.inv_freq = cfg.inv_freq().to(self.device, torch.float32)
         self.pos = 0
         # tensor-parallel emulation hook: applied to every row-parallel output (mixer out-proj,
         # FFN down) before the residual add; identity for the single-device oracle
         self.reduce = lambda t: t
         B, Hkv, D = batch, cfg.n_kv_heads, cfg.head_dim
+        z = lambda *shape: torch.zeros(*shape, device=self.device)
         self.state = []
         for k in self.kinds:
             if k in (FA, SWA):
-                self.state.append({"k": torch.zeros(B, max_len, Hkv, D), "v": torch.zeros(B, max_len, Hkv, D)})
+                self.state.append({"k": z(B, max_len, Hkv, D), "v": z(B, max_len, Hkv, D)})
             elif k == GDN:
                 C, Hv, Dg = cfg.gdn_conv_channels, cfg.gdn_v_heads, cfg.gdn_head_dim
-                self.state.append({"S": torch.zeros(B, Hv, Dg, Dg), "hist": torch.zeros(B, C, cfg.conv_width - 1)})
+                self.state.append({"S": z(B, Hv, Dg, Dg), "hist": z(B, C, cfg.conv_width - 1)})
             else:
                 C, H, Dk = cfg.kda_conv_channels, cfg.kda_heads, cfg.kda_head_dim
-                self.state.append({"S": torch.zeros(B, H, Dk, Dk), "hist": torch.zeros(B, C, cfg.conv_width - 1)})
+                self.state.append({"S": z(B, H, Dk, Dk), "hist": z(B, C, cfg.conv_width - 1)})
 
     # ------------------------------------------------------------ mixers
     def _attention(self, l, xn, kind):
@@ -103,7 +130,7 @@ class OracleSupernet:
         q = p[:, : Hq * D].view(B, Hq, D)
         k = p[:, Hq * D: (Hq + Hkv) * D].view(B, Hkv, D)
         v = p[:, (Hq + Hkv) * D:].view(B, Hkv, D)
-        pos = torch.full((B,), self.pos, dtype=torch.long)
+        pos = torch.full((B,), self.pos, dtype=torch.long, device=self.device)
         q, k = rope(q, pos, self.inv_freq), rope(k, pos, self.inv_freq)
         st["k"][:, self.pos], st["v"][:, self.pos] = k, v
         lo = max(0, self.pos - cfg.window + 1) if kind == SWA else 0
@@ -128,7 +155,7 @@ class OracleSupernet:
         cfg, w = self.cfg, self.w
         if self.pos >= self.max_len:
             raise ValueError("oracle max_len exceeded")
-        x = w["embed"][torch.as_tensor(tokens, dtype=torch.long)]
+        x = w["embed"][torch.as_tensor(tokens, dtype=torch.long).to(self.device)]
         for l, kind in enumerate(self.kinds):
             lw = w["layers"][l]
             xn = rmsnorm(x, lw["norm1"], cfg.norm_eps)
@@ -202,10 +229,10 @@ def gdn_core(cfg, p, hist, S, w):
     G = Hv // Hk  # value head h reads key head h // G (GVA)
     q = (l2norm(q, cfg.l2_eps) / math.sqrt(D)).repeat_interleave(G, dim=1)
     k = l2norm(k, cfg.l2_eps).repeat_interleave(G, dim=1)
-    g = -w["A_log"].exp() * F.softplus(a_raw + w["dt_bias"])  # [B, Hv]
+    g = gdn_gate(a_raw, w["A_log"], w["dt_bias"])  # [B, Hv]
     beta = torch.sigmoid(b_raw)
     o, S = delta_step(S, q, k, v, beta, g)
-    o = rmsnorm(o, w["norm_w"], cfg.mixer_norm_eps) * F.silu(z)
+    o = gated_rmsnorm(o, w["norm_w"], z, cfg.mixer_norm_eps, "silu")
     return o.reshape(B, Hv * D), hist, S
 
 
@@ -219,13 +246,13 @@ def kda_core(cfg, p, hist, S, w):
     g1 = p[:, 3 * HD + R: 3 * HD + 2 * R]
     b_raw = p[:, 3 * HD + 2 * R: 3 * HD + 2 * R + H]
     f = f1 @ w["f2"].T
-    g = -w["A_log"].exp()[:, None] * F.softplus((f + w["dt_bias"]).view(B, H, D))
+    g = kda_gate(f.view(B, H, D), w["A_log"], w["dt_bias"])
     gate = (g1 @ w["g2"].T + w["g2_b"]).view(B, H, D)
     q = l2norm(q, cfg.l2_eps) / math.sqrt(D)
     k = l2norm(k, cfg.l2_eps)
     beta = torch.sigmoid(b_raw)
     o, S = delta_step(S, q, k, v, beta, g)
-    o = rmsnorm(o, w["norm_w"], cfg.mixer_norm_eps) * torch.sigmoid(gate)
+    o = gated_rmsnorm(o, w["norm_w"], gate, cfg.mixer_norm_eps, "sigmoid")
     return o.reshape(B, HD), hist, S
 
 

@@ -27,9 +27,11 @@ class DecodeGraph:
         self.model = model
         self.feedback = feedback
         self.graph = torch.cuda.CUDAGraph()
+        # the snapshot copies are enqueued on the current stream BEFORE the side stream is told
+        # to wait for it: the warm-up steps below must not start while the copies still read
+        saved = self._snapshot(warmup) if preserve_state else None
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        saved = self._snapshot(warmup) if preserve_state else None
         with torch.cuda.stream(s):
             for _ in range(warmup):
                 model.decode_body()

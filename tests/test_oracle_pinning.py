@@ -94,3 +94,65 @@ def test_prefill_equals_stepwise():
     o = OracleSupernet(TINY, kinds, w, batch=2, max_len=40)
     b = torch.cat([o.run(toks[:, :17]), o.run(toks[:, 17:])], dim=1)
     assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------- FLA module kernels
+# tests/golden/fla_modules.pt holds the outputs of FLA 0.5.1's own gate functions, L2 norm,
+# short causal conv (prefill + ShortConvolution.step) and FusedRMSNormGated, run on a B200 by
+# tools/make_golden_fla_gpu.py (those FLA modules are Triton-only).  The oracle's restatements
+# that gdn_core / kda_core call must reproduce them.
+MOD = torch.load(os.path.join(GOLD, "fla_modules.pt"))
+
+
+def test_gdn_gate_matches_fla():
+    from oracle.supernet_oracle import gdn_gate
+    x = MOD["gdn_gate"]
+    ours = gdn_gate(x["a"], x["A_log"], x["dt_bias"])
+    assert _max_rel(ours, x["naive"]) < 1e-6
+    assert _max_rel(ours, x["fused"]) < 1e-5
+
+
+def test_kda_gate_matches_fla():
+    from oracle.supernet_oracle import kda_gate
+    x = MOD["kda_gate"]
+    ours = kda_gate(x["f"], x["A_log"], x["dt_bias"])
+    assert _max_rel(ours, x["naive"]) < 1e-6
+    assert _max_rel(ours, x["fused"]) < 1e-5
+
+
+def test_l2norm_matches_fla():
+    from oracle.supernet_oracle import l2norm
+    x = MOD["l2norm"]
+    assert _max_rel(l2norm(x["x"], x["eps"]), x["y"]) < 1e-5
+    # the tiny row: eps inside the root, not a clamp on the norm
+    assert torch.allclose(l2norm(x["x"][3], x["eps"]), x["y"][3], rtol=1e-4, atol=1e-6)
+
+
+def test_short_conv_prefill_and_step_match_fla():
+    """The oracle's conv step (history of the previous W-1 inputs, SiLU) run token by token
+    reproduces FLA's prefill convolution, its final cache (the last W inputs) and three
+    ShortConvolution.step calls from that cache."""
+    from oracle.supernet_oracle import causal_conv_step
+    x = MOD["short_conv"]
+    w, xs = x["weight"], x["x"]
+    B, T, C = xs.shape
+    W = w.shape[1]
+    hist = torch.zeros(B, C, W - 1)
+    ys = []
+    for t in range(T):
+        y, hist = causal_conv_step(xs[:, t], hist, w)
+        ys.append(y)
+    assert _max_rel(torch.stack(ys, 1), x["y"]) < 1e-5
+    assert torch.allclose(hist, x["cache_prefill"][..., 1:], atol=1e-6)
+    for t in range(3):
+        y, hist = causal_conv_step(x["steps"][t][:, 0], hist, w)
+        assert _max_rel(y, x["y_steps"][t][:, 0]) < 1e-5
+    assert torch.allclose(hist, x["cache_steps"][..., 1:], atol=1e-6)
+
+
+@pytest.mark.parametrize("act", ["silu", "sigmoid"])
+def test_gated_rmsnorm_matches_fla(act):
+    from oracle.supernet_oracle import gated_rmsnorm
+    x = MOD["gated_norm"]
+    ours = gated_rmsnorm(x["o"], x["weight"], x["gate"], x["eps"], act)
+    assert _max_rel(ours, x["swish" if act == "silu" else "sigmoid"]) < 1e-5
