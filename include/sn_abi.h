@@ -288,6 +288,60 @@ sn_status sn_gemm_decode_attn_in(const void* x, int M, int K, int ldx, const voi
                                  int Hq, int Hkv, int D, int page_size, int max_blocks,
                                  int window, int32_t* err_flag, int dtype, void* stream);
 
+/* ---------------------------------------------------------------- fused decode chain
+ * Everything between two mixer kernels of the decode step in ONE persistent launch
+ * (R/PAPER.md:175-182 trunk + the mixers' projections, R/PAPER.md:1540-1625): e.g.
+ * out-proj(l) -> add+RMSNorm -> FFN gate/up (SwiGLU) -> down -> add+RMSNorm -> in-proj(l+1)
+ * [-> KDA gate factors].  GEMM phases are the decode GEMM above (same plans and epilogues);
+ * NORM phases are sn_add_rmsnorm with split-K slabs, one batch row per CTA.  A grid-wide
+ * barrier separates a phase from the one it depends on; the weights of the next GEMM phase
+ * stream into shared memory while CTAs wait at it, so HBM never idles between projections.
+ * One CTA per SM (grid <= #SMs, all co-resident).  bf16, M <= 128.
+ * counter: one 64-bit device word per chain call site, zero-initialised once and never
+ * reset (the barrier targets are taken modulo the per-launch arrival count).          */
+typedef enum { SN_CHAIN_GEMM = 0, SN_CHAIN_NORM = 1 } sn_chain_kind;
+typedef struct {
+  int kind;      /* sn_chain_kind */
+  int depends;   /* 1: reads what the phase before it wrote (a grid barrier separates them) */
+  /* GEMM: out (+)= x[M][K] @ w[N][K]^T with the sn_gemm_mode epilogue `mode` */
+  const void* x;
+  int K, ldx;
+  const void* w;
+  int N, ldw;
+  void* out;
+  int ldo, mode;
+  /* SN_GEMM_ATTN_IN epilogue (see sn_gemm_decode_attn_in) */
+  const int32_t* positions;
+  const float* inv_freq;
+  void* q_out;
+  void* k_cache;
+  void* v_cache;
+  const int32_t* block_table;
+  int Hq, Hkv, D, page_size, max_blocks, window;
+  int32_t* err_flag;
+  /* NORM: residual[M][dim] += sum of slabs partials[0..nsplit) (slab order; nsplit < 0: the K
+   * splits of the latest PARTIAL GEMM phase before it); norm_out = rmsnorm(residual) * weight */
+  const float* partials;
+  int nsplit;
+  float* residual;
+  const void* weight;
+  void* norm_out;
+  int dim;
+  float eps;
+  /* GEMM SN_GEMM_RESID: optional [blocks][M] fp32 per-row sums of squares of the updated residual
+   * over each weight block's columns; NORM: take the row's sum of squares from such a buffer
+   * (n_ss blocks; n_ss < 0: the blocks of the latest RESID GEMM phase before it) */
+  float* ss_out;
+  const float* ss_in;
+  int n_ss;
+  int splits;    /* out: K splits the planner chose for a PARTIAL GEMM phase */
+} sn_chain_phase;
+sn_status sn_decode_chain(sn_chain_phase* phases, int n_phases, int M, unsigned long long* counter,
+                          void* stream);
+/* instrumentation: later launches write per-CTA %globaltimer stamps to buf ([grid][40] u64:
+ * start, end, and per phase: inputs ready, outputs done, arrival, norm release); NULL = off */
+void sn_decode_chain_trace(unsigned long long* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,11 +45,28 @@ SIGNATURES = {
     "sn_gemm_decode_tune": [I, I, I, I],
     "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, I, P],
     "sn_gemm_decode_attn_in": [P, I, I, I, P, I, P, P, P, P, P, P, I, I, I, I, I, I, P, I, P],
+    "sn_decode_chain": [P, I, I, P, P],
+    "sn_decode_chain_trace": [P],
 }
+
+
+class ChainPhase(ctypes.Structure):
+    """Mirror of include/sn_abi.h sn_chain_phase (field order and types must match)."""
+    _fields_ = [
+        ("kind", I), ("depends", I),
+        ("x", P), ("K", I), ("ldx", I), ("w", P), ("N", I), ("ldw", I), ("out", P), ("ldo", I), ("mode", I),
+        ("positions", P), ("inv_freq", P), ("q_out", P), ("k_cache", P), ("v_cache", P), ("block_table", P),
+        ("Hq", I), ("Hkv", I), ("D", I), ("page_size", I), ("max_blocks", I), ("window", I), ("err_flag", P),
+        ("partials", P), ("nsplit", I), ("residual", P), ("weight", P), ("norm_out", P), ("dim", I), ("eps", Fl),
+        ("ss_out", P), ("ss_in", P), ("n_ss", I), ("splits", I),
+    ]
+
+
+SN_CHAIN_GEMM, SN_CHAIN_NORM = 0, 1
 RESTYPES = {"sn_gdn_chunk_workspace_bytes": ctypes.c_size_t, "sn_kda_chunk_workspace_bytes": ctypes.c_size_t,
             "sn_attn_decode_workspace_bytes": ctypes.c_size_t,
             "sn_abi_version": ctypes.c_int, "sn_gemm_swiglu_block": ctypes.c_int, "sn_gemm_decode_plan": ctypes.c_int,
-            "sn_gemm_decode_tune": None}
+            "sn_gemm_decode_tune": None, "sn_decode_chain_trace": None}
 
 SN_F32, SN_BF16 = 0, 1
 SN_GEMM_STORE, SN_GEMM_RESID, SN_GEMM_PARTIAL, SN_GEMM_SWIGLU_IL, SN_GEMM_ATTN_IN = 0, 2, 3, 4, 6

@@ -36,6 +36,8 @@ struct Args {
   const int32_t* block_table;
   int Hq, Hkv, D, page_size, max_blocks, window;
   int32_t* err;  // set to 1 when a position falls outside the block table (nothing is written)
+  float* ss_out;  // RESID: per-row sum of squares of the updated residual over this block's columns,
+                  // [block][M] (the fused chain's next RMSNorm sums the blocks in order)
 };
 
 template <typename T>
@@ -158,6 +160,7 @@ __device__ __forceinline__ void finalize(const Args& a, int m, bool row_ok, int 
     return;
   }
   // STORE / RESID / PARTIAL: 32 contiguous columns per round
+  float ss = 0.f;
   for (int c = 0; c < br; c += 32) {
     const int n = blk * br + c;
     if (n >= a.N) break;
@@ -181,10 +184,16 @@ __device__ __forceinline__ void finalize(const Args& a, int m, bool row_ok, int 
           for (int e = 0; e < 32; ++e)
             if (e < nv) v[e] += o[e];
         }
+        if (a.ss_out) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < nv) ss += v[e] * v[e];
+        }
       }
       store32<float>(o, v, nv, vec);
     }
   }
+  if (mode == SN_GEMM_RESID && a.ss_out && row_ok) a.ss_out[(size_t)blk * a.M + m] = ss;
 }
 
 }  // namespace epi

@@ -62,7 +62,7 @@ class Supernet:
 
     def __init__(self, cfg: SupernetConfig, placement, *, batch: int, max_len: int, dtype=torch.bfloat16,
                  device="cuda", seed: int = 0, weights=None, fa_block_table=None, tp_group=None,
-                 tp_transport: str = "p2p"):
+                 tp_transport: str = "p2p", fused_chain: bool = False):
         _load_lib()  # fail loudly if the extension is missing
         self.B, self.max_len, self.dtype = batch, max_len, dtype
         self.device = torch.device(device)
@@ -84,6 +84,7 @@ class Supernet:
                 weights = shard_weights(cfg, self.kinds, weights, self.tp, rank)
                 cfg = tp_config(cfg, self.tp)
         self.cfg = cfg
+        self._fused_chain = fused_chain
         self.w = cast_weights(weights, self.device, dtype)
         del weights  # self.w may alias it; the FFN interleave below must free the original rows
         self.inv_freq = cfg.inv_freq().to(device=self.device, dtype=torch.float32)
@@ -186,6 +187,13 @@ class Supernet:
         self.act = e(B, cfg.ffn)
         self.logits = e(B, cfg.vocab)
         self.err_flag = torch.zeros(1, device=dev, dtype=torch.int32)  # KV append past the block table
+        # fused decode chains (bf16, one GPU): one grid-barrier counter per call site, on its own
+        # 64-byte line; zeroed once, never reset (csrc/sn_chain.cu)
+        # Measured (profiles/r02_chain.md): 10.47 ms/step fused vs 10.22 separate at B=64 / 32K —
+        # each grid-wide norm dependency costs ~5 us of L2 round trips under full HBM load, more
+        # than the kernel boundaries it removes; off by default, kept under test.
+        self.use_chain = bool(self._fused_chain) and dt == torch.bfloat16 and self.tp == 1 and B <= 128
+        self.chain_ctr = torch.zeros(len(self.kinds) + 1, 8, device=dev, dtype=torch.int64)[:, 0]
         # fp32 K-split slabs of the residual-updating projections (o-proj, FFN down), summed into
         # the residual in slab order by the next add + RMSNorm
         self.slab = e(8, B, cfg.hidden, d=torch.float32)
@@ -304,6 +312,8 @@ class Supernet:
     def decode_body(self):
         """One decode step on the current stream: step_tokens -> logits, next_tokens.
         Graph-capturable: every size/position it needs is read from device buffers."""
+        if self.use_chain:
+            return self._decode_body_chain()
         w = self.w
         self._probe_begin("embed", fine=True)
         ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
@@ -327,9 +337,100 @@ class Supernet:
         ops.argmax(self.logits, self.next_tokens)
         self._probe_end("argmax", fine=True)
 
+    # ------------------------------------------------------------------ fused decode chain
+    def _in_proj_phases(self, l):
+        """Chain phases of layer l's mixer in-projection (the rows its mixer kernel reads)."""
+        cfg, kind, st, d = self.cfg, self.kinds[l], self.state[l], self.dec
+        w = self.w["layers"][l]["mixer"]
+        if kind in (FA, SWA):
+            return [ops.chain_gemm(self.h, w["qkv_il"], None, "attn_in", positions=self.positions,
+                                   inv_freq=self.inv_freq, q_out=d["q"], k_cache=st["k"], v_cache=st["v"],
+                                   block_table=self.swa_block_table if kind == SWA else self.fa_block_table,
+                                   Hq=cfg.n_q_heads, Hkv=cfg.n_kv_heads, D=cfg.head_dim, page_size=cfg.page_size,
+                                   window=cfg.window if kind == SWA else 0, err_flag=self.err_flag)]
+        if kind == GDN:
+            return [ops.chain_gemm(self.h, w["w_in"], d["gdn_proj"], "store")]
+        H, D, R = cfg.kda_heads, cfg.kda_head_dim, cfg.kda_rank
+        proj, f1 = d["kda_proj"], 3 * H * D
+        return [ops.chain_gemm(self.h, w["w_in"], proj, "store"),
+                ops.chain_gemm(proj[:, f1:f1 + R], w["f2"], d["kda_fg"][0], "store"),
+                ops.chain_gemm(proj[:, f1 + R:f1 + 2 * R], w["g2"], d["kda_fg"][1], "store", depends=False)]
+
+    def _mixer_decode(self, l):
+        """Layer l's mixer kernel (its in-projection ran at the end of the previous chain)."""
+        cfg, kind, st, d = self.cfg, self.kinds[l], self.state[l], self.dec
+        w = self.w["layers"][l]["mixer"]
+        if kind in (FA, SWA):
+            window = cfg.window if kind == SWA else 0
+            bt = self.swa_block_table if kind == SWA else self.fa_block_table
+            sp, _ = self.attn_split[kind]
+            name = "swa_decode" if kind == SWA else "fa_decode"
+            self._probe_begin(name)
+            ops.attn_decode(d["q"], st["k"], st["v"], bt, self.seq_lens, d["attn"], d["ws"], d["counters"],
+                            cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size, window, sp,
+                            self.ws_max_splits, self.scale_attn)
+            self._probe_end(name)
+            return d["attn"]
+        if kind == GDN:
+            D = cfg.gdn_head_dim
+            self._probe_begin("gdn_decode")
+            ops.gdn_decode(d["gdn_proj"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
+                           w["dt_bias"], w["norm_w"], d["gdn_out"], cfg.gdn_k_heads, cfg.gdn_v_heads, D,
+                           cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+            self._probe_end("gdn_decode")
+            return d["gdn_out"]
+        D = cfg.kda_head_dim
+        self._probe_begin("kda_decode")
+        ops.kda_decode(d["kda_proj"], d["kda_fg"], st["conv"], w["conv_w"], st["S"], None, self.positions,
+                       w["A_log"], w["dt_bias"], w["g2_b"], w["norm_w"], d["kda_out"], cfg.kda_heads, D,
+                       cfg.kda_rank, cfg.conv_width, 1.0 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
+        self._probe_end("kda_decode")
+        return d["kda_out"]
+
+    def _chain(self, site, phases):
+        self._probe_begin("chain")
+        ops.decode_chain(phases, self.B, self.chain_ctr[site])
+        self._probe_end("chain")
+
+    def _decode_body_chain(self):
+        """bf16 single-GPU decode step as 1 + 2L + 2 launches: embed, then per layer one fused
+        chain (out-proj -> add+RMSNorm -> FFN gate/up -> down -> add+RMSNorm -> next in-proj,
+        csrc/sn_chain.cu) and the layer's mixer kernel, then argmax."""
+        w, cfg, L = self.w, self.cfg, len(self.kinds)
+        layers = w["layers"]
+        self._probe_begin("embed", fine=True)
+        ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
+        self._probe_end("embed", fine=True)
+        self._chain(0, [ops.chain_norm(self.residual, layers[0]["norm1"], self.h, cfg.norm_eps)]
+                    + self._in_proj_phases(0))
+        for l in range(L):
+            lw = layers[l]
+            mix = self._mixer_decode(l)
+            # the residual projections add straight into the residual stream (one writer per
+            # element, no split-K slabs) and leave per-block row sums of squares for the norm
+            # residual projections: fp32 split-K slabs (PARTIAL) that the next NORM phase adds to
+            # the residual in slab order.  (RESID straight into the residual with per-block
+            # sums of squares for the norm was measured slower: the S=1 plans leave fewer weight
+            # bytes in flight per SM — 10.06 vs 9.13 ms/step, profiles/r02_chain.md.)
+            rp = lambda x, wt: ops.chain_gemm(x, wt, self.slab, "partial")
+            nm = lambda wt: ops.chain_norm(self.residual, wt, self.h, cfg.norm_eps, partials=self.slab)
+            ph = [rp(mix, lw["mixer"]["o"]), nm(lw["norm2"]),
+                  ops.chain_gemm(self.h, lw["ffn_gu_il"], self.act, "swiglu_il"),
+                  rp(self.act, lw["ffn_down"])]
+            if l + 1 < L:
+                ph += [nm(layers[l + 1]["norm1"])] + self._in_proj_phases(l + 1)
+            else:
+                ph += [nm(w["final_norm"]), ops.chain_gemm(self.h, w["lm_head"], self.logits, "store")]
+            self._chain(l + 1, ph)
+        self._probe_begin("argmax", fine=True)
+        ops.argmax(self.logits, self.next_tokens)
+        self._probe_end("argmax", fine=True)
+
     def kernels_per_step(self) -> dict:
         """Launch census of one decode step (all libsn100 kernels; the decode step launches no
         library GEMMs).  NCCL all-reduces of the head-parallel NCCL transport are counted apart."""
+        if self.use_chain:  # embed, L + 1 chains, L mixer kernels, argmax
+            return {"sn": 2 * len(self.kinds) + 3, "cublas": 0, "nccl": 0}
         sn = 4                                     # embed, final norm, LM head, argmax
         for kind in self.kinds:
             sn += 2 + 4 + 1 + (2 if kind == KDA else 0)  # norms, in/out-proj, gate/up, down, mixer (+KDA gates)

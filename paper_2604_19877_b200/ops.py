@@ -11,7 +11,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (SN_BF16, SN_F32, SN_GEMM_ATTN_IN, SN_GEMM_PARTIAL, SN_GEMM_RESID, SN_GEMM_STORE, SN_GEMM_SWIGLU_IL,
+from ._lib import (SN_BF16, SN_CHAIN_GEMM, SN_CHAIN_NORM, SN_F32, ChainPhase, SN_GEMM_ATTN_IN, SN_GEMM_PARTIAL, SN_GEMM_RESID, SN_GEMM_STORE, SN_GEMM_SWIGLU_IL,
                    call)
 
 _DT = {torch.bfloat16: SN_BF16, torch.float32: SN_F32}
@@ -267,3 +267,65 @@ def tp_allreduce_add_rmsnorm(peer_slabs, peer_counters, world, rank, nsplit, res
     rows, dim = residual.shape
     call("sn_tp_allreduce_add_rmsnorm", _p(peer_slabs), _p(peer_counters), world, rank, nsplit, _p(residual),
          _p(weight), _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
+
+
+# ------------------------------------------------------------------ fused decode chain
+def chain_gemm(x, w, out, mode, depends=True, ss_out=None, **attn):
+    """A GEMM phase of decode_chain (see gemm_decode for the modes; attention in-projection:
+    mode "attn_in" with positions, inv_freq, q_out, k_cache, v_cache, block_table, Hq, Hkv, D,
+    page_size, window, err_flag)."""
+    M, K = x.shape
+    N = out.shape[-1] if mode != "attn_in" else (attn["Hq"] + 2 * attn["Hkv"]) * attn["D"]
+    assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and x.stride(1) == 1 and w.stride(1) == 1
+    if mode == "swiglu_il":
+        h = gemm_swiglu_block(N)
+        assert w.shape[0] == -(-N // h) * 2 * h, "weight not in the interleaved layout for this shape"
+    elif mode != "attn_in":
+        assert w.shape[0] == N
+    ph = dict(kind=SN_CHAIN_GEMM, depends=int(depends), x=_p(x), K=K, ldx=x.stride(0), w=_p(w), N=N,
+              ldw=w.stride(0), mode=GEMM_MODES[mode], keep=(x, w, out))
+    if mode == "attn_in":
+        bt = attn["block_table"]
+        ph.update(out=attn["q_out"].data_ptr(), ldo=0, positions=_p(attn["positions"]),
+                  inv_freq=_p(attn["inv_freq"]), q_out=_p(attn["q_out"]), k_cache=_p(attn["k_cache"]),
+                  v_cache=_p(attn["v_cache"]), block_table=_p(bt), Hq=attn["Hq"], Hkv=attn["Hkv"], D=attn["D"],
+                  page_size=attn["page_size"], max_blocks=bt.shape[1], window=attn["window"],
+                  err_flag=_p(attn.get("err_flag")))
+    else:
+        assert out.dtype == (torch.float32 if mode in ("resid", "partial") else torch.bfloat16)
+        if mode == "partial":
+            assert out.dim() == 3 and out.shape[1] == M and out.is_contiguous()
+        ph.update(out=_p(out), ldo=out.stride(-2))
+    if ss_out is not None:
+        assert mode == "resid" and ss_out.dtype == torch.float32 and ss_out.is_contiguous()
+        ph.update(ss_out=_p(ss_out))
+    return ph
+
+
+def chain_norm(residual, weight, out, eps, partials=None, nsplit=-1, ss_in=None, n_ss=-1, depends=True):
+    """A NORM phase: residual += sum of the slabs (nsplit < 0: the splits of the latest PARTIAL
+    GEMM phase before it); out = rmsnorm(residual) * weight.  ss_in: take each row's sum of
+    squares from the per-block sums a RESID GEMM phase wrote (n_ss < 0: its block count)."""
+    assert residual.dtype == torch.float32 and residual.is_contiguous() and out.dtype == torch.bfloat16
+    if partials is None:
+        nsplit = 0
+    if ss_in is None:
+        n_ss = 0
+    return dict(kind=SN_CHAIN_NORM, depends=int(depends), partials=_p(partials), nsplit=nsplit,
+                residual=_p(residual), weight=_p(weight), norm_out=_p(out), dim=residual.shape[1], eps=float(eps),
+                ss_in=_p(ss_in), n_ss=n_ss, keep=(residual, weight, out, partials, ss_in))
+
+
+def decode_chain(phases, M, counter):
+    """Run the phases (chain_gemm / chain_norm dicts) as one persistent launch; counter: an
+    int64 device word for this call site (zero-initialised once, never reset).  Returns the K
+    split count of every phase (PARTIAL GEMMs and the norms that consume them)."""
+    n = len(phases)
+    arr = (ChainPhase * n)()
+    for i, ph in enumerate(phases):
+        for k, v in ph.items():
+            if k != "keep":
+                setattr(arr[i], k, v)
+    assert counter.dtype == torch.int64 and counter.is_cuda
+    call("sn_decode_chain", ctypes.cast(arr, ctypes.c_void_p), n, M, _p(counter), _s())
+    return [arr[i].splits for i in range(n)]

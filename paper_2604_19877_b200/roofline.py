@@ -83,4 +83,8 @@ def role_step_bytes(cfg: SupernetConfig, kinds, role: str, B: int, ctx: int, elt
     if role == "gemm_out_proj":
         o_in = {FA: cfg.attn_o_in, SWA: cfg.attn_o_in, GDN: cfg.gdn_value_dim, KDA: cfg.kda_dim}
         return sum(gemm(d, o_in[k]) for k in kinds)
+    if role == "chain":  # fused decode chains (csrc/sn_chain.cu): every projection of the step
+        kda_gates = sum(1 for k in kinds if k == KDA) * 2 * gemm(cfg.kda_dim, cfg.kda_rank)
+        return sum(role_step_bytes(cfg, kinds, r, B, ctx, elt) for r in
+                   ("gemm_ffn_gate_up", "gemm_ffn_down", "gemm_lm_head", "gemm_in_proj", "gemm_out_proj")) + kda_gates
     return None

@@ -2,7 +2,7 @@
 
 The tiny configuration (d=256, head dim 64) never reaches the kernels the benchmark runs:
 the tcgen05 attention prefill (head dim 128 only), the decode-GEMM plans of a d=5120 trunk
-(split-K slabs, the SwiGLU-interleaved 256-row blocks, the 14336-wide down-projection, the
+(split-K slabs, the SwiGLU-interleaved 224-row blocks, the 14336-wide down-projection, the
 131072-row LM head), and the delta-rule decode CTAs at 128x128 states in both widths (the
 512-thread CTAs of small batches and the 256-thread ones of B=64).  Here every layer has the
 Apriel-1.6 shapes (R/PAPER.md:175-182, 1540-1625) and only the depth is cut to 4 layers, one
@@ -46,9 +46,10 @@ def _no_tf32():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("placement", ["SKGA", "AGKS"])
-@pytest.mark.parametrize("B", [64, 1])
-def test_apriel_shapes_ragged_prefill_graph_decode(placement, B):
+@pytest.mark.parametrize("placement,B,chain", [("SKGA", 64, False), ("AGKS", 64, False), ("SKGA", 1, False),
+                                               ("AGKS", 1, False), ("AGKS", 64, True), ("SKGA", 1, True)])
+def test_apriel_shapes_ragged_prefill_graph_decode(placement, B, chain):
+    """chain=True: the decode step through the fused decode chains (csrc/sn_chain.cu)."""
     from paper_2604_19877_b200.graphs import DecodeGraph
     from paper_2604_19877_b200.model import Supernet
 
@@ -60,7 +61,8 @@ def test_apriel_shapes_ragged_prefill_graph_decode(placement, B):
     seqs = [torch.randint(0, CFG.vocab, (L + STEPS,), generator=g) for L in lens]
     max_len = max(lens) + STEPS
 
-    model = Supernet(CFG, placement, batch=B, max_len=max_len, dtype=torch.bfloat16, weights=w)
+    model = Supernet(CFG, placement, batch=B, max_len=max_len, dtype=torch.bfloat16, weights=w, fused_chain=chain)
+    assert model.use_chain == chain
     pre = model.prefill([s[:L] for s, L in zip(seqs, lens)], return_all=True)
     graph = DecodeGraph(model, preserve_state=True)
     dec = []

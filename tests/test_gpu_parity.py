@@ -21,7 +21,7 @@ def rel_err(a, b):
     return ((a - b).abs().max() / b.abs().max().clamp_min(1e-6)).item()
 
 
-def run_pair(placement, dtype, B, T_prefill, n_decode, cfg=TINY, seed=0, graph=False, force_simt=False):
+def run_pair(placement, dtype, B, T_prefill, n_decode, cfg=TINY, seed=0, graph=False, force_simt=False, chain=False):
     from paper_2604_19877_b200.model import Supernet
     kinds = layer_kinds(placement)
     w = init_weights(cfg, kinds, seed=seed)
@@ -30,7 +30,7 @@ def run_pair(placement, dtype, B, T_prefill, n_decode, cfg=TINY, seed=0, graph=F
     toks = torch.randint(0, cfg.vocab, (B, T_prefill + n_decode), generator=g)
     oracle = OracleSupernet(cfg, kinds, w, batch=B, max_len=T_prefill + n_decode)
     ref = oracle.run(toks)
-    model = Supernet(cfg, placement, batch=B, max_len=T_prefill + n_decode, dtype=dtype, weights=w)
+    model = Supernet(cfg, placement, batch=B, max_len=T_prefill + n_decode, dtype=dtype, weights=w, fused_chain=chain)
     model.force_simt = force_simt
     pre = model.prefill(toks[:, :T_prefill], return_all=True)
     outs = [pre]
@@ -209,3 +209,17 @@ def test_chunked_prompt_append_matches_oracle(placement):
         out = torch.cat(got[b])
         assert out.shape[0] == T + steps
         assert rel_err(out, ref) <= TOL[torch.bfloat16], (b, rel_err(out, ref))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("placement", ["ASKG", "GKSA"])
+@pytest.mark.parametrize("B", [2, 96])
+def test_fused_chain_decode_matches_oracle(placement, B):
+    """The fused decode chains (one persistent launch per layer boundary, csrc/sn_chain.cu):
+    eager and graphed decode within the bf16 tolerance, graph bit-identical to eager."""
+    m1, oracle, eager, ref = run_pair(placement, torch.bfloat16, B=B, T_prefill=70, n_decode=10, chain=True)
+    assert m1.use_chain
+    assert rel_err(eager, ref) <= TOL[torch.bfloat16]
+    check_states(m1, oracle, TOL[torch.bfloat16])
+    _, _, graphed, _ = run_pair(placement, torch.bfloat16, B=B, T_prefill=70, n_decode=10, graph=True, chain=True)
+    assert torch.equal(eager.cpu(), graphed.cpu())

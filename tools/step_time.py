@@ -19,9 +19,10 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--context", type=int, default=32768)
 ap.add_argument("--steps", type=int, default=30)
 a = ap.parse_args()
-m = Supernet(APRIEL, PRESETS[a.preset].layer_string, batch=a.batch, max_len=a.context + 128, dtype=torch.bfloat16)
-fill_synthetic(m, a.context)
-g = DecodeGraph(m, feedback=True, preserve_state=False)
+m = Supernet(APRIEL, PRESETS[a.preset].layer_string, batch=a.batch, max_len=a.context + 128, dtype=torch.bfloat16,
+             fused_chain=bool(os.environ.get("SN_CHAIN")))  # A/B: fused decode chains
+g = DecodeGraph(m, feedback=True, preserve_state=False)  # warm-up + capture on the empty engine (it resets)
+fill_synthetic(m, a.context)  # then fill the KV / states to the context
 for _ in range(5):
     g.replay()
 torch.cuda.synchronize()
@@ -35,5 +36,5 @@ for rep in range(3):
     torch.cuda.synchronize()
     best.append(e0.elapsed_time(e1) / a.steps)
 ms = min(best)
-print(f"SN_DECODE_GEMMS={os.environ.get('SN_DECODE_GEMMS', '(default)')}: {ms:.3f} ms/step "
+print(f"{'fused chains' if m.use_chain else 'separate kernels'}: {ms:.3f} ms/step "
       f"{a.batch / ms * 1e3:.0f} tok/s  (reps {', '.join(f'{b:.3f}' for b in best)})")
