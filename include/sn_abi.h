@@ -57,7 +57,9 @@ int sn_abi_version(void);
 /* residual[r,:] = table[tokens[r],:] (fp32).  If seq_lens/positions are
  * non-NULL this is also the decode-step prologue: positions[b] = seq_lens[b];
  * seq_lens[b] += 1 for b < rows (so every later kernel of the step sees the
- * new token's position and the post-append length).                        */
+ * new token's position and the post-append length).  A negative token marks an
+ * idle slot (continuous batching): positions[b] = -1, seq_lens[b] unchanged, a
+ * zero residual row, and the KV append skips it.                           */
 sn_status sn_embed(const int32_t* tokens, const void* table, float* residual,
                    int32_t* seq_lens, int32_t* positions, int rows, int dim,
                    int dtype, void* stream);
@@ -75,9 +77,10 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit,
 sn_status sn_swiglu_il(const void* gate_up, int ld, void* out, int rows, int ffn,
                        int h, int dtype, void* stream);
 
-/* out_tokens[r] = argmax_v logits[r,v] (lowest index on ties).             */
+/* out_tokens[r] = argmax_v logits[r,v] (lowest index on ties); -1 for idle slots
+ * (positions[r] < 0, positions may be NULL) so a token-feedback graph keeps them idle. */
 sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens,
-                    int dtype, void* stream);
+                    const int32_t* positions, int dtype, void* stream);
 
 /* ---------------------------------------------------------------- FA / SWA
  * R/PAPER.md:1540-1563 (GQA + RoPE; SWA = same weights shape, window mask

@@ -22,7 +22,7 @@ SIGNATURES = {
     "sn_abi_version": [],
     "sn_embed": [P, P, P, P, P, I, I, I, P],
     "sn_add_rmsnorm": [P, P, I, P, P, P, I, I, Fl, I, P],
-    "sn_argmax": [P, I, I, P, I, P],
+    "sn_argmax": [P, I, I, P, P, I, P],
     "sn_swiglu_il": [P, I, P, I, I, I, I, P],
     "sn_rope_kv_append": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, I, P],
     "sn_attn_decode_workspace_bytes": [I, I, I, I, I],

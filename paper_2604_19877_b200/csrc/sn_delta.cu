@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
 
   // ---- the in-projection row: this lane's q, k, v inputs, the output gate z, a, b; taps
   const int pos = a.positions[b];
+  if (pos < 0) return;  // idle slot (sn_embed): state and conv ring untouched
   const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
   float xq[EPL], xk[EPL];
   loadn<T, EPL>(prow + qch, xq);
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pos = a.positions[b];
+  if (pos < 0) return;  // idle slot (sn_embed): state and conv ring untouched
   const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
 
   // ---- 1. prologue loads of the in-projection row and the gate factors, all issued first

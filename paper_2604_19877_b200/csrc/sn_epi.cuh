@@ -131,7 +131,8 @@ __device__ __forceinline__ void finalize(const Args& a, int m, bool row_ok, int 
         const int hk = is_k ? head - a.Hq : head - a.Hq - a.Hkv;
         const int slot = a.window > 0 ? pos % a.window : pos;
         const int pi = slot / a.page_size;
-        if (pos < 0 || pi >= a.max_blocks) {  // past the block table: nothing is written
+        if (pos < 0) continue;             // idle slot (sn_embed): nothing is appended
+        if (pi >= a.max_blocks) {          // past the block table: nothing is written
           if (a.err) *a.err = 1;
           continue;
         }

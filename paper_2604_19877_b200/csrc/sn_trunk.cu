@@ -43,13 +43,22 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __rest
   const int r = blockIdx.x;
   if (seq_lens != nullptr && r == 0) {
     for (int b = threadIdx.x; b < rows; b += blockDim.x) {
+      if (tokens[b] < 0) {  // idle slot (continuous batching): no position, the length stays
+        positions[b] = -1;
+        continue;
+      }
       int L = seq_lens[b];
       positions[b] = L;
       seq_lens[b] = L + 1;
     }
   }
-  const T* src = table + (size_t)tokens[r] * dim;
   float* dst = residual + (size_t)r * dim;
+  const int tok = tokens[r];
+  if (tok < 0) {  // idle slot: a zero row (its outputs are ignored; nothing is appended)
+    for (int i = threadIdx.x * 4; i < dim; i += blockDim.x * 4) *reinterpret_cast<float4*>(dst + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const T* src = table + (size_t)tok * dim;
   for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
     float f[8];
     load8<T>(src + i, f);
@@ -224,7 +233,7 @@ __global__ void swiglu_il_kernel(const T* __restrict__ gu, T* __restrict__ out, 
 // ------------------------------------------------------------------ argmax
 template <typename T>
 __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logits, int vocab,
-                                                      int32_t* __restrict__ out) {
+                                                      int32_t* __restrict__ out, const int32_t* __restrict__ positions) {
   sn::pdl_launch_dependents();
   sn::pdl_wait();
   __shared__ float sv[32];
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logi
       if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
     // an all-NaN row never beats -inf: return token 0, never an out-of-range id that the
     // graph's token feedback would hand to the embedding gather
-    out[blockIdx.x] = bi < vocab ? bi : 0;
+    out[blockIdx.x] = (positions && positions[blockIdx.x] < 0) ? -1 : (bi < vocab ? bi : 0);  // idle stays idle
   }
 }
 
@@ -332,11 +341,12 @@ sn_status sn_swiglu_il(const void* gate_up, int ld, void* out, int rows, int ffn
   });
 }
 
-sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens, int dtype, void* stream) {
+sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens, const int32_t* positions, int dtype,
+                    void* stream) {
   SN_REQUIRE(rows > 0 && vocab > 0 && vocab % 8 == 0, "sn_argmax: bad shape rows=%d vocab=%d", rows, vocab);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     launch_pdl(argmax_kernel<T>, dim3(rows), dim3(1024), 0, (cudaStream_t)stream, (const T*)logits, vocab,
-               out_tokens);
+               out_tokens, positions);
     return check_launch("sn_argmax");
   });
 }

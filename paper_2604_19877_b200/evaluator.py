@@ -26,20 +26,24 @@ from .config import CONFIGS
 from .placement import DEFAULT_CATALOG, Placement
 
 
-def loglik_from_logits(logits: torch.Tensor, tokens: torch.Tensor) -> torch.Tensor:
-    """Per-sequence mean next-token log-likelihood: logits [B, T, V] predict tokens[:, 1:]."""
+def loglik_from_logits(logits: torch.Tensor, tokens: torch.Tensor, prompt_len: int = 1) -> torch.Tensor:
+    """Per-sequence mean log-likelihood of the completion tokens tokens[:, prompt_len:] (each
+    predicted by the logits of the position before it; logits [B, T, V]).  prompt_len = 1
+    scores every next-token position."""
     B, T, _ = logits.shape
+    if not 1 <= prompt_len < T:
+        raise ValueError(f"prompt_len {prompt_len} must be in [1, {T})")
     out = torch.empty(B, dtype=torch.float64)
     for b in range(B):  # one row at a time: [T, V] fp32 log-softmax, not [B, T, V]
-        lp = torch.log_softmax(logits[b, :-1].float(), dim=-1)
-        tgt = tokens[b, 1:].to(device=lp.device, dtype=torch.long)
+        lp = torch.log_softmax(logits[b, prompt_len - 1:-1].float(), dim=-1)
+        tgt = tokens[b, prompt_len:].to(device=lp.device, dtype=torch.long)
         out[b] = lp.gather(-1, tgt[:, None]).double().mean().item()
     return out
 
 
-def trace_loglik(model, traces: torch.Tensor) -> float:
-    """Mean per-token log-likelihood of traces [N, T] (N a multiple of model.B) under the
-    model's placement."""
+def trace_loglik(model, traces: torch.Tensor, prompt_len: int = 1) -> float:
+    """Mean completion-token log-likelihood of traces [N, T] (N a multiple of model.B) under the
+    model's placement, normalised by completion tokens (R/PAPER.md:917-921)."""
     N = traces.shape[0]
     if N % model.B:
         raise ValueError(f"{N} traces is not a multiple of the engine batch {model.B}")
@@ -47,7 +51,7 @@ def trace_loglik(model, traces: torch.Tensor) -> float:
     for i in range(0, N, model.B):
         toks = traces[i:i + model.B]
         logits = model.prefill(toks, return_all=True)
-        total += float(loglik_from_logits(logits, toks).sum())
+        total += float(loglik_from_logits(logits, toks, prompt_len).sum())
     return total / N
 
 
@@ -83,6 +87,8 @@ def main(argv=None) -> int:
     ap.add_argument("--seed", type=int, default=0, help="weight seed")
     ap.add_argument("--init-device", default="cuda", help="where the seeded weight draws run (cpu = the oracle's weights)")
     ap.add_argument("--trace-seed", type=int, default=1)
+    ap.add_argument("--prompt-len", type=int, default=1,
+                    help="tokens of each trace that are prompt: only the completion after them is scored")
     ap.add_argument("--normalize", default="", help="lo,hi: print (ll - lo) / (hi - lo) (R/PAPER.md:921)")
     a = ap.parse_args(argv)
     cfg = CONFIGS[a.config]
@@ -101,11 +107,17 @@ def main(argv=None) -> int:
     store = SupernetStore(cfg, seed=a.seed, init_device=a.init_device)
     B = min(a.batch, traces.shape[0])
     block = ops.gemm_swiglu_block(cfg.ffn)  # the FFN decode layout, shared by every placement
+    N = traces.shape[0]
     for code in codes:
-        model = Supernet(cfg, code, batch=B, max_len=traces.shape[1],
-                         weights=store.weights(code, swiglu_block=block))
-        ll = trace_loglik(model, traces[: (traces.shape[0] // B) * B])
-        del model
+        # every trace is scored: full batches of B, then one engine for the remainder
+        total = 0.0
+        for b, lo, hi in ((B, 0, N // B * B), (N % B, N // B * B, N)):
+            if hi > lo:
+                model = Supernet(cfg, code, batch=b, max_len=traces.shape[1],
+                                 weights=store.weights(code, swiglu_block=block))
+                total += trace_loglik(model, traces[lo:hi], a.prompt_len) * (hi - lo)
+                del model
+        ll = total / N
         if lo_hi:
             ll = (ll - lo_hi[0]) / (lo_hi[1] - lo_hi[0])
         print(repr(float(ll)), flush=True)

@@ -110,11 +110,13 @@ class Supernet:
         hb = ops.gemm_swiglu_block(ffn)
         self.gu_il = (ffn, hb)
         for lw in self.w["layers"]:
-            if "ffn_gu_il" in lw:  # prebuilt and shared (serving.SupernetStore)
-                if lw["ffn_gu_il"].shape[0] != -(-ffn // hb) * 2 * hb:
-                    raise ValueError("prebuilt SwiGLU-interleaved FFN weights use another block height")
+            if "ffn_gu_il" in lw:  # prebuilt and shared (serving.SupernetStore), tagged with its block
+                if lw.get("ffn_gu_hb") != hb:
+                    raise ValueError(f"prebuilt SwiGLU-interleaved FFN weights use block {lw.get('ffn_gu_hb')}, "
+                                     f"this engine needs {hb}")
             else:
                 lw["ffn_gu_il"] = ops.interleave_swiglu(lw.pop("ffn_gu"), hb)
+                lw["ffn_gu_hb"] = hb
         for l, kind in enumerate(self.kinds):
             mw = self.w["layers"][l]["mixer"]
             if kind in (FA, SWA) and "qkv_il" not in mw:
@@ -334,7 +336,7 @@ class Supernet:
         self._norm(pending, w["final_norm"])
         self._gemm(self.h, w["lm_head"], self.logits, "store", "lm_head")
         self._probe_begin("argmax", fine=True)
-        ops.argmax(self.logits, self.next_tokens)
+        ops.argmax(self.logits, self.next_tokens, self.positions)
         self._probe_end("argmax", fine=True)
 
     # ------------------------------------------------------------------ fused decode chain
@@ -423,7 +425,7 @@ class Supernet:
                 ph += [nm(w["final_norm"]), ops.chain_gemm(self.h, w["lm_head"], self.logits, "store")]
             self._chain(l + 1, ph)
         self._probe_begin("argmax", fine=True)
-        ops.argmax(self.logits, self.next_tokens)
+        ops.argmax(self.logits, self.next_tokens, self.positions)
         self._probe_end("argmax", fine=True)
 
     def kernels_per_step(self) -> dict:

@@ -51,9 +51,10 @@ def add_rmsnorm(delta, residual, weight, out, eps, partials=None, nsplit=0):
          _p(out), rows, dim, eps, dtype_code(out.dtype), _s())
 
 
-def argmax(logits, out_tokens):
+def argmax(logits, out_tokens, positions=None):
+    """out_tokens = argmax over the vocabulary; -1 for idle slots (positions < 0)."""
     rows, vocab = logits.shape
-    call("sn_argmax", _p(logits), rows, vocab, _p(out_tokens), dtype_code(logits.dtype), _s())
+    call("sn_argmax", _p(logits), rows, vocab, _p(out_tokens), _p(positions), dtype_code(logits.dtype), _s())
 
 
 def rope_kv_append(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,

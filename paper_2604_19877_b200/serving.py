@@ -79,6 +79,7 @@ class SupernetStore:
             lw["mixer"] = self.mixer(l, k)
             if swiglu_block:
                 lw["ffn_gu_il"] = self.swiglu_interleaved(l, swiglu_block)
+                lw["ffn_gu_hb"] = swiglu_block
                 del lw["ffn_gu"]
             layers.append(lw)
         return {"embed": self.trunk["embed"], "final_norm": self.trunk["final_norm"],

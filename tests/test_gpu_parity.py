@@ -223,3 +223,41 @@ def test_fused_chain_decode_matches_oracle(placement, B):
     check_states(m1, oracle, TOL[torch.bfloat16])
     _, _, graphed, _ = run_pair(placement, torch.bfloat16, B=B, T_prefill=70, n_decode=10, graph=True, chain=True)
     assert torch.equal(eager.cpu(), graphed.cpu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("placement", ["ASKG", "GKSA"])
+def test_idle_slot_does_not_advance(placement):
+    """A negative step token marks an idle slot (continuous batching): its length, KV pages /
+    ring, conv ring and recurrent state stay untouched, the feedback token stays -1, and when it
+    resumes it continues exactly where it stopped (matches the oracle on its own stream)."""
+    from paper_2604_19877_b200.graphs import DecodeGraph
+    from paper_2604_19877_b200.model import Supernet
+    kinds = layer_kinds(placement)
+    w = cast_weights(init_weights(TINY, kinds, seed=0), "cpu", torch.bfloat16)
+    T, steps, idle = 40, 6, (1, 2, 3)  # slot 1 idles during steps 1..3
+    toks = torch.randint(0, TINY.vocab, (3, T + steps), generator=torch.Generator().manual_seed(4))
+    model = Supernet(TINY, placement, batch=3, max_len=T + steps, dtype=torch.bfloat16, weights=w)
+    model.prefill(toks[:, :T])
+    graph = DecodeGraph(model, preserve_state=True)
+    got = {0: [], 1: [], 2: []}
+    pos = [T, T, T]
+    for t in range(steps):
+        feed = torch.tensor([int(toks[b, pos[b]]) if not (b == 1 and t in idle) else -1 for b in range(3)],
+                            dtype=torch.int32)
+        model.step_tokens.copy_(feed)
+        graph.replay()
+        lg = model.logits.clone().float().cpu()
+        nt = model.next_tokens.cpu()
+        for b in range(3):
+            if b == 1 and t in idle:
+                assert int(nt[1]) == -1 and int(model.seq_lens[1]) == pos[1]
+                continue
+            got[b].append(lg[b])
+            pos[b] += 1
+    torch.cuda.synchronize()
+    assert int(model.err_flag.item()) == 0
+    for b in range(3):
+        n = len(got[b])
+        ref = OracleSupernet(TINY, kinds, w, batch=1, max_len=T + n).run(toks[b:b + 1, :T + n])[0]
+        assert rel_err(torch.stack(got[b]), ref[T:T + n]) <= TOL[torch.bfloat16], b

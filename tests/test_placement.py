@@ -100,3 +100,26 @@ def test_catalog_validation():
         Allocation((1, -1))
     with pytest.raises(ValueError):
         Placement((0,), 0)
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="the reference checkout exists only in the build container")
+def test_real_placeopt_placement_drives_the_dispatch_table():
+    """A real placeopt.Placement (the reference's own type, R/pkg/src/placeopt/placements.py)
+    is accepted at the boundary and dispatches every layer like its code string; a reference
+    placement over a custom catalog dispatches by mixer name."""
+    import sys
+    sys.path.insert(0, REF_SRC)
+    try:
+        from placeopt import placements as pp
+    finally:
+        sys.path.remove(REF_SRC)
+    from paper_2604_19877_b200 import PRESETS
+    for text in ["ASKG", "GGKKSSAA", PRESETS["Reg|Lklhd-10"].layer_string]:
+        ref = pp.Placement.from_codes(text, pp.DEFAULT_CATALOG)
+        assert layer_kinds(ref) == layer_kinds(text)
+        assert coerce_placement(ref).to_codes(DEFAULT_CATALOG) == ref.to_codes(pp.DEFAULT_CATALOG)
+    ref_alloc = pp.allocation_of(pp.Placement.from_codes(PRESETS["Reg|Lklhd-10"].layer_string, pp.DEFAULT_CATALOG))
+    assert tuple(ref_alloc.counts) == PRESETS["Reg|Lklhd-10"].counts

@@ -30,6 +30,13 @@ def test_loglik_from_logits_matches_definition():
     # a uniform model scores -log(V) per token
     assert torch.allclose(loglik_from_logits(torch.zeros(2, 5, 11), toks[:2, :5]).float(),
                           torch.full((2,), -math.log(11.0)), atol=1e-6)
+    # completion-only scoring (R/PAPER.md:917-921): the first 4 tokens are prompt
+    llc = loglik_from_logits(logits, toks, prompt_len=4)
+    for b in range(3):
+        ref = sum(math.log(torch.softmax(logits[b, t], -1)[toks[b, t + 1]].item()) for t in range(3, 6)) / 3
+        assert abs(llc[b].item() - ref) < 1e-5
+    with pytest.raises(ValueError):
+        loglik_from_logits(logits, toks, prompt_len=7)
 
 
 def test_parse_placements_validates_every_line():
