@@ -46,6 +46,7 @@ SIGNATURES = {
     "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, I, P],
     "sn_gemm_decode_attn_in": [P, I, I, I, P, I, P, P, P, P, P, P, I, I, I, I, I, I, P, I, P],
     "sn_decode_chain": [P, I, I, P, P],
+    "sn_gemm_prefill": [P, I, I, I, P, I, I, P, I, I, I, P],
     "sn_decode_chain_trace": [P],
 }
 

@@ -536,18 +536,29 @@ class Supernet:
             self._tp_sum(mix)
             ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
             act = e(rows, cfg.ffn)
-            ops.swiglu_il(h @ lw["ffn_gu_il"].t(), act, *self.gu_il)
-            torch.mm(act, lw["ffn_down"].t(), out=ffn_o)
+            self._mm(h, lw["ffn_gu_il"], act, swiglu=True)
+            self._mm(act, lw["ffn_down"], ffn_o)
             self._tp_sum(ffn_o)
             delta = ffn_o
         ops.add_rmsnorm(delta, resid, w["final_norm"], h, cfg.norm_eps)
         if return_all:
-            logits = h @ w["lm_head"].t()
+            logits = self._mm(h, w["lm_head"])
             if ragged:
                 return [logits[a:b] for a, b in zip(cu_host[:-1], cu_host[1:])]
             return logits.view(B, T, cfg.vocab)
         last = h[cu[1:].long() - 1]
-        return last @ w["lm_head"].t()
+        return self._mm(last.contiguous(), w["lm_head"])
+
+    def _mm(self, x, w, out=None, swiglu=False):
+        """Prefill projection out = x @ w.T: the tcgen05 prefill GEMM (csrc/sn_pgemm.cu) in bf16
+        (swiglu: w in the SwiGLU-interleaved layout, out = silu(gate) * up); torch in the fp32
+        numerics mode, which is the reference-precision path, not a fallback."""
+        if x.dtype == torch.bfloat16:
+            return ops.gemm_prefill(x, w, out, swiglu_h=self.gu_il[1] if swiglu else 0)
+        if swiglu:
+            ops.swiglu_il(x @ w.t(), out, *self.gu_il)
+            return out
+        return torch.mm(x, w.t(), out=out) if out is not None else x @ w.t()
 
     def _tp_sum(self, t):
         """Prefill: sum a row-parallel projection output over the TP group (in fp32)."""
@@ -566,7 +577,7 @@ class Supernet:
         rows = h.shape[0]
         window = cfg.window if kind == SWA else 0
         bt = self.swa_block_table if kind == SWA else self.fa_block_table
-        qkv = h @ w["qkv_il"].t()
+        qkv = self._mm(h, w["qkv_il"])
         q = torch.empty(rows, Hq, D, device=h.device, dtype=h.dtype)
         k = torch.empty(rows, Hkv, D, device=h.device, dtype=h.dtype)
         v = torch.empty_like(k)
@@ -590,7 +601,7 @@ class Supernet:
             i32 = dict(device=h.device, dtype=torch.int32)
             ops.attn_prefill(q, torch.cat(ks), torch.cat(vs), cu, o, Hq, Hkv, D, window, self.scale_attn,
                              cu_k=torch.tensor(cu_k, **i32), q_off=torch.tensor(q_off, **i32))
-        torch.mm(o, w["o"].t(), out=out)
+        self._mm(o, w["o"], out)
 
     def _gather_prefix(self, st, bt, window, pos0):
         """K / V of the cached positions [k0, pos0) of each prefilled slot (k0 = 0 for FA, the
@@ -613,7 +624,9 @@ class Supernet:
         cfg, st, w = self.cfg, self.state[l], self.w["layers"][l]["mixer"]
         rows = h.shape[0]
         dev = h.device
-        proj = h @ w["w_in"].t()
+        n_in = w["w_in"].shape[0]
+        proj = torch.empty(rows, -(-n_in // 8) * 8, device=dev, dtype=h.dtype)[:, :n_in]  # 16-byte row pitch
+        self._mm(h, w["w_in"], proj)
         if kind == GDN:
             Hk, Hv, D = cfg.gdn_k_heads, cfg.gdn_v_heads, cfg.gdn_head_dim
             C = cfg.gdn_conv_channels
@@ -626,8 +639,8 @@ class Supernet:
             D, R = cfg.kda_head_dim, cfg.kda_rank
             C = cfg.kda_conv_channels
             f1_off, g1_off, b_off, a_off = C, C + R, C + 2 * R, 0
-            f = (proj[:, f1_off:f1_off + R] @ w["f2"].t()).contiguous()
-            gate = (proj[:, g1_off:g1_off + R] @ w["g2"].t() + w["g2_b"]).contiguous()
+            f = self._mm(proj[:, f1_off:f1_off + R], w["f2"])
+            gate = self._mm(proj[:, g1_off:g1_off + R], w["g2"]).add_(w["g2_b"])
             gate_stride = gate.stride(0)
         y = torch.empty(rows, C, device=dev, dtype=h.dtype)
         cont = getattr(self, "_append", None)
@@ -656,7 +669,7 @@ class Supernet:
                            init_state=cont is not None)
         y_out = torch.empty(rows, Hv * D, device=dev, dtype=h.dtype)
         ops.gated_rmsnorm(o, gate, gate_stride, w["norm_w"], y_out, Hv, D, cfg.mixer_norm_eps, act=k_code)
-        torch.mm(y_out, w["o"].t(), out=out)
+        self._mm(y_out, w["o"], out)
 
     def _chunked_delta(self, kind, qn, kn, y, v_off, glog, beta, o, S, cu, Hk, Hv, D, ws_cap=2 << 30):
         """Two-phase chunked prefill over groups of consecutive sequences whose chunk workspace

@@ -330,3 +330,24 @@ def decode_chain(phases, M, counter):
     assert counter.dtype == torch.int64 and counter.is_cuda
     call("sn_decode_chain", ctypes.cast(arr, ctypes.c_void_p), n, M, _p(counter), _s())
     return [arr[i].splits for i in range(n)]
+
+
+# ------------------------------------------------------------------ prefill GEMM
+def gemm_prefill(a, w, out=None, swiglu_h=0):
+    """out [M, N] = a [M, K] @ w [N, K]^T (bf16, tcgen05).  swiglu_h > 0: w is the
+    SwiGLU-interleaved gate/up layout (interleave_swiglu, block swiglu_h) and out [M, F] =
+    silu(gate) * up with F = the FFN width (out must be given)."""
+    M, K = a.shape
+    assert a.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and a.stride(1) == 1 and w.stride(1) == 1
+    if swiglu_h:
+        assert out is not None
+        N = out.shape[1]
+        assert w.shape[0] == -(-N // swiglu_h) * 2 * swiglu_h
+    else:
+        N = w.shape[0]
+        if out is None:
+            out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16)
+    assert out.dtype == torch.bfloat16 and out.stride(1) == 1 and out.shape[0] == M
+    call("sn_gemm_prefill", _p(a), M, K, a.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(0),
+         SN_GEMM_SWIGLU_IL if swiglu_h else SN_GEMM_STORE, swiglu_h, _s())
+    return out
