@@ -45,6 +45,7 @@ struct DeltaDecodeArgs {
   const void* norm_w;
   void* out;
   int Hk, Hv, rank, conv_channels;
+  int B;  // batch (the GDN kernel's persistent item count is Hv * B)
   int q_off, k_off, v_off, z_off, b_off, a_off, f1_off, g1_off;
   float scale, eps_l2, eps_norm;
 };
@@ -183,156 +184,182 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
   __shared__ float s_red[NW];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int h = blockIdx.x, b = blockIdx.y;
-  const int G = a.Hv / a.Hk, kh = h / G;
-  const int slot = a.slot_idx ? a.slot_idx[b] : b;
+  const int G = a.Hv / a.Hk;
+  const int items = a.Hv * a.B;
+  // items (value head, sequence) = blockIdx.x, + gridDim.x, ...; with a smaller grid the first
+  // state columns of the next item are requested before this item's norm epilogue (the launch
+  // uses one item per CTA: measured faster, see launch_delta_decode_t)
+  int item = blockIdx.x;
+  if (item >= items) return;
+  int h = item % a.Hv, b = item / a.Hv;
+  int slot = a.slot_idx ? a.slot_idx[b] : b;
   float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
   float s_nx[NB][EPL];
 #pragma unroll
   for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
-
-  // ring slots (this layer's previous step): before the wait; the conv taps are L2-resident
-  // weights loaded after it, in the same round trip as the projection row
-  T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * 4;
-  const T* cw = reinterpret_cast<const T*>(a.conv_w);
-  const int qch = a.q_off + kh * D + lane * EPL, kch = a.k_off + kh * D + lane * EPL;
-  const int vcol = warp * CPW + (lane < CPW ? lane : 0);
-  const int vch = a.v_off + h * D + vcol;
-  Packed<T, 4 * EPL> rgq, rgk;
-  Packed<T, 4> rgv;
-  rgq.load(ring + (size_t)qch * 4);
-  rgk.load(ring + (size_t)kch * 4);
-  rgv.load(ring + (size_t)vch * 4);
-  const float negA = -expf(a.A_log[h]);
-  const float dtb = a.dt_bias[h];
   const T* nwp = reinterpret_cast<const T*>(a.norm_w);
   const float nw = tid < D ? io<T>::ld(nwp + tid) : 0.f;
+  const T* cw = reinterpret_cast<const T*>(a.conv_w);
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  // ---- the in-projection row: this lane's q, k, v inputs, the output gate z, a, b; taps
-  const int pos = a.positions[b];
-  if (pos < 0) return;  // idle slot (sn_embed): state and conv ring untouched
-  const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
-  float xq[EPL], xk[EPL];
-  loadn<T, EPL>(prow + qch, xq);
-  loadn<T, EPL>(prow + kch, xk);
-  const float xv = io<T>::ld(prow + vch);
-  const float zval = tid < D ? io<T>::ld(prow + a.z_off + h * D + tid) : 0.f;
-  const float braw = io<T>::ld(prow + a.b_off + h);
-  const float graw = io<T>::ld(prow + a.a_off + h) + dtb;
-  Packed<T, 4 * EPL> wq, wk;
-  Packed<T, 4> wv;
-  wq.load(cw + (size_t)qch * 4);
-  wk.load(cw + (size_t)kch * 4);
-  wv.load(cw + (size_t)vch * 4);
-
-  // ---- conv + SiLU in registers; ring slot pos % 4 takes the new input (q/k channels are
-  //      shared by the G value heads of a key head: the first of them writes)
-  float qv[EPL], kv[EPL], vv = 0.f;
-  auto conv_all = [&](auto P) {
-    constexpr int p = decltype(P)::value;
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      qv[e] = silu_f(conv4p<p>(wq, rgq, e, xq[e], pos));
-      kv[e] = silu_f(conv4p<p>(wk, rgk, e, xk[e], pos));
-    }
-    vv = silu_f(conv4p<p>(wv, rgv, 0, xv, pos));
-  };
-  switch (pos & 3) {
-    case 0: conv_all(std::integral_constant<int, 0>{}); break;
-    case 1: conv_all(std::integral_constant<int, 1>{}); break;
-    case 2: conv_all(std::integral_constant<int, 2>{}); break;
-    default: conv_all(std::integral_constant<int, 3>{}); break;
-  }
-  if ((h % G) == 0 && warp == 0) {
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      io<T>::st(ring + (size_t)(qch + e) * 4 + (pos & 3), xq[e]);
-      io<T>::st(ring + (size_t)(kch + e) * 4 + (pos & 3), xk[e]);
-    }
-  }
-  if (lane < CPW) io<T>::st(ring + (size_t)vch * 4 + (pos & 3), xv);
-
-  // ---- L2 norms and q.k by warp shuffles (every warp holds all D entries of q and k)
-  float qq = 0.f, kk = 0.f, qkr = 0.f;
-#pragma unroll
-  for (int e = 0; e < EPL; ++e) {
-    qq += qv[e] * qv[e];
-    kk += kv[e] * kv[e];
-    qkr += qv[e] * kv[e];
-  }
-  qq = warp_sum(qq);
-  kk = warp_sum(kk);
-  qkr = warp_sum(qkr);
-  const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
-  const float eg = expf(negA * softplus_f(graw));
-  const float beta = sigmoid_f(braw);
-  const float qk = qkr * rq * rk;
-  float kr[EPL], kg[EPL], qg[EPL];
-#pragma unroll
-  for (int e = 0; e < EPL; ++e) {
-    kr[e] = kv[e] * rk;
-    kg[e] = kr[e] * eg;
-    qg[e] = qv[e] * rq * eg;
-  }
-
-  // ---- stream the state
 #pragma unroll 1
-  for (int j0 = 0; j0 < CPW; j0 += NB) {
-    const int c0 = warp * CPW + j0;
-    float s[NB][EPL];
+  for (;;) {
+    const int kh = h / G;
+    const int next = item + gridDim.x;
+    // ---- the in-projection row and the ring slots (this layer's previous step): this lane's
+    //      q, k, v inputs, the output gate z, a, b; the conv taps (L2-resident weights)
+    const int pos = a.positions[b];
+    T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * 4;
+    const int qch = a.q_off + kh * D + lane * EPL, kch = a.k_off + kh * D + lane * EPL;
+    const int vcol = warp * CPW + (lane < CPW ? lane : 0);
+    const int vch = a.v_off + h * D + vcol;
+    const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
+    if (pos >= 0) {  // (idle slot, sn_embed: state and conv ring untouched)
+      Packed<T, 4 * EPL> rgq, rgk, wq, wk;
+      Packed<T, 4> rgv, wv;
+      rgq.load(ring + (size_t)qch * 4);
+      rgk.load(ring + (size_t)kch * 4);
+      rgv.load(ring + (size_t)vch * 4);
+      float xq[EPL], xk[EPL];
+      loadn<T, EPL>(prow + qch, xq);
+      loadn<T, EPL>(prow + kch, xk);
+      const float xv = io<T>::ld(prow + vch);
+      const float zval = tid < D ? io<T>::ld(prow + a.z_off + h * D + tid) : 0.f;
+      const float braw = io<T>::ld(prow + a.b_off + h);
+      const float graw = io<T>::ld(prow + a.a_off + h) + a.dt_bias[h];
+      const float negA = -expf(a.A_log[h]);
+      wq.load(cw + (size_t)qch * 4);
+      wk.load(cw + (size_t)kch * 4);
+      wv.load(cw + (size_t)vch * 4);
+
+      // ---- conv + SiLU in registers; ring slot pos % 4 takes the new input (q/k channels are
+      //      shared by the G value heads of a key head: the first of them writes)
+      float qv[EPL], kv[EPL], vv = 0.f;
+      auto conv_all = [&](auto P) {
+        constexpr int p = decltype(P)::value;
 #pragma unroll
-    for (int n = 0; n < NB; ++n)
+        for (int e = 0; e < EPL; ++e) {
+          qv[e] = silu_f(conv4p<p>(wq, rgq, e, xq[e], pos));
+          kv[e] = silu_f(conv4p<p>(wk, rgk, e, xk[e], pos));
+        }
+        vv = silu_f(conv4p<p>(wv, rgv, 0, xv, pos));
+      };
+      switch (pos & 3) {
+        case 0: conv_all(std::integral_constant<int, 0>{}); break;
+        case 1: conv_all(std::integral_constant<int, 1>{}); break;
+        case 2: conv_all(std::integral_constant<int, 2>{}); break;
+        default: conv_all(std::integral_constant<int, 3>{}); break;
+      }
+      if ((h % G) == 0 && warp == 0) {
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) s[n][e] = s_nx[n][e];
-    if (j0 + NB < CPW) {
-#pragma unroll
-      for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + NB + n) * D + lane * EPL, s_nx[n]);
-    }
-    float kd[NB], qd[NB];
-#pragma unroll
-    for (int n = 0; n < NB; ++n) {
-      kd[n] = 0.f;
-      qd[n] = 0.f;
+        for (int e = 0; e < EPL; ++e) {
+          io<T>::st(ring + (size_t)(qch + e) * 4 + (pos & 3), xq[e]);
+          io<T>::st(ring + (size_t)(kch + e) * 4 + (pos & 3), xk[e]);
+        }
+      }
+      if (lane < CPW) io<T>::st(ring + (size_t)vch * 4 + (pos & 3), xv);
+
+      // ---- L2 norms and q.k by warp shuffles (every warp holds all D entries of q and k)
+      float qq = 0.f, kk = 0.f, qkr = 0.f;
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        kd[n] += kg[e] * s[n][e];
-        qd[n] += qg[e] * s[n][e];
+        qq += qv[e] * qv[e];
+        kk += kv[e] * kv[e];
+        qkr += qv[e] * kv[e];
       }
-    }
+      qq = warp_sum(qq);
+      kk = warp_sum(kk);
+      qkr = warp_sum(qkr);
+      const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
+      const float eg = expf(negA * softplus_f(graw));
+      const float beta = sigmoid_f(braw);
+      const float qk = qkr * rq * rk;
+      float kr[EPL], kg[EPL], qg[EPL];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int n = 0; n < NB; ++n) {
-        kd[n] += __shfl_xor_sync(0xffffffffu, kd[n], o);
-        qd[n] += __shfl_xor_sync(0xffffffffu, qd[n], o);
+      for (int e = 0; e < EPL; ++e) {
+        kr[e] = kv[e] * rk;
+        kg[e] = kr[e] * eg;
+        qg[e] = qv[e] * rq * eg;
       }
-    }
-#pragma unroll
-    for (int n = 0; n < NB; ++n) {
-      const float vcn = __shfl_sync(0xffffffffu, vv, j0 + n);
-      const float u = beta * (vcn - kd[n]);
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) s[n][e] = eg * s[n][e] + kr[e] * u;
-      vecf<EPL>::st(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
-      if (lane == 0) s_o[c0 + n] = qd[n] + qk * u;
-    }
-  }
-  __syncthreads();
 
-  // ---- gated RMSNorm over the head: out = RMSNorm(o) * w * silu(z)
-  float oo = 0.f;
-  for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
-  oo = warp_sum(oo);
-  if (lane == 0) s_red[warp] = oo;
-  __syncthreads();
-  oo = 0.f;
+      // ---- stream the state; the last batch's registers then take the next item's first columns
+#pragma unroll 1
+      for (int j0 = 0; j0 < CPW; j0 += NB) {
+        const int c0 = warp * CPW + j0;
+        float s[NB][EPL];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) oo += s_red[w];
-  const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
-  if (tid < D) {
-    T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
-    io<T>::st(out + tid, s_o[tid] * rstd * nw * silu_f(zval));
+        for (int n = 0; n < NB; ++n)
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) s[n][e] = s_nx[n][e];
+        if (j0 + NB < CPW) {
+#pragma unroll
+          for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + NB + n) * D + lane * EPL, s_nx[n]);
+        } else if (next < items) {
+          const int hn = next % a.Hv, bn = next / a.Hv;
+          const int sn_ = a.slot_idx ? a.slot_idx[bn] : bn;
+          const float* Sn = a.state + ((size_t)sn_ * a.Hv + hn) * D * D;
+#pragma unroll
+          for (int n = 0; n < NB; ++n) vecf<EPL>::ld(Sn + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
+        }
+        float kd[NB], qd[NB];
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          kd[n] = 0.f;
+          qd[n] = 0.f;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) {
+            kd[n] += kg[e] * s[n][e];
+            qd[n] += qg[e] * s[n][e];
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int n = 0; n < NB; ++n) {
+            kd[n] += __shfl_xor_sync(0xffffffffu, kd[n], o);
+            qd[n] += __shfl_xor_sync(0xffffffffu, qd[n], o);
+          }
+        }
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          const float vcn = __shfl_sync(0xffffffffu, vv, j0 + n);
+          const float u = beta * (vcn - kd[n]);
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) s[n][e] = eg * s[n][e] + kr[e] * u;
+          vecf<EPL>::st(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
+          if (lane == 0) s_o[c0 + n] = qd[n] + qk * u;
+        }
+      }
+      __syncthreads();
+
+      // ---- gated RMSNorm over the head: out = RMSNorm(o) * w * silu(z)
+      float oo = 0.f;
+      for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
+      oo = warp_sum(oo);
+      if (lane == 0) s_red[warp] = oo;
+      __syncthreads();
+      oo = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) oo += s_red[w];
+      const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
+      if (tid < D) {
+        T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
+        io<T>::st(out + tid, s_o[tid] * rstd * nw * silu_f(zval));
+      }
+      __syncthreads();  // s_o / s_red are reused by the next item
+    } else if (next < items) {  // idle slot: still hand the next item its first columns
+      const int hn = next % a.Hv, bn = next / a.Hv;
+      const int sn_ = a.slot_idx ? a.slot_idx[bn] : bn;
+      const float* Sn = a.state + ((size_t)sn_ * a.Hv + hn) * D * D;
+#pragma unroll
+      for (int n = 0; n < NB; ++n) vecf<EPL>::ld(Sn + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
+    }
+    if (next >= items) break;
+    item = next;
+    h = item % a.Hv;
+    b = item / a.Hv;
+    slot = a.slot_idx ? a.slot_idx[b] : b;
+    S = a.state + ((size_t)slot * a.Hv + h) * D * D;
   }
 }
 
@@ -787,6 +814,10 @@ static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStre
   cudaLaunchConfig_t cfg = {};
   const bool wide = a.Hv * B < 148;
   cfg.gridDim = dim3(a.Hv, B);
+  // GDN: one item (value head, sequence) per CTA, 1-D grid.  The kernel can also walk items
+  // persistently (grid = 4 CTAs per SM, the next item's state requested before the norm
+  // epilogue), but that measured slower at B=64: 52.7 vs 48.0 us (tools/bench_delta.py).
+  if (!KDA) cfg.gridDim = dim3(a.Hv * B);
   cfg.blockDim = dim3(wide ? 2 * kDecodeThreads : kDecodeThreads);
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -855,7 +886,7 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring, cons
   DeltaDecodeArgs a{};
   a.proj = proj; a.proj_stride = proj_stride; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
   a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias; a.norm_w = norm_w;
-  a.out = out; a.Hk = Hk; a.Hv = Hv; a.rank = 0;
+  a.out = out; a.Hk = Hk; a.Hv = Hv; a.rank = 0; a.B = B;
   a.conv_channels = 2 * Hk * D + Hv * D;
   a.q_off = 0; a.k_off = Hk * D; a.v_off = 2 * Hk * D; a.z_off = 2 * Hk * D + Hv * D;
   a.b_off = 2 * Hk * D + 2 * Hv * D; a.a_off = a.b_off + Hv;
@@ -876,7 +907,7 @@ sn_status sn_kda_decode(const void* proj, int proj_stride, const void* fg, void*
   DeltaDecodeArgs a{};
   a.proj = proj; a.proj_stride = proj_stride; a.fg = fg; a.conv_ring = conv_ring; a.conv_w = conv_w; a.state = state;
   a.slot_idx = slot_idx; a.positions = positions; a.A_log = A_log; a.dt_bias = dt_bias;
-  a.g2_b = g2_b; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank;
+  a.g2_b = g2_b; a.norm_w = norm_w; a.out = out; a.Hk = H; a.Hv = H; a.rank = rank; a.B = B;
   a.conv_channels = 3 * H * D;
   a.q_off = 0; a.k_off = H * D; a.v_off = 2 * H * D; a.f1_off = 3 * H * D; a.g1_off = 3 * H * D + rank;
   a.b_off = 3 * H * D + 2 * rank;

@@ -26,23 +26,16 @@ for kind in (GDN, KDA):
     pos = torch.full((B,), 1000, dtype=torch.int32, device="cuda")
     out = torch.empty(B, Hv * D, device="cuda", dtype=torch.bfloat16)
     if kind == KDA:
-        fg2T = torch.stack([w["f2"].t(), w["g2"].t()]).contiguous()
         fgbuf = torch.empty(2, B, cfg.kda_dim, device="cuda", dtype=torch.bfloat16)
 
     def run(l):
         if kind == GDN:
             ops.gdn_decode(proj, rings[l], w["conv_w"], states[l], None, pos, w["A_log"], w["dt_bias"], w["norm_w"],
                            out, cfg.gdn_k_heads, Hv, D, 4, 1 / math.sqrt(D), 1e-6, 1e-5)
-        else:
-            fg = None
-            if os.environ.get("KDA_FG", "1") == "1":
-                HD, R = cfg.kda_dim, cfg.kda_rank
-                f1g1 = proj[:, 3 * HD:3 * HD + 2 * R].view(B, 2, R).transpose(0, 1)
-                fg = fgbuf
-                torch.bmm(f1g1, fg2T, out=fg)
-            ops.kda_decode(proj, rings[l], w["conv_w"], states[l], None, pos, w["A_log"], w["dt_bias"], w["f2"],
-                           w["g2"], w["g2_b"], w["norm_w"], out, Hv, D, cfg.kda_rank, 4, 1 / math.sqrt(D), 1e-6, 1e-5,
-                           fg=fg)
+        else:  # the decode step's own gate-factor GEMMs, then the KDA kernel
+            ops.kda_gate_factors(proj, w["f2"], w["g2"], fgbuf, Hv, D, cfg.kda_rank)
+            ops.kda_decode(proj, fgbuf, rings[l], w["conv_w"], states[l], None, pos, w["A_log"], w["dt_bias"],
+                           w["g2_b"], w["norm_w"], out, Hv, D, cfg.kda_rank, 4, 1 / math.sqrt(D), 1e-6, 1e-5)
     for l in range(L):
         run(l)
     torch.cuda.synchronize()
