@@ -181,10 +181,10 @@ sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv
  * (f = pre-softplus gate [rows][Hv*D] from the f2 GEMM, b from proj).       */
 sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj,
                         int proj_stride, int b_off, int a_off, const void* f,
-                        const float* A_log, const float* dt_bias, float* qn,
-                        float* kn, float* gexp, float* glog, float* beta, int rows,
-                        int Hk, int Hv, int D, float scale, float eps_l2, int dtype,
-                        void* stream);
+                        const float* A_log, const float* dt_bias, void* qn,
+                        void* kn, float* gexp, float* glog, float* beta, int rows,
+                        int Hk, int Hv, int D, float scale, float eps_l2, int qk_dtype,
+                        int dtype, void* stream);
 /* (glog, optional, GDN only: the log decay g per [row][Hv], for the chunked prefill) */
 
 /* Recurrent scan over each sequence: o[t] (fp32 [rows][Hv][D]) and the final
@@ -197,19 +197,20 @@ sn_status sn_delta_scan(int kind, const float* qn, const float* kn,
                         int D, int init_state, int dtype, void* stream);
 
 /* Two-phase chunked GDN prefill (long prompts): phase 1 computes every chunk's
- * local WY tiles in parallel (one CTA per (chunk, value head)), phase 2 runs the
+ * local WY tiles in parallel (one CTA per (chunk, value head), TMA-fed tcgen05 /
+ * TMEM products: K K^T, Q K^T, T diag(b e^G) K, T diag(b) V), phase 2 runs the
  * sequential state pass over precomputed bf16 tiles streamed through
- * double-buffered shared memory.  chunks: int32 [num_chunks][2] = (first token,
+ * double-buffered shared memory.  qn / kn: bf16 [rows][Hk][D] (sn_delta_prep with
+ * qk_dtype SN_BF16); qkv_conv [rows][qkv_stride] bf16 (v_off a multiple of 64).  chunks: int32 [num_chunks][2] = (first token,
  * length <= 64) in sequence order; seq_chunk0: int32 [num_seqs+1] chunk offsets.
  * workspace: sn_gdn_chunk_workspace_bytes(num_chunks, Hv, D).                     */
 size_t sn_gdn_chunk_workspace_bytes(int num_chunks, int Hv, int D);
-sn_status sn_gdn_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv,
-                                int v_off, int qkv_stride, const float* glog,
+sn_status sn_gdn_chunk_prefill2(const void* qn, const void* kn, const void* qkv_conv,
+                                int v_off, int qkv_stride, int rows, const float* glog,
                                 const float* beta, const int32_t* chunks,
                                 const int32_t* seq_chunk0, int num_chunks, void* workspace,
-                                float* o, float* state, const int32_t* slot_idx,
-                                int num_seqs, int Hk, int Hv, int D, int init_state,
-                                int dtype, void* stream);
+                                float* o, float* state, const int32_t* slot_idx, int num_seqs,
+                                int Hk, int Hv, int D, int init_state, int dtype, void* stream);
 
 /* Two-phase chunked KDA prefill: the same WY chunk form with a per-key-channel
  * gate (FLA naive_chunk_kda, 3P-FLA/ops/kda/naive.py:69-166).  Hk = Hv = H;

@@ -31,9 +31,9 @@ SIGNATURES = {
     "sn_gdn_decode": [P, I, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
     "sn_kda_decode": [P, I, P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, I, Fl, Fl, Fl, I, P],
     "sn_conv_prefill": [P, I, P, P, P, P, P, P, P, I, I, I, I, I, P],
-    "sn_delta_prep": [I, P, P, I, I, I, P, P, P, P, P, P, P, P, I, I, I, I, Fl, Fl, I, P],
+    "sn_delta_prep": [I, P, P, I, I, I, P, P, P, P, P, P, P, P, I, I, I, I, Fl, Fl, I, I, P],
     "sn_gdn_chunk_workspace_bytes": [I, I, I],
-    "sn_gdn_chunk_prefill2": [P, P, P, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, I, P],
+    "sn_gdn_chunk_prefill2": [P, P, P, I, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, I, P],
     "sn_kda_chunk_workspace_bytes": [I, I, I],
     "sn_tp_arrive": [P, P],
     "sn_tp_allreduce_add_rmsnorm": [P, P, I, I, I, P, P, P, I, I, Fl, I, P],

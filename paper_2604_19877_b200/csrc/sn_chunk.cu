@@ -12,6 +12,7 @@
 // fp32 accumulate); the state S stays in registers (fp32) across chunks.  One CTA (4 warps)
 // per (sequence, value head, 64-wide value tile); chunks run in order inside it.
 #include "sn_mma.cuh"
+#include "sn_tc.cuh"
 
 namespace sn {
 namespace chunk {
@@ -162,55 +163,104 @@ __device__ __forceinline__ void load_f32_tiles(const float* const* src, int head
 // Workspace per (chunk, head), bf16: W, Qg, Kd, U [64][D] and P [64][64]; glast fp32.
 
 template <int D>
-struct IntraSmem {  // ~74 KB at D = 128: three CTAs per SM
-  static constexpr int LDK = D + 8, LDC = C + 8;
-  union {
-    __nv_bfloat16 q[C * LDK];   // Q until e^G o Q is written out
-    float x[C][C + 1];          // then the fp32 inverse
-    __nv_bfloat16 vb[C * LDK];  // then b o V
-  } qv;
-  __nv_bfloat16 k[C * LDK];
-  __nv_bfloat16 kb[C * LDK];
-  union {
-    float l[C][C + 1];            // L until inverted
-    __nv_bfloat16 t[C * LDC];     // then T (bf16 operand)
-  } lt;
-  float scr[4 * 16 * 17];
-  float g[C], beta[C];
-};
-
-template <int D>
 __device__ __forceinline__ size_t ws_tile(int n, int h, int Hv) {  // offset of one (chunk, head) record
   return ((size_t)n * Hv + h) * (4 * (size_t)C * D + (size_t)C * C);
 }
 
-template <typename T, int D>
+// ---- GDN chunk-local phase on tcgen05 / TMEM, TMA-fed.  One CTA (4 warps) per (chunk, value
+// head).  TMA brings Q, K (bf16, from sn_delta_prep) and V (the conv output) as [64 x D] tiles of
+// 128B-swizzled [64 x 64] atoms; the four chunk products run as single-thread UMMAs (M = 64):
+//   K K^T, Q K^T           (A, B K-major: the K tile serves both)        -> TMEM cols [0, 128)
+//   W = T2 K, U = T1 V     (A = T2 / T1 written swizzled by the CTA, B = K / V MN-major)
+//                                                                        -> TMEM cols [0, 2D)
+// with T1 = T diag(b), T2 = T diag(b e^G): the beta / decay scaling of the right operands is
+// folded into the columns of T, so K and V are consumed straight from their TMA tiles.  The
+// inverse T = (I - L)^-1 stays on the CUDA cores (invert_unit_lower, fp32).  Rows past the
+// chunk length are whatever the TMA box covers (the next chunk, or zeros past the tensor):
+// their beta is 0, so their columns of T1 / T2 are 0, and P / Qg / Kd mask them explicitly.
+template <int D>
+struct TcIntraSmem {
+  static constexpr int AT = 64 * 128;  // one [64 rows x 64 bf16] 128B-swizzled atom
+  static constexpr int NA = D / 64;    // atoms per [64 x D] tile
+  uint8_t q[NA * AT];
+  uint8_t k[NA * AT];
+  uint8_t v[NA * AT];
+  uint8_t t1[AT];
+  uint8_t t2[AT];
+  float l[C][C + 1];
+  float x[C][C + 1];
+  float scr[4 * 16 * 17];
+  float g[C], beta[C], bg[C];  // bg = b e^G (the column scale of T2)
+  uint64_t bar_qk, bar_v, bar_m1, bar_m2;
+  uint32_t tmem_base;
+};
+
+// byte offset of element (r, c) in a [64 x D] tile of 128B-swizzled [64 x 64] atoms
+__device__ __forceinline__ uint32_t sw_off(int r, int c) {
+  const int atom = c >> 6, cc = c & 63;
+  return atom * (64 * 128) + r * 128 + ((((cc >> 3) ^ (r & 7)) & 7) << 4) + ((cc & 7) << 1);
+}
+
+// MN-major SW128 operand (B of W = T2 K, U = T1 V: N = head dim contiguous, K = chunk rows):
+// LBO = stride between the 64-element N atoms, SBO = 8 K rows x 128 B
+__device__ __forceinline__ uint64_t desc_mn_sw128_c(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((64 * 128) >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+template <int D>
 __global__ void __launch_bounds__(kThreads)
-    gdn_chunk_intra_kernel(const float* __restrict__ qn, const float* __restrict__ kn, const T* __restrict__ qkv,
-                           int v_off, int qkv_stride, const float* __restrict__ glog, const float* __restrict__ beta,
-                           const int32_t* __restrict__ chunks, __nv_bfloat16* __restrict__ ws,
-                           float* __restrict__ glast, int Hk, int Hv) {
+    gdn_chunk_intra_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                              const __grid_constant__ CUtensorMap vmap, int v_off, const float* __restrict__ glog,
+                              const float* __restrict__ beta, const int32_t* __restrict__ chunks,
+                              __nv_bfloat16* __restrict__ ws, float* __restrict__ glast, int Hk, int Hv) {
   pdl_launch_dependents();
-  using SM = IntraSmem<D>;
-  constexpr int LDK = SM::LDK, LDC = SM::LDC;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  using SM = TcIntraSmem<D>;
+  constexpr int AT = SM::AT, NA = SM::NA;
+  constexpr uint32_t kCols = D == 128 ? 256 : 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g4 = lane >> 2, t4 = lane & 3;
   const int n = blockIdx.x, h = blockIdx.y;
-  const int G = Hv / Hk, kh = h / G;
-  const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
-  {
-    const float* src[2] = {qn, kn};
-    __nv_bfloat16* dst[2] = {sm.qv.q, sm.k};
-    load_f32_tiles<D, 2>(src, Hk, kh, c0, len, dst, LDK);
+  const int kh = h / (Hv / Hk);
+  if (tid == 0) {
+    tc::mbar_init(&sm.bar_qk, 1);
+    tc::mbar_init(&sm.bar_v, 1);
+    tc::mbar_init(&sm.bar_m1, 1);
+    tc::mbar_init(&sm.bar_m2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&sm.tmem_base)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  pdl_wait();
+  const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
   if (tid < C) {
     sm.g[tid] = tid < len ? glog[(size_t)(c0 + tid) * Hv + h] : 0.f;
     sm.beta[tid] = tid < len ? beta[(size_t)(c0 + tid) * Hv + h] : 0.f;
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  if (tid == 0) {  // the three tiles, one TMA box per 64-column atom
+    const uint64_t pol = tc::policy_evict_first();
+    tc::mbar_expect_tx(&sm.bar_qk, 2 * NA * AT);
+    for (int a = 0; a < NA; ++a) {
+      tc::tma_load_2d(sm.q + a * AT, &qmap, kh * D + 64 * a, c0, &sm.bar_qk, pol);
+      tc::tma_load_2d(sm.k + a * AT, &kmap, kh * D + 64 * a, c0, &sm.bar_qk, pol);
+    }
+    tc::mbar_expect_tx(&sm.bar_v, NA * AT);
+    for (int a = 0; a < NA; ++a) tc::tma_load_2d(sm.v + a * AT, &vmap, v_off + h * D + 64 * a, c0, &sm.bar_v, pol);
+  }
+  if (warp == 0) {  // in-chunk cumulative log decay
     float a0 = sm.g[lane], a1 = sm.g[32 + lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -220,108 +270,153 @@ __global__ void __launch_bounds__(kThreads)
     a1 += __shfl_sync(0xffffffffu, a0, 31);
     sm.g[lane] = a0;
     sm.g[32 + lane] = a1;
+    sm.bg[lane] = sm.beta[lane] * expf(a0);
+    sm.bg[32 + lane] = sm.beta[32 + lane] * expf(a1);
+  } else if (warp == 1) {  // K K^T -> TMEM [0, 64), Q K^T -> [64, 128)
+    tc::mbar_wait(&sm.bar_qk, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t sq = tc::smem_u32(sm.q), sk = tc::smem_u32(sm.k), id = tc::idesc_bf16(64, 64);
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint32_t off = (kk >> 2) * AT + (kk & 3) * 32;
+      tc::umma_w(tmem, tc::desc_sw128(sk + off), tc::desc_sw128(sk + off), id, kk > 0 ? 1u : 0u);
+      tc::umma_w(tmem + 64, tc::desc_sw128(sq + off), tc::desc_sw128(sk + off), id, kk > 0 ? 1u : 0u);
+    }
+    tc::commit_w(&sm.bar_m1);
   }
-  __syncthreads();
+  __syncthreads();  // the cumulative decays
+
   __nv_bfloat16* rec = ws + ws_tile<D>(n, h, Hv);
   __nv_bfloat16* wW = rec;
   __nv_bfloat16* wQg = rec + C * D;
   __nv_bfloat16* wKd = rec + 2 * C * D;
   __nv_bfloat16* wU = rec + 3 * C * D;
   __nv_bfloat16* wP = rec + 4 * C * D;
-  // K K^T -> L, Q K^T -> P (straight to the workspace)
-  {
-    float kk[8][4], qk[8][4];
+  // e^G o Q and e^{G_C - G} o K straight from the swizzled tiles (8 columns per step)
+  tc::mbar_wait(&sm.bar_qk, 0);
+  const float gl = sm.g[C - 1];
+  for (int idx = tid; idx < C * D / 8; idx += kThreads) {
+    const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
+    const uint4 qv = *reinterpret_cast<const uint4*>(sm.q + sw_off(r, c8));
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + sw_off(r, c8));
+    const bool ok = r < len;
+    const float eg = ok ? expf(sm.g[r]) : 0.f, ed = ok ? expf(gl - sm.g[r]) : 0.f;
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(&qv);
+    const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
+    uint4 qo, ko;
+    uint32_t* qoa = reinterpret_cast<uint32_t*>(&qo);
+    uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) kk[nt][e] = qk[nt][e] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < D; ks += 16) {
-      uint32_t ak[4], aq[4];
-      lda(sm.k, LDK, warp * 16, ks, ak);
-      lda(sm.qv.q, LDK, warp * 16, ks, aq);
-#pragma unroll
-      for (int nt = 0; nt < 8; nt += 2) {
-        uint32_t b0, b1, b2, b3;
-        ldb_nk(sm.k, LDK, nt * 8, ks, b0, b1, b2, b3);
-        mma_bf16(kk[nt], ak, b0, b1);
-        mma_bf16(kk[nt + 1], ak, b2, b3);
-        mma_bf16(qk[nt], aq, b0, b1);
-        mma_bf16(qk[nt + 1], aq, b2, b3);
-      }
+    for (int e = 0; e < 4; ++e) {
+      const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
+      const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+      qoa[e] = pack_bf16(qf.x * eg, qf.y * eg);
+      koa[e] = pack_bf16(kf.x * ed, kf.y * ed);
     }
+    *reinterpret_cast<uint4*>(wQg + r * D + c8) = qo;
+    *reinterpret_cast<uint4*>(wKd + r * D + c8) = ko;
+  }
+  if (tid == 0) glast[(size_t)n * Hv + h] = gl;
+
+  // L = -tril(b K K^T o Gamma, -1) -> shared memory, P = tril(Q K^T o Gamma) -> workspace.
+  // M = 64 accumulator: row 16w + i sits in TMEM lane 32w + i (i < 16).
+  tc::mbar_wait(&sm.bar_m1, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int i = 16 * warp + (lane & 15);
+    const bool row = lane < 16;
+    const uint32_t la = tmem + ((uint32_t)(32 * warp) << 16);
+    const float gi = sm.g[i], bi = sm.beta[i];
+#pragma unroll 1
+    for (int j0 = 0; j0 < C; j0 += 16) {
+      float kk[16], qk[16];
+      tc::tmem_ld16_async(la + j0, kk);
+      tc::tmem_ld16_async(la + 64 + j0, qk);
+      tc::tmem_wait_ld();
+      tc::reg_fence16(kk);
+      tc::reg_fence16(qk);
+      if (row) {
+        uint32_t pk[8];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+        for (int e = 0; e < 16; e += 2) {
+          float pv[2];
 #pragma unroll
-      for (int e = 0; e < 4; e += 2) {
-        const int i = warp * 16 + g4 + ((e >> 1) << 3), j = nt * 8 + t4 * 2;
-        float pv[2];
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-          const float gam = i >= j + d ? expf(sm.g[i] - sm.g[j + d]) : 0.f;
-          sm.lt.l[i][j + d] = i > j + d ? -sm.beta[i] * kk[nt][e + d] * gam : 0.f;
-          pv[d] = qk[nt][e + d] * gam;
+          for (int d = 0; d < 2; ++d) {
+            const int j = j0 + e + d;
+            const bool ok = i < len && j < len && i >= j;
+            const float gam = ok ? expf(gi - sm.g[j]) : 0.f;
+            sm.l[i][j] = (ok && i > j) ? -bi * kk[e + d] * gam : 0.f;
+            pv[d] = qk[e + d] * gam;
+          }
+          pk[e >> 1] = pack_bf16(pv[0], pv[1]);
         }
-        *reinterpret_cast<uint32_t*>(wP + i * C + j) = pack_bf16(pv[0], pv[1]);
-      }
-  }
-  {
-    const float gl = sm.g[C - 1];
-    for (int idx = tid; idx < C * D / 2; idx += kThreads) {
-      const int r = idx / (D / 2), cc = (idx % (D / 2)) * 2;
-      const float eg = expf(sm.g[r]), ed = expf(gl - sm.g[r]);
-      const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[r * LDK + cc]));
-      const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.qv.q[r * LDK + cc]));
-      *reinterpret_cast<uint32_t*>(&sm.kb[r * LDK + cc]) = pack_bf16(kv.x * sm.beta[r] * eg, kv.y * sm.beta[r] * eg);
-      *reinterpret_cast<uint32_t*>(wKd + r * D + cc) = pack_bf16(kv.x * ed, kv.y * ed);
-      *reinterpret_cast<uint32_t*>(wQg + r * D + cc) = pack_bf16(qv.x * eg, qv.y * eg);
-    }
-    if (tid == 0) glast[(size_t)n * Hv + h] = gl;
-  }
-  __syncthreads();
-  // T = (I - L)^{-1}: 16x16 diagonal blocks, then the block rows below them.  Q is dead
-  // (e^G o Q went out): its tile holds the fp32 inverse, then b o V (the shared memory fits
-  // three CTAs per SM instead of two; the V loads no longer overlap the inverse, the other
-  // CTAs on the SM cover that latency)
-  invert_unit_lower(sm.lt.l, sm.qv.x, sm.scr);
-  for (int idx = tid; idx < C * C; idx += kThreads) {
-    const int i = idx / C, j = idx % C;
-    sm.lt.t[i * LDC + j] = __float2bfloat16_rn(sm.qv.x[i][j]);
-  }
-  __syncthreads();
-  load_vb_tile<T, D>(qkv, qkv_stride, v_off, h, c0, len, sm.beta, sm.qv.vb, LDK);
-  __syncthreads();
-  // W = T Kb, U = T Vb  (both [64][D]) -> workspace
-  {
-    float wacc[D / 8][4], uacc[D / 8][4];
-#pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) wacc[nt][e] = uacc[nt][e] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < C; ks += 16) {
-      uint32_t a[4];
-      lda(sm.lt.t, LDC, warp * 16, ks, a);
-#pragma unroll
-      for (int nt = 0; nt < D / 8; nt += 2) {
-        uint32_t b0, b1, b2, b3;
-        ldb_kn(sm.kb, LDK, nt * 8, ks, b0, b1, b2, b3);
-        mma_bf16(wacc[nt], a, b0, b1);
-        mma_bf16(wacc[nt + 1], a, b2, b3);
-        ldb_kn(sm.qv.vb, LDK, nt * 8, ks, b0, b1, b2, b3);
-        mma_bf16(uacc[nt], a, b0, b1);
-        mma_bf16(uacc[nt + 1], a, b2, b3);
+        *reinterpret_cast<uint4*>(wP + i * C + j0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(wP + i * C + j0 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     }
-#pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; e += 2) {
-        const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = nt * 8 + t4 * 2;
-        *reinterpret_cast<uint32_t*>(wW + r * D + cc) = pack_bf16(wacc[nt][e], wacc[nt][e + 1]);
-        *reinterpret_cast<uint32_t*>(wU + r * D + cc) = pack_bf16(uacc[nt][e], uacc[nt][e + 1]);
-      }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  invert_unit_lower(sm.l, sm.x, sm.scr);  // x = T = (I - L)^-1 (fp32)
+  // T1 = T diag(b), T2 = T diag(b e^G) as bf16 K-major A operands (swizzled like a TMA atom)
+  for (int idx = tid; idx < C * C / 8; idx += kThreads) {
+    const int i = idx >> 3, j8 = (idx & 7) * 8;
+    uint32_t p1[4], p2[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float x0 = sm.x[i][j8 + e], x1 = sm.x[i][j8 + e + 1];
+      p1[e >> 1] = pack_bf16(x0 * sm.beta[j8 + e], x1 * sm.beta[j8 + e + 1]);
+      p2[e >> 1] = pack_bf16(x0 * sm.bg[j8 + e], x1 * sm.bg[j8 + e + 1]);
+    }
+    *reinterpret_cast<uint4*>(sm.t1 + sw_off(i, j8)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+    *reinterpret_cast<uint4*>(sm.t2 + sw_off(i, j8)) = make_uint4(p2[0], p2[1], p2[2], p2[3]);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's reads
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {  // W = T2 K -> TMEM [0, D), U = T1 V -> [D, 2D)
+    tc::mbar_wait(&sm.bar_v, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t id = tc::idesc_bf16(64, D) | (1u << 16);  // B MN-major
+    const uint32_t s1 = tc::smem_u32(sm.t1), s2 = tc::smem_u32(sm.t2);
+    const uint32_t sk = tc::smem_u32(sm.k), sv = tc::smem_u32(sm.v);
+#pragma unroll
+    for (int kk = 0; kk < C / 16; ++kk) {
+      tc::umma_w(tmem, tc::desc_sw128(s2 + kk * 32), desc_mn_sw128_c(sk + kk * 2048), id, kk > 0 ? 1u : 0u);
+      tc::umma_w(tmem + D, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sv + kk * 2048), id, kk > 0 ? 1u : 0u);
+    }
+    tc::commit_w(&sm.bar_m2);
+  }
+  tc::mbar_wait(&sm.bar_m2, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int i = 16 * warp + (lane & 15);
+    const uint32_t la = tmem + ((uint32_t)(32 * warp) << 16);
+#pragma unroll 1
+    for (int c = 0; c < D; c += 16) {
+      float wv[16], uv[16];
+      tc::tmem_ld16_async(la + c, wv);
+      tc::tmem_ld16_async(la + D + c, uv);
+      tc::tmem_wait_ld();
+      tc::reg_fence16(wv);
+      tc::reg_fence16(uv);
+      if (lane < 16) {
+        uint32_t pw[8], pu[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          pw[e] = pack_bf16(wv[2 * e], wv[2 * e + 1]);
+          pu[e] = pack_bf16(uv[2 * e], uv[2 * e + 1]);
+        }
+        *reinterpret_cast<uint4*>(wW + i * D + c) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+        *reinterpret_cast<uint4*>(wW + i * D + c + 8) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+        *reinterpret_cast<uint4*>(wU + i * D + c) = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+        *reinterpret_cast<uint4*>(wU + i * D + c + 8) = make_uint4(pu[4], pu[5], pu[6], pu[7]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
 template <int D, int VTT = VT>
@@ -569,22 +664,33 @@ static void launch_state_pass(const __nv_bfloat16* ws, const float* glast, const
         ws, glast, chunks, seq_chunk0, o, state, slot_idx, H, init_state);
 }
 
-template <typename T, int D>
-static sn_status launch_two_phase(const float* qn, const float* kn, const void* qkv, int v_off, int qkv_stride,
-                                  const float* glog, const float* beta, const int32_t* chunks,
+template <int D>
+static sn_status launch_two_phase(const void* qb, const void* kb, const void* qkv, int v_off, int qkv_stride,
+                                  int rows, const float* glog, const float* beta, const int32_t* chunks,
                                   const int32_t* seq_chunk0, int num_chunks, void* ws, float* glast, float* o,
                                   float* state, const int32_t* slot_idx, int num_seqs, int Hk, int Hv,
                                   int init_state, cudaStream_t st) {
-  const int smem_a = (int)sizeof(IntraSmem<D>);
+  const int smem = (int)sizeof(TcIntraSmem<D>) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gdn_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
+    cudaFuncSetAttribute(gdn_chunk_intra_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  gdn_chunk_intra_kernel<T, D><<<dim3(num_chunks, Hv), kThreads, smem_a, st>>>(
-      qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, Hk, Hv);
-  sn_status e = check_launch("sn_gdn_chunk_prefill(intra)");
-  if (e != SN_OK) return e;
+  CUtensorMap qm, km, vm;
+  if (!tc::map_2d(&qm, qb, rows, (uint64_t)Hk * D, (uint64_t)Hk * D, 64) ||
+      !tc::map_2d(&km, kb, rows, (uint64_t)Hk * D, (uint64_t)Hk * D, 64) ||
+      !tc::map_2d(&vm, qkv, rows, qkv_stride, qkv_stride, 64)) {
+    set_error("sn_gdn_chunk_prefill2: cuTensorMapEncodeTiled failed");
+    return SN_ECUDA;
+  }
+  cudaError_t e = launch_pdl(gdn_chunk_intra_tc_kernel<D>, dim3(num_chunks, Hv), dim3(kThreads), (size_t)smem, st, qm,
+                             km, vm, v_off, glog, beta, chunks, (__nv_bfloat16*)ws, glast, Hk, Hv);
+  if (e != cudaSuccess) {
+    set_error("sn_gdn_chunk_prefill2(intra) launch: %s", cudaGetErrorString(e));
+    return SN_ECUDA;
+  }
+  sn_status s = check_launch("sn_gdn_chunk_prefill(intra)");
+  if (s != SN_OK) return s;
   launch_state_pass<D, false>((const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, num_seqs, Hv,
                               init_state, st);
   return check_launch("sn_gdn_chunk_prefill(state)");
@@ -893,26 +999,29 @@ size_t sn_gdn_chunk_workspace_bytes(int num_chunks, int Hv, int D) {
          (size_t)num_chunks * Hv * sizeof(float);
 }
 
-sn_status sn_gdn_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv, int v_off, int qkv_stride,
-                                const float* glog, const float* beta, const int32_t* chunks,
+sn_status sn_gdn_chunk_prefill2(const void* qn, const void* kn, const void* qkv_conv, int v_off, int qkv_stride,
+                                int rows, const float* glog, const float* beta, const int32_t* chunks,
                                 const int32_t* seq_chunk0, int num_chunks, void* workspace, float* o, float* state,
                                 const int32_t* slot_idx, int num_seqs, int Hk, int Hv, int D, int init_state,
                                 int dtype, void* stream) {
   SN_REQUIRE(qn && kn && qkv_conv && glog && beta && chunks && seq_chunk0 && workspace && o && state,
              "sn_gdn_chunk_prefill2: NULL pointer");
-  SN_REQUIRE(num_seqs > 0 && num_chunks > 0 && Hk > 0 && Hv % Hk == 0, "sn_gdn_chunk_prefill2: bad shape");
+  SN_REQUIRE(num_seqs > 0 && num_chunks > 0 && Hk > 0 && Hv % Hk == 0 && rows > 0, "sn_gdn_chunk_prefill2: bad shape");
   SN_REQUIRE(D == 64 || D == 128, "sn_gdn_chunk_prefill2: D=%d unsupported", D);
   SN_REQUIRE(dtype == SN_BF16, "sn_gdn_chunk_prefill2: bf16 only");
+  SN_REQUIRE(((uintptr_t)qn % 16) == 0 && ((uintptr_t)kn % 16) == 0 && ((uintptr_t)qkv_conv % 16) == 0 &&
+                 (qkv_stride * 2) % 16 == 0 && (v_off % 64) == 0,
+             "sn_gdn_chunk_prefill2: TMA operands must be 16-byte aligned (v_off a multiple of 64)");
   cudaStream_t st = (cudaStream_t)stream;
   float* glast = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
                                           (size_t)num_chunks * Hv * (4 * (size_t)chunk::C * D + (size_t)chunk::C * chunk::C) * 2);
   if (D == 128)
-    return chunk::launch_two_phase<__nv_bfloat16, 128>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, chunks,
-                                                        seq_chunk0, num_chunks, workspace, glast, o, state, slot_idx,
-                                                        num_seqs, Hk, Hv, init_state, st);
-  return chunk::launch_two_phase<__nv_bfloat16, 64>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, chunks,
-                                                     seq_chunk0, num_chunks, workspace, glast, o, state, slot_idx,
-                                                     num_seqs, Hk, Hv, init_state, st);
+    return chunk::launch_two_phase<128>(qn, kn, qkv_conv, v_off, qkv_stride, rows, glog, beta, chunks, seq_chunk0,
+                                        num_chunks, workspace, glast, o, state, slot_idx, num_seqs, Hk, Hv,
+                                        init_state, st);
+  return chunk::launch_two_phase<64>(qn, kn, qkv_conv, v_off, qkv_stride, rows, glog, beta, chunks, seq_chunk0,
+                                     num_chunks, workspace, glast, o, state, slot_idx, num_seqs, Hk, Hv, init_state,
+                                     st);
 }
 
 }  // extern "C"

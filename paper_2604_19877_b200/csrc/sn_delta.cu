@@ -668,10 +668,10 @@ template <typename T, int D, bool KDA>
 __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv, const T* __restrict__ proj,
                                                        int proj_stride, int b_off, int a_off,
                                                        const T* __restrict__ f, const float* __restrict__ A_log,
-                                                       const float* __restrict__ dt_bias, float* __restrict__ qn,
-                                                       float* __restrict__ kn, float* __restrict__ gexp,
+                                                       const float* __restrict__ dt_bias, void* __restrict__ qn,
+                                                       void* __restrict__ kn, float* __restrict__ gexp,
                                                        float* __restrict__ glog, float* __restrict__ beta, int Hk,
-                                                       int Hv, float scale, float eps_l2) {
+                                                       int Hv, float scale, float eps_l2, int qk_bf16) {
   __shared__ float red[2 * (D / 32)];
   const int r = blockIdx.x, kh = blockIdx.y, i = threadIdx.x;  // rows on x: > 65535 tokens
   const int G = Hv / Hk;
@@ -694,8 +694,14 @@ __global__ void __launch_bounds__(D) delta_prep_kernel(const T* __restrict__ qkv
   kk = 0.f;
 #pragma unroll
   for (int w = 0; w < D / 32; ++w) { qq += red[w]; kk += red[D / 32 + w]; }
-  qn[((size_t)r * Hk + kh) * D + i] = q * rsqrtf(qq + eps_l2) * scale;
-  kn[((size_t)r * Hk + kh) * D + i] = k * rsqrtf(kk + eps_l2);
+  const size_t qi = ((size_t)r * Hk + kh) * D + i;
+  if (qk_bf16) {  // the chunked GDN prefill reads q / k as bf16 TMA tiles
+    reinterpret_cast<__nv_bfloat16*>(qn)[qi] = __float2bfloat16_rn(q * rsqrtf(qq + eps_l2) * scale);
+    reinterpret_cast<__nv_bfloat16*>(kn)[qi] = __float2bfloat16_rn(k * rsqrtf(kk + eps_l2));
+  } else {
+    reinterpret_cast<float*>(qn)[qi] = q * rsqrtf(qq + eps_l2) * scale;
+    reinterpret_cast<float*>(kn)[qi] = k * rsqrtf(kk + eps_l2);
+  }
   if (KDA) {
     const int h = kh;
     const float gl = -expf(A_log[h]) * softplus_f(fv + dt_bias[h * D + i]);
@@ -856,11 +862,12 @@ using namespace sn;
 namespace sn {
 template <typename T, int D, bool K>
 static void launch_prep(dim3 grid, cudaStream_t st, const void* qkv_conv, const void* proj, int proj_stride,
-                        int b_off, int a_off, const void* f, const float* A_log, const float* dt_bias, float* qn,
-                        float* kn, float* gexp, float* glog, float* beta, int Hk, int Hv, float scale, float eps_l2) {
+                        int b_off, int a_off, const void* f, const float* A_log, const float* dt_bias, void* qn,
+                        void* kn, float* gexp, float* glog, float* beta, int Hk, int Hv, float scale, float eps_l2,
+                        int qk_bf16) {
   delta_prep_kernel<T, D, K><<<grid, D, 0, st>>>((const T*)qkv_conv, (const T*)proj, proj_stride, b_off, a_off,
                                                  (const T*)f, A_log, dt_bias, qn, kn, gexp, glog, beta, Hk, Hv,
-                                                 scale, eps_l2);
+                                                 scale, eps_l2, qk_bf16);
 }
 
 template <typename T, int D, bool K>
@@ -941,9 +948,10 @@ sn_status sn_conv_prefill(const void* x, int x_stride, void* y, const void* conv
 }
 
 sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int proj_stride, int b_off, int a_off,
-                        const void* f, const float* A_log, const float* dt_bias, float* qn, float* kn, float* gexp,
+                        const void* f, const float* A_log, const float* dt_bias, void* qn, void* kn, float* gexp,
                         float* glog, float* beta, int rows, int Hk, int Hv, int D, float scale, float eps_l2,
-                        int dtype, void* stream) {
+                        int qk_dtype, int dtype, void* stream) {
+  SN_REQUIRE(qk_dtype == SN_F32 || qk_dtype == SN_BF16, "sn_delta_prep: q/k dtype %d", qk_dtype);
   SN_REQUIRE(kind == 0 || kind == 1, "sn_delta_prep: kind %d", kind);
   SN_REQUIRE(rows > 0 && Hk > 0 && Hv % Hk == 0, "sn_delta_prep: bad shape");
   SN_REQUIRE(kind == 0 || f != nullptr, "sn_delta_prep: KDA needs f");
@@ -956,7 +964,7 @@ sn_status sn_delta_prep(int kind, const void* qkv_conv, const void* proj, int pr
     auto fn = D == 128 ? (kind ? launch_prep<T, 128, true> : launch_prep<T, 128, false>)
                        : (kind ? launch_prep<T, 64, true> : launch_prep<T, 64, false>);
     fn(grid, st, qkv_conv, proj, proj_stride, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, glog, beta, Hk, Hv,
-       scale, eps_l2);
+       scale, eps_l2, qk_dtype == SN_BF16);
     return check_launch("sn_delta_prep");
   });
 }

@@ -651,13 +651,16 @@ class Supernet:
         ops.conv_prefill(proj, proj.stride(0), y, w["conv_w"], st["conv"], cu, self._slot_idx, C, cfg.conv_width,
                          ring_hist=hist, pos0=None if cont is None else cont[1])
         f32 = dict(device=dev, dtype=torch.float32)
-        qn, kn = torch.empty(rows, Hk, D, **f32), torch.empty(rows, Hk, D, **f32)
-        gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
-        beta = torch.empty(rows, Hv, **f32)
-        k_code = 1 if kind == KDA else 0
         # bf16: chunked WY prefill on tensor cores (GDN scalar gate / KDA per-channel gate);
         # fp32 I/O (1e-4 parity mode): the recurrent scan (same outputs, token-sequential)
         chunked = h.dtype == torch.bfloat16 and getattr(self, "chunked_prefill", True)
+        # the chunked GDN pass reads q / k as bf16 TMA tiles
+        qk_dt = torch.bfloat16 if (chunked and kind == GDN) else torch.float32
+        qn = torch.empty(rows, Hk, D, device=dev, dtype=qk_dt)
+        kn = torch.empty(rows, Hk, D, device=dev, dtype=qk_dt)
+        gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)
+        beta = torch.empty(rows, Hv, **f32)
+        k_code = 1 if kind == KDA else 0
         glog = (torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)) if chunked else None
         ops.delta_prep(k_code, y, proj, b_off, a_off, f, w["A_log"], w["dt_bias"], qn, kn, gexp, beta, Hk, Hv, D,
                        1.0 / math.sqrt(D), cfg.l2_eps, glog=glog)

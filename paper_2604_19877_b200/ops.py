@@ -121,9 +121,11 @@ def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channe
 
 def delta_prep(kind, qkv_conv, proj, b_off, a_off, f, A_log, dt_bias, qn, kn, gexp, beta, Hk, Hv, D, scale, eps_l2,
                glog=None):
+    """qn / kn: fp32 (the token scan, the KDA chunk pass) or bf16 (the chunked GDN prefill's TMA tiles)."""
+    assert qn.dtype == kn.dtype
     call("sn_delta_prep", kind, _p(qkv_conv), _p(proj), proj.stride(0), b_off, a_off, _p(f), _p(A_log), _p(dt_bias),
          _p(qn), _p(kn), _p(gexp), _p(glog), _p(beta), qkv_conv.shape[0], Hk, Hv, D, scale, eps_l2,
-         dtype_code(qkv_conv.dtype), _s())
+         dtype_code(qn.dtype), dtype_code(qkv_conv.dtype), _s())
 
 
 def delta_scan(kind, qn, kn, qkv_conv, v_off, gexp, beta, o, state, slot_idx, cu_seqlens, Hk, Hv, D, init_state):
@@ -233,7 +235,11 @@ def gdn_chunk_prefill2(qn, kn, qkv_conv, v_off, glog, beta, chunks, seq_chunk0, 
     nbytes = _lib.load().sn_gdn_chunk_workspace_bytes(n, Hv, D)
     if workspace is None or workspace.numel() < nbytes:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=qn.device)
-    call("sn_gdn_chunk_prefill2", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(glog), _p(beta),
+    if qn.dtype != torch.bfloat16:  # the kernel reads bf16 TMA tiles (sn_delta_prep emits them directly)
+        qn, kn = qn.to(torch.bfloat16), kn.to(torch.bfloat16)
+    assert qn.is_contiguous() and kn.is_contiguous()
+    call("sn_gdn_chunk_prefill2", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), qkv_conv.shape[0],
+         _p(glog), _p(beta),
          _p(chunks), _p(seq_chunk0), n, _p(workspace), _p(o), _p(state), _p(slot_idx), seq_chunk0.numel() - 1, Hk, Hv,
          D, int(init_state), dtype_code(qkv_conv.dtype), _s())
     return workspace
