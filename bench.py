@@ -119,7 +119,7 @@ def self_launch(n: int) -> int:
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")  # the driver can see the communicator's rank count
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(sys.argv[0])] + sys.argv[1:]
     return subprocess.call(cmd, env=env)
 
 

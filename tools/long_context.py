@@ -1,7 +1,7 @@
 """BASELINE.json config 5: one long sequence — chunked prefill of T tokens, then graphed decode.
 
   python tools/long_context.py --tokens 131072 [--preset 'Reg|Lklhd-10'] [--decode 64]
-  torchrun --nproc-per-node N tools/long_context.py ...   # head-parallel TP over N GPUs
+  python tools/long_context.py --gpus N ...   # head-parallel TP over N GPUs (self-launches torchrun)
                                                            # (one all-reduce per row-parallel projection)
 Prints one JSON line: prefill tokens/s and decode tokens/s (B = 1), timed with CUDA events
 (max over ranks under torchrun).
@@ -24,7 +24,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--preset", default="Reg|Lklhd-10")
 ap.add_argument("--tokens", type=int, default=131072)
 ap.add_argument("--decode", type=int, default=64)
+ap.add_argument("--gpus", type=int, default=1, help="head-parallel ranks (self-launches torchrun, one per GPU)")
 a = ap.parse_args()
+if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    from bench import self_launch
+    sys.exit(self_launch(a.gpus))  # fails loudly when the box has fewer GPUs
+if int(os.environ.get("WORLD_SIZE", "1")) != a.gpus:
+    sys.exit(f"long_context.py: --gpus {a.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
 ws, rank, _ = dist_setup()
 tp_group = None
 if ws > 1:
@@ -41,7 +47,7 @@ m.prefill(toks)
 e1.record()
 torch.cuda.synchronize()
 prefill_ms = max_over_ranks(e0.elapsed_time(e1), ws)
-g = DecodeGraph(m, feedback=True, preserve_state=False)
+g = DecodeGraph(m, feedback=True, preserve_state=True)  # decode continues the prefilled context
 for _ in range(3):
     g.replay()
 barrier(ws)
