@@ -21,10 +21,12 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--context", type=int, default=32768)
 ap.add_argument("--replays", type=int, default=1)
 ap.add_argument("--eager", action="store_true")
+ap.add_argument("--chain", action="store_true", help="the opt-in fused decode chains")
 a = ap.parse_args()
-m = Supernet(APRIEL, PRESETS[a.preset].layer_string, batch=a.batch, max_len=a.context + 64, dtype=torch.bfloat16)
-fill_synthetic(m, a.context)
-g = DecodeGraph(m, feedback=True, preserve_state=False)
+m = Supernet(APRIEL, PRESETS[a.preset].layer_string, batch=a.batch, max_len=a.context + 64, dtype=torch.bfloat16,
+             fused_chain=a.chain)
+g = DecodeGraph(m, feedback=True, preserve_state=False)  # warm-up + capture on the empty engine (it resets)
+fill_synthetic(m, a.context)  # then the KV pools / states at the context length
 for _ in range(3):
     g.replay()
 torch.cuda.synchronize()
