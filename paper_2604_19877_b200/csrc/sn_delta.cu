@@ -109,6 +109,10 @@ __device__ __forceinline__ void block_sum3(float& x, float& y, float& z, float* 
 
 constexpr int kDecodeThreads = 256;
 
+__device__ __forceinline__ uint32_t dl_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // Width-4 causal conv of one channel at position pos: the ring holds the inputs of
 // positions pos-1..pos-3 at slots (pos-d) & 3; x is the new input.
 __device__ __forceinline__ float conv4(const float* w, const float* ring, float x, int pos) {
@@ -364,6 +368,178 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
 }
 
 // ---------------------------------------------------------------------------------------
+// GDN decode, D = 128, state staged through shared memory with cp.async: every warp keeps
+// NBUF - 1 batches of NB columns in flight in its own smem ring (lane l copies and later reads
+// its own 16-byte slice of each column, so no barrier is needed), the conv / norm / gate prologue
+// running under the first batches' latency.  Measured at B=64 (tools/bench_delta.py): 45.0 us
+// vs 48.0 for the register pipeline (gdn_decode_kernel, kept for D = 64 and the 512-thread
+// small-batch CTAs), and the decode step 10.23 -> 9.77 ms; NBUF = 3 measured 46.0 us.
+// One CTA (8 warps) per (value head, sequence).
+template <typename T, int NBUF>
+__global__ void __launch_bounds__(kDecodeThreads, 4) gdn_decode_cpa_kernel(const DeltaDecodeArgs a) {
+  sn::pdl_launch_dependents();
+  constexpr int D = 128, THREADS = kDecodeThreads, NW = THREADS / 32;
+  constexpr int EPL = D / 32, CPW = D / NW, NB = 4, NBATCH = CPW / NB;
+  static_assert(EPL == 4 && NBATCH >= NBUF - 1, "cp.async staging assumes 16-byte lane slices");
+  extern __shared__ __align__(16) float ring_all[];  // [NW][NBUF][NB][D]
+  __shared__ __align__(16) float s_o[D];
+  __shared__ float s_red[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = a.Hv / a.Hk;
+  const int h = blockIdx.x % a.Hv, b = blockIdx.x / a.Hv;
+  const int slot = a.slot_idx ? a.slot_idx[b] : b;
+  float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
+  float* ring = ring_all + (size_t)warp * NBUF * NB * D;
+  auto issue = [&](int jb) {  // batch jb of this warp's columns -> ring slot jb % NBUF
+    float* dst = ring + (jb % NBUF) * NB * D + lane * EPL;
+    const float* src = S + (size_t)(warp * CPW + jb * NB) * D + lane * EPL;
+#pragma unroll
+    for (int n = 0; n < NB; ++n)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dl_smem_u32(dst + n * D)), "l"(src + (size_t)n * D)
+                   : "memory");
+  };
+#pragma unroll
+  for (int jb = 0; jb < NBUF - 1; ++jb) {
+    issue(jb);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const T* nwp = reinterpret_cast<const T*>(a.norm_w);
+  const float nw = tid < D ? io<T>::ld(nwp + tid) : 0.f;
+  const T* cw = reinterpret_cast<const T*>(a.conv_w);
+  const int kh = h / G;
+  T* ring_c = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * 4;
+  const int qch = a.q_off + kh * D + lane * EPL, kch = a.k_off + kh * D + lane * EPL;
+  const int vcol = warp * CPW + (lane < CPW ? lane : 0);
+  const int vch = a.v_off + h * D + vcol;
+  Packed<T, 4 * EPL> rgq, rgk, wq, wk;
+  Packed<T, 4> rgv, wv;
+  rgq.load(ring_c + (size_t)qch * 4);
+  rgk.load(ring_c + (size_t)kch * 4);
+  rgv.load(ring_c + (size_t)vch * 4);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int pos = a.positions[b];
+  if (pos < 0) {  // idle slot (sn_embed): state and conv ring untouched
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  // the conv taps (L2-resident weights) in the same round trip as the projection row
+  wq.load(cw + (size_t)qch * 4);
+  wk.load(cw + (size_t)kch * 4);
+  wv.load(cw + (size_t)vch * 4);
+  const float negA = -expf(a.A_log[h]);
+  const float dtb = a.dt_bias[h];
+  const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
+  float xq[EPL], xk[EPL];
+  loadn<T, EPL>(prow + qch, xq);
+  loadn<T, EPL>(prow + kch, xk);
+  const float xv = io<T>::ld(prow + vch);
+  const float zval = tid < D ? io<T>::ld(prow + a.z_off + h * D + tid) : 0.f;
+  const float braw = io<T>::ld(prow + a.b_off + h);
+  const float graw = io<T>::ld(prow + a.a_off + h) + dtb;
+  float qv[EPL], kv[EPL], vv = 0.f;
+  auto conv_all = [&](auto P) {
+    constexpr int p = decltype(P)::value;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      qv[e] = silu_f(conv4p<p>(wq, rgq, e, xq[e], pos));
+      kv[e] = silu_f(conv4p<p>(wk, rgk, e, xk[e], pos));
+    }
+    vv = silu_f(conv4p<p>(wv, rgv, 0, xv, pos));
+  };
+  switch (pos & 3) {
+    case 0: conv_all(std::integral_constant<int, 0>{}); break;
+    case 1: conv_all(std::integral_constant<int, 1>{}); break;
+    case 2: conv_all(std::integral_constant<int, 2>{}); break;
+    default: conv_all(std::integral_constant<int, 3>{}); break;
+  }
+  if ((h % G) == 0 && warp == 0) {
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      io<T>::st(ring_c + (size_t)(qch + e) * 4 + (pos & 3), xq[e]);
+      io<T>::st(ring_c + (size_t)(kch + e) * 4 + (pos & 3), xk[e]);
+    }
+  }
+  if (lane < CPW) io<T>::st(ring_c + (size_t)vch * 4 + (pos & 3), xv);
+  float qq = 0.f, kk = 0.f, qkr = 0.f;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    qq += qv[e] * qv[e];
+    kk += kv[e] * kv[e];
+    qkr += qv[e] * kv[e];
+  }
+  qq = warp_sum(qq);
+  kk = warp_sum(kk);
+  qkr = warp_sum(qkr);
+  const float rq = rsqrtf(qq + a.eps_l2) * a.scale, rk = rsqrtf(kk + a.eps_l2);
+  const float eg = expf(negA * softplus_f(graw));
+  const float beta = sigmoid_f(braw);
+  const float qk = qkr * rq * rk;
+  float kr[EPL], kg[EPL], qg[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    kr[e] = kv[e] * rk;
+    kg[e] = kr[e] * eg;
+    qg[e] = qv[e] * rq * eg;
+  }
+#pragma unroll 1
+  for (int jb = 0; jb < NBATCH; ++jb) {
+    if (jb + NBUF - 1 < NBATCH) issue(jb + NBUF - 1);  // its slot was read in iteration jb - 1
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(NBUF - 1) : "memory");
+    const int c0 = warp * CPW + jb * NB;
+    const float* src = ring + (jb % NBUF) * NB * D + lane * EPL;
+    float s[NB][EPL];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const float4 t = *reinterpret_cast<const float4*>(src + n * D);
+      s[n][0] = t.x; s[n][1] = t.y; s[n][2] = t.z; s[n][3] = t.w;
+    }
+    float kd[NB], qd[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      kd[n] = 0.f;
+      qd[n] = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        kd[n] += kg[e] * s[n][e];
+        qd[n] += qg[e] * s[n][e];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int n = 0; n < NB; ++n) {
+        kd[n] += __shfl_xor_sync(0xffffffffu, kd[n], o);
+        qd[n] += __shfl_xor_sync(0xffffffffu, qd[n], o);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const float vcn = __shfl_sync(0xffffffffu, vv, jb * NB + n);
+      const float u = beta * (vcn - kd[n]);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) s[n][e] = eg * s[n][e] + kr[e] * u;
+      vecf<EPL>::st(S + (size_t)(c0 + n) * D + lane * EPL, s[n]);
+      if (lane == 0) s_o[c0 + n] = qd[n] + qk * u;
+    }
+  }
+  __syncthreads();
+  float oo = 0.f;
+  for (int j = tid; j < D; j += THREADS) oo += s_o[j] * s_o[j];
+  oo = warp_sum(oo);
+  if (lane == 0) s_red[warp] = oo;
+  __syncthreads();
+  oo = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) oo += s_red[w];
+  const float rstd = rsqrtf(oo / (float)D + a.eps_norm);
+  if (tid < D) {
+    T* out = reinterpret_cast<T*>(a.out) + (size_t)b * a.Hv * D + (size_t)h * D;
+    io<T>::st(out + tid, s_o[tid] * rstd * nw * silu_f(zval));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // KDA decode: one CTA per (head, sequence).  The CTA
 //   1. runs the conv update of its q/k/v channels against the per-sequence conv ring
 //      (KDA heads are not shared: the CTA owns its channels' ring slots),
@@ -372,7 +548,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
 //      fg = [2][B][H*D]) and beta,
 //   3. streams the fp32 state once as in the GDN kernel, with per-key-channel decays,
 //   4. applies the gated RMSNorm (sigmoid gate).
-template <typename T, int D, int THREADS = kDecodeThreads>
+template <typename T, int D, int THREADS = kDecodeThreads, bool CPA = false>
 __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
     kda_decode_kernel(const DeltaDecodeArgs a) {
   sn::pdl_launch_dependents();
@@ -394,9 +570,28 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
   const int h = blockIdx.x, b = blockIdx.y;
   const int slot = a.slot_idx ? a.slot_idx[b] : b;
   float* S = a.state + ((size_t)slot * a.Hv + h) * D * D;
-  float s_nx[NB][EPL];
+  // CPA (D = 128, 256 threads): the state batches are staged through a per-warp shared-memory
+  // ring with cp.async (as gdn_decode_cpa_kernel: one batch in flight, no registers held);
+  // otherwise the next batch waits in registers
+  extern __shared__ __align__(16) float kring_all[];  // CPA: [NW][2][NB][D]
+  float* kring = kring_all + (size_t)warp * 2 * NB * D;
+  auto issue = [&](int c0, int sl) {
+    if constexpr (CPA) {
 #pragma unroll
-  for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
+      for (int n = 0; n < NB; ++n)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dl_smem_u32(kring + (sl * NB + n) * D + lane * EPL)),
+                     "l"(S + (size_t)(c0 + n) * D + lane * EPL)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
+  float s_nx[NB][EPL];
+  if constexpr (CPA) {
+    issue(warp * CPW, 0);
+  } else {
+#pragma unroll
+    for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(warp * CPW + n) * D + lane * EPL, s_nx[n]);
+  }
   T* ring = reinterpret_cast<T*>(a.conv_ring) + (size_t)slot * a.conv_channels * 4;
   const T* cw = reinterpret_cast<const T*>(a.conv_w);
   constexpr int NCH = (3 * D + THREADS - 1) / THREADS;
@@ -422,7 +617,10 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pos = a.positions[b];
-  if (pos < 0) return;  // idle slot (sn_embed): state and conv ring untouched
+  if (pos < 0) {  // idle slot (sn_embed): state and conv ring untouched
+    if constexpr (CPA) asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
   const T* prow = reinterpret_cast<const T*>(a.proj) + (size_t)b * a.proj_stride;
 
   // ---- 1. prologue loads of the in-projection row and the gate factors, all issued first
@@ -479,13 +677,25 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
 #pragma unroll 1
   for (int c0 = warp * CPW; c0 < (warp + 1) * CPW; c0 += NB) {
     float s[NB][EPL];
+    if constexpr (CPA) {
+      const int sl = ((c0 - warp * CPW) / NB) & 1;
+      if (c0 + NB < (warp + 1) * CPW) issue(c0 + NB, sl ^ 1);  // that slot was read last iteration
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll
-    for (int n = 0; n < NB; ++n)
+      for (int n = 0; n < NB; ++n) {
+        const float4 t = *reinterpret_cast<const float4*>(kring + (sl * NB + n) * D + lane * EPL);
+        s[n][0] = t.x; s[n][1] = t.y; s[n][2] = t.z; s[n][3] = t.w;
+      }
+    } else {
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) s[n][e] = s_nx[n][e];
-    if (c0 + NB < (warp + 1) * CPW) {
+      for (int n = 0; n < NB; ++n)
 #pragma unroll
-      for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + NB + n) * D + lane * EPL, s_nx[n]);
+        for (int e = 0; e < EPL; ++e) s[n][e] = s_nx[n][e];
+      if (c0 + NB < (warp + 1) * CPW) {
+#pragma unroll
+        for (int n = 0; n < NB; ++n) vecf<EPL>::ld(S + (size_t)(c0 + NB + n) * D + lane * EPL, s_nx[n]);
+      }
     }
     float kd[NB], qd[NB];
 #pragma unroll
@@ -831,8 +1041,33 @@ static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStre
   attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+  if (!KDA && D == 128 && !wide) {  // the state staged through shared memory (cp.async ring)
+    constexpr int NBUF = 2;
+    cfg.dynamicSmemBytes = (size_t)(kDecodeThreads / 32) * NBUF * 4 * 128 * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gdn_decode_cpa_kernel<T, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)cfg.dynamicSmemBytes);
+      attr = true;
+    }
+    cudaError_t e2 = cudaLaunchKernelEx(&cfg, gdn_decode_cpa_kernel<T, NBUF>, a);
+    if (e2 != cudaSuccess) {
+      set_error("sn_gdn_decode launch: %s", cudaGetErrorString(e2));
+      return SN_ECUDA;
+    }
+    return check_launch("sn_gdn_decode");
+  }
   cudaError_t e;
-  if (KDA)
+  if (KDA && D == 128 && !wide) {  // the state staged through shared memory (cp.async ring)
+    cfg.dynamicSmemBytes = (size_t)(kDecodeThreads / 32) * 2 * 4 * 128 * sizeof(float);
+    static bool kattr = false;
+    if (!kattr) {
+      cudaFuncSetAttribute(kda_decode_kernel<T, D, kDecodeThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)cfg.dynamicSmemBytes);
+      kattr = true;
+    }
+    e = cudaLaunchKernelEx(&cfg, kda_decode_kernel<T, D, kDecodeThreads, true>, a);
+  } else if (KDA)
     e = wide ? cudaLaunchKernelEx(&cfg, kda_decode_kernel<T, D, 2 * kDecodeThreads>, a)
              : cudaLaunchKernelEx(&cfg, kda_decode_kernel<T, D>, a);
   else
