@@ -225,11 +225,10 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
 sn_status attn_prefill_tc_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                int num_seqs, int rows, int Hq, int Hkv, int D, int window, float scale,
                                const int32_t* cu_k, const int32_t* q_off, int rows_k, cudaStream_t st) {
-  // D = 128: tcgen05/TMEM kernel; SN_ATTN_PREFILL=mma keeps the mma.sync kernel (A/B, D = 64)
-  static const bool mma = getenv("SN_ATTN_PREFILL") && getenv("SN_ATTN_PREFILL")[0] == 'm';
-  if (D == 128 && !mma)
+  // head dim 128 (every Apriel attention layer): the tcgen05/TMEM kernel; head dim 64 (the tiny
+  // test configuration only): the mma.sync kernel of this file
+  if (D == 128)
     return attn_prefill_umma_bf16(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off, rows_k, st);
-  if (D == 128) return fa::launch<128>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off, st);
   if (D == 64) return fa::launch<64>(q, k, v, cu, out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off, st);
   set_error("sn_attn_prefill: D=%d unsupported", D);
   return SN_EUNSUPPORTED;

@@ -26,44 +26,10 @@ namespace fa5 {
 using namespace sn::tc;
 
 constexpr int BM = 128, BN = 128, HD = 128;
-template <int NS>
-constexpr int threads_for() { return NS * 128 + 96; }  // softmax warps, MMA warp, K/Q TMA warp, V TMA warp
 constexpr float kLazy = 8.f;  // log2 headroom of the stale running max
 constexpr uint32_t ATOM = 128 * 128;  // one [128 rows x 64 bf16] 128B-swizzled atom (16 KB)
 constexpr uint32_t TILE = 2 * ATOM;   // [128 x 128] bf16
-
-// PT = false: P (bf16) goes through shared memory (double-buffered), K / V rings of 2 stages.
-// PT = true: P is written over its own scores in TMEM (packed bf16, tcgen05.st) and the PV
-// product reads A from TMEM; the freed 64 KB give the K and V rings a third stage, so the next
-// K tile is requested a block earlier (the issuer waited ~220 cycles per block for it).
-template <bool PT>
-struct Smem;
-template <>
-struct Smem<false> {  // 224 KB, 1024-byte aligned
-  static constexpr int KVS = 2;
-  uint8_t q[TILE];
-  uint8_t k[KVS][TILE];
-  uint8_t v[KVS][TILE];
-  uint8_t p[2][TILE];  // double-buffered: softmax(j+1) writes while PV(j) reads
-};
-template <>
-struct Smem<true> {   // 224 KB
-  static constexpr int KVS = 3;
-  uint8_t q[TILE];
-  uint8_t k[KVS][TILE];
-  uint8_t v[KVS][TILE];
-};
-struct Sync {          // in front of the tiles, inside the dynamic allocation
-  uint64_t q_full, k_full[3], k_empty[3], v_full[3], v_empty[3], s_full[3], p_full[3], o_done[2];
-  uint32_t tmem_base;
-  float red[3][BM];  // row max of iteration j in red[j % 3] (float atomic max over the slices)
-  float lsum[BM];    // final row sums
-};
-constexpr int kSyncBytes = 3072;
 constexpr int kSmemBytes = 227 * 1024;
-static_assert(sizeof(Sync) <= kSyncBytes, "sync block");
-static_assert(sizeof(Smem<false>) + kSyncBytes <= kSmemBytes, "tiles");
-static_assert(sizeof(Smem<true>) + kSyncBytes <= kSmemBytes, "tiles");
 
 // MN-major operand (V as the B operand of P V: N = head dim contiguous, K = keys):
 // LBO = stride between 64-element N chunks (the second TMA box), SBO = stride between
@@ -163,321 +129,6 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 
-template <int NS, bool PT, int POLY = 1>
-__global__ void __launch_bounds__(threads_for<NS>(), 1)
-    attn_prefill_umma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-                             const __grid_constant__ CUtensorMap vmap, const int32_t* __restrict__ cu,
-                             __nv_bfloat16* __restrict__ out, int num_seqs, int rows, int Hq, int Hkv, int window,
-                             float scale, const int32_t* __restrict__ cu_k, const int32_t* __restrict__ q_off,
-                             unsigned long long* __restrict__ dbg, int skip_softmax) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Sync& sy = *reinterpret_cast<Sync*>(smem_raw);
-  uint8_t* base = smem_raw + kSyncBytes;
-  base += (1024 - (smem_u32(base) & 1023)) & 1023;
-  using SM = Smem<PT>;
-  constexpr int KVS = SM::KVS;
-  // TMEM score buffers: 2 (P in smem) or 3 (P in TMEM: S(j+2) is issued before PV(j), so the
-  // tensor pipe always has a score product queued while the issuer waits for P(j)); O after them
-  constexpr int SB = PT ? 3 : 2;
-  constexpr uint32_t O_COL = SB * 128;
-  if (base + sizeof(SM) > smem_raw + kSmemBytes) __trap();  // dynamic smem base not 1 KB aligned
-  SM& sm = *reinterpret_cast<SM*>(base);
-  uint64_t &q_full = sy.q_full, *k_full = sy.k_full, *k_empty = sy.k_empty, *v_full = sy.v_full;
-  uint64_t *v_empty = sy.v_empty, *s_full = sy.s_full;
-  uint64_t *p_full = sy.p_full, *o_done = sy.o_done;
-  uint32_t& tmem_base_s = sy.tmem_base;
-  constexpr int SW = 4 * NS;       // softmax warps
-  constexpr int COLS = BN / NS;    // key columns (and head-dim columns of O) per softmax warp
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles = (rows + BM - 1) / BM;
-  const int r0 = (tiles - 1 - (int)blockIdx.x) * BM;  // heavy (late) tiles first
-  const int h = blockIdx.y, hk = h / (Hq / Hkv);
-  const int r_last = min(r0 + BM - 1, rows - 1);
-  const KeyBounds kb0 = key_bounds(cu, cu_k, q_off, num_seqs, r0, window);
-  const KeyBounds kbl = key_bounds(cu, cu_k, q_off, num_seqs, r_last, window);
-  const int j_lo = kb0.lo, j_hi = kbl.hi;
-  const int nblk = (j_hi - j_lo) / BN + 1;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&q_full, 1);
-    for (int i = 0; i < KVS; ++i) {
-      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < SB; ++i) mbar_init(&s_full[i], 1);
-    // P(j) completes p_full[j % SB]: the softmax can run at most one block ahead of the MMA
-    // issuer's wait (S(j+2) is issued after P(j) was consumed), so the phase parity is exact
-    for (int i = 0; i < SB; ++i) mbar_init(&p_full[i], SW * 32);
-    for (int i = 0; i < 2; ++i) mbar_init(&o_done[i], 1);
-  }
-  if (threadIdx.x < BM) {
-    for (int i = 0; i < 3; ++i) sy.red[i][threadIdx.x] = -INFINITY;
-    sy.lsum[threadIdx.x] = 0.f;
-  }
-  if (threadIdx.x == 0) {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_s;  // S buffers: columns [128 b, 128 b + 128); O: [O_COL, O_COL + 128)
-
-  if (warp > SW) {
-    // ---------------- TMA producers: warp 9 loads Q and the K ring, warp 10 the V ring.  K and
-    // V have their own stages: K(j+2) only waits for S(j), V(j+2) for PV(j).
-    if (lane == 0) {
-      const bool is_k = warp == SW + 1;
-      const CUtensorMap* map = is_k ? &kmap : &vmap;
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-      const uint64_t keep = policy_evict_last();  // K/V blocks are re-read by the other q heads of the group
-      if (is_k) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
-        mbar_expect_tx(&q_full, TILE);
-        tma_load_2d(sm.q, &qmap, h * HD, r0, &q_full, policy_evict_first());
-        tma_load_2d(sm.q + ATOM, &qmap, h * HD + 64, r0, &q_full, policy_evict_first());
-      }
-      uint64_t* full = is_k ? k_full : v_full;
-      uint64_t* empty = is_k ? k_empty : v_empty;
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j % KVS;
-        if (j >= KVS) mbar_wait(&empty[st], ((j / KVS) - 1) & 1);
-        const int jb = j_lo + j * BN;
-        uint8_t* dst = is_k ? sm.k[st] : sm.v[st];
-        mbar_expect_tx(&full[st], TILE);
-        tma_load_2d(dst, map, hk * HD, jb, &full[st], keep);
-        tma_load_2d(dst + ATOM, map, hk * HD + 64, jb, &full[st], keep);
-      }
-    }
-  } else if (warp == SW) {
-    {  // ---------------- MMA issuer (whole warp, one elected lane issues)
-      const uint32_t id_s = idesc_bf16(BM, BN);
-      const uint32_t id_o = idesc_bf16(BM, HD) | (1u << 16);  // B (= V) MN-major
-      const uint32_t sq = smem_u32(sm.q);
-      mbar_wait(&q_full, 0);
-      // S(j+1) is issued before PV(j) waits for P(j): the tensor core computes the next scores
-      // while the softmax warps work on the current block (S double-buffered in TMEM).
-      const bool rec = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
-      auto stamp = [&](int j, int what) {
-        if (rec && lane == 0 && j < 64) dbg[j * 8 + what] = clock64();
-      };
-      auto issue_s = [&](int j) {
-        const int st = j % SB, ks = j % KVS;
-        mbar_wait(&k_full[ks], (j / KVS) & 1);
-        stamp(j, 0);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(sm.k[ks]);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_w(tmem + st * 128, desc_sw128(sq + (k >> 2) * ATOM + (k & 3) * 32),
-               desc_sw128(sk + (k >> 2) * ATOM + (k & 3) * 32), id_s, k > 0 ? 1u : 0u);
-        commit_w(&s_full[st]);
-        commit_w(&k_empty[ks]);
-      };
-      issue_s(0);
-      if (SB == 3 && nblk > 1) issue_s(1);
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j % SB;
-        // its S buffer was last read as S / P of block j+1-SB, whose PV was issued before (in order)
-        if (j + SB - 1 < nblk) issue_s(j + SB - 1);
-        stamp(j, 1);
-        const int vs = j % KVS;
-        mbar_wait(&v_full[vs], (j / KVS) & 1);
-        mbar_wait(&p_full[st], (j / SB) & 1);
-        stamp(j, 2);
-        tc_fence_after();
-        const uint32_t sv = smem_u32(sm.v[vs]);
-        if constexpr (PT) {  // P(j): packed bf16 over the first 64 columns of its score buffer
-#pragma unroll
-          for (int k = 0; k < BN / 16; ++k)
-            umma_ts_w(tmem + O_COL, tmem + st * 128 + k * 8, desc_mn_sw128(sv + k * 2048), id_o,
-                    (j > 0 || k > 0) ? 1u : 0u);
-        } else {
-          const uint32_t sp = smem_u32(sm.p[st]);
-#pragma unroll
-          for (int k = 0; k < BN / 16; ++k)
-            umma_w(tmem + O_COL, desc_sw128(sp + (k >> 2) * ATOM + (k & 3) * 32), desc_mn_sw128(sv + k * 2048), id_o,
-                 (j > 0 || k > 0) ? 1u : 0u);
-        }
-        commit_w(&o_done[j & 1]);
-        commit_w(&v_empty[vs]);
-        stamp(j, 3);
-      }
-    }
-  } else {
-    // ---------------- softmax: warps w, w+4, .. share TMEM lanes 32(w%4).. (query rows), each
-    // taking COLS of the 128 key columns (and of the head dim for O).
-    const int sub = warp & 3, part = warp >> 2;
-    const int t = sub * 32 + lane;
-    const int r = r0 + t;
-    const KeyBounds kbr = key_bounds(cu, cu_k, q_off, num_seqs, min(r, rows - 1), window);
-    const int lo = kbr.lo, hi = kbr.hi;
-    const float qs = scale * 1.4426950408889634f;
-    const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + part * COLS, o_addr = tmem + O_COL + lane_addr + part * COLS;
-    // P slice: keys part*COLS.. live in atom (part*COLS)/64, 16-byte chunks from ((part*COLS)%64)/8
-    uint8_t* prow0 = nullptr;
-    if constexpr (!PT) prow0 = &sm.p[0][0] + ((part * COLS) >> 6) * ATOM + t * 128;
-    static_assert(!PT || COLS == 64 || COLS == 32, "P in TMEM: one x32 / x16 store of packed columns per slice");
-    const int chunk0 = ((part * COLS) & 63) >> 3;
-    float m = -INFINITY, l = 0.f;
-    const bool srec = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0;
-    auto sstamp = [&](int j, int what) {
-      if (srec && j < 64) dbg[j * 8 + what] = clock64();
-    };
-    for (int j = 0; j < nblk; ++j) {
-      const int jb = j_lo + j * BN;
-      const int sb = j % SB;
-      mbar_wait(&s_full[sb], (j / SB) & 1);
-      sstamp(j, 4);
-      tc_fence_after();
-      if (skip_softmax) {  // experiment: the MMA / TMA pipeline alone (results wrong)
-        tc_fence_before();
-        mbar_arrive(&p_full[sb]);
-        continue;
-      }
-      float s[COLS];
-#pragma unroll
-      for (int c = 0; c < COLS; c += 32) tmem_ld32(s_addr + sb * 128 + c, s + c);
-      tmem_wait_ld();
-      sstamp(j, 5);
-      const bool full = jb >= kbl.lo && jb + BN - 1 <= kb0.hi;
-      float mx = -INFINITY;
-      if (!full) {
-#pragma unroll
-        for (int i = 0; i < COLS; ++i) {
-          const int jj = jb + part * COLS + i;
-          if (jj > hi || jj < lo) s[i] = -INFINITY;
-        }
-      }
-      {  // four independent three-input max chains
-        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < COLS; i += 8) {
-          m0 = max3(m0, s[i], s[i + 1]);
-          m1 = max3(m1, s[i + 2], s[i + 3]);
-          m2 = max3(m2, s[i + 4], s[i + 5]);
-          m3 = max3(m3, s[i + 6], s[i + 7]);
-        }
-        mx = max3(max3(m0, m1, m2), m3, mx);
-      }
-      // Row max over the slices: red[j % 3] was reset (to -inf) by slice 0 in iteration j-2,
-      // after every slice had read it in iteration j-3 (the barrier of j-2 orders both).
-      float* red = sy.red[j % 3];
-      smem_max_f32(red + t, mx);
-      if (PT) tc_fence_before();  // every slice's S loads complete before any P overwrites the buffer
-      named_bar(1 + sub, NS * 32);
-      if (PT) tc_fence_after();
-      sstamp(j, 6);
-      mx = red[t] * qs;  // scores stay unscaled; the max is scaled
-      if (part == 0) sy.red[(j + 2) % 3][t] = -INFINITY;
-      // Lazy rescaling (FA4): the running max only moves when the block max exceeds it by more
-      // than 2^8, so P = 2^(s - m) <= 256 (exact after the final 1/l) and O is rarely rescaled —
-      // each rescale must wait for PV(j-1), which serialises the softmax behind the tensor core.
-      const float mn = mx > m + kLazy ? mx : m;
-      const float base_m = mn == -INFINITY ? 0.f : mn;
-      const float alpha = ex2(m - base_m);
-      // P(j) goes to buffer j&1, last read by PV(j-2) — complete, since S(j) was committed after
-      // it.  O is only touched when a row max moved: then PV(j-1) must have finished (o_done of
-      // its parity; PV(j-3) on the same barrier completed before S(j-1), so the parity wait is
-      // exact).
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < COLS; c += 32) {
-          float o[32];
-          tmem_ld32(o_addr + c, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] *= alpha;
-          tmem_st32(o_addr + c, o);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      }
-      float2 rs2 = make_float2(0.f, 0.f);
-      const float2 qs2 = make_float2(qs, qs), nb2 = make_float2(-base_m, -base_m);
-      uint32_t p32[PT ? COLS / 2 : 1];
-#pragma unroll
-      for (int c = 0; c < COLS / 8; ++c) {
-        float2 p[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 x = ffma2(make_float2(s[c * 8 + 2 * e], s[c * 8 + 2 * e + 1]), qs2, nb2);
-          // POLY of every 4 pairs on the FMA pipe (cubic exp2), the rest on MUFU.EX2
-          p[e] = (e >= 4 - POLY) ? exp2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
-          rs2 = fadd2(rs2, p[e]);
-        }
-        if constexpr (PT) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) p32[c * 4 + e] = pack_bf16(p[e].x, p[e].y);
-        } else {
-          uint4 pk;
-          pk.x = pack_bf16(p[0].x, p[0].y);
-          pk.y = pack_bf16(p[1].x, p[1].y);
-          pk.z = pack_bf16(p[2].x, p[2].y);
-          pk.w = pack_bf16(p[3].x, p[3].y);
-          *reinterpret_cast<uint4*>(prow0 + (j & 1) * TILE + (((chunk0 + c) ^ (t & 7)) << 4)) = pk;
-        }
-      }
-      const float rs = rs2.x + rs2.y;
-      l = l * alpha + rs;
-      m = mn;
-      if constexpr (PT) {  // P over the scores: keys 64*part.. -> columns 32*part.. of the buffer
-        const uint32_t pa = tmem + lane_addr + sb * 128 + part * (COLS / 2);
-        if constexpr (COLS == 64) tmem_st32(pa, reinterpret_cast<const float*>(p32));
-        else tmem_st16u(pa, p32);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      } else {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
-      }
-      tc_fence_before();
-      sstamp(j, 7);
-      mbar_arrive(&p_full[sb]);
-    }
-    atomicAdd(&sy.lsum[t], l);  // row sum: the slices' partial sums
-    named_bar(1 + sub, NS * 32);
-    l = sy.lsum[t];
-    mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = out + (size_t)min(r, rows - 1) * Hq * HD + h * HD + part * COLS;
-#pragma unroll 1
-    for (int c = 0; c < COLS; c += 32) {
-      float o[32];
-      tmem_ld32(o_addr + c, o);
-      tmem_wait_ld();
-      if (r < rows) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          uint4 pk;
-          pk.x = pack_bf16(o[e] * inv, o[e + 1] * inv);
-          pk.y = pack_bf16(o[e + 2] * inv, o[e + 3] * inv);
-          pk.z = pack_bf16(o[e + 4] * inv, o[e + 5] * inv);
-          pk.w = pack_bf16(o[e + 6] * inv, o[e + 7] * inv);
-          *reinterpret_cast<uint4*>(orow + c + e) = pk;
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// ---------------------------------------------------------------------------------------------
-// Two query tiles per CTA (FA4's ping-pong): CTA = 256 query rows (tiles A, B of 128) x one q
-// head; every K / V tile feeds both tiles' products, and while one tile's softmax runs the
-// tensor pipe works on the other tile's products, so neither the softmax chain nor the issue
-// order leaves the tensor pipe idle.  TMEM: S_A [0,128), O_A [128,256), S_B [256,384),
-// O_B [384,512); P written over its scores.  Issue order per key block j:
-//   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
-// Warps 0-7 softmax of tile A, 8-15 tile B (two per TMEM lane quadrant, half a row each),
-// 16 MMA (converged, elected issue), 17 Q + K ring, 18 V ring.
 constexpr int kThreads2 = 16 * 32 + 96;
 struct Smem2 {
   uint8_t q[2][TILE];
@@ -739,9 +390,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
 }  // namespace fa5
 
-static unsigned long long* g_fa5_dbg = nullptr;
-extern "C" void sn_experimental_fa5_timeline(unsigned long long* p) { g_fa5_dbg = p; }
-
 sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, const int32_t* cu, void* out,
                                  int num_seqs, int rows, int Hq, int Hkv, int window, float scale,
                                  const int32_t* cu_k, const int32_t* q_off, int rows_k, cudaStream_t st) {
@@ -753,50 +401,17 @@ sn_status attn_prefill_umma_bf16(const void* q, const void* k, const void* v, co
     set_error("sn_attn_prefill: cuTensorMapEncodeTiled failed");
     return SN_ECUDA;
   }
-  const int smem = kSmemBytes;
-  static int ns = 0, skip = 0, pt = 1, poly = 1, two = 1;
-  if (!ns) {
-    // softmax slices per row: 2 (8 softmax warps) by default; 4 (16 warps) measured no faster
-    // (1025 vs 1044 TFLOP/s causal at 16K) — the per-block chain is the MMA issue order, not
-    // softmax latency.  SN_FA5_SLICES=4 (with SN_FA5_PTMEM=0) is the A/B switch.
-    const char* e = getenv("SN_FA5_SLICES");
-    const char* d = getenv("SN_FA5_SKIP_SOFTMAX");
-    const char* t = getenv("SN_FA5_PTMEM");  // P in TMEM + 3-stage K/V rings (default) or in smem
-    ns = e && atoi(e) == 4 ? 4 : 2;
-    skip = d && atoi(d) == 1;
-    pt = !(t && atoi(t) == 0);
-    const char* y = getenv("SN_FA5_POLY");  // pairs of 4 whose exp2 runs on the FMA pipe (1 or 2)
-    poly = y && atoi(y) == 2 ? 2 : 1;
-    const char* w2 = getenv("SN_FA5_TWO");  // two query tiles per CTA (default) or one
-    two = !(w2 && atoi(w2) == 0);
-    cudaFuncSetAttribute(attn_prefill_umma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_prefill_umma_kernel<2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // The round-1 A/B variants (one query tile per CTA with 3-stage K/V rings, P through shared
+  // memory, 16 softmax warps, more exponentials on the FMA pipe) all measured at or below this
+  // kernel (profiles/r01_attn_prefill_umma_ncu.txt) and were removed.
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_prefill_umma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr = true;
   }
-  if (two && !skip && ns == 2 && pt && poly == 1) {
-    attn_prefill_umma2_kernel<<<dim3((rows + 2 * BM - 1) / (2 * BM), Hq), kThreads2, smem, st>>>(
-        qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off);
-    return check_launch("sn_attn_prefill(umma2)");
-  }
-  dim3 grid((rows + BM - 1) / BM, Hq);
-  auto go = [&](auto kern, int threads) {
-    kern<<<grid, threads, smem, st>>>(qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq, Hkv, window, scale,
-                                      cu_k, q_off, g_fa5_dbg, skip);
-  };
-  if (ns == 4 && pt)
-    go(attn_prefill_umma_kernel<4, true>, threads_for<4>());
-  else if (ns == 4)
-    go(attn_prefill_umma_kernel<4, false>, threads_for<4>());
-  else if (pt && poly == 2)
-    go(attn_prefill_umma_kernel<2, true, 2>, threads_for<2>());
-  else if (pt)
-    go(attn_prefill_umma_kernel<2, true>, threads_for<2>());
-  else
-    go(attn_prefill_umma_kernel<2, false>, threads_for<2>());
-  return check_launch("sn_attn_prefill(umma)");
+  attn_prefill_umma2_kernel<<<dim3((rows + 2 * BM - 1) / (2 * BM), Hq), kThreads2, kSmemBytes, st>>>(
+      qm, km, vm, cu, (__nv_bfloat16*)out, num_seqs, rows, Hq, Hkv, window, scale, cu_k, q_off);
+  return check_launch("sn_attn_prefill(umma2)");
 }
 
 }  // namespace sn

@@ -67,8 +67,6 @@ struct Params {
   unsigned long long* counter;
   int nph, nbar;
   unsigned long long* trace;  // sn_decode_chain_trace: per-CTA globaltimer stamps (tools/chain_trace.py)
-  int dbg;  // SN_CHAIN_DBG timing experiments: 1 skip norm rows, 2 producer ignores barriers (both: wrong
-            // results), 4 norm-row CTAs do not prefetch the phase after the norm
   int8_t kind[kMaxPhases], idx[kMaxPhases];
   int8_t wait_bar[kMaxPhases];  // barrier whose completion the phase's inputs need (-1: the previous kernel)
   int8_t arrive[kMaxPhases];    // 1: every CTA arrives at the next barrier after the phase
@@ -185,8 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         };
         auto next = [&](int slot) { return slot + 1 == g.ns ? 0 : slot + 1; };
         // the weights of the first stages do not depend on the barrier: requested before it
-        int npre = min(g.ns, units);
-        if ((P.dbg >> 8) && P.wait_bar[p] >= 0 && P.kind[p - 1] == SN_CHAIN_NORM) npre = min(npre, P.dbg >> 8);
+        const int npre = min(g.ns, units);
         const int s0 = s;
         for (int u = 0; u < npre; ++u) {
           acquire(s);
@@ -196,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         }
         if (units > 0) {
           if (P.wait_bar[p] < 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-          else if (!(P.dbg & 2)) bar_wait(P.counter, base, P.wait_bar[p]);
+          else bar_wait(P.counter, base, P.wait_bar[p]);
           fence_proxy_async_global();
           SN_TRACE(2 + 4 * p);
         }
@@ -298,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           named_bar(2, kNormThreads);
         }
         const int nch = n.dim >> 2;  // float4 chunks of a row
-        for (int r = (P.dbg & 1) ? n.rows : q; r < n.rows; r += G) {
+        for (int r = q; r < n.rows; r += G) {
           // the residual and up to 4 slabs are requested together: one L2 round trip per row
           // (the slabs were just written by other CTAs, so they are L2 hits)
           float4 v[kNormVec];
@@ -499,8 +496,6 @@ g.br = pl.br; g.nblocks = pl.nblocks; g.splits = pl.splits; g.ks = pl.ks; g.ku =
   SN_REQUIRE(nbar == 0 || counter != nullptr, "sn_decode_chain: barriers need a counter");
   if (grid > sms) grid = sms;
   P.nbar = nbar;
-  static const int dbg = getenv("SN_CHAIN_DBG") ? atoi(getenv("SN_CHAIN_DBG")) : 0;
-  P.dbg = dbg;
   P.trace = g_chain_trace;
   const int smem = smem_max + 1024;
   return um == 64 ? chain::launch<64>(P, grid, smem, (cudaStream_t)stream)

@@ -114,15 +114,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // Launch with programmatic dependent launch: the kernel's CTAs may become resident while
 // the previous kernel is still running; everything before its pdl_wait() must touch only
 // data no earlier kernel of the stream writes (weights, its own state).
-// Experiments: SN_NO_PDL=1 launches everything with plain stream serialization.
-inline bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SN_NO_PDL");
-    on = (e && atoi(e)) ? 0 : 1;
-  }
-  return on == 1;
-}
 
 // Key bounds [lo, hi] of packed query row r in prefill attention (mask j in (i - w, i],
 // SURVEY.md App. A item 3).  Plain prefill: queries and keys share the packed index space
@@ -162,7 +153,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -1038,7 +1038,7 @@ static sn_status launch_delta_decode_t(const DeltaDecodeArgs& a, int B, cudaStre
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // state prefetch overlaps the in-proj tail
-  attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   if (!KDA && D == 128 && !wide) {  // the state staged through shared memory (cp.async ring)

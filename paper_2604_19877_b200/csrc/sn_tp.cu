@@ -135,7 +135,7 @@ sn_status sn_tp_allreduce_add_rmsnorm(const unsigned long long* peer_slabs, cons
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tp_allreduce_add_rmsnorm_kernel<T>, peer_slabs, peer_counters, world,

@@ -314,7 +314,7 @@ sn_status sn_add_rmsnorm(const void* delta, const float* partials, int nsplit, f
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, add_rmsnorm_kernel<T>, (const T*)delta, partials, nsplit, residual,

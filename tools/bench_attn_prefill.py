@@ -1,6 +1,6 @@
 """Prefill attention kernel alone (Apriel heads: 32 q / 8 kv x 128): tokens/s and TFLOP/s of
 the masked attention, causal (FA) and window 4096 (SWA), for one long sequence.
-SN_ATTN_PREFILL=mma selects the mma.sync kernel instead of the tcgen05 one."""
+"""
 import math
 import os
 import sys
@@ -29,5 +29,5 @@ for T in [int(x) for x in (sys.argv[1:] or ["4096", "16384"])]:
         ms = e0.elapsed_time(e1) / 5
         pairs = sum(min(i + 1, window) if window else i + 1 for i in range(T))
         flops = 4.0 * pairs * Hq * D
-        print(f"{os.environ.get('SN_ATTN_PREFILL', 'umma'):5s} T={T:6d} window={window:5d}: {ms:8.3f} ms  "
+        print(f"tcgen05 T={T:6d} window={window:5d}: {ms:8.3f} ms  "
               f"{flops / ms / 1e9:7.1f} TFLOP/s")
