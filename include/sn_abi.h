@@ -59,10 +59,13 @@ int sn_abi_version(void);
  * seq_lens[b] += 1 for b < rows (so every later kernel of the step sees the
  * new token's position and the post-append length).  A negative token marks an
  * idle slot (continuous batching): positions[b] = -1, seq_lens[b] unchanged, a
- * zero residual row, and the KV append skips it.                           */
+ * zero residual row, and the KV append skips it.  rope_cs (optional, fp32
+ * [rows][half][2]): the step's rotary (cos, sin) per pair at each row's position
+ * (inv_freq [half]), read by the attention in-projection epilogue instead of
+ * evaluating sincosf per head.                                              */
 sn_status sn_embed(const int32_t* tokens, const void* table, float* residual,
-                   int32_t* seq_lens, int32_t* positions, int rows, int dim,
-                   int dtype, void* stream);
+                   int32_t* seq_lens, int32_t* positions, const float* inv_freq,
+                   void* rope_cs, int half, int rows, int dim, int dtype, void* stream);
 
 /* residual += delta (if non-NULL) + sum_{s<nsplit} partials[s] (the fp32 K-split slabs
  * [nsplit][rows][dim] of SN_GEMM_PARTIAL, added in slab order: deterministic);
@@ -290,7 +293,8 @@ sn_status sn_gemm_decode_attn_in(const void* x, int M, int K, int ldx, const voi
                                  const int32_t* positions, const float* inv_freq, void* q_out,
                                  void* k_cache, void* v_cache, const int32_t* block_table,
                                  int Hq, int Hkv, int D, int page_size, int max_blocks,
-                                 int window, int32_t* err_flag, int dtype, void* stream);
+                                 int window, int32_t* err_flag, const void* rope_cs, int dtype,
+                                 void* stream);
 
 /* ---------------------------------------------------------------- fused decode chain
  * Everything between two mixer kernels of the decode step in ONE persistent launch
@@ -323,6 +327,7 @@ typedef struct {
   const int32_t* block_table;
   int Hq, Hkv, D, page_size, max_blocks, window;
   int32_t* err_flag;
+  const void* rope_cs;  /* optional (cos, sin) table from sn_embed */
   /* NORM: residual[M][dim] += sum of slabs partials[0..nsplit) (slab order; nsplit < 0: the K
    * splits of the latest PARTIAL GEMM phase before it); norm_out = rmsnorm(residual) * weight */
   const float* partials;

@@ -20,7 +20,7 @@ Fl = ctypes.c_float
 # name -> argtypes (restype is int status unless noted)
 SIGNATURES = {
     "sn_abi_version": [],
-    "sn_embed": [P, P, P, P, P, I, I, I, P],
+    "sn_embed": [P, P, P, P, P, P, P, I, I, I, I, P],
     "sn_add_rmsnorm": [P, P, I, P, P, P, I, I, Fl, I, P],
     "sn_argmax": [P, I, I, P, P, I, P],
     "sn_swiglu_il": [P, I, P, I, I, I, I, P],
@@ -44,7 +44,7 @@ SIGNATURES = {
     "sn_gemm_decode_plan": [I, I, I, I, P],
     "sn_gemm_decode_tune": [I, I, I, I],
     "sn_gemm_decode": [P, I, I, I, P, I, I, P, I, I, P, I, P],
-    "sn_gemm_decode_attn_in": [P, I, I, I, P, I, P, P, P, P, P, P, I, I, I, I, I, I, P, I, P],
+    "sn_gemm_decode_attn_in": [P, I, I, I, P, I, P, P, P, P, P, P, I, I, I, I, I, I, P, P, I, P],
     "sn_decode_chain": [P, I, I, P, P],
     "sn_gemm_prefill": [P, I, I, I, P, I, I, P, I, I, I, P],
     "sn_decode_chain_trace": [P],
@@ -58,6 +58,7 @@ class ChainPhase(ctypes.Structure):
         ("x", P), ("K", I), ("ldx", I), ("w", P), ("N", I), ("ldw", I), ("out", P), ("ldo", I), ("mode", I),
         ("positions", P), ("inv_freq", P), ("q_out", P), ("k_cache", P), ("v_cache", P), ("block_table", P),
         ("Hq", I), ("Hkv", I), ("D", I), ("page_size", I), ("max_blocks", I), ("window", I), ("err_flag", P),
+        ("rope_cs", P),
         ("partials", P), ("nsplit", I), ("residual", P), ("weight", P), ("norm_out", P), ("dim", I), ("eps", Fl),
         ("ss_out", P), ("ss_in", P), ("n_ss", I), ("splits", I),
     ]

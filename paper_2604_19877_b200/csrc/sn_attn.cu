@@ -11,6 +11,18 @@
 
 namespace sn {
 
+// two adjacent elements <-> float2 (one 4-byte access for bf16, 8 for fp32)
+template <typename T> __device__ __forceinline__ float2 bf2_or_f2(const T* p);
+template <> __device__ __forceinline__ float2 bf2_or_f2<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+template <> __device__ __forceinline__ float2 bf2_or_f2<float>(const float* p) { return *reinterpret_cast<const float2*>(p); }
+template <typename T> __device__ __forceinline__ void st2(T* p, float a, float b);
+template <> __device__ __forceinline__ void st2<__nv_bfloat16>(__nv_bfloat16* p, float a, float b) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+template <> __device__ __forceinline__ void st2<float>(float* p, float a, float b) { *reinterpret_cast<float2*>(p) = make_float2(a, b); }
+
 // ------------------------------------------------------------------ RoPE + append
 // grid (rows, Hq + 2*Hkv): one CTA per (row, head); heads < Hq are query heads
 // (rotate, write q_out), the next Hkv are key heads (rotate, append to the cache),
@@ -90,7 +102,10 @@ __global__ void rope_kv_append_kernel(const T* __restrict__ qkv, const int32_t* 
                  Hkv, D, page_size, max_blocks, window, blockIdx.x, blockIdx.y, threadIdx.x, pair_il);
 }
 
-// Prefill (many rows): a 256-thread CTA per row loops over every (head, pair) of the row.
+// Prefill (many rows): a 256-thread CTA per row.  The rotation angles depend only on the
+// position and the pair index, so the row's D/2 (cos, sin) pairs are computed once into shared
+// memory (not once per head: 40 of them at Apriel widths); each thread then rotates two
+// adjacent pairs of one head per step with 8-byte loads and 4-byte stores.
 template <typename T>
 __global__ void __launch_bounds__(256) rope_kv_append_rows_kernel(
     const T* __restrict__ qkv, const int32_t* __restrict__ row_seq, const int32_t* __restrict__ row_pos,
@@ -100,10 +115,60 @@ __global__ void __launch_bounds__(256) rope_kv_append_rows_kernel(
     int pair_il) {
   sn::pdl_launch_dependents();
   sn::pdl_wait();
-  const int half = D / 2, n = (Hq + 2 * Hkv) * half;
-  for (int idx = threadIdx.x; idx < n; idx += blockDim.x)
-    rope_kv_one<T>(qkv, row_seq, row_pos, seq_lens, inv_freq, q_out, k_out, v_out, k_cache, v_cache, block_table,
-                   Hq, Hkv, D, page_size, max_blocks, window, blockIdx.x, idx / half, idx % half, pair_il);
+  __shared__ float s_cs[64], s_sn[64];
+  const int half = D / 2, r = blockIdx.x;
+  const int seq = row_seq ? row_seq[r] : r;
+  const int pos = row_pos[r];
+  if ((int)threadIdx.x < half) sincosf((float)pos * inv_freq[threadIdx.x], &s_sn[threadIdx.x], &s_cs[threadIdx.x]);
+  __syncthreads();
+  const int slot = window > 0 ? pos % window : pos;
+  const bool write = !(window > 0 && seq_lens != nullptr && pos < seq_lens[seq] - window) && pos >= 0 &&
+                     slot / page_size < max_blocks;
+  const int page = write ? block_table[(size_t)seq * max_blocks + slot / page_size] : 0;
+  const int npp = half / 2;  // pairs of adjacent rotation pairs per head
+  const int n = (Hq + 2 * Hkv) * npp;
+  const T* row = qkv + (size_t)r * (Hq + 2 * Hkv) * D;
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int head = idx / npp, i = (idx - head * npp) * 2;  // pairs i, i + 1
+    const T* src = row + (size_t)head * D;
+    float y1[2], y2[2];
+    if (head >= Hq + Hkv) {  // value head: plain copy of dims (i, i+1) and (i + D/2, +1)
+      const float2 a = bf2_or_f2<T>(src + i), c = bf2_or_f2<T>(src + i + half);
+      y1[0] = a.x; y1[1] = a.y; y2[0] = c.x; y2[1] = c.y;
+    } else {
+      float x1[2], x2[2];
+      if (pair_il) {  // columns 2i, 2i+1, 2i+2, 2i+3 = (x1, x2) of pair i, then of pair i+1
+        const float2 a = bf2_or_f2<T>(src + 2 * i), c = bf2_or_f2<T>(src + 2 * i + 2);
+        x1[0] = a.x; x2[0] = a.y; x1[1] = c.x; x2[1] = c.y;
+      } else {
+        const float2 a = bf2_or_f2<T>(src + i), c = bf2_or_f2<T>(src + i + half);
+        x1[0] = a.x; x1[1] = a.y; x2[0] = c.x; x2[1] = c.y;
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float cs = s_cs[i + e], sn = s_sn[i + e];
+        y1[e] = x1[e] * cs - x2[e] * sn;
+        y2[e] = x2[e] * cs + x1[e] * sn;
+      }
+    }
+    T* dst;
+    if (head < Hq) {
+      dst = q_out + ((size_t)r * Hq + head) * D;
+    } else {
+      const bool is_k = head < Hq + Hkv;
+      const int hk = is_k ? head - Hq : head - Hq - Hkv;
+      T* extra = is_k ? k_out : v_out;
+      if (extra) {
+        T* e2 = extra + ((size_t)r * Hkv + hk) * D;
+        st2<T>(e2 + i, y1[0], y1[1]);
+        st2<T>(e2 + i + half, y2[0], y2[1]);
+      }
+      if (!write) continue;
+      dst = (is_k ? k_cache : v_cache) + (((size_t)page * Hkv + hk) * page_size + slot % page_size) * D;
+    }
+    st2<T>(dst + i, y1[0], y1[1]);
+    st2<T>(dst + i + half, y2[0], y2[1]);
+  }
 }
 
 // ------------------------------------------------------------------ CUDA-core decode
@@ -275,7 +340,7 @@ sn_status sn_rope_kv_append(const void* qkv, const int32_t* row_seq, const int32
                             void* v_out, void* k_cache, void* v_cache, const int32_t* block_table, int rows,
                             int Hq, int Hkv, int D, int page_size, int max_blocks, int window, int pair_il,
                             int dtype, void* stream) {
-  SN_REQUIRE(rows > 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0 && D % 2 == 0, "sn_rope_kv_append: bad shape");
+  SN_REQUIRE(rows > 0 && Hq > 0 && Hkv > 0 && Hq % Hkv == 0 && D % 4 == 0 && D <= 128, "sn_rope_kv_append: bad shape");
   SN_REQUIRE(page_size > 0 && (window == 0 || window % page_size == 0),
              "sn_rope_kv_append: window %d must be a multiple of page_size %d", window, page_size);
   SN_REQUIRE(qkv && row_pos && inv_freq && q_out && k_cache && v_cache && block_table,

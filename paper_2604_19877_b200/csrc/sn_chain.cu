@@ -463,6 +463,7 @@ g.br = pl.br; g.nblocks = pl.nblocks; g.splits = pl.splits; g.ks = pl.ks; g.ku =
       g.e.positions = c.positions; g.e.inv_freq = c.inv_freq; g.e.q_out = c.q_out; g.e.k_cache = c.k_cache;
       g.e.v_cache = c.v_cache; g.e.block_table = c.block_table; g.e.Hq = c.Hq; g.e.Hkv = c.Hkv; g.e.D = c.D;
       g.e.page_size = c.page_size; g.e.max_blocks = c.max_blocks; g.e.window = c.window; g.e.err = c.err_flag;
+      g.e.rope_cs = reinterpret_cast<const float2*>(c.rope_cs);
       SN_REQUIRE(c.ss_out == nullptr || c.mode == SN_GEMM_RESID, "sn_decode_chain: phase %d: ss_out needs RESID", i);
       g.e.ss_out = c.ss_out;
       if (c.ss_out) last_ss_blocks = pl.nblocks;

@@ -479,7 +479,8 @@ sn_status sn_gemm_decode(const void* x, int M, int K, int ldx, const void* w, in
 sn_status sn_gemm_decode_attn_in(const void* x, int M, int K, int ldx, const void* w, int ldw,
                                  const int32_t* positions, const float* inv_freq, void* q_out, void* k_cache,
                                  void* v_cache, const int32_t* block_table, int Hq, int Hkv, int D, int page_size,
-                                 int max_blocks, int window, int32_t* err_flag, int dtype, void* stream) {
+                                 int max_blocks, int window, int32_t* err_flag, const void* rope_cs, int dtype,
+                                 void* stream) {
   const int N = (Hq + 2 * Hkv) * D;
   sn_status s = check_common(x, M, K, ldx, w, N, ldw, dtype);
   if (s != SN_OK) return s;
@@ -504,6 +505,7 @@ sn_status sn_gemm_decode_attn_in(const void* x, int M, int K, int ldx, const voi
   ea.max_blocks = max_blocks;
   ea.window = window;
   ea.err = err_flag;
+  ea.rope_cs = reinterpret_cast<const float2*>(rope_cs);
   return dgemm::run(x, M, K, ldx, w, N, ldw, ea, nullptr, dtype, (cudaStream_t)stream);
 }
 

@@ -36,6 +36,7 @@ struct Args {
   const int32_t* block_table;
   int Hq, Hkv, D, page_size, max_blocks, window;
   int32_t* err;  // set to 1 when a position falls outside the block table (nothing is written)
+  const float2* rope_cs;  // ATTN_IN: the step's (cos, sin) per (row, rotary pair) from sn_embed (NULL: sincosf)
   float* ss_out;  // RESID: per-row sum of squares of the updated residual over this block's columns,
                   // [block][M] (the fused chain's next RMSNorm sums the blocks in order)
 };
@@ -146,7 +147,13 @@ __device__ __forceinline__ void finalize(const Args& a, int m, bool row_ok, int 
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           float sn, cs;
-          sincosf((float)pos * a.inv_freq[p0 + e], &sn, &cs);
+          if (a.rope_cs) {
+            const float2 t = a.rope_cs[(size_t)m * half + p0 + e];
+            cs = t.x;
+            sn = t.y;
+          } else {
+            sincosf((float)pos * a.inv_freq[p0 + e], &sn, &cs);
+          }
           const float x1 = v[2 * e], x2 = v[2 * e + 1];
           lo[e] = x1 * cs - x2 * sn;
           hi[e] = x2 * cs + x1 * sn;

@@ -37,23 +37,34 @@ sn_status check_launch(const char* what) {
 template <typename T>
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __restrict__ table,
                              float* __restrict__ residual, int32_t* seq_lens, int32_t* positions,
-                             int rows, int dim) {
+                             const float* __restrict__ inv_freq, float2* __restrict__ rope_cs, int half, int rows,
+                             int dim) {
   sn::pdl_launch_dependents();
   sn::pdl_wait();
+  __shared__ int s_pos;
   const int r = blockIdx.x;
-  if (seq_lens != nullptr && r == 0) {
-    for (int b = threadIdx.x; b < rows; b += blockDim.x) {
-      if (tokens[b] < 0) {  // idle slot (continuous batching): no position, the length stays
-        positions[b] = -1;
-        continue;
+  const int tok = tokens[r];
+  if (seq_lens != nullptr) {  // decode-step prologue: CTA r owns row r's bookkeeping
+    if (threadIdx.x == 0) {
+      int L = -1;  // idle slot (continuous batching): no position, the length stays
+      if (tok >= 0) {
+        L = seq_lens[r];
+        seq_lens[r] = L + 1;
       }
-      int L = seq_lens[b];
-      positions[b] = L;
-      seq_lens[b] = L + 1;
+      positions[r] = L;
+      s_pos = L;
+    }
+    if (rope_cs != nullptr) {  // the step's rotary (cos, sin) per pair, for the fused in-projection epilogue
+      __syncthreads();
+      const int pos = s_pos;
+      for (int t = threadIdx.x; t < half; t += blockDim.x) {
+        float sn = 0.f, cs = 1.f;
+        if (pos >= 0) sincosf((float)pos * inv_freq[t], &sn, &cs);
+        rope_cs[(size_t)r * half + t] = make_float2(cs, sn);
+      }
     }
   }
   float* dst = residual + (size_t)r * dim;
-  const int tok = tokens[r];
   if (tok < 0) {  // idle slot: a zero row (its outputs are ignored; nothing is appended)
     for (int i = threadIdx.x * 4; i < dim; i += blockDim.x * 4) *reinterpret_cast<float4*>(dst + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
@@ -276,12 +287,15 @@ const char* sn_last_error(void) { return sn::g_err; }
 int sn_abi_version(void) { return SN_ABI_VERSION; }
 
 sn_status sn_embed(const int32_t* tokens, const void* table, float* residual, int32_t* seq_lens,
-                   int32_t* positions, int rows, int dim, int dtype, void* stream) {
+                   int32_t* positions, const float* inv_freq, void* rope_cs, int half, int rows, int dim, int dtype,
+                   void* stream) {
   SN_REQUIRE(rows > 0 && dim > 0 && dim % 8 == 0, "sn_embed: bad shape rows=%d dim=%d", rows, dim);
   SN_REQUIRE((seq_lens == nullptr) == (positions == nullptr), "sn_embed: seq_lens/positions must be both set or both NULL");
+  SN_REQUIRE(rope_cs == nullptr || (inv_freq != nullptr && half > 0 && seq_lens != nullptr),
+             "sn_embed: the rotary table needs inv_freq, half > 0 and the decode prologue");
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
     launch_pdl(embed_kernel<T>, dim3(rows), dim3(128), 0, (cudaStream_t)stream, tokens, (const T*)table, residual,
-               seq_lens, positions, rows, dim);
+               seq_lens, positions, inv_freq, (float2*)rope_cs, half, rows, dim);
     return check_launch("sn_embed");
   });
 }

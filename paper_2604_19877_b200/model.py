@@ -206,6 +206,8 @@ class Supernet:
             self.dec["q"] = e(B, Hq, D)
             self.dec["attn"] = e(B, Hq * D)
             self.dec["counters"] = torch.zeros(B * Hkv, device=dev, dtype=torch.int32)
+            # the step's rotary (cos, sin) per (slot, pair), written by the embed kernel
+            self.dec["rope_cs"] = e(B, D // 2, 2, d=torch.float32)
             self.attn_split = {}
             for kind, max_keys in ((FA, self.max_len), (SWA, cfg.window)):
                 if kind in kinds:
@@ -239,7 +241,7 @@ class Supernet:
         # in-projection with RoPE + the KV append fused into its epilogue
         self._probe_begin("gemm_in_proj", fine=True)
         ops.gemm_decode_attn_in(h, w["qkv_il"], self.positions, self.inv_freq, d["q"], st["k"], st["v"], bt, Hq, Hkv,
-                                D, P, window, self.err_flag)
+                                D, P, window, self.err_flag, rope_cs=d["rope_cs"])
         self._probe_end("gemm_in_proj", fine=True)
         sp, _ = self.attn_split[kind]
         name = "swa_decode" if kind == SWA else "fa_decode"
@@ -318,7 +320,8 @@ class Supernet:
             return self._decode_body_chain()
         w = self.w
         self._probe_begin("embed", fine=True)
-        ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
+        ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions, self.inv_freq,
+                  self.dec.get("rope_cs"))
         self._probe_end("embed", fine=True)
         pending = None
         for l, kind in enumerate(self.kinds):
@@ -349,7 +352,8 @@ class Supernet:
                                    inv_freq=self.inv_freq, q_out=d["q"], k_cache=st["k"], v_cache=st["v"],
                                    block_table=self.swa_block_table if kind == SWA else self.fa_block_table,
                                    Hq=cfg.n_q_heads, Hkv=cfg.n_kv_heads, D=cfg.head_dim, page_size=cfg.page_size,
-                                   window=cfg.window if kind == SWA else 0, err_flag=self.err_flag)]
+                                   window=cfg.window if kind == SWA else 0, err_flag=self.err_flag,
+                                   rope_cs=d["rope_cs"])]
         if kind == GDN:
             return [ops.chain_gemm(self.h, w["w_in"], d["gdn_proj"], "store")]
         H, D, R = cfg.kda_heads, cfg.kda_head_dim, cfg.kda_rank
@@ -401,7 +405,8 @@ class Supernet:
         w, cfg, L = self.w, self.cfg, len(self.kinds)
         layers = w["layers"]
         self._probe_begin("embed", fine=True)
-        ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions)
+        ops.embed(self.step_tokens, w["embed"], self.residual, self.seq_lens, self.positions, self.inv_freq,
+                  self.dec.get("rope_cs"))
         self._probe_end("embed", fine=True)
         self._chain(0, [ops.chain_norm(self.residual, layers[0]["norm1"], self.h, cfg.norm_eps)]
                     + self._in_proj_phases(0))

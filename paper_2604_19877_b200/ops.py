@@ -36,10 +36,13 @@ def _s():
     return torch.cuda.current_stream().cuda_stream
 
 
-def embed(tokens, table, residual, seq_lens=None, positions=None):
+def embed(tokens, table, residual, seq_lens=None, positions=None, inv_freq=None, rope_cs=None):
+    """residual = table[tokens]; with seq_lens / positions the decode-step prologue; rope_cs
+    ([rows, D/2, 2] fp32) also receives the step's rotary (cos, sin) table."""
     assert tokens.dtype == torch.int32 and residual.dtype == torch.float32
-    call("sn_embed", _p(tokens), _p(table), _p(residual), _p(seq_lens), _p(positions), tokens.numel(),
-         table.shape[1], dtype_code(table.dtype), _s())
+    half = rope_cs.shape[1] if rope_cs is not None else 0
+    call("sn_embed", _p(tokens), _p(table), _p(residual), _p(seq_lens), _p(positions), _p(inv_freq), _p(rope_cs),
+         half, tokens.numel(), table.shape[1], dtype_code(table.dtype), _s())
 
 
 def add_rmsnorm(delta, residual, weight, out, eps, partials=None, nsplit=0):
@@ -210,12 +213,13 @@ def gemm_decode(x, w, out, mode):
 
 
 def gemm_decode_attn_in(x, w, positions, inv_freq, q_out, k_cache, v_cache, block_table, Hq, Hkv, D, page_size,
-                        window, err_flag):
-    """Attention in-projection with RoPE + KV append fused; w in rope_pair_interleave order."""
+                        window, err_flag, rope_cs=None):
+    """Attention in-projection with RoPE + KV append fused; w in rope_pair_interleave order;
+    rope_cs: the step's (cos, sin) table from embed (default: evaluated per head)."""
     M, K = x.shape
     call("sn_gemm_decode_attn_in", _p(x), M, K, x.stride(0), _p(w), w.stride(0), _p(positions), _p(inv_freq),
          _p(q_out), _p(k_cache), _p(v_cache), _p(block_table), Hq, Hkv, D, page_size, block_table.shape[1], window,
-         _p(err_flag), dtype_code(x.dtype), _s())
+         _p(err_flag), _p(rope_cs), dtype_code(x.dtype), _s())
 
 
 def chunk_plan(cu_seqlens_host, chunk=64, device="cuda"):
@@ -297,7 +301,7 @@ def chain_gemm(x, w, out, mode, depends=True, ss_out=None, **attn):
                   inv_freq=_p(attn["inv_freq"]), q_out=_p(attn["q_out"]), k_cache=_p(attn["k_cache"]),
                   v_cache=_p(attn["v_cache"]), block_table=_p(bt), Hq=attn["Hq"], Hkv=attn["Hkv"], D=attn["D"],
                   page_size=attn["page_size"], max_blocks=bt.shape[1], window=attn["window"],
-                  err_flag=_p(attn.get("err_flag")))
+                  err_flag=_p(attn.get("err_flag")), rope_cs=_p(attn.get("rope_cs")))
     else:
         assert out.dtype == (torch.float32 if mode in ("resid", "partial") else torch.bfloat16)
         if mode == "partial":
