@@ -208,6 +208,13 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & kPeerMask), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_2sm_nh(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & kPeerMask)
+      : "memory");
+}
 __device__ __forceinline__ void umma2_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
@@ -287,8 +294,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (leader) mbar_expect_tx(&full_bar[s], 2 * stage);
           uint8_t* st = smem + s * stage;
-          tma_load_2d_2sm(st, &amap, k * BK, mt * 256 + (int)rank * 128, &full_bar[s], pa);
-          tma_load_2d_2sm(st + A_BYTES, &wmap, k * BK, nb * g.br + (int)rank * wr, &full_bar[s], pw);
+          if (g.pol & 8) {
+            tma_load_2d_2sm_nh(st, &amap, k * BK, mt * 256 + (int)rank * 128, &full_bar[s]);
+            tma_load_2d_2sm_nh(st + A_BYTES, &wmap, k * BK, nb * g.br + (int)rank * wr, &full_bar[s]);
+          } else {
+            tma_load_2d_2sm(st, &amap, k * BK, mt * 256 + (int)rank * 128, &full_bar[s], pa);
+            tma_load_2d_2sm(st + A_BYTES, &wmap, k * BK, nb * g.br + (int)rank * wr, &full_bar[s], pw);
+          }
           if (++s == kStages2) { s = 0; ph ^= 1; }
         }
       }
@@ -401,7 +413,10 @@ extern "C" sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const
   static const bool two = getenv("SN_PG2") && atoi(getenv("SN_PG2"));  // EXPERIMENT A/B
   if (two && br % 32 == 0) {
     CUtensorMap wm2, am2;
-    if (!tc::map_2d(&wm2, w, wrows, K, ldw, br / 2) || !tc::map_2d(&am2, a, M, K, lda, 128)) {
+    const int pe = getenv("SN_PG_PROMO") ? atoi(getenv("SN_PG_PROMO")) : 256;
+    const CUtensorMapL2promotion pr = pe == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : pe == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : pe == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (!tc::map_2d(&wm2, w, wrows, K, ldw, br / 2, pr) || !tc::map_2d(&am2, a, M, K, lda, 128, pr)) {
       set_error("sn_gemm_prefill: cuTensorMapEncodeTiled failed");
       return SN_ECUDA;
     }
@@ -411,7 +426,9 @@ extern "C" sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const
     g2.band = band2_env > 0 ? band2_env : 8;
     if (g2.mtiles * g2.nblocks < num_sms() / 2) g2.die = 0;
     const int tiles2 = g2.mtiles * g2.nblocks;
-    const int pairs = tiles2 < num_sms() / 2 ? tiles2 : num_sms() / 2;
+    const bool np = getenv("SN_PG2_NP") && atoi(getenv("SN_PG2_NP"));
+    const int pairs = np ? tiles2 : tiles2 < num_sms() / 2 ? tiles2 : num_sms() / 2;
+    if (np) g2.die = 0;
     const int smem2 = kStages2 * (128 + br / 2) * tc::BK * 2 + 1024;
     static bool attr2 = false;
     if (!attr2) {
