@@ -218,11 +218,12 @@ sn_status sn_gdn_chunk_prefill2(const void* qn, const void* kn, const void* qkv_
 /* Two-phase chunked KDA prefill: the same WY chunk form with a per-key-channel
  * gate (FLA naive_chunk_kda, 3P-FLA/ops/kda/naive.py:69-166).  Hk = Hv = H;
  * glog: fp32 [rows][H][D] per-channel log gates (sn_delta_prep kind 1 with glog);
+ * qn / kn: bf16 [rows][H][D] (TMA tiles; sn_delta_prep with qk_dtype SN_BF16);
  * workspace: sn_kda_chunk_workspace_bytes(num_chunks, H, D).  Replaces the
  * token-sequential sn_delta_scan(kind=1) for bf16 prompts.                      */
 size_t sn_kda_chunk_workspace_bytes(int num_chunks, int H, int D);
-sn_status sn_kda_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv,
-                                int v_off, int qkv_stride, const float* glog,
+sn_status sn_kda_chunk_prefill2(const void* qn, const void* kn, const void* qkv_conv,
+                                int v_off, int qkv_stride, int rows, const float* glog,
                                 const float* beta, const int32_t* chunks,
                                 const int32_t* seq_chunk0, int num_chunks, void* workspace,
                                 float* o, float* state, const int32_t* slot_idx,

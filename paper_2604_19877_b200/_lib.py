@@ -37,7 +37,7 @@ SIGNATURES = {
     "sn_kda_chunk_workspace_bytes": [I, I, I],
     "sn_tp_arrive": [P, P],
     "sn_tp_allreduce_add_rmsnorm": [P, P, I, I, I, P, P, P, I, I, Fl, I, P],
-    "sn_kda_chunk_prefill2": [P, P, P, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, P],
+    "sn_kda_chunk_prefill2": [P, P, P, I, I, I, P, P, P, P, I, P, P, P, P, I, I, I, I, I, P],
     "sn_delta_scan": [I, P, P, P, I, I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "sn_gated_rmsnorm": [P, P, I, P, P, I, I, I, Fl, I, I, P],
     "sn_gemm_swiglu_block": [I],

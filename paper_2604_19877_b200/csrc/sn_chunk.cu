@@ -90,71 +90,6 @@ __device__ __forceinline__ void invert_unit_lower(const float (*l)[C + 1], float
 }
 
 
-// Chunk-tile loaders with the global loads batched ahead of their conversions (one
-// dependent memory round trip per batch instead of one per element: the loops were the
-// top long-scoreboard stall of the intra kernels).
-// b o V tile [64][D] (bf16, row stride LDK) from the conv output rows c0.. (rows >= len zero).
-template <typename T, int D>
-__device__ __forceinline__ void load_vb_tile(const T* __restrict__ qkv, int qkv_stride, int v_off, int h, int c0,
-                                             int len, const float* beta_s, __nv_bfloat16* dst, int ldk) {
-  constexpr int IT = C * D / 8 / kThreads, BATCH = IT < 4 ? IT : 4;
-#pragma unroll
-  for (int i0 = 0; i0 < IT; i0 += BATCH) {
-    float v[BATCH][8];
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int idx = threadIdx.x + (i0 + u) * kThreads;
-      const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
-      if (r < len) load8<T>(qkv + (size_t)(c0 + r) * qkv_stride + v_off + h * D + c8, v[u]);
-      else
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int idx = threadIdx.x + (i0 + u) * kThreads;
-      const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
-      const float b = beta_s[r];
-      uint4 pk;
-      pk.x = pack_bf16(v[u][0] * b, v[u][1] * b);
-      pk.y = pack_bf16(v[u][2] * b, v[u][3] * b);
-      pk.z = pack_bf16(v[u][4] * b, v[u][5] * b);
-      pk.w = pack_bf16(v[u][6] * b, v[u][7] * b);
-      *reinterpret_cast<uint4*>(dst + r * ldk + c8) = pk;
-    }
-  }
-}
-
-// fp32 [rows][heads][D] row slices (head hh, rows c0.. < len, else zero) -> bf16 tile [64][D]
-// (row stride ldk); NSRC tensors loaded together.
-template <int D, int NSRC>
-__device__ __forceinline__ void load_f32_tiles(const float* const* src, int heads, int hh, int c0, int len,
-                                               __nv_bfloat16* const* dst, int ldk) {
-  constexpr int IT = C * D / 4 / kThreads, BATCH = IT < 4 ? IT : 4;
-#pragma unroll
-  for (int i0 = 0; i0 < IT; i0 += BATCH) {
-    float4 v[NSRC][BATCH];
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int idx = threadIdx.x + (i0 + u) * kThreads;
-      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
-#pragma unroll
-      for (int t = 0; t < NSRC; ++t)
-        v[t][u] = r < len ? *reinterpret_cast<const float4*>(src[t] + ((size_t)(c0 + r) * heads + hh) * D + c4)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int idx = threadIdx.x + (i0 + u) * kThreads;
-      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4;
-#pragma unroll
-      for (int t = 0; t < NSRC; ++t)
-        *reinterpret_cast<uint2*>(dst[t] + r * ldk + c4) =
-            make_uint2(pack_bf16(v[t][u].x, v[t][u].y), pack_bf16(v[t][u].z, v[t][u].w));
-    }
-  }
-}
-
 // =====================================================================================
 // Two-phase version (the long-prefill path): the chunk-local work (inverse, W, U, P and
 // the decayed operands) of all chunks runs in parallel, one CTA per (chunk, value head);
@@ -709,51 +644,93 @@ static sn_status launch_two_phase(const void* qb, const void* kb, const void* qk
 // 16-token sub-chunk) factorises the blocks left of its diagonal around its own
 // reference row r = 16w:
 //   e^{G_i - G_j} = e^{G_i - G_r} . e^{G_r - G_j},   e^{G_i - G_r} <= 1 (i >= r), e^{G_r - G_j} <= 1 (j < r)
-// — the left operand is the warp's own 16 rows, the right operand (the 16w rows j < r of K
-// scaled to reference r) a per-warp shared-memory tile, both products on mma.sync.  The
-// diagonal 16x16 block (r <= j <= i) is computed exactly in fp32 with e^{G_i - G_j} <= 1
+// The diagonal 16x16 block (r <= j <= i) is computed exactly in fp32 with e^{G_i - G_j} <= 1
 // per term (a factorised form would need e^{G_r - G_j} > 1, which overflows for strong
 // gates).
+//
 
+// On tcgen05 / TMEM, TMA-fed (one CTA of 4 warps per (chunk, head)): Q, K, V arrive as [64 x D]
+// tiles of 128B-swizzled [64 x 64] atoms.  The off-diagonal blocks of all three sub-chunks run
+// as two UMMAs (M = 64, N = 96) against one stacked right operand
+//   KL[i] = k_i o e^{G_i - G_r(i)},  QL[i] = q_i o e^{G_i - G_r(i)}   (r(i) = 16 floor(i / 16))
+//   KR    = [ k_j o e^{G_16 - G_j}, j < 16 ; k_j o e^{G_32 - G_j}, j < 32 ; k_j o e^{G_48 - G_j}, j < 48 ]
+// so row i of KL KR^T holds, in the 16 r(i) columns of its own reference block, the factorised
+// A_kk[i][j] of every j < r(i) (all exponents <= 0).  The diagonal blocks stay exact fp32 on the
+// CUDA cores.  Then W = T1 (e^G o K), U = T1 V with T1 = T diag(b) (the CTA writes T1 and
+// e^G o K swizzled; V is the TMA tile).  Rows past the chunk length hold whatever the TMA box
+// covers: b = 0 there (zero columns of T1), and P / Qg / Kd mask them.
 template <int D>
-struct KdaIntraSmem {
-  static constexpr int LDK = D + 8, LDC = C + 8;
-  static constexpr int KR_ROWS = 16 * (0 + 1 + 2 + 3);  // per-warp right operands (rows j < 16w)
-  __nv_bfloat16 q[C * LDK];
-  __nv_bfloat16 k[C * LDK];
-  union {
-    struct { __nv_bfloat16 ql[C * LDK]; __nv_bfloat16 kl[C * LDK]; } a;  // A step: left operands
-    struct { __nv_bfloat16 kb[C * LDK]; __nv_bfloat16 vb[C * LDK]; } w;  // W/U step
-  } u1;
-  union {
-    __nv_bfloat16 kr[KR_ROWS * LDK];
-    struct { float l[C][C + 1]; float x[C][C + 1]; } lx;
-  } u2;
-  __nv_bfloat16 t[C * LDC];
+struct KdaTcSmem {
+  static constexpr int AT = 64 * 128;  // [64 rows x 64 bf16] 128B-swizzled atom
+  static constexpr int RT = 96 * 128;  // the stacked right operand's atom: 96 rows
+  static constexpr int NA = D / 64;
+  uint8_t q[NA * AT];
+  uint8_t k[NA * AT];
+  uint8_t v[NA * AT];
+  uint8_t ql[NA * AT];
+  uint8_t kl[NA * AT];
+  uint8_t kr[NA * RT];
+  uint8_t kg[NA * AT];  // e^G o K (B of W, MN-major)
+  uint8_t t1[AT];
+  float l[C][C + 1];
+  float x[C][C + 1];
   float scr[4 * 16 * 17];
-  float g[C * D];  // G[r][d]: cumulative log decay
+  float g[C * D];  // G[r][d]: in-chunk cumulative log decay
   float beta[C];
+  uint64_t bar_qk, bar_v, bar_m1, bar_m2;
+  uint32_t tmem_base;
 };
 
-template <typename T, int D>
+// byte offset of (r, c) in a tile of 128B-swizzled [rows x 64] atoms of `atom` bytes
+__device__ __forceinline__ uint32_t sw_off_a(int r, int c, int atom) {
+  const int cc = c & 63;
+  return (c >> 6) * atom + r * 128 + ((((cc >> 3) ^ (r & 7)) & 7) << 4) + ((cc & 7) << 1);
+}
+
+template <int D>
 __global__ void __launch_bounds__(kThreads)
-    kda_chunk_intra_kernel(const float* __restrict__ qn, const float* __restrict__ kn, const T* __restrict__ qkv,
-                           int v_off, int qkv_stride, const float* __restrict__ glog, const float* __restrict__ beta,
-                           const int32_t* __restrict__ chunks, __nv_bfloat16* __restrict__ ws,
-                           float* __restrict__ glast, int H) {
+    kda_chunk_intra_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                              const __grid_constant__ CUtensorMap vmap, int v_off, const float* __restrict__ glog,
+                              const float* __restrict__ beta, const int32_t* __restrict__ chunks,
+                              __nv_bfloat16* __restrict__ ws, float* __restrict__ glast, int H) {
   pdl_launch_dependents();
-  using SM = KdaIntraSmem<D>;
-  constexpr int LDK = SM::LDK, LDC = SM::LDC;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  using SM = KdaTcSmem<D>;
+  constexpr int AT = SM::AT, RT = SM::RT, NA = SM::NA;
+  constexpr uint32_t kCols = 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g4 = lane >> 2, t4 = lane & 3;
   const int n = blockIdx.x, h = blockIdx.y;
+  if (tid == 0) {
+    tc::mbar_init(&sm.bar_qk, 1);
+    tc::mbar_init(&sm.bar_v, 1);
+    tc::mbar_init(&sm.bar_m1, 1);
+    tc::mbar_init(&sm.bar_m2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&sm.tmem_base)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  pdl_wait();
   const int c0 = chunks[2 * n], len = chunks[2 * n + 1];
-  {
-    const float* src[2] = {qn, kn};
-    __nv_bfloat16* dst[2] = {sm.q, sm.k};
-    load_f32_tiles<D, 2>(src, H, h, c0, len, dst, LDK);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  if (tid == 0) {
+    const uint64_t pol = tc::policy_evict_first();
+    tc::mbar_expect_tx(&sm.bar_qk, 2 * NA * AT);
+    for (int a = 0; a < NA; ++a) {
+      tc::tma_load_2d(sm.q + a * AT, &qmap, h * D + 64 * a, c0, &sm.bar_qk, pol);
+      tc::tma_load_2d(sm.k + a * AT, &kmap, h * D + 64 * a, c0, &sm.bar_qk, pol);
+    }
+    tc::mbar_expect_tx(&sm.bar_v, NA * AT);
+    for (int a = 0; a < NA; ++a) tc::tma_load_2d(sm.v + a * AT, &vmap, v_off + h * D + 64 * a, c0, &sm.bar_v, pol);
+  }
+  {  // per-channel log decays (rows past the chunk: 0, so G stays flat there)
     constexpr int IT = C * D / 4 / kThreads;
     float4 gv[IT];
 #pragma unroll
@@ -771,7 +748,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (tid < C) sm.beta[tid] = tid < len ? beta[(size_t)(c0 + tid) * H + h] : 0.f;
   __syncthreads();
-  for (int d = tid; d < D; d += kThreads) {  // per-channel prefix sum over the chunk
+  for (int d = tid; d < D; d += kThreads) {  // in-chunk cumulative sum per channel
     float acc = 0.f;
 #pragma unroll 8
     for (int r = 0; r < C; ++r) {
@@ -780,67 +757,99 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   __syncthreads();
-  // ---- per-warp operands around reference row r0 = 16 * warp (off-diagonal blocks j < r0)
-  const int r0 = 16 * warp, nrows = 16 * warp;
-  __nv_bfloat16* kr = sm.u2.kr + 16 * (warp * (warp - 1) / 2) * LDK;
-  for (int idx = lane; idx < 16 * D / 2; idx += 32) {
-    const int r = r0 + idx / (D / 2), cc = (idx % (D / 2)) * 2;
-    const float e0 = expf(sm.g[r * D + cc] - sm.g[r0 * D + cc]), e1 = expf(sm.g[r * D + cc + 1] - sm.g[r0 * D + cc + 1]);
-    const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[r * LDK + cc]));
-    const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[r * LDK + cc]));
-    *reinterpret_cast<uint32_t*>(&sm.u1.a.ql[r * LDK + cc]) = pack_bf16(qv.x * e0, qv.y * e1);
-    *reinterpret_cast<uint32_t*>(&sm.u1.a.kl[r * LDK + cc]) = pack_bf16(kv.x * e0, kv.y * e1);
-  }
-  for (int idx = lane; idx < nrows * D / 2; idx += 32) {
-    const int j = idx / (D / 2), cc = (idx % (D / 2)) * 2;
-    const float e0 = expf(sm.g[r0 * D + cc] - sm.g[j * D + cc]), e1 = expf(sm.g[r0 * D + cc + 1] - sm.g[j * D + cc + 1]);
-    const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[j * LDK + cc]));
-    *reinterpret_cast<uint32_t*>(&kr[j * LDK + cc]) = pack_bf16(kv.x * e0, kv.y * e1);
-  }
-  __syncwarp();
-  float kk[8][4], qk[8][4];
+  tc::mbar_wait(&sm.bar_qk, 0);
+  // left operands (row i to its sub-chunk reference) and e^G o K, 8 columns per step
+  for (int idx = tid; idx < C * D / 8; idx += kThreads) {
+    const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8, rr = r & ~15;
+    const uint32_t o = sw_off_a(r, c8, AT);
+    const uint4 qv = *reinterpret_cast<const uint4*>(sm.q + o);
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + o);
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(&qv);
+    const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
+    uint4 qo, ko, go;
+    uint32_t* qoa = reinterpret_cast<uint32_t*>(&qo);
+    uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
+    uint32_t* goa = reinterpret_cast<uint32_t*>(&go);
+    const float* gr = sm.g + r * D + c8;
+    const float* g0 = sm.g + rr * D + c8;
 #pragma unroll
-  for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) kk[nt][e] = qk[nt][e] = 0.f;
-#pragma unroll
-  for (int ks = 0; ks < D; ks += 16) {
-    uint32_t ak[4], aq[4];
-    lda(sm.u1.a.kl, LDK, r0, ks, ak);
-    lda(sm.u1.a.ql, LDK, r0, ks, aq);
-#pragma unroll
-    for (int nt = 0; nt < 8; nt += 2) {
-      if (nt * 8 < nrows) {  // warp-uniform: only the column blocks left of the diagonal block
-        uint32_t b0, b1, b2, b3;
-        ldb_nk(kr, LDK, nt * 8, ks, b0, b1, b2, b3);
-        mma_bf16(kk[nt], ak, b0, b1);
-        mma_bf16(kk[nt + 1], ak, b2, b3);
-        mma_bf16(qk[nt], aq, b0, b1);
-        mma_bf16(qk[nt + 1], aq, b2, b3);
-      }
+    for (int e = 0; e < 4; ++e) {
+      const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
+      const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+      const float e0 = expf(gr[2 * e] - g0[2 * e]), e1 = expf(gr[2 * e + 1] - g0[2 * e + 1]);
+      qoa[e] = pack_bf16(qf.x * e0, qf.y * e1);
+      koa[e] = pack_bf16(kf.x * e0, kf.y * e1);
+      goa[e] = pack_bf16(kf.x * expf(gr[2 * e]), kf.y * expf(gr[2 * e + 1]));
     }
+    *reinterpret_cast<uint4*>(sm.ql + o) = qo;
+    *reinterpret_cast<uint4*>(sm.kl + o) = ko;
+    *reinterpret_cast<uint4*>(sm.kg + o) = go;
   }
-  // diagonal block, exact: pairs (i, j) = (r0 + a, r0 + b), 0 <= b <= a < 16, 136 per warp
+  // the stacked right operand: block s (s = 1, 2, 3) = rows j < 16 s scaled to reference 16 s
+  for (int idx = tid; idx < 96 * D / 8; idx += kThreads) {
+    const int row = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
+    const int s = row < 16 ? 1 : row < 48 ? 2 : 3;
+    const int j = row - (s == 1 ? 0 : s == 2 ? 16 : 48), rr = 16 * s;
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + sw_off_a(j, c8, AT));
+    const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
+    uint4 ko;
+    uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
+    const float* gj = sm.g + j * D + c8;
+    const float* g0 = sm.g + rr * D + c8;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+      koa[e] = pack_bf16(kf.x * expf(g0[2 * e] - gj[2 * e]), kf.y * expf(g0[2 * e + 1] - gj[2 * e + 1]));
+    }
+    *reinterpret_cast<uint4*>(sm.kr + sw_off_a(row, c8, RT)) = ko;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's reads
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {  // KL KR^T -> TMEM [0, 96), QL KR^T -> [96, 192)
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t sq = tc::smem_u32(sm.ql), sk = tc::smem_u32(sm.kl), sr = tc::smem_u32(sm.kr);
+    const uint32_t id = tc::idesc_bf16(64, 96);
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint32_t off = (kk >> 2) * AT + (kk & 3) * 32, roff = (kk >> 2) * RT + (kk & 3) * 32;
+      tc::umma_w(tmem, tc::desc_sw128(sk + off), tc::desc_sw128(sr + roff), id, kk > 0 ? 1u : 0u);
+      tc::umma_w(tmem + 96, tc::desc_sw128(sq + off), tc::desc_sw128(sr + roff), id, kk > 0 ? 1u : 0u);
+    }
+    tc::commit_w(&sm.bar_m1);
+  }
+  __nv_bfloat16* rec = ws + ws_tile<D>(n, h, H);
+  __nv_bfloat16* wW = rec;
+  __nv_bfloat16* wQg = rec + C * D;
+  __nv_bfloat16* wKd = rec + 2 * C * D;
+  __nv_bfloat16* wU = rec + 3 * C * D;
+  __nv_bfloat16* wP = rec + 4 * C * D;
+  // diagonal blocks, exact: pairs (i, j) = (r0 + a, r0 + b), 0 <= b <= a < 16, 136 per warp
+  const int r0 = 16 * warp;
   constexpr int kPairs = 136, kPerLane = (kPairs + 31) / 32;
   float dkk[kPerLane], dqk[kPerLane];
+  int di[kPerLane], dj[kPerLane];
 #pragma unroll
   for (int u = 0; u < kPerLane; ++u) {
     const int p = lane + 32 * u;
     dkk[u] = dqk[u] = 0.f;
+    di[u] = dj[u] = -1;
     if (p < kPairs) {
       int a = (int)((sqrtf(8.f * p + 1.f) - 1.f) * 0.5f);
       if ((a + 1) * (a + 2) / 2 <= p) ++a;
       if (a * (a + 1) / 2 > p) --a;
       const int b = p - a * (a + 1) / 2;
       const int i = r0 + a, j = r0 + b;
+      di[u] = i;
+      dj[u] = j;
       const float* gi = sm.g + i * D;
       const float* gj = sm.g + j * D;
       float sk = 0.f, sq = 0.f;
 #pragma unroll 4
       for (int d = 0; d < D; d += 2) {
-        const float2 ki = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[i * LDK + d]));
-        const float2 qi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[i * LDK + d]));
-        const float2 kj = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[j * LDK + d]));
+        const float2 ki = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.k + sw_off_a(i, d, AT)));
+        const float2 qi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.q + sw_off_a(i, d, AT)));
+        const float2 kj = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.k + sw_off_a(j, d, AT)));
         const float e0 = expf(gi[d] - gj[d]) * kj.x, e1 = expf(gi[d + 1] - gj[d + 1]) * kj.y;
         sk += ki.x * e0 + ki.y * e1;
         sq += qi.x * e0 + qi.y * e1;
@@ -849,112 +858,168 @@ __global__ void __launch_bounds__(kThreads)
       dqk[u] = sq;
     }
   }
-  __syncthreads();  // every warp is done with kr before l / x (aliased) are written
-  __nv_bfloat16* rec = ws + ws_tile<D>(n, h, H);
-  __nv_bfloat16* wW = rec;
-  __nv_bfloat16* wQg = rec + C * D;
-  __nv_bfloat16* wKd = rec + 2 * C * D;
-  __nv_bfloat16* wU = rec + 3 * C * D;
-  __nv_bfloat16* wP = rec + 4 * C * D;
+  // e^G o Q and e^{G_C - G} o K -> workspace (state pass operands); the chunk's last decays
+  for (int idx = tid; idx < C * D / 8; idx += kThreads) {
+    const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
+    const uint32_t o = sw_off_a(r, c8, AT);
+    const uint4 qv = *reinterpret_cast<const uint4*>(sm.q + o);
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + o);
+    const uint32_t* qa = reinterpret_cast<const uint32_t*>(&qv);
+    const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
+    const bool ok = r < len;
+    const float* gr = sm.g + r * D + c8;
+    const float* gl = sm.g + (C - 1) * D + c8;
+    uint4 qo, ko;
+    uint32_t* qoa = reinterpret_cast<uint32_t*>(&qo);
+    uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
 #pragma unroll
-  for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; e += 2) {
-      const int i = r0 + g4 + ((e >> 1) << 3), j = nt * 8 + t4 * 2;
-      float pv[2];
-#pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        const bool in = j + d < nrows;
-        sm.u2.lx.l[i][j + d] = in && i > j + d ? -sm.beta[i] * kk[nt][e + d] : 0.f;
-        pv[d] = in && i >= j + d ? qk[nt][e + d] : 0.f;
-      }
-      *reinterpret_cast<uint32_t*>(wP + i * C + j) = pack_bf16(pv[0], pv[1]);
+    for (int e = 0; e < 4; ++e) {
+      const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
+      const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+      qoa[e] = ok ? pack_bf16(qf.x * expf(gr[2 * e]), qf.y * expf(gr[2 * e + 1])) : 0u;
+      koa[e] = ok ? pack_bf16(kf.x * expf(gl[2 * e] - gr[2 * e]), kf.y * expf(gl[2 * e + 1] - gr[2 * e + 1])) : 0u;
     }
+    *reinterpret_cast<uint4*>(wQg + r * D + c8) = qo;
+    *reinterpret_cast<uint4*>(wKd + r * D + c8) = ko;
+  }
+  for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.g[(C - 1) * D + d];
+
+  // L = -b_i A_kk (strictly lower) -> shared memory, P = A_qk (lower incl. diagonal) -> workspace.
+  // Warp w reads its own sub-chunk's rows: row 16w + i in TMEM lane 32w + i (i < 16); its
+  // reference block's columns start at 0 / 16 / 48 (w = 1 / 2 / 3).
+  tc::mbar_wait(&sm.bar_m1, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int i = 16 * warp + (lane & 15);
+    const bool row = lane < 16;
+    const int cbase = warp == 1 ? 0 : warp == 2 ? 16 : 48;
+    const uint32_t la = tmem + ((uint32_t)(32 * warp) << 16);
+    const float bi = sm.beta[i];
+#pragma unroll 1
+    for (int j0 = 0; j0 < C; j0 += 16) {
+      float kk[16], qk[16];
+      const bool off = j0 < r0;  // warp-uniform: a block left of the diagonal
+      if (off) {
+        tc::tmem_ld16_async(la + cbase + j0, kk);
+        tc::tmem_ld16_async(la + 96 + cbase + j0, qk);
+        tc::tmem_wait_ld();
+        tc::reg_fence16(kk);
+        tc::reg_fence16(qk);
+      }
+      if (row) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          float pv[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const int j = j0 + e + d;
+            const bool ok = off && i < len && j < len;
+            sm.l[i][j] = ok ? -bi * kk[e + d] : 0.f;
+            pv[d] = ok ? qk[e + d] : 0.f;
+          }
+          pk[e >> 1] = pack_bf16(pv[0], pv[1]);
+        }
+        *reinterpret_cast<uint4*>(wP + i * C + j0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(wP + i * C + j0 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
   __syncwarp();
 #pragma unroll
-  for (int u = 0; u < kPerLane; ++u) {
-    const int p = lane + 32 * u;
-    if (p < kPairs) {
-      int a = (int)((sqrtf(8.f * p + 1.f) - 1.f) * 0.5f);
-      if ((a + 1) * (a + 2) / 2 <= p) ++a;
-      if (a * (a + 1) / 2 > p) --a;
-      const int b = p - a * (a + 1) / 2;
-      const int i = r0 + a, j = r0 + b;
-      if (a > b) sm.u2.lx.l[i][j] = -sm.beta[i] * dkk[u];
-      wP[i * C + j] = __float2bfloat16_rn(dqk[u]);
+  for (int u = 0; u < kPerLane; ++u) {  // the diagonal blocks over the zeros written above
+    const int i = di[u], j = dj[u];
+    if (i >= 0) {
+      const bool ok = i < len && j < len;
+      if (i > j) sm.l[i][j] = ok ? -sm.beta[i] * dkk[u] : 0.f;
+      wP[i * C + j] = __float2bfloat16_rn(ok ? dqk[u] : 0.f);
     }
   }
-  // chunk-global operands: b e^G K, b V (W/U step), e^G Q and e^{G_C - G} K (state pass)
-  for (int idx = tid; idx < C * D / 2; idx += kThreads) {
-    const int r = idx / (D / 2), cc = (idx % (D / 2)) * 2;
-    const float g0 = sm.g[r * D + cc], g1 = sm.g[r * D + cc + 1];
-    const float gl0 = sm.g[(C - 1) * D + cc], gl1 = sm.g[(C - 1) * D + cc + 1];
-    const float2 kv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.k[r * LDK + cc]));
-    const float2 qv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sm.q[r * LDK + cc]));
-    const float b = sm.beta[r];
-    *reinterpret_cast<uint32_t*>(&sm.u1.w.kb[r * LDK + cc]) = pack_bf16(kv.x * b * expf(g0), kv.y * b * expf(g1));
-    *reinterpret_cast<uint32_t*>(wKd + r * D + cc) = pack_bf16(kv.x * expf(gl0 - g0), kv.y * expf(gl1 - g1));
-    *reinterpret_cast<uint32_t*>(wQg + r * D + cc) = pack_bf16(qv.x * expf(g0), qv.y * expf(g1));
-  }
-  load_vb_tile<T, D>(qkv, qkv_stride, v_off, h, c0, len, sm.beta, sm.u1.w.vb, LDK);
-  for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.g[(C - 1) * D + d];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  // T = (I - L)^{-1}
-  invert_unit_lower(sm.u2.lx.l, sm.u2.lx.x, sm.scr);
-  for (int idx = tid; idx < C * C; idx += kThreads) {
-    const int i = idx / C, j = idx % C;
-    sm.t[i * LDC + j] = __float2bfloat16_rn(sm.u2.lx.x[i][j]);
+  invert_unit_lower(sm.l, sm.x, sm.scr);  // x = T = (I - L)^-1 (fp32)
+  for (int idx = tid; idx < C * C / 8; idx += kThreads) {  // T1 = T diag(b), swizzled K-major
+    const int i = idx >> 3, j8 = (idx & 7) * 8;
+    uint32_t p1[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2)
+      p1[e >> 1] = pack_bf16(sm.x[i][j8 + e] * sm.beta[j8 + e], sm.x[i][j8 + e + 1] * sm.beta[j8 + e + 1]);
+    *reinterpret_cast<uint4*>(sm.t1 + sw_off_a(i, j8, AT)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  // W = T Kb, U = T Vb -> workspace
+  if (warp == 1) {  // W = T1 (e^G o K) -> TMEM [0, D), U = T1 V -> [D, 2D)
+    tc::mbar_wait(&sm.bar_v, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t id = tc::idesc_bf16(64, D) | (1u << 16);  // B MN-major
+    const uint32_t s1 = tc::smem_u32(sm.t1), sg = tc::smem_u32(sm.kg), sv = tc::smem_u32(sm.v);
+#pragma unroll
+    for (int kk = 0; kk < C / 16; ++kk) {
+      tc::umma_w(tmem, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sg + kk * 2048), id, kk > 0 ? 1u : 0u);
+      tc::umma_w(tmem + D, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sv + kk * 2048), id, kk > 0 ? 1u : 0u);
+    }
+    tc::commit_w(&sm.bar_m2);
+  }
+  tc::mbar_wait(&sm.bar_m2, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   {
-    float wacc[D / 8][4], uacc[D / 8][4];
+    const int i = 16 * warp + (lane & 15);
+    const uint32_t la = tmem + ((uint32_t)(32 * warp) << 16);
+#pragma unroll 1
+    for (int c = 0; c < D; c += 16) {
+      float wv[16], uv[16];
+      tc::tmem_ld16_async(la + c, wv);
+      tc::tmem_ld16_async(la + D + c, uv);
+      tc::tmem_wait_ld();
+      tc::reg_fence16(wv);
+      tc::reg_fence16(uv);
+      if (lane < 16) {
+        uint32_t pw[8], pu[8];
 #pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) wacc[nt][e] = uacc[nt][e] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < C; ks += 16) {
-      uint32_t a[4];
-      lda(sm.t, LDC, warp * 16, ks, a);
-#pragma unroll
-      for (int nt = 0; nt < D / 8; nt += 2) {
-        uint32_t b0, b1, b2, b3;
-        ldb_kn(sm.u1.w.kb, LDK, nt * 8, ks, b0, b1, b2, b3);
-        mma_bf16(wacc[nt], a, b0, b1);
-        mma_bf16(wacc[nt + 1], a, b2, b3);
-        ldb_kn(sm.u1.w.vb, LDK, nt * 8, ks, b0, b1, b2, b3);
-        mma_bf16(uacc[nt], a, b0, b1);
-        mma_bf16(uacc[nt + 1], a, b2, b3);
+        for (int e = 0; e < 8; ++e) {
+          pw[e] = pack_bf16(wv[2 * e], wv[2 * e + 1]);
+          pu[e] = pack_bf16(uv[2 * e], uv[2 * e + 1]);
+        }
+        *reinterpret_cast<uint4*>(wW + i * D + c) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+        *reinterpret_cast<uint4*>(wW + i * D + c + 8) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+        *reinterpret_cast<uint4*>(wU + i * D + c) = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+        *reinterpret_cast<uint4*>(wU + i * D + c + 8) = make_uint4(pu[4], pu[5], pu[6], pu[7]);
       }
     }
-#pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; e += 2) {
-        const int r = warp * 16 + g4 + ((e >> 1) << 3), cc = nt * 8 + t4 * 2;
-        *reinterpret_cast<uint32_t*>(wW + r * D + cc) = pack_bf16(wacc[nt][e], wacc[nt][e + 1]);
-        *reinterpret_cast<uint32_t*>(wU + r * D + cc) = pack_bf16(uacc[nt][e], uacc[nt][e + 1]);
-      }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
-template <typename T, int D>
-static sn_status launch_kda_two_phase(const float* qn, const float* kn, const void* qkv, int v_off, int qkv_stride,
-                                      const float* glog, const float* beta, const int32_t* chunks,
+template <int D>
+static sn_status launch_kda_two_phase(const void* qb, const void* kb, const void* qkv, int v_off, int qkv_stride,
+                                      int rows, const float* glog, const float* beta, const int32_t* chunks,
                                       const int32_t* seq_chunk0, int num_chunks, void* ws, float* glast, float* o,
                                       float* state, const int32_t* slot_idx, int num_seqs, int H, int init_state,
                                       cudaStream_t st) {
-  const int smem_a = (int)sizeof(KdaIntraSmem<D>);
+  const int smem = (int)sizeof(KdaTcSmem<D>) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kda_chunk_intra_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
+    cudaFuncSetAttribute(kda_chunk_intra_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  kda_chunk_intra_kernel<T, D><<<dim3(num_chunks, H), kThreads, smem_a, st>>>(
-      qn, kn, (const T*)qkv, v_off, qkv_stride, glog, beta, chunks, (__nv_bfloat16*)ws, glast, H);
-  sn_status e = check_launch("sn_kda_chunk_prefill(intra)");
-  if (e != SN_OK) return e;
+  CUtensorMap qm, km, vm;
+  if (!tc::map_2d(&qm, qb, rows, (uint64_t)H * D, (uint64_t)H * D, 64) ||
+      !tc::map_2d(&km, kb, rows, (uint64_t)H * D, (uint64_t)H * D, 64) ||
+      !tc::map_2d(&vm, qkv, rows, (uint64_t)qkv_stride, (uint64_t)qkv_stride, 64)) {
+    set_error("sn_kda_chunk_prefill2: cuTensorMapEncodeTiled failed");
+    return SN_ECUDA;
+  }
+  cudaError_t e = launch_pdl(kda_chunk_intra_tc_kernel<D>, dim3(num_chunks, H), dim3(kThreads), (size_t)smem, st, qm,
+                             km, vm, v_off, glog, beta, chunks, (__nv_bfloat16*)ws, glast, H);
+  if (e != cudaSuccess) {
+    set_error("sn_kda_chunk_prefill2(intra) launch: %s", cudaGetErrorString(e));
+    return SN_ECUDA;
+  }
+  sn_status s = check_launch("sn_kda_chunk_prefill(intra)");
+  if (s != SN_OK) return s;
   launch_state_pass<D, true>((const __nv_bfloat16*)ws, glast, chunks, seq_chunk0, o, state, slot_idx, num_seqs, H,
                              init_state, st);
   return check_launch("sn_kda_chunk_prefill(state)");
@@ -972,24 +1037,27 @@ size_t sn_kda_chunk_workspace_bytes(int num_chunks, int H, int D) {
          (size_t)num_chunks * H * D * sizeof(float);
 }
 
-sn_status sn_kda_chunk_prefill2(const float* qn, const float* kn, const void* qkv_conv, int v_off, int qkv_stride,
-                                const float* glog, const float* beta, const int32_t* chunks,
+sn_status sn_kda_chunk_prefill2(const void* qn, const void* kn, const void* qkv_conv, int v_off, int qkv_stride,
+                                int rows, const float* glog, const float* beta, const int32_t* chunks,
                                 const int32_t* seq_chunk0, int num_chunks, void* workspace, float* o, float* state,
                                 const int32_t* slot_idx, int num_seqs, int H, int D, int init_state, int dtype,
                                 void* stream) {
   SN_REQUIRE(qn && kn && qkv_conv && glog && beta && chunks && seq_chunk0 && workspace && o && state,
              "sn_kda_chunk_prefill2: NULL pointer");
-  SN_REQUIRE(num_seqs > 0 && num_chunks > 0 && H > 0, "sn_kda_chunk_prefill2: bad shape");
+  SN_REQUIRE(num_seqs > 0 && num_chunks > 0 && H > 0 && rows > 0, "sn_kda_chunk_prefill2: bad shape");
   SN_REQUIRE(D == 64 || D == 128, "sn_kda_chunk_prefill2: D=%d unsupported", D);
   SN_REQUIRE(dtype == SN_BF16, "sn_kda_chunk_prefill2: bf16 only");
+  SN_REQUIRE(((uintptr_t)qn % 16) == 0 && ((uintptr_t)kn % 16) == 0 && ((uintptr_t)qkv_conv % 16) == 0 &&
+                 (qkv_stride * 2) % 16 == 0 && (v_off % 64) == 0,
+             "sn_kda_chunk_prefill2: TMA operands must be 16-byte aligned (v_off a multiple of 64)");
   cudaStream_t st = (cudaStream_t)stream;
   float* glast = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
                                           (size_t)num_chunks * H * (4 * (size_t)chunk::C * D + (size_t)chunk::C * chunk::C) * 2);
   if (D == 128)
-    return chunk::launch_kda_two_phase<__nv_bfloat16, 128>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, chunks,
+    return chunk::launch_kda_two_phase<128>(qn, kn, qkv_conv, v_off, qkv_stride, rows, glog, beta, chunks,
                                                             seq_chunk0, num_chunks, workspace, glast, o, state,
                                                             slot_idx, num_seqs, H, init_state, st);
-  return chunk::launch_kda_two_phase<__nv_bfloat16, 64>(qn, kn, qkv_conv, v_off, qkv_stride, glog, beta, chunks,
+  return chunk::launch_kda_two_phase<64>(qn, kn, qkv_conv, v_off, qkv_stride, rows, glog, beta, chunks,
                                                          seq_chunk0, num_chunks, workspace, glast, o, state, slot_idx,
                                                          num_seqs, H, init_state, st);
 }

@@ -659,8 +659,8 @@ class Supernet:
         # bf16: chunked WY prefill on tensor cores (GDN scalar gate / KDA per-channel gate);
         # fp32 I/O (1e-4 parity mode): the recurrent scan (same outputs, token-sequential)
         chunked = h.dtype == torch.bfloat16 and getattr(self, "chunked_prefill", True)
-        # the chunked GDN pass reads q / k as bf16 TMA tiles
-        qk_dt = torch.bfloat16 if (chunked and kind == GDN) else torch.float32
+        # the chunked passes read q / k as bf16 TMA tiles
+        qk_dt = torch.bfloat16 if chunked else torch.float32
         qn = torch.empty(rows, Hk, D, device=dev, dtype=qk_dt)
         kn = torch.empty(rows, Hk, D, device=dev, dtype=qk_dt)
         gexp = torch.empty(rows, Hv, D, **f32) if kind == KDA else torch.empty(rows, Hv, **f32)

@@ -257,7 +257,11 @@ def kda_chunk_prefill2(qn, kn, qkv_conv, v_off, glog, beta, chunks, seq_chunk0, 
     nbytes = _lib.load().sn_kda_chunk_workspace_bytes(n, H, D)
     if workspace is None or workspace.numel() < nbytes:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=qn.device)
-    call("sn_kda_chunk_prefill2", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), _p(glog), _p(beta),
+    if qn.dtype != torch.bfloat16:  # the kernel reads bf16 TMA tiles (sn_delta_prep emits them directly)
+        qn, kn = qn.to(torch.bfloat16), kn.to(torch.bfloat16)
+    assert qn.is_contiguous() and kn.is_contiguous()
+    call("sn_kda_chunk_prefill2", _p(qn), _p(kn), _p(qkv_conv), v_off, qkv_conv.stride(0), qkv_conv.shape[0],
+         _p(glog), _p(beta),
          _p(chunks), _p(seq_chunk0), n, _p(workspace), _p(o), _p(state), _p(slot_idx), seq_chunk0.numel() - 1, H, D,
          int(init_state), dtype_code(qkv_conv.dtype), _s())
     return workspace

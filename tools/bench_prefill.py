@@ -59,13 +59,14 @@ for T in (512, 4096, 16384):
     o = torch.empty(T, H, D, device="cuda")
     gexp = glog.exp()
     chunks, c0 = ops.chunk_plan([0, T])
+    qb, kb = qn.to(torch.bfloat16), kn.to(torch.bfloat16)  # sn_delta_prep emits these in the model
     ws = None
     res = {}
     for name in ("chunk2", "scan"):
         def run():
             global ws
             if name == "chunk2":
-                ws = ops.kda_chunk_prefill2(qn, kn, qkv, 2 * H * D, glog, beta, chunks, c0, o, S, None, H, D,
+                ws = ops.kda_chunk_prefill2(qb, kb, qkv, 2 * H * D, glog, beta, chunks, c0, o, S, None, H, D,
                                             init_state=False, workspace=ws)
             else:
                 ops.delta_scan(1, qn, kn, qkv, 2 * H * D, gexp, beta, o, S, None, cu, H, H, D, init_state=False)
