@@ -50,7 +50,6 @@ struct Args {
   int ks;         // atoms per unit (pipeline stage)
   int ku;         // units per item
   int ns, stage_bytes, acc_cols;
-  int npf;        // units whose weights are prefetched into L2 before griddepcontrol.wait
   epi::Args e;
 };
 
@@ -119,19 +118,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx_noarrive(&full_bar[s], KS * w_bytes);
         load(true, false);
         advance();
-      }
-      // and the next npf units' weights go to L2 (no smem needed): HBM streams them while the
-      // previous kernel finishes, the later TMA loads hit L2
-#pragma unroll 1
-      for (int u = npre; u < min(my_units, npre + g.npf); ++u) {
-        const int j = q + (u / KU) * G;
-        const int kc0 = ((j % S) * KU + u % KU) * KS * BK;
-#pragma unroll 1
-        for (int a = 0; a < KS; ++a)
-          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                           reinterpret_cast<uint64_t>(&wmap)),
-                       "r"(kc0 + a * BK), "r"((j / S) * BR)
-                       : "memory");
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       it = 0; ku = 0; s = 0; ph = 0;
@@ -378,8 +364,6 @@ template <int UM>
 static sn_status launch(const CUtensorMap& wm, const CUtensorMap& xm, const Plan& p, Args g, cudaStream_t st) {
   g.br = p.br; g.nblocks = p.nblocks; g.splits = p.splits; g.ks = p.ks; g.ku = p.ku;
   g.ns = p.ns; g.stage_bytes = p.stage;
-  static const int pf_kb = getenv("SN_DG_PF_KB") ? atoi(getenv("SN_DG_PF_KB")) : 0;  // EXPERIMENT
-  g.npf = pf_kb * 1024 / (p.ks * p.br * tc::BK * 2);
   int cols = 32;
   while (cols < p.br) cols <<= 1;
   g.acc_cols = cols;
