@@ -354,10 +354,12 @@ void sn_decode_chain_trace(unsigned long long* buf);
 
 /* ---------------------------------------------------------------- prefill GEMM
  * The projections of a prefill (every packed prompt row at once): C[m][n] = sum_k A[m][k]
- * W[n][k], A [M][lda] bf16, W [N][ldw] bf16 (nn.Linear layout), out bf16 [M][ldo].
- * tcgen05/TMEM/TMA, 128 x br output tiles on a persistent grid in L2-friendly bands.
- * mode SN_GEMM_STORE (br = 256) or SN_GEMM_SWIGLU_IL (W in blocks of swiglu_h gate rows then
- * swiglu_h up rows, out = silu(gate) * up, N = FFN width; swiglu_h a multiple of 16 <= 128).
+ * W[n][k], A [M][lda] bf16, W [N][ldw] bf16 (nn.Linear layout), out [M][ldo].
+ * tcgen05/TMEM/TMA, 2-CTA (cta_group::2) 256 x br output tiles on a persistent grid of CTA
+ * pairs in L2-friendly bands.  mode SN_GEMM_STORE (out bf16), SN_GEMM_PARTIAL (out fp32: the
+ * row-parallel projections whose partials a tensor-parallel prefill sums in fp32) or
+ * SN_GEMM_SWIGLU_IL (W in blocks of swiglu_h gate rows then swiglu_h up rows, out bf16 =
+ * silu(gate) * up, N = FFN width; swiglu_h a multiple of 16 <= 128).
  * Replaces the cuBLAS projections of the prefill (R/PAPER.md:845-848 dual path).          */
 sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const void* w, int N, int ldw,
                           void* out, int ldo, int mode, int swiglu_h, void* stream);

@@ -236,7 +236,8 @@ extern "C" sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const
   SN_REQUIRE(lda >= K && ldw >= K && ((uintptr_t)a % 16) == 0 && ((uintptr_t)w % 16) == 0 && (lda * 2) % 16 == 0 &&
                  (ldw * 2) % 16 == 0,
              "sn_gemm_prefill: operands must be 16-byte aligned with row pitch >= K");
-  SN_REQUIRE(mode == SN_GEMM_STORE || mode == SN_GEMM_SWIGLU_IL, "sn_gemm_prefill: mode %d (STORE or SWIGLU_IL)", mode);
+  SN_REQUIRE(mode == SN_GEMM_STORE || mode == SN_GEMM_SWIGLU_IL || mode == SN_GEMM_PARTIAL,
+             "sn_gemm_prefill: mode %d (STORE, SWIGLU_IL or PARTIAL = fp32 store)", mode);
   SN_REQUIRE(ldo >= N && (ldo % 8) == 0, "sn_gemm_prefill: ldo %d", ldo);
   const bool swiglu = mode == SN_GEMM_SWIGLU_IL;
   if (swiglu)

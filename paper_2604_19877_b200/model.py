@@ -526,12 +526,22 @@ class Supernet:
             self.seq_lens.index_copy_(0, idx, lens_t)
         e = lambda *s, d=dt: torch.empty(*s, device=dev, dtype=d)
         resid = e(rows, cfg.hidden, d=torch.float32)
-        h, mix, ffn_o = e(rows, cfg.hidden), e(rows, cfg.hidden), e(rows, cfg.hidden)
+        # tensor parallel: the row-parallel projections (out-proj, FFN down) leave fp32 partials
+        # that are summed over the group in fp32 and added to the residual before the norm
+        rp_dt = torch.float32 if self.tp > 1 else dt
+        h, mix, ffn_o = e(rows, cfg.hidden), e(rows, cfg.hidden, d=rp_dt), e(rows, cfg.hidden, d=rp_dt)
+
+        def add_norm(delta, weight):
+            if delta is not None and delta.dtype != h.dtype:
+                resid.add_(delta)
+                delta = None
+            ops.add_rmsnorm(delta, resid, weight, h, cfg.norm_eps)
+
         ops.embed(flat, w["embed"], resid)
         delta = None
         for l, kind in enumerate(self.kinds):
             lw = w["layers"][l]
-            ops.add_rmsnorm(delta, resid, lw["norm1"], h, cfg.norm_eps)
+            add_norm(delta, lw["norm1"])
             if kind in (FA, SWA):
                 self._attn_prefill(l, kind, h, mix, cu, row_seq, row_pos)
             elif kind == GDN:
@@ -539,13 +549,13 @@ class Supernet:
             else:
                 self._kda_prefill(l, h, mix, cu)
             self._tp_sum(mix)
-            ops.add_rmsnorm(mix, resid, lw["norm2"], h, cfg.norm_eps)
+            add_norm(mix, lw["norm2"])
             act = e(rows, cfg.ffn)
             self._mm(h, lw["ffn_gu_il"], act, swiglu=True)
             self._mm(act, lw["ffn_down"], ffn_o)
             self._tp_sum(ffn_o)
             delta = ffn_o
-        ops.add_rmsnorm(delta, resid, w["final_norm"], h, cfg.norm_eps)
+        add_norm(delta, w["final_norm"])
         if return_all:
             logits = self._mm(h, w["lm_head"])
             if ragged:
@@ -566,15 +576,11 @@ class Supernet:
         return torch.mm(x, w.t(), out=out) if out is not None else x @ w.t()
 
     def _tp_sum(self, t):
-        """Prefill: sum a row-parallel projection output over the TP group (in fp32)."""
+        """Prefill: sum a row-parallel projection output (fp32 partials) over the TP group."""
         if self.tp > 1:
             from .dist import allreduce_sum_
-            if t.dtype == torch.float32:
-                allreduce_sum_(t, self.tp_group)
-            else:
-                t32 = t.float()
-                allreduce_sum_(t32, self.tp_group)
-                t.copy_(t32)
+            assert t.dtype == torch.float32
+            allreduce_sum_(t, self.tp_group)
 
     def _attn_prefill(self, l, kind, h, out, cu, row_seq, row_pos):
         cfg, st, w = self.cfg, self.state[l], self.w["layers"][l]["mixer"]

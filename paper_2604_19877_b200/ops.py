@@ -348,9 +348,10 @@ def decode_chain(phases, M, counter):
 
 # ------------------------------------------------------------------ prefill GEMM
 def gemm_prefill(a, w, out=None, swiglu_h=0):
-    """out [M, N] = a [M, K] @ w [N, K]^T (bf16, tcgen05).  swiglu_h > 0: w is the
-    SwiGLU-interleaved gate/up layout (interleave_swiglu, block swiglu_h) and out [M, F] =
-    silu(gate) * up with F = the FFN width (out must be given)."""
+    """out [M, N] = a [M, K] @ w [N, K]^T (bf16 operands, tcgen05; out bf16, or fp32 when an
+    fp32 out is given).  swiglu_h > 0: w is the SwiGLU-interleaved gate/up layout
+    (interleave_swiglu, block swiglu_h) and out [M, F] = silu(gate) * up with F = the FFN width
+    (out must be given)."""
     M, K = a.shape
     assert a.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and a.stride(1) == 1 and w.stride(1) == 1
     if swiglu_h:
@@ -361,7 +362,9 @@ def gemm_prefill(a, w, out=None, swiglu_h=0):
         N = w.shape[0]
         if out is None:
             out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16)
-    assert out.dtype == torch.bfloat16 and out.stride(1) == 1 and out.shape[0] == M
-    call("sn_gemm_prefill", _p(a), M, K, a.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(0),
-         SN_GEMM_SWIGLU_IL if swiglu_h else SN_GEMM_STORE, swiglu_h, _s())
+    f32 = out.dtype == torch.float32
+    assert (out.dtype == torch.bfloat16 or (f32 and not swiglu_h)) and out.stride(1) == 1 and out.shape[0] == M
+    mode = SN_GEMM_SWIGLU_IL if swiglu_h else (GEMM_MODES["partial"] if f32 else SN_GEMM_STORE)
+    call("sn_gemm_prefill", _p(a), M, K, a.stride(0), _p(w), N, w.stride(0), _p(out), out.stride(0), mode,
+         swiglu_h, _s())
     return out

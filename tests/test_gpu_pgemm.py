@@ -65,3 +65,16 @@ def test_strided_operands():
     w = (torch.randn(512, 128, device="cuda") * 0.05).to(torch.bfloat16)
     out = ops.gemm_prefill(a, w)
     assert rel(out, a.float() @ w.float().t()) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K", [(70, 256, 128), (3000, 5120, 512)])
+def test_fp32_out_for_row_parallel_partials(M, N, K):
+    """fp32 out (SN_GEMM_PARTIAL): the tensor-parallel prefill sums these partials in fp32."""
+    from paper_2604_19877_b200 import ops
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda") * 0.05).to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    ops.gemm_prefill(a, w, out)
+    ref = a.float() @ w.float().t()
+    assert ((out - ref).abs().max() / ref.abs().max()).item() <= 1e-4
