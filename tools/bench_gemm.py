@@ -15,9 +15,9 @@ from paper_2604_19877_b200._lib import load  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 64
 c = APRIEL
-SHAPES = [("ffn_gate_up", c.ffn, c.hidden, "swiglu_il"), ("ffn_down", c.hidden, c.ffn, "resid"),
-          ("gdn_in", c.gdn_in_width, c.hidden, "store"), ("gdn_out", c.hidden, c.gdn_value_dim, "resid"),
-          ("kda_in", c.kda_in_width, c.hidden, "store"), ("attn_out", c.hidden, c.attn_o_in, "resid"),
+SHAPES = [("ffn_gate_up", c.ffn, c.hidden, "swiglu_il"), ("ffn_down", c.hidden, c.ffn, "partial"),
+          ("gdn_in", c.gdn_in_width, c.hidden, "store"), ("gdn_out", c.hidden, c.gdn_value_dim, "partial"),
+          ("kda_in", c.kda_in_width, c.hidden, "store"), ("attn_out", c.hidden, c.attn_o_in, "partial"),
           ("lm_head", c.vocab, c.hidden, "store")]
 
 
@@ -26,17 +26,19 @@ def time_gemm(N, K, mode, it=30):
     nbuf = max(2, min(8, int(3e9 // (rows * K * 2))))
     Ws = [torch.randn(rows, K, device="cuda").to(torch.bfloat16) for _ in range(nbuf)]
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-    out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if mode == "resid" else torch.bfloat16)
-    ws = ops.gemm_decode_workspace(M, "cuda")
+    if mode == "partial":
+        out = torch.zeros(8, M, N, device="cuda", dtype=torch.float32)
+    else:
+        out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if mode == "resid" else torch.bfloat16)
     for i in range(3):
-        ops.gemm_decode(x, Ws[i % nbuf], out, mode, ws)
+        ops.gemm_decode(x, Ws[i % nbuf], out, mode)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.graph(g, stream=s):
         for i in range(it):
-            ops.gemm_decode(x, Ws[i % nbuf], out, mode, ws)
+            ops.gemm_decode(x, Ws[i % nbuf], out, mode)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
