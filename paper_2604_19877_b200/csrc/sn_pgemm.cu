@@ -11,7 +11,7 @@
 //    bytes per flop of a 128-row tile); the leader issues every MMA, both CTAs' TMA loads
 //    complete on the leader's barrier, the MMA commits multicast to both CTAs' barriers and each
 //    CTA drains its own 128 accumulator lanes.  br is chosen per shape to minimise the last
-//    wave's idle pairs (STORE: 128-256 in steps of 32; SwiGLU: 2h).
+//    wave's idle pairs (STORE: 256 or 224; SwiGLU: 2h).
 // Warp roles as in the decode GEMM (sn_dgemm.cu): 0 = TMA producer, 1 = MMA issuer, 2 = TMEM
 // allocator, 4-7 = epilogue; two TMEM accumulators (2 x 256 columns) so one tile's epilogue
 // overlaps the next tile's MMAs.  The epilogue is sn_epi.cuh's (STORE / SwiGLU-interleaved).
@@ -247,9 +247,11 @@ extern "C" sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const
   int br = 256;
   if (swiglu) {
     br = 2 * swiglu_h;
-  } else {  // the block height whose last wave leaves the fewest pairs idle
+  } else {  // the block height whose last wave leaves the fewest pairs idle, among 256 / 224
+    // (narrower tiles re-read A more per flop: 192 ran at 0.86 and 128-160 at 0.71-0.74 of
+    // cuBLAS at 64K-128K rows, where the wave quantisation they save is negligible)
     long best = -1;
-    for (int c = 256; c >= 128; c -= 32) {
+    for (int c = 256; c >= 224; c -= 32) {
       const long waves = ((long)((N + c - 1) / c) * mtiles + slots - 1) / slots;
       if (best < 0 || waves * c < best) { best = waves * c; br = c; }
     }
