@@ -1,6 +1,6 @@
 """Prefill projection GEMM (2-CTA tcgen05, csrc/sn_pgemm.cu) against a plain PyTorch fp32
 reference of the same op: STORE and the fused SwiGLU epilogue, ragged M / N, K from one atom to
-the FFN width, every block height the wave-filling rule picks (128-256), more tiles than CTA
+the FFN width, both block heights the wave-filling rule picks (224, 256), more tiles than CTA
 pairs (the persistent walk), M not a multiple of the 256-row pair tile.  Tolerance: max-abs
 error / max |ref| <= 1e-2 (bf16 output rounding, fp32 accumulate)."""
 import pytest
@@ -16,7 +16,7 @@ def rel(a, b):
 @pytest.mark.gpu
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (127, 1000, 256), (300, 6144, 5120), (2100, 10304, 5120),
                                    (257, 5120, 14336), (4096, 256, 128),
-                                   # Apriel widths at prompt sizes where the rule picks 224 / 160 / 192
+                                   # Apriel widths at prompt sizes where the rule picks 224 or 256
                                    (16384, 5120, 256), (9000, 10304, 128), (5000, 6144, 192),
                                    (12345, 4000, 64)])
 def test_store_matches_fp32_reference(M, N, K):
@@ -47,10 +47,10 @@ def test_swiglu_epilogue_matches_reference(M, F, K):
 
 @pytest.mark.gpu
 def test_block_height_rule():
-    """The block height fills the last wave of CTA pairs (host-side choice, checked through
-    the results at each height: N = 5120 at 16384 rows picks 224, at 512 rows 256)."""
+    """The block height fills the last wave of CTA pairs (host-side choice between 256 and 224,
+    checked through the results: N = 5120 picks 224 at 16384 rows, 256 at 131072)."""
     from paper_2604_19877_b200 import ops
-    for M in (512, 16384):
+    for M in (16384, 131072):
         a = torch.randn(M, 128, device="cuda").to(torch.bfloat16)
         w = (torch.randn(5120, 128, device="cuda") * 0.05).to(torch.bfloat16)
         assert rel(ops.gemm_prefill(a, w), a.float() @ w.float().t()) <= TOL
