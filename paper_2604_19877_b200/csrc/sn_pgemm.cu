@@ -16,7 +16,7 @@
 // allocator, 4-7 = epilogue; two TMEM accumulators (2 x 256 columns) so one tile's epilogue
 // overlaps the next tile's MMAs.  The epilogue is sn_epi.cuh's (STORE / SwiGLU-interleaved).
 //
-// Rasterisation: tiles are walked in bands of 8 row tiles (2048 rows),
+// Rasterisation: tiles are walked in bands of 16 (8 for long K) row tiles,
 // the weight block changing slowest inside a band, so the tiles in flight at a time share a
 // few A row tiles and weight blocks through L2.
 //
@@ -57,7 +57,11 @@ __device__ __forceinline__ void tile_of(const Args& g, int j, int& mt, int& nb) 
 // barriers, and each CTA drains its own 128 accumulator lanes.  SwiGLU (br = 2h): the leader
 // holds the gate rows of a block, the peer the up rows; every accumulator row has both halves.
 constexpr int kStages2 = 7;
-constexpr int kBand = 8;  // 256-row tiles per rasterisation band (8 / 12 / 16 equal within noise; 32 -5 %)
+// 256-row tiles per rasterisation band: the band's A rows stay L2-resident while it sweeps the
+// weight blocks, so the weights are re-read once per band.  16 for K <= 8192 (K = 5120: a 42 MB
+// band; gate/up at 128K rows 0.90 -> 0.92-1.06 of cuBLAS vs 8), 8 for the long-K down-projection
+// (K = 14336: 16 would be a 117 MB band).  At 16K rows 8 / 16 / 24 are equal within noise.
+constexpr int kBandShortK = 16, kBandLongK = 8;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the CTA-rank bit: the leader's copy of a barrier
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -260,7 +264,7 @@ extern "C" sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const
   const uint64_t wrows = swiglu ? (uint64_t)nblocks * br : (uint64_t)N;
   Args g{};
   g.M = M; g.K = K; g.kb = K / tc::BK; g.br = br; g.mtiles = mtiles; g.nblocks = nblocks;
-  g.band = kBand;
+  g.band = K <= 8192 ? kBandShortK : kBandLongK;
   g.e.mode = mode; g.e.M = M; g.e.N = N; g.e.out = out; g.e.ldo = ldo; g.e.S = 1;
   CUtensorMap wm, am;
   if (!tc::map_2d(&wm, w, wrows, K, ldw, br / 2) || !tc::map_2d(&am, a, M, K, lda, 128)) {
