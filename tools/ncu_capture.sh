@@ -20,7 +20,7 @@ $NCU --profile-from-start off -k regex:chain_kernel -s 3 -c 1 -o gpurun_out/ncu_
 # the chunked GDN and KDA phases (the T=16384 launches of tools/bench_prefill.py)
 $NCU -k regex:pgemm_kernel -s 1 -c 1 -o gpurun_out/ncu_pgemm python tools/bench_pgemm.py 16384 > /dev/null 2>&1
 $NCU -k regex:"gdn_chunk_(intra|state)" -s 16 -c 2 -o gpurun_out/ncu_gdn_chunk python tools/bench_prefill.py > /dev/null 2>&1
-$NCU -k regex:"kda_chunk_intra|chunk_state_kernel<128, 1" -s 16 -c 2 -o gpurun_out/ncu_kda_chunk python tools/bench_prefill.py > /dev/null 2>&1
+$NCU -k regex:kda_chunk_intra -s 8 -c 1 -o gpurun_out/ncu_kda_chunk python tools/bench_prefill.py > /dev/null 2>&1
 for f in gdn_decode kda_decode swa_decode dgemm chain pgemm gdn_chunk kda_chunk; do
   ncu -i gpurun_out/ncu_$f.ncu-rep --page raw --csv > gpurun_out/ncu_${f}_raw.csv 2>/dev/null
 done
