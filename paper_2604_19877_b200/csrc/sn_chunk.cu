@@ -726,18 +726,22 @@ struct KdaTcSmem {
   static constexpr int AT = 64 * 128;  // [64 rows x 64 bf16] 128B-swizzled atom
   static constexpr int RT = 96 * 128;  // the stacked right operand's atom: 96 rows
   static constexpr int NA = D / 64;
-  uint8_t q[NA * AT];
-  uint8_t k[NA * AT];
-  uint8_t v[NA * AT];
-  uint8_t ql[NA * AT];
-  uint8_t kl[NA * AT];
-  uint8_t kr[NA * RT];
-  uint8_t kg[NA * AT];  // e^G o K (B of W, MN-major)
-  uint8_t t1[AT];
-  float l[C][C + 1];
-  float x[C][C + 1];
-  float scr[4 * 16 * 17];
-  float g[C * D];  // G[r][d]: in-chunk cumulative log decay
+  uint8_t kg[NA * AT];  // e^G o K (B of W, MN-major): lives through both phases
+  union {  // phase 1 (operands of the A_kk / A_qk products) / phase 2 (inverse, W / U operands)
+    struct {
+      uint8_t q[NA * AT];   // Q, then (in place) QL
+      uint8_t k[NA * AT];   // K, then (in place) KL
+      uint8_t kr[NA * RT];
+      float g[C * D];       // G[r][d]: in-chunk cumulative log decay
+    } a;
+    struct {
+      uint8_t t1[AT];
+      uint8_t v[NA * AT];   // TMA-loaded once the phase-1 products have consumed the region
+      float l[C][C + 1];
+      float x[C][C + 1];
+      float scr[4 * 16 * 17];
+    } b;
+  } u;
   float beta[C];
   uint64_t bar_qk, bar_v, bar_m1, bar_m2;
   uint32_t tmem_base;
@@ -786,11 +790,9 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t pol = tc::policy_evict_first();
     tc::mbar_expect_tx(&sm.bar_qk, 2 * NA * AT);
     for (int a = 0; a < NA; ++a) {
-      tc::tma_load_2d(sm.q + a * AT, &qmap, h * D + 64 * a, c0, &sm.bar_qk, pol);
-      tc::tma_load_2d(sm.k + a * AT, &kmap, h * D + 64 * a, c0, &sm.bar_qk, pol);
+      tc::tma_load_2d(sm.u.a.q + a * AT, &qmap, h * D + 64 * a, c0, &sm.bar_qk, pol);
+      tc::tma_load_2d(sm.u.a.k + a * AT, &kmap, h * D + 64 * a, c0, &sm.bar_qk, pol);
     }
-    tc::mbar_expect_tx(&sm.bar_v, NA * AT);
-    for (int a = 0; a < NA; ++a) tc::tma_load_2d(sm.v + a * AT, &vmap, v_off + h * D + 64 * a, c0, &sm.bar_v, pol);
   }
   {  // per-channel log decays (rows past the chunk: 0, so G stays flat there)
     constexpr int IT = C * D / 4 / kThreads;
@@ -805,7 +807,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int u = 0; u < IT; ++u) {
       const int idx = tid + u * kThreads;
-      *reinterpret_cast<float4*>(&sm.g[(idx / (D / 4)) * D + (idx % (D / 4)) * 4]) = gv[u];
+      *reinterpret_cast<float4*>(&sm.u.a.g[(idx / (D / 4)) * D + (idx % (D / 4)) * 4]) = gv[u];
     }
   }
   if (tid < C) sm.beta[tid] = tid < len ? beta[(size_t)(c0 + tid) * H + h] : 0.f;
@@ -814,37 +816,26 @@ __global__ void __launch_bounds__(kThreads)
     float acc = 0.f;
 #pragma unroll 8
     for (int r = 0; r < C; ++r) {
-      acc += sm.g[r * D + d];
-      sm.g[r * D + d] = acc;
+      acc += sm.u.a.g[r * D + d];
+      sm.u.a.g[r * D + d] = acc;
     }
   }
   __syncthreads();
   tc::mbar_wait(&sm.bar_qk, 0);
-  // left operands (row i to its sub-chunk reference) and e^G o K, 8 columns per step
+  // e^G o K (the B operand of W), 8 columns per step
   for (int idx = tid; idx < C * D / 8; idx += kThreads) {
-    const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8, rr = r & ~15;
+    const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
     const uint32_t o = sw_off_a(r, c8, AT);
-    const uint4 qv = *reinterpret_cast<const uint4*>(sm.q + o);
-    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + o);
-    const uint32_t* qa = reinterpret_cast<const uint32_t*>(&qv);
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.u.a.k + o);
     const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
-    uint4 qo, ko, go;
-    uint32_t* qoa = reinterpret_cast<uint32_t*>(&qo);
-    uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
+    uint4 go;
     uint32_t* goa = reinterpret_cast<uint32_t*>(&go);
-    const float* gr = sm.g + r * D + c8;
-    const float* g0 = sm.g + rr * D + c8;
+    const float* gr = sm.u.a.g + r * D + c8;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
       const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
-      const float e0 = expf(gr[2 * e] - g0[2 * e]), e1 = expf(gr[2 * e + 1] - g0[2 * e + 1]);
-      qoa[e] = pack_bf16(qf.x * e0, qf.y * e1);
-      koa[e] = pack_bf16(kf.x * e0, kf.y * e1);
       goa[e] = pack_bf16(kf.x * expf(gr[2 * e]), kf.y * expf(gr[2 * e + 1]));
     }
-    *reinterpret_cast<uint4*>(sm.ql + o) = qo;
-    *reinterpret_cast<uint4*>(sm.kl + o) = ko;
     *reinterpret_cast<uint4*>(sm.kg + o) = go;
   }
   // the stacked right operand: block s (s = 1, 2, 3) = rows j < 16 s scaled to reference 16 s
@@ -852,33 +843,18 @@ __global__ void __launch_bounds__(kThreads)
     const int row = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
     const int s = row < 16 ? 1 : row < 48 ? 2 : 3;
     const int j = row - (s == 1 ? 0 : s == 2 ? 16 : 48), rr = 16 * s;
-    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + sw_off_a(j, c8, AT));
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.u.a.k + sw_off_a(j, c8, AT));
     const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
     uint4 ko;
     uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
-    const float* gj = sm.g + j * D + c8;
-    const float* g0 = sm.g + rr * D + c8;
+    const float* gj = sm.u.a.g + j * D + c8;
+    const float* g0 = sm.u.a.g + rr * D + c8;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
       koa[e] = pack_bf16(kf.x * expf(g0[2 * e] - gj[2 * e]), kf.y * expf(g0[2 * e + 1] - gj[2 * e + 1]));
     }
-    *reinterpret_cast<uint4*>(sm.kr + sw_off_a(row, c8, RT)) = ko;
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's reads
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1) {  // KL KR^T -> TMEM [0, 96), QL KR^T -> [96, 192)
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t sq = tc::smem_u32(sm.ql), sk = tc::smem_u32(sm.kl), sr = tc::smem_u32(sm.kr);
-    const uint32_t id = tc::idesc_bf16(64, 96);
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const uint32_t off = (kk >> 2) * AT + (kk & 3) * 32, roff = (kk >> 2) * RT + (kk & 3) * 32;
-      tc::umma_w(tmem, tc::desc_sw128(sk + off), tc::desc_sw128(sr + roff), id, kk > 0 ? 1u : 0u);
-      tc::umma_w(tmem + 96, tc::desc_sw128(sq + off), tc::desc_sw128(sr + roff), id, kk > 0 ? 1u : 0u);
-    }
-    tc::commit_w(&sm.bar_m1);
+    *reinterpret_cast<uint4*>(sm.u.a.kr + sw_off_a(row, c8, RT)) = ko;
   }
   __nv_bfloat16* rec = ws + ws_tile<D>(n, h, H);
   __nv_bfloat16* wW = rec;
@@ -904,14 +880,14 @@ __global__ void __launch_bounds__(kThreads)
       const int i = r0 + a, j = r0 + b;
       di[u] = i;
       dj[u] = j;
-      const float* gi = sm.g + i * D;
-      const float* gj = sm.g + j * D;
+      const float* gi = sm.u.a.g + i * D;
+      const float* gj = sm.u.a.g + j * D;
       float sk = 0.f, sq = 0.f;
 #pragma unroll 4
       for (int d = 0; d < D; d += 2) {
-        const float2 ki = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.k + sw_off_a(i, d, AT)));
-        const float2 qi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.q + sw_off_a(i, d, AT)));
-        const float2 kj = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.k + sw_off_a(j, d, AT)));
+        const float2 ki = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.u.a.k + sw_off_a(i, d, AT)));
+        const float2 qi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.u.a.q + sw_off_a(i, d, AT)));
+        const float2 kj = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sm.u.a.k + sw_off_a(j, d, AT)));
         const float e0 = expf(gi[d] - gj[d]) * kj.x, e1 = expf(gi[d + 1] - gj[d + 1]) * kj.y;
         sk += ki.x * e0 + ki.y * e1;
         sq += qi.x * e0 + qi.y * e1;
@@ -924,13 +900,13 @@ __global__ void __launch_bounds__(kThreads)
   for (int idx = tid; idx < C * D / 8; idx += kThreads) {
     const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
     const uint32_t o = sw_off_a(r, c8, AT);
-    const uint4 qv = *reinterpret_cast<const uint4*>(sm.q + o);
-    const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + o);
+    const uint4 qv = *reinterpret_cast<const uint4*>(sm.u.a.q + o);
+    const uint4 kv = *reinterpret_cast<const uint4*>(sm.u.a.k + o);
     const uint32_t* qa = reinterpret_cast<const uint32_t*>(&qv);
     const uint32_t* ka = reinterpret_cast<const uint32_t*>(&kv);
     const bool ok = r < len;
-    const float* gr = sm.g + r * D + c8;
-    const float* gl = sm.g + (C - 1) * D + c8;
+    const float* gr = sm.u.a.g + r * D + c8;
+    const float* gl = sm.u.a.g + (C - 1) * D + c8;
     uint4 qo, ko;
     uint32_t* qoa = reinterpret_cast<uint32_t*>(&qo);
     uint32_t* koa = reinterpret_cast<uint32_t*>(&ko);
@@ -944,13 +920,53 @@ __global__ void __launch_bounds__(kThreads)
     *reinterpret_cast<uint4*>(wQg + r * D + c8) = qo;
     *reinterpret_cast<uint4*>(wKd + r * D + c8) = ko;
   }
-  for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.g[(C - 1) * D + d];
-
+  for (int d = tid; d < D; d += kThreads) glast[((size_t)n * H + h) * D + d] = sm.u.a.g[(C - 1) * D + d];
+  __syncthreads();  // every raw Q / K read is done: the left operands are built in place
+  for (int idx = tid; idx < C * D / 8; idx += kThreads) {  // row i scaled to its sub-chunk reference
+    const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8, rr = r & ~15;
+    const uint32_t o = sw_off_a(r, c8, AT);
+    uint4 qv = *reinterpret_cast<const uint4*>(sm.u.a.q + o);
+    uint4 kv = *reinterpret_cast<const uint4*>(sm.u.a.k + o);
+    uint32_t* qa = reinterpret_cast<uint32_t*>(&qv);
+    uint32_t* ka = reinterpret_cast<uint32_t*>(&kv);
+    const float* gr = sm.u.a.g + r * D + c8;
+    const float* g0 = sm.u.a.g + rr * D + c8;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[e]));
+      const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ka[e]));
+      const float e0 = expf(gr[2 * e] - g0[2 * e]), e1 = expf(gr[2 * e + 1] - g0[2 * e + 1]);
+      qa[e] = pack_bf16(qf.x * e0, qf.y * e1);
+      ka[e] = pack_bf16(kf.x * e0, kf.y * e1);
+    }
+    *reinterpret_cast<uint4*>(sm.u.a.q + o) = qv;
+    *reinterpret_cast<uint4*>(sm.u.a.k + o) = kv;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's reads
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {  // KL KR^T -> TMEM [0, 96), QL KR^T -> [96, 192)
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t sq = tc::smem_u32(sm.u.a.q), sk = tc::smem_u32(sm.u.a.k), sr = tc::smem_u32(sm.u.a.kr);
+    const uint32_t id = tc::idesc_bf16(64, 96);
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint32_t off = (kk >> 2) * AT + (kk & 3) * 32, roff = (kk >> 2) * RT + (kk & 3) * 32;
+      tc::umma_w(tmem, tc::desc_sw128(sk + off), tc::desc_sw128(sr + roff), id, kk > 0 ? 1u : 0u);
+      tc::umma_w(tmem + 96, tc::desc_sw128(sq + off), tc::desc_sw128(sr + roff), id, kk > 0 ? 1u : 0u);
+    }
+    tc::commit_w(&sm.bar_m1);
+  }
   // L = -b_i A_kk (strictly lower) -> shared memory, P = A_qk (lower incl. diagonal) -> workspace.
   // Warp w reads its own sub-chunk's rows: row 16w + i in TMEM lane 32w + i (i < 16); its
   // reference block's columns start at 0 / 16 / 48 (w = 1 / 2 / 3).
-  tc::mbar_wait(&sm.bar_m1, 0);
+  tc::mbar_wait(&sm.bar_m1, 0);  // the phase-1 products have read QL / KL / KR
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {  // V into the phase-2 region (the inverse overlaps its latency)
+    tc::mbar_expect_tx(&sm.bar_v, NA * AT);
+    for (int a = 0; a < NA; ++a)
+      tc::tma_load_2d(sm.u.b.v + a * AT, &vmap, v_off + h * D + 64 * a, c0, &sm.bar_v, tc::policy_evict_first());
+  }
   {
     const int i = 16 * warp + (lane & 15);
     const bool row = lane < 16;
@@ -977,7 +993,7 @@ __global__ void __launch_bounds__(kThreads)
           for (int d = 0; d < 2; ++d) {
             const int j = j0 + e + d;
             const bool ok = off && i < len && j < len;
-            sm.l[i][j] = ok ? -bi * kk[e + d] : 0.f;
+            sm.u.b.l[i][j] = ok ? -bi * kk[e + d] : 0.f;
             pv[d] = ok ? qk[e + d] : 0.f;
           }
           pk[e >> 1] = pack_bf16(pv[0], pv[1]);
@@ -993,20 +1009,20 @@ __global__ void __launch_bounds__(kThreads)
     const int i = di[u], j = dj[u];
     if (i >= 0) {
       const bool ok = i < len && j < len;
-      if (i > j) sm.l[i][j] = ok ? -sm.beta[i] * dkk[u] : 0.f;
+      if (i > j) sm.u.b.l[i][j] = ok ? -sm.beta[i] * dkk[u] : 0.f;
       wP[i * C + j] = __float2bfloat16_rn(ok ? dqk[u] : 0.f);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  invert_unit_lower(sm.l, sm.x, sm.scr);  // x = T = (I - L)^-1 (fp32)
+  invert_unit_lower(sm.u.b.l, sm.u.b.x, sm.u.b.scr);  // x = T = (I - L)^-1 (fp32)
   for (int idx = tid; idx < C * C / 8; idx += kThreads) {  // T1 = T diag(b), swizzled K-major
     const int i = idx >> 3, j8 = (idx & 7) * 8;
     uint32_t p1[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2)
-      p1[e >> 1] = pack_bf16(sm.x[i][j8 + e] * sm.beta[j8 + e], sm.x[i][j8 + e + 1] * sm.beta[j8 + e + 1]);
-    *reinterpret_cast<uint4*>(sm.t1 + sw_off_a(i, j8, AT)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+      p1[e >> 1] = pack_bf16(sm.u.b.x[i][j8 + e] * sm.beta[j8 + e], sm.u.b.x[i][j8 + e + 1] * sm.beta[j8 + e + 1]);
+    *reinterpret_cast<uint4*>(sm.u.b.t1 + sw_off_a(i, j8, AT)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1015,7 +1031,7 @@ __global__ void __launch_bounds__(kThreads)
     tc::mbar_wait(&sm.bar_v, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t id = tc::idesc_bf16(64, D) | (1u << 16);  // B MN-major
-    const uint32_t s1 = tc::smem_u32(sm.t1), sg = tc::smem_u32(sm.kg), sv = tc::smem_u32(sm.v);
+    const uint32_t s1 = tc::smem_u32(sm.u.b.t1), sg = tc::smem_u32(sm.kg), sv = tc::smem_u32(sm.u.b.v);
 #pragma unroll
     for (int kk = 0; kk < C / 16; ++kk) {
       tc::umma_w(tmem, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sg + kk * 2048), id, kk > 0 ? 1u : 0u);
