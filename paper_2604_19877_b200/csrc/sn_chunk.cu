@@ -117,16 +117,21 @@ template <int D>
 struct TcIntraSmem {
   static constexpr int AT = 64 * 128;  // one [64 rows x 64 bf16] 128B-swizzled atom
   static constexpr int NA = D / 64;    // atoms per [64 x D] tile
-  uint8_t q[NA * AT];
   uint8_t k[NA * AT];
   uint8_t v[NA * AT];
-  uint8_t t1[AT];
-  uint8_t t2[AT];
-  float l[C][C + 1];
-  float x[C][C + 1];
-  float scr[4 * 16 * 17];
+  union {  // Q until its products / outputs are done, then the inverse and T1 / T2 (over L)
+    uint8_t q[NA * AT];
+    struct {
+      union {
+        float l[C][C + 1];
+        struct { uint8_t t1[AT]; uint8_t t2[AT]; } t;
+      } lt;
+      float x[C][C + 1];
+      float scr[4 * 16 * 17];
+    } b;
+  } u;
   float g[C], beta[C], bg[C];  // bg = b e^G (the column scale of T2)
-  uint64_t bar_qk, bar_v, bar_m1, bar_m2;
+  uint64_t bar_qk, bar_v, bar_m1, bar_m2, bar_m3;
   uint32_t tmem_base;
 };
 
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(kThreads)
   pdl_launch_dependents();
   using SM = TcIntraSmem<D>;
   constexpr int AT = SM::AT, NA = SM::NA;
-  constexpr uint32_t kCols = D == 128 ? 256 : 128;
+  constexpr uint32_t kCols = 128;  // K K^T | Q K^T, then W, then U (3 CTAs per SM)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -167,6 +172,7 @@ __global__ void __launch_bounds__(kThreads)
     tc::mbar_init(&sm.bar_v, 1);
     tc::mbar_init(&sm.bar_m1, 1);
     tc::mbar_init(&sm.bar_m2, 1);
+    tc::mbar_init(&sm.bar_m3, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t pol = tc::policy_evict_first();
     tc::mbar_expect_tx(&sm.bar_qk, 2 * NA * AT);
     for (int a = 0; a < NA; ++a) {
-      tc::tma_load_2d(sm.q + a * AT, &qmap, kh * D + 64 * a, c0, &sm.bar_qk, pol);
+      tc::tma_load_2d(sm.u.q + a * AT, &qmap, kh * D + 64 * a, c0, &sm.bar_qk, pol);
       tc::tma_load_2d(sm.k + a * AT, &kmap, kh * D + 64 * a, c0, &sm.bar_qk, pol);
     }
     tc::mbar_expect_tx(&sm.bar_v, NA * AT);
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(kThreads)
   } else if (warp == 1) {  // K K^T -> TMEM [0, 64), Q K^T -> [64, 128)
     tc::mbar_wait(&sm.bar_qk, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t sq = tc::smem_u32(sm.q), sk = tc::smem_u32(sm.k), id = tc::idesc_bf16(64, 64);
+    const uint32_t sq = tc::smem_u32(sm.u.q), sk = tc::smem_u32(sm.k), id = tc::idesc_bf16(64, 64);
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
       const uint32_t off = (kk >> 2) * AT + (kk & 3) * 32;
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kThreads)
   const float gl = sm.g[C - 1];
   for (int idx = tid; idx < C * D / 8; idx += kThreads) {
     const int r = idx / (D / 8), c8 = (idx % (D / 8)) * 8;
-    const uint4 qv = *reinterpret_cast<const uint4*>(sm.q + sw_off(r, c8));
+    const uint4 qv = *reinterpret_cast<const uint4*>(sm.u.q + sw_off(r, c8));
     const uint4 kv = *reinterpret_cast<const uint4*>(sm.k + sw_off(r, c8));
     const bool ok = r < len;
     const float eg = ok ? expf(sm.g[r]) : 0.f, ed = ok ? expf(gl - sm.g[r]) : 0.f;
@@ -252,6 +258,7 @@ __global__ void __launch_bounds__(kThreads)
     *reinterpret_cast<uint4*>(wKd + r * D + c8) = ko;
   }
   if (tid == 0) glast[(size_t)n * Hv + h] = gl;
+  __syncthreads();  // every read of Q is done: L / X take its place
 
   // L = -tril(b K K^T o Gamma, -1) -> shared memory, P = tril(Q K^T o Gamma) -> workspace.
   // M = 64 accumulator: row 16w + i sits in TMEM lane 32w + i (i < 16).
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(kThreads)
             const int j = j0 + e + d;
             const bool ok = i < len && j < len && i >= j;
             const float gam = ok ? expf(gi - sm.g[j]) : 0.f;
-            sm.l[i][j] = (ok && i > j) ? -bi * kk[e + d] * gam : 0.f;
+            sm.u.b.lt.l[i][j] = (ok && i > j) ? -bi * kk[e + d] * gam : 0.f;
             pv[d] = qk[e + d] * gam;
           }
           pk[e >> 1] = pack_bf16(pv[0], pv[1]);
@@ -292,63 +299,76 @@ __global__ void __launch_bounds__(kThreads)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  invert_unit_lower(sm.l, sm.x, sm.scr);  // x = T = (I - L)^-1 (fp32)
+  invert_unit_lower(sm.u.b.lt.l, sm.u.b.x, sm.u.b.scr);  // x = T = (I - L)^-1 (fp32); L is dead after
   // T1 = T diag(b), T2 = T diag(b e^G) as bf16 K-major A operands (swizzled like a TMA atom)
   for (int idx = tid; idx < C * C / 8; idx += kThreads) {
     const int i = idx >> 3, j8 = (idx & 7) * 8;
     uint32_t p1[4], p2[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const float x0 = sm.x[i][j8 + e], x1 = sm.x[i][j8 + e + 1];
+      const float x0 = sm.u.b.x[i][j8 + e], x1 = sm.u.b.x[i][j8 + e + 1];
       p1[e >> 1] = pack_bf16(x0 * sm.beta[j8 + e], x1 * sm.beta[j8 + e + 1]);
       p2[e >> 1] = pack_bf16(x0 * sm.bg[j8 + e], x1 * sm.bg[j8 + e + 1]);
     }
-    *reinterpret_cast<uint4*>(sm.t1 + sw_off(i, j8)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
-    *reinterpret_cast<uint4*>(sm.t2 + sw_off(i, j8)) = make_uint4(p2[0], p2[1], p2[2], p2[3]);
+    *reinterpret_cast<uint4*>(sm.u.b.lt.t.t1 + sw_off(i, j8)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+    *reinterpret_cast<uint4*>(sm.u.b.lt.t.t2 + sw_off(i, j8)) = make_uint4(p2[0], p2[1], p2[2], p2[3]);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's reads
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) {  // W = T2 K -> TMEM [0, D), U = T1 V -> [D, 2D)
-    tc::mbar_wait(&sm.bar_v, 0);
+  // W = T2 K, then U = T1 V, each through TMEM columns [0, D) (K and V read MN-major from
+  // their TMA tiles); the U product is issued once every warp has drained W
+  const uint32_t idw = tc::idesc_bf16(64, D) | (1u << 16);  // B MN-major
+  if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t id = tc::idesc_bf16(64, D) | (1u << 16);  // B MN-major
-    const uint32_t s1 = tc::smem_u32(sm.t1), s2 = tc::smem_u32(sm.t2);
-    const uint32_t sk = tc::smem_u32(sm.k), sv = tc::smem_u32(sm.v);
+    const uint32_t s2 = tc::smem_u32(sm.u.b.lt.t.t2), sk = tc::smem_u32(sm.k);
 #pragma unroll
-    for (int kk = 0; kk < C / 16; ++kk) {
-      tc::umma_w(tmem, tc::desc_sw128(s2 + kk * 32), desc_mn_sw128_c(sk + kk * 2048), id, kk > 0 ? 1u : 0u);
-      tc::umma_w(tmem + D, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sv + kk * 2048), id, kk > 0 ? 1u : 0u);
-    }
+    for (int kk = 0; kk < C / 16; ++kk)
+      tc::umma_w(tmem, tc::desc_sw128(s2 + kk * 32), desc_mn_sw128_c(sk + kk * 2048), idw, kk > 0 ? 1u : 0u);
     tc::commit_w(&sm.bar_m2);
   }
-  tc::mbar_wait(&sm.bar_m2, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  {
+  auto drain = [&](__nv_bfloat16* dst) {  // TMEM [0, D) -> bf16 rows of the workspace
     const int i = 16 * warp + (lane & 15);
     const uint32_t la = tmem + ((uint32_t)(32 * warp) << 16);
 #pragma unroll 1
-    for (int c = 0; c < D; c += 16) {
-      float wv[16], uv[16];
-      tc::tmem_ld16_async(la + c, wv);
-      tc::tmem_ld16_async(la + D + c, uv);
+    for (int c = 0; c < D; c += 32) {
+      float va[16], vb[16];
+      tc::tmem_ld16_async(la + c, va);
+      tc::tmem_ld16_async(la + c + 16, vb);
       tc::tmem_wait_ld();
-      tc::reg_fence16(wv);
-      tc::reg_fence16(uv);
+      tc::reg_fence16(va);
+      tc::reg_fence16(vb);
       if (lane < 16) {
-        uint32_t pw[8], pu[8];
+        uint32_t pa[8], pb[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          pw[e] = pack_bf16(wv[2 * e], wv[2 * e + 1]);
-          pu[e] = pack_bf16(uv[2 * e], uv[2 * e + 1]);
+          pa[e] = pack_bf16(va[2 * e], va[2 * e + 1]);
+          pb[e] = pack_bf16(vb[2 * e], vb[2 * e + 1]);
         }
-        *reinterpret_cast<uint4*>(wW + i * D + c) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-        *reinterpret_cast<uint4*>(wW + i * D + c + 8) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
-        *reinterpret_cast<uint4*>(wU + i * D + c) = make_uint4(pu[0], pu[1], pu[2], pu[3]);
-        *reinterpret_cast<uint4*>(wU + i * D + c + 8) = make_uint4(pu[4], pu[5], pu[6], pu[7]);
+        *reinterpret_cast<uint4*>(dst + i * D + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+        *reinterpret_cast<uint4*>(dst + i * D + c + 8) = make_uint4(pa[4], pa[5], pa[6], pa[7]);
+        *reinterpret_cast<uint4*>(dst + i * D + c + 16) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
+        *reinterpret_cast<uint4*>(dst + i * D + c + 24) = make_uint4(pb[4], pb[5], pb[6], pb[7]);
       }
     }
+  };
+  tc::mbar_wait(&sm.bar_m2, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  drain(wW);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();  // W drained: U reuses its columns
+  if (warp == 1) {
+    tc::mbar_wait(&sm.bar_v, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t s1 = tc::smem_u32(sm.u.b.lt.t.t1), sv = tc::smem_u32(sm.v);
+#pragma unroll
+    for (int kk = 0; kk < C / 16; ++kk)
+      tc::umma_w(tmem, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sv + kk * 2048), idw, kk > 0 ? 1u : 0u);
+    tc::commit_w(&sm.bar_m3);
   }
+  tc::mbar_wait(&sm.bar_m3, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  drain(wU);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
