@@ -3,15 +3,15 @@
 // in-projections (R/PAPER.md:1542-1544, 1584-1587, 1614-1622), the out-projections, the FFN
 // gate/up (SwiGLU fused into the epilogue) and down-projection, and the LM head.
 //
-// tcgen05 + TMEM + TMA, persistent grid of CTA pairs over output tiles:
-//  * pgemm_kernel: a cluster of two CTAs on one TPC computes a 256 x br
-//    tile with one cta_group::2 UMMA stream (M = 256, N = br <= 256, K = 16 per instruction).
-//    Each CTA stages its own 128 rows of A and br / 2 rows of W per 64-column atom through a
-//    7-stage ring, so the pair reads each operand byte once per 256 x br tile (half the L2 -> SM
-//    bytes per flop of a 128-row tile); the leader issues every MMA, both CTAs' TMA loads
-//    complete on the leader's barrier, the MMA commits multicast to both CTAs' barriers and each
-//    CTA drains its own 128 accumulator lanes.  br is chosen per shape to minimise the last
-//    wave's idle pairs (STORE: 256 or 224; SwiGLU: 2h).
+// tcgen05 + TMEM + TMA, persistent grid of CTA pairs over output tiles (pgemm_kernel): a
+// cluster of two CTAs on one TPC computes a 256 x br tile with one cta_group::2 UMMA stream
+// (M = 256, N = br <= 256, K = 16 per instruction).  Each CTA stages its own 128 rows of A and
+// br / 2 rows of W per 64-column atom through a 7-stage ring, so the pair reads each operand
+// byte once per 256 x br tile (half the L2 -> SM bytes per flop of a 128-row tile); the leader
+// issues every MMA, both CTAs' TMA loads complete on the leader's barrier, the MMA commits
+// multicast to both CTAs' barriers and each CTA drains its own 128 accumulator lanes.  br is
+// chosen per shape to minimise the last wave's idle pairs (STORE / fp32 store: 256 or 224;
+// SwiGLU: 2h).  mbarrier waits carry a suspend-time hint (sn_tc.cuh).
 // Warp roles as in the decode GEMM (sn_dgemm.cu): 0 = TMA producer, 1 = MMA issuer, 2 = TMEM
 // allocator, 4-7 = epilogue; two TMEM accumulators (2 x 256 columns) so one tile's epilogue
 // overlaps the next tile's MMAs.  The epilogue is sn_epi.cuh's (STORE / SwiGLU-interleaved).
@@ -21,8 +21,11 @@
 // few A row tiles and weight blocks through L2.
 //
 // Measured (tools/bench_pgemm.py, Apriel shapes, same box): 16K-token prompt 1.55-1.61 PFLOP/s,
-// 0.95-1.01 of cuBLAS; 0.9-1.2x cuBLAS at 256-4096 rows.  A 1-CTA 128 x 256 tile kernel (4-stage
-// ring) reached 0.87-0.95 at 16K and 0.5-0.9x the 2-CTA kernel at every M; removed.
+// 0.93-1.01 of cuBLAS; 0.9-1.2x at 256-4096 rows; 0.90-1.10x at 64K-128K rows.  A whole 16K
+// prefill with these projections matches the cuBLAS-projection prefill (433-446 vs 429-432 ms
+// under the sustained power cap).  A 1-CTA 128 x 256 tile kernel (4-stage ring) reached
+// 0.87-0.95 at 16K and 0.5-0.9x the 2-CTA kernel at every M; removed.  Clusters of four
+// (multicasting A between two pairs) fit only 33 at a time (132 SMs); not used.
 #include <cuda.h>
 #include <stdlib.h>
 
