@@ -21,8 +21,8 @@ ap.add_argument("--context", type=int, default=32768)
 ap.add_argument("--steps", type=int, default=10)
 a = ap.parse_args()
 m = Supernet(APRIEL, PRESETS[a.preset].layer_string, batch=a.batch, max_len=a.context + 128, dtype=torch.bfloat16)
-fill_synthetic(m, a.context)
-g = DecodeGraph(m, feedback=True, preserve_state=False)
+g = DecodeGraph(m, feedback=True, preserve_state=False)  # warm-up + capture on the empty engine (it resets)
+fill_synthetic(m, a.context)  # then the KV pools / states at the context length
 for _ in range(3):
     g.replay()
 torch.cuda.synchronize()

@@ -57,8 +57,8 @@ def random_allocations(n, L, seed=7):
 
 def measure(cfg, layer_string, B, ctx, steps, warmup, ws):
     m = Supernet(cfg, layer_string, batch=B, max_len=ctx + warmup + steps + 8, dtype=torch.bfloat16, seed=0)
-    fill_synthetic(m, ctx)
-    g = DecodeGraph(m, feedback=True, preserve_state=False)
+    g = DecodeGraph(m, feedback=True, preserve_state=False)  # warm-up + capture on the empty engine (it resets)
+    fill_synthetic(m, ctx)  # then the KV pools / states at the context length
     for _ in range(warmup):
         g.replay()
     barrier(ws)
