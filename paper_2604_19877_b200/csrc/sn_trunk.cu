@@ -242,17 +242,27 @@ __global__ void swiglu_il_kernel(const T* __restrict__ gu, T* __restrict__ out, 
 }
 
 // ------------------------------------------------------------------ argmax
+// A row is split across a cluster of CS CTAs (CS = 8 for the 131072-entry vocabulary: 512 CTAs
+// for a 64-row batch instead of 64 long ones); each CTA reduces its slice, rank 0 combines the
+// CS candidates through distributed shared memory.  Ties resolve to the lowest index at every
+// level (deterministic, torch.argmax's first occurrence).
 template <typename T>
-__global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logits, int vocab,
-                                                      int32_t* __restrict__ out, const int32_t* __restrict__ positions) {
+__global__ void __launch_bounds__(256) argmax_kernel(const T* __restrict__ logits, int vocab, int per_cta,
+                                                     int32_t* __restrict__ out, const int32_t* __restrict__ positions) {
   sn::pdl_launch_dependents();
   sn::pdl_wait();
-  __shared__ float sv[32];
-  __shared__ int si[32];
-  const T* row = logits + (size_t)blockIdx.x * vocab;
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  __shared__ float cta_v;
+  __shared__ int cta_i;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks(), part = (int)cluster.block_rank();
+  const int r = blockIdx.x / CS;
+  const T* row = logits + (size_t)r * vocab;
+  const int i0 = part * per_cta, i1 = min(vocab, i0 + per_cta);
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x * 8; i < vocab; i += blockDim.x * 8) {
+  for (int i = i0 + threadIdx.x * 8; i < i1; i += blockDim.x * 8) {
     float f[8];
     load8<T>(row + i, f);
 #pragma unroll
@@ -271,10 +281,21 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const T* __restrict__ logi
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
       if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+    cta_v = best;
+    cta_i = bi;
+  }
+  cluster.sync();
+  if (part == 0 && threadIdx.x == 0) {
+    for (int q = 1; q < CS; ++q) {
+      const float v = *cluster.map_shared_rank(&cta_v, q);
+      const int ix = *cluster.map_shared_rank(&cta_i, q);
+      if (v > best || (v == best && ix < bi)) { best = v; bi = ix; }
+    }
     // an all-NaN row never beats -inf: return token 0, never an out-of-range id that the
     // graph's token feedback would hand to the embedding gather
-    out[blockIdx.x] = (positions && positions[blockIdx.x] < 0) ? -1 : (bi < vocab ? bi : 0);  // idle stays idle
+    out[r] = (positions && positions[r] < 0) ? -1 : (bi < vocab ? bi : 0);  // idle stays idle
   }
+  cluster.sync();  // keep every CTA's candidate alive until rank 0 has read it
 }
 
 }  // namespace sn
@@ -359,8 +380,27 @@ sn_status sn_argmax(const void* logits, int rows, int vocab, int32_t* out_tokens
                     void* stream) {
   SN_REQUIRE(rows > 0 && vocab > 0 && vocab % 8 == 0, "sn_argmax: bad shape rows=%d vocab=%d", rows, vocab);
   return SN_DISPATCH_DTYPE(dtype, T, [&] {
-    launch_pdl(argmax_kernel<T>, dim3(rows), dim3(1024), 0, (cudaStream_t)stream, (const T*)logits, vocab,
-               out_tokens, positions);
+    int cs = 1;
+    while (cs < 8 && vocab / (cs * 2) >= 8192) cs *= 2;  // >= 8K entries per CTA
+    const int per_cta = ((vocab + cs * 8 - 1) / (cs * 8)) * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(rows * cs);
+    cfg.blockDim = dim3(256);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = cs;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, argmax_kernel<T>, (const T*)logits, vocab, per_cta, out_tokens, positions);
+    if (e != cudaSuccess) {
+      set_error("sn_argmax launch: %s", cudaGetErrorString(e));
+      return SN_ECUDA;
+    }
     return check_launch("sn_argmax");
   });
 }

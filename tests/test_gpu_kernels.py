@@ -181,3 +181,30 @@ def test_delta_decode_steps(cfg, kind, B, dtype):
     for d in range(1, W):
         pos = 6 - d
         assert torch.equal(ring_c[:, :, bk.conv_ring_slot(pos, W)].float(), hist[:, :, W - 1 - d])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("rows,vocab", [(1, 4096), (3, 16392), (64, 131072), (5, 100000)])
+def test_argmax_matches_torch_first_occurrence(dtype, rows, vocab):
+    """sn_argmax (a cluster of CTAs per row for large vocabularies) against torch.argmax: the
+    first occurrence on ties, including ties across the CTAs of a row; -1 for idle slots; an
+    all-NaN row gives token 0."""
+    from paper_2604_19877_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(rows * vocab)
+    x = torch.randn(rows, vocab, device="cuda", generator=g).to(dtype)
+    if rows >= 3:  # ties: the max value at several positions spread over the row
+        for r in range(rows):
+            m = x[r].float().max().item() + 1.0
+            for j in (vocab - 1, vocab // 2 + 5, 7 + r):
+                x[r, j] = m
+    out = torch.empty(rows, dtype=torch.int32, device="cuda")
+    ops.argmax(x, out)
+    assert torch.equal(out.long(), torch.argmax(x.float(), dim=-1))
+    pos = torch.arange(rows, dtype=torch.int32, device="cuda")
+    pos[0] = -1  # idle slot
+    ops.argmax(x, out, pos)
+    assert out[0].item() == -1 and torch.equal(out[1:].long(), torch.argmax(x[1:].float(), dim=-1))
+    x[0] = float("nan")
+    ops.argmax(x, out)
+    assert out[0].item() == 0
