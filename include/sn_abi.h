@@ -156,8 +156,9 @@ sn_status sn_gdn_decode(const void* proj, int proj_stride, void* conv_ring,
 /* KDA proj row layout: [ q H*D | k H*D | v H*D | f1 R | g1 R | b H ]
  *   g[h,i] = -exp(A_log[h]) * softplus(f[h*D+i] + dt_bias[h*D+i]),  f = f1 @ f2_w^T
  *   out = RMSNorm(o) * norm_w * sigmoid(g1 @ g2_w^T + g2_b)
- * fg = [2][B][H*D] dtype: (f1 @ f2_w^T, g1 @ g2_w^T), the second low-rank factors, from two
- * decode GEMMs on the f1 / g1 columns of proj (R/PAPER.md:1614-1622).                   */
+ * fg = [B][2*H*D] dtype: row b = [f1 @ f2_w^T | g1 @ g2_w^T], the second low-rank factors,
+ * from one decode GEMM of the adjacent [f1 | g1] columns of proj against the block-diagonal
+ * [f2_w 0; 0 g2_w] (R/PAPER.md:1614-1622).                                              */
 sn_status sn_kda_decode(const void* proj, int proj_stride, const void* fg, void* conv_ring,
                         const void* conv_w, float* state, const int32_t* slot_idx,
                         const int32_t* positions, const float* A_log,

@@ -630,9 +630,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == kDecodeThreads ? 4 : 1)
   float fpre = 0.f, gpre = 0.f;
   if (tid < D) {
     const size_t HD = (size_t)a.Hv * D;
-    const T* fgp = reinterpret_cast<const T*>(a.fg) + (size_t)b * HD + h * D + tid;
+    const T* fgp = reinterpret_cast<const T*>(a.fg) + (size_t)b * 2 * HD + h * D + tid;  // [B][f | g]
     fpre = io<T>::ld(fgp) + dtb;
-    gpre = io<T>::ld(fgp + gridDim.y * HD) + g2b;
+    gpre = io<T>::ld(fgp + HD) + g2b;
   }
   const float braw = io<T>::ld(prow + a.b_off + h);
 

@@ -121,6 +121,8 @@ class Supernet:
             mw = self.w["layers"][l]["mixer"]
             if kind in (FA, SWA) and "qkv_il" not in mw:
                 mw["qkv_il"] = ops.rope_pair_interleave(mw.pop("qkv"), cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim)
+            if kind == KDA and "fg2" not in mw:  # the two low-rank gate factors as one decode GEMM
+                mw["fg2"] = torch.block_diag(mw["f2"], mw["g2"]).contiguous()
 
     # ------------------------------------------------------------------ state pools
     def _alloc_state(self, fa_block_table):
@@ -224,7 +226,7 @@ class Supernet:
         if KDA in kinds:
             self.dec["kda_proj"] = e(B, pad8(cfg.kda_in_width))[:, :cfg.kda_in_width]
             self.dec["kda_out"] = e(B, cfg.kda_dim)
-            self.dec["kda_fg"] = e(2, B, cfg.kda_dim)
+            self.dec["kda_fg"] = e(B, 2 * cfg.kda_dim)  # [f | g] per row
 
     # ------------------------------------------------------------------ decode
     def _gemm(self, x, w, out, mode, role):
@@ -267,7 +269,8 @@ class Supernet:
         D = cfg.kda_head_dim
         self._gemm(h, w["w_in"], d["kda_proj"], "store", "in_proj")
         self._probe_begin("kda_gates", fine=True)
-        ops.kda_gate_factors(d["kda_proj"], w["f2"], w["g2"], d["kda_fg"], cfg.kda_heads, D, cfg.kda_rank)
+        ops.kda_gate_factors(d["kda_proj"], w["f2"], w["g2"], d["kda_fg"], cfg.kda_heads, D, cfg.kda_rank,
+                             fg2=w["fg2"])
         self._probe_end("kda_gates", fine=True)
         self._probe_begin("kda_decode")
         ops.kda_decode(d["kda_proj"], d["kda_fg"], st["conv"], w["conv_w"], st["S"], None, self.positions, w["A_log"],
@@ -359,8 +362,7 @@ class Supernet:
         H, D, R = cfg.kda_heads, cfg.kda_head_dim, cfg.kda_rank
         proj, f1 = d["kda_proj"], 3 * H * D
         return [ops.chain_gemm(self.h, w["w_in"], proj, "store"),
-                ops.chain_gemm(proj[:, f1:f1 + R], w["f2"], d["kda_fg"][0], "store"),
-                ops.chain_gemm(proj[:, f1 + R:f1 + 2 * R], w["g2"], d["kda_fg"][1], "store", depends=False)]
+                ops.chain_gemm(proj[:, f1:f1 + 2 * R], w["fg2"], d["kda_fg"], "store")]
 
     def _mixer_decode(self, l):
         """Layer l's mixer kernel (its in-projection ran at the end of the previous chain)."""

@@ -101,19 +101,24 @@ def gdn_decode(proj, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bi
 
 def kda_decode(proj, fg, conv_ring, conv_w, state, slot_idx, positions, A_log, dt_bias, g2_b, norm_w, out, H, D,
                rank, width, scale, eps_l2, eps_norm):
-    """proj: the in-projection rows [B, N_in]; fg [2, B, H*D] = (f1 @ f2^T, g1 @ g2^T) (dtype of out)."""
+    """proj: the in-projection rows [B, N_in]; fg [B, 2*H*D] = [f1 @ f2^T | g1 @ g2^T] (dtype of out)."""
     B = positions.shape[0]
     call("sn_kda_decode", _p(proj), proj.stride(0), _p(fg), _p(conv_ring), _p(conv_w), _p(state), _p(slot_idx),
          _p(positions), _p(A_log), _p(dt_bias), _p(g2_b), _p(norm_w), _p(out), B, H, D, rank, width,
          scale, eps_l2, eps_norm, dtype_code(out.dtype), _s())
 
 
-def kda_gate_factors(proj, f2, g2, fg, H, D, rank):
-    """fg[0] = f1 @ f2^T, fg[1] = g1 @ g2^T from the f1 / g1 columns of the KDA in-projection
-    (two decode GEMMs: 2 x H*D x rank weights, read once per step)."""
+def kda_gate_factors(proj, f2, g2, fg, H, D, rank, fg2=None):
+    """fg [B, 2*H*D] = [f1 @ f2^T | g1 @ g2^T] from the adjacent f1 / g1 columns of the KDA
+    in-projection: one decode GEMM against the block-diagonal fg2 = [f2 0; 0 g2] (2*H*D x
+    2*rank, built once by the model), or two GEMMs into the two halves when fg2 is not given."""
     f1_off = 3 * H * D
-    gemm_decode(proj[:, f1_off:f1_off + rank], f2, fg[0], "store")
-    gemm_decode(proj[:, f1_off + rank:f1_off + 2 * rank], g2, fg[1], "store")
+    HD = H * D
+    if fg2 is not None:
+        gemm_decode(proj[:, f1_off:f1_off + 2 * rank], fg2, fg, "store")
+        return
+    gemm_decode(proj[:, f1_off:f1_off + rank], f2, fg[:, :HD], "store")
+    gemm_decode(proj[:, f1_off + rank:f1_off + 2 * rank], g2, fg[:, HD:], "store")
 
 
 def conv_prefill(x, x_stride, y, conv_w, conv_ring, cu_seqlens, slot_idx, channels, width, ring_hist=None,

@@ -168,7 +168,7 @@ def test_delta_decode_steps(cfg, kind, B, dtype):
             o_ref, hist, S_ref = kda_core(cfg, p.float(), hist, S_ref, wf)
             pc = torch.zeros(B, -(-width // 8) * 8, dtype=dtype, device="cuda")[:, :width]  # 16-byte row pitch
             pc.copy_(p)
-            fg = torch.empty(2, B, Hv * D, dtype=dtype, device="cuda")
+            fg = torch.empty(B, 2 * Hv * D, dtype=dtype, device="cuda")
             ops.kda_gate_factors(pc, wd["f2"], wd["g2"], fg, Hv, D, cfg.kda_rank)
             ops.kda_decode(pc, fg, ring, wd["conv_w"], S_dev, None, positions, wd["A_log"], wd["dt_bias"],
                            wd["g2_b"], wd["norm_w"], out, Hv, D, cfg.kda_rank, W, 1 / math.sqrt(D), cfg.l2_eps,

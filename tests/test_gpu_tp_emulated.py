@@ -32,7 +32,7 @@ def _run_delta(cfg, kind, w, x, S0):
         ops.gdn_decode(proj, ring, wd["conv_w"], S, None, pos, wd["A_log"], wd["dt_bias"], wd["norm_w"], out, Hk, Hv,
                        D, cfg.conv_width, 1 / math.sqrt(D), cfg.l2_eps, cfg.mixer_norm_eps)
     else:
-        fg = torch.empty(2, B, Hv * D, dtype=x.dtype, device=dev)
+        fg = torch.empty(B, 2 * Hv * D, dtype=x.dtype, device=dev)
         ops.kda_gate_factors(proj, wd["f2"], wd["g2"], fg, Hv, D, cfg.kda_rank)
         ops.kda_decode(proj, fg, ring, wd["conv_w"], S, None, pos, wd["A_log"], wd["dt_bias"], wd["g2_b"],
                        wd["norm_w"], out, Hv, D, cfg.kda_rank, cfg.conv_width, 1 / math.sqrt(D), cfg.l2_eps,

@@ -26,7 +26,7 @@ for kind in (GDN, KDA):
     pos = torch.full((B,), 1000, dtype=torch.int32, device="cuda")
     out = torch.empty(B, Hv * D, device="cuda", dtype=torch.bfloat16)
     if kind == KDA:
-        fgbuf = torch.empty(2, B, cfg.kda_dim, device="cuda", dtype=torch.bfloat16)
+        fgbuf = torch.empty(B, 2 * cfg.kda_dim, device="cuda", dtype=torch.bfloat16)
 
     def run(l):
         if kind == GDN:
