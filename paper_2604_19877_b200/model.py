@@ -442,7 +442,7 @@ class Supernet:
             return {"sn": 2 * len(self.kinds) + 3, "cublas": 0, "nccl": 0}
         sn = 4                                     # embed, final norm, LM head, argmax
         for kind in self.kinds:
-            sn += 2 + 4 + 1 + (2 if kind == KDA else 0)  # norms, in/out-proj, gate/up, down, mixer (+KDA gates)
+            sn += 2 + 4 + 1 + (1 if kind == KDA else 0)  # norms, in/out-proj, gate/up, down, mixer (+KDA gates GEMM)
         nccl = 2 * len(self.kinds) if (self.tp > 1 and self.sym is None) else 0
         return {"sn": sn + (2 * len(self.kinds) if self.sym is not None else 0), "cublas": 0, "nccl": nccl}
 
