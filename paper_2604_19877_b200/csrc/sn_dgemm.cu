@@ -271,7 +271,7 @@ int swiglu_block(int N) {
   const int sms = num_sms();
   int best = 128;
   long best_cost = -1;
-  for (int h = 128; h >= 64; h -= 16) {
+  for (int h = 128; h >= 64; h -= 16) {  // (steps of 8: h = 104, 138 blocks on 138 SMs, measured no faster in decode, 0.95 vs 0.97 of cuBLAS in prefill)
     const long blocks = (N + h - 1) / h;
     const long cost = (blocks + sms - 1) / sms * h;
     if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = h; }

@@ -98,16 +98,17 @@ __device__ __forceinline__ void finalize(const Args& a, int m, bool row_ok, int 
       if (n >= a.N) break;
       get(c, half + c, v);
       if (row_ok) {
+        const int nv = min(min(16, half - c), a.N - n);  // h = 8 mod 16: the last group is half full
         float o[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) o[e] = silu_f(v[e]) * v[16 + e];
         T* dst = reinterpret_cast<T*>(a.out) + (size_t)m * a.ldo + n;
-        if (n + 16 <= a.N && (a.ldo & 7) == 0) {
+        if (nv == 16 && (a.ldo & 7) == 0) {
           store16<T>(dst, o);
         } else {
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            if (n + e < a.N) io<T>::st(dst + e, o[e]);
+            if (e < nv) io<T>::st(dst + e, o[e]);
         }
       }
     }

@@ -248,7 +248,7 @@ extern "C" sn_status sn_gemm_prefill(const void* a, int M, int K, int lda, const
   SN_REQUIRE(ldo >= N && (ldo % 8) == 0, "sn_gemm_prefill: ldo %d", ldo);
   const bool swiglu = mode == SN_GEMM_SWIGLU_IL;
   if (swiglu)
-    SN_REQUIRE(swiglu_h >= 16 && swiglu_h <= 128 && swiglu_h % 16 == 0, "sn_gemm_prefill: SwiGLU block %d", swiglu_h);
+    SN_REQUIRE(swiglu_h >= 16 && swiglu_h <= 128 && swiglu_h % 8 == 0, "sn_gemm_prefill: SwiGLU block %d", swiglu_h);
   const int mtiles = (M + 255) / 256;
   const int slots = num_sms() / 2;  // CTA pairs in flight
   int br = 256;
