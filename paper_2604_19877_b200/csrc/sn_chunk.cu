@@ -90,6 +90,68 @@ __device__ __forceinline__ void invert_unit_lower(const float (*l)[C + 1], float
 }
 
 
+// The same inverse computed in place (T overwrites L: saves the second 64 x 65 fp32 tile).
+// Diagonal blocks first (a warp's lanes read their block of L before any lane writes T into
+// it); then, per block row bi, every warp first accumulates sum_k L_ik T_kj from blocks of
+// row bi that still hold L, a barrier, and only then the T_ij replace them.
+__device__ __forceinline__ void invert_unit_lower_inplace(float (*lx)[C + 1], float* scr) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {  // diagonal blocks (the blocks above the diagonal already hold zeros: L is strictly lower)
+    const int b0 = 16 * warp, j = lane;
+    float xc[16];
+    if (lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float acc = 0.f;
+#pragma unroll
+        for (int m = 0; m < i; ++m) acc += lx[b0 + i][b0 + m] * xc[m];
+        xc[i] = i < j ? 0.f : (i == j ? 1.f : acc);
+      }
+    }
+    __syncwarp();
+    if (lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) lx[b0 + i][b0 + j] = xc[i];
+    }
+  }
+  __syncthreads();
+  const int r = lane >> 1, c0 = (lane & 1) * 8;
+  float* M = scr + warp * 16 * 17;
+  for (int bi = 1; bi < 4; ++bi) {
+    if (warp < bi) {
+      const int bj = warp;
+      float acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+      for (int k = bj; k < bi; ++k)
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const float a = lx[16 * bi + r][16 * k + m];  // L (row bi is replaced only below)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] += a * lx[16 * k + m][16 * bj + c0 + c];
+        }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) M[r * 17 + c0 + c] = acc[c];
+    }
+    __syncthreads();  // every L block of row bi has been read
+    if (warp < bi) {
+      const int bj = warp;
+      float res[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) res[c] = 0.f;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const float a = lx[16 * bi + r][16 * bi + m];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) res[c] += a * M[m * 17 + c0 + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) lx[16 * bi + r][16 * bj + c0 + c] = res[c];
+    }
+    __syncthreads();
+  }
+}
+
 // =====================================================================================
 // Two-phase version (the long-prefill path): the chunk-local work (inverse, W, U, P and
 // the decayed operands) of all chunks runs in parallel, one CTA per (chunk, value head);
@@ -119,16 +181,13 @@ struct TcIntraSmem {
   static constexpr int NA = D / 64;    // atoms per [64 x D] tile
   uint8_t k[NA * AT];
   uint8_t v[NA * AT];
-  union {  // Q until its products / outputs are done, then the inverse and T1 / T2 (over L)
+  union {  // Q until its products / outputs are done, then L -> T in place, then T1 / T2
     uint8_t q[NA * AT];
     struct {
-      union {
-        float l[C][C + 1];
-        struct { uint8_t t1[AT]; uint8_t t2[AT]; } t;
-      } lt;
-      float x[C][C + 1];
+      float lx[C][C + 1];
       float scr[4 * 16 * 17];
     } b;
+    struct { uint8_t t1[AT]; uint8_t t2[AT]; } t;
   } u;
   float g[C], beta[C], bg[C];  // bg = b e^G (the column scale of T2)
   uint64_t bar_qk, bar_v, bar_m1, bar_m2, bar_m3;
@@ -287,7 +346,7 @@ __global__ void __launch_bounds__(kThreads)
             const int j = j0 + e + d;
             const bool ok = i < len && j < len && i >= j;
             const float gam = ok ? expf(gi - sm.g[j]) : 0.f;
-            sm.u.b.lt.l[i][j] = (ok && i > j) ? -bi * kk[e + d] * gam : 0.f;
+            sm.u.b.lx[i][j] = (ok && i > j) ? -bi * kk[e + d] * gam : 0.f;
             pv[d] = qk[e + d] * gam;
           }
           pk[e >> 1] = pack_bf16(pv[0], pv[1]);
@@ -299,19 +358,27 @@ __global__ void __launch_bounds__(kThreads)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  invert_unit_lower(sm.u.b.lt.l, sm.u.b.x, sm.u.b.scr);  // x = T = (I - L)^-1 (fp32); L is dead after
-  // T1 = T diag(b), T2 = T diag(b e^G) as bf16 K-major A operands (swizzled like a TMA atom)
-  for (int idx = tid; idx < C * C / 8; idx += kThreads) {
-    const int i = idx >> 3, j8 = (idx & 7) * 8;
-    uint32_t p1[4], p2[4];
+  invert_unit_lower_inplace(sm.u.b.lx, sm.u.b.scr);  // lx = T = (I - L)^-1 (fp32)
+  // T1 = T diag(b), T2 = T diag(b e^G) as bf16 K-major A operands (swizzled like a TMA atom),
+  // written over T itself: every thread first holds its 4 x 8 entries of T in registers
+  constexpr int TI = C * C / 8 / kThreads;
+  uint32_t p1[TI][4], p2[TI][4];
+#pragma unroll
+  for (int u = 0; u < TI; ++u) {
+    const int idx = tid + u * kThreads, i = idx >> 3, j8 = (idx & 7) * 8;
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const float x0 = sm.u.b.x[i][j8 + e], x1 = sm.u.b.x[i][j8 + e + 1];
-      p1[e >> 1] = pack_bf16(x0 * sm.beta[j8 + e], x1 * sm.beta[j8 + e + 1]);
-      p2[e >> 1] = pack_bf16(x0 * sm.bg[j8 + e], x1 * sm.bg[j8 + e + 1]);
+      const float x0 = sm.u.b.lx[i][j8 + e], x1 = sm.u.b.lx[i][j8 + e + 1];
+      p1[u][e >> 1] = pack_bf16(x0 * sm.beta[j8 + e], x1 * sm.beta[j8 + e + 1]);
+      p2[u][e >> 1] = pack_bf16(x0 * sm.bg[j8 + e], x1 * sm.bg[j8 + e + 1]);
     }
-    *reinterpret_cast<uint4*>(sm.u.b.lt.t.t1 + sw_off(i, j8)) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
-    *reinterpret_cast<uint4*>(sm.u.b.lt.t.t2 + sw_off(i, j8)) = make_uint4(p2[0], p2[1], p2[2], p2[3]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < TI; ++u) {
+    const int idx = tid + u * kThreads, i = idx >> 3, j8 = (idx & 7) * 8;
+    *reinterpret_cast<uint4*>(sm.u.t.t1 + sw_off(i, j8)) = make_uint4(p1[u][0], p1[u][1], p1[u][2], p1[u][3]);
+    *reinterpret_cast<uint4*>(sm.u.t.t2 + sw_off(i, j8)) = make_uint4(p2[u][0], p2[u][1], p2[u][2], p2[u][3]);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's reads
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -321,7 +388,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t idw = tc::idesc_bf16(64, D) | (1u << 16);  // B MN-major
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t s2 = tc::smem_u32(sm.u.b.lt.t.t2), sk = tc::smem_u32(sm.k);
+    const uint32_t s2 = tc::smem_u32(sm.u.t.t2), sk = tc::smem_u32(sm.k);
 #pragma unroll
     for (int kk = 0; kk < C / 16; ++kk)
       tc::umma_w(tmem, tc::desc_sw128(s2 + kk * 32), desc_mn_sw128_c(sk + kk * 2048), idw, kk > 0 ? 1u : 0u);
@@ -360,7 +427,7 @@ __global__ void __launch_bounds__(kThreads)
   if (warp == 1) {
     tc::mbar_wait(&sm.bar_v, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t s1 = tc::smem_u32(sm.u.b.lt.t.t1), sv = tc::smem_u32(sm.v);
+    const uint32_t s1 = tc::smem_u32(sm.u.t.t1), sv = tc::smem_u32(sm.v);
 #pragma unroll
     for (int kk = 0; kk < C / 16; ++kk)
       tc::umma_w(tmem, tc::desc_sw128(s1 + kk * 32), desc_mn_sw128_c(sv + kk * 2048), idw, kk > 0 ? 1u : 0u);
